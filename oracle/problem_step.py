@@ -1,0 +1,325 @@
+"""The reduced-hybrid recursion (4)/(12) driven by a problem description - the
+thing the GPU path must match (survey §8(c) O8, reading R8).
+
+A *problem description* is the fp64 data both sides consume (F13 shared-input
+rule): coarse per-unknown coefficients through a material table, interface
+rows, reduced blocks, sources, probes, initial state.  Its field list is in
+DESIGN.md §6.  This module parses it on its own (it shares no code with the
+binding or the C library) and advances
+
+    (R~ + F~)(x^{n+1} - x^n) = -2 F~ x^n + B~ u^{n+1}            (from (4), (12))
+
+with x = [E_c ; e~ ; H_c ; h~] and the hybrid curl
+    K~ = [[K_cc , S_E],
+          [ 0   , K~'_rr]]            (K_fc = 0, survey O6)
+by forward substitution with the inverse diagonal blocks given as data:
+G_E = cb (coarse), c_if (interface rows), g_e (reduced); G_H = ch, g_h.
+K_cc is the oracle's *own* incidence matrix of the coarse grid
+(oracle.yee.incidence), restricted to the active unknowns; interface rows
+use the problem's W_if instead.  H rows use K^T except that surface H rows are
+divided by their common factor (reading R8: a row scaling of the H equations,
+which leaves the solution of (4) unchanged), so they carry +-1 with the
+regular ch, exactly as stated in the problem.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import yee
+from .matrix_form import step_leapfrog
+
+
+def storage_size(dim, n):
+    return int(np.prod(yee.storage_shape(dim, n)))
+
+
+@dataclass
+class HybridRecursion:
+    dim: int
+    n: tuple
+    S: int                   # storage size per component
+    e_ids: np.ndarray        # flat unknown ids (comp*S + flat) of active coarse E
+    h_ids: np.ndarray
+    n_red: tuple             # total reduced unknowns (E side, H side)
+    red_off: list            # per block: (E, H) offsets of instance 0
+    KE: sp.csr_matrix        # rows [E_c ; e~], cols [H_c ; h~]
+    KH: sp.csr_matrix        # rows [H_c ; h~], cols [E_c ; e~]
+    GE: np.ndarray
+    GH: np.ndarray
+    src_row: np.ndarray      # E row of each source
+    src_coef: np.ndarray
+    wave: np.ndarray         # [n_wave][n_src][B]
+    probe_rows: list         # per probe: (side, sparse row vector over that side)
+
+
+def build(problem) -> HybridRecursion:
+    dim = int(problem["dim"])
+    n = tuple(int(v) for v in problem["n"]) + ((1,) if len(problem["n"]) == 2 else ())
+    d = float(problem["delta"])
+    shp = yee.storage_shape(dim, n)
+    S = int(np.prod(shp))
+    ys = yee.assemble(dim, n, (d, d, d), 1.0, 1.0, eliminate_pec=True)
+    Kinc = yee.incidence(ys)          # +-1 (E rows: K = -curl_H)
+    ecomps, hcomps = ys.e_comps, ys.h_comps
+
+    # ---- per-unknown coefficients from the material table --------------------
+    def coef_of(comp):
+        if problem.get("mat_id") is None:
+            return np.full(shp, float(problem["uniform_coef"][comp]))
+        mid = np.asarray(problem["mat_id"]).reshape(shp)
+        return np.asarray(problem["mat_coef"], dtype=np.float64)[:, comp][mid]
+
+    def ifbit(comp):
+        if problem.get("mat_id") is None:
+            return np.zeros(shp, bool)
+        mid = np.asarray(problem["mat_id"]).reshape(shp)
+        return (np.asarray(problem["mat_ifmask"]).astype(np.int64)[mid] >> comp) & 1 == 1
+
+    itf = problem.get("interface")
+    if_ids = np.asarray(itf["unknown"], dtype=np.int64) if itf is not None else np.zeros(0, np.int64)
+    # the material table's interface bits must mark exactly the interface rows
+    marked = np.concatenate([c * S + np.nonzero(ifbit(c).ravel())[0] for c in ecomps])
+    if not np.array_equal(np.sort(marked), np.sort(if_ids)):
+        raise ValueError("interface rows and material interface bits disagree")
+
+    # active coarse E: regular (cb != 0) or interface rows; yee index gives the
+    # wall-PEC elimination and the column numbering of Kinc.
+    e_sel, e_ids, e_G, e_isif = [], [], [], []
+    for c in ecomps:
+        cb = coef_of(c)
+        m = ys.index[c] >= 0
+        reg = m & (cb != 0.0) & ~ifbit(c)
+        e_sel.append((c, reg))
+    h_sel = []
+    for c in hcomps:
+        ch = coef_of(c)
+        m = (ys.index[c] >= 0) & (ch != 0.0)
+        h_sel.append((c, m))
+
+    # regular E rows
+    rows_yee, GE_reg, ids_reg = [], [], []
+    for c, reg in e_sel:
+        pos = np.nonzero(reg.ravel())[0]
+        rows_yee.append(ys.index[c].ravel()[pos])
+        GE_reg.append(coef_of(c).ravel()[pos])
+        ids_reg.append(c * S + pos)
+    rows_yee = np.concatenate(rows_yee)
+    GE_reg = np.concatenate(GE_reg)
+    ids_reg = np.concatenate(ids_reg)
+    cols_yee, GH_c, h_ids = [], [], []
+    for c, m in h_sel:
+        pos = np.nonzero(m.ravel())[0]
+        cols_yee.append(ys.index[c].ravel()[pos] )
+        GH_c.append(coef_of(c).ravel()[pos])
+        h_ids.append(c * S + pos)
+    cols_yee = np.concatenate(cols_yee)
+    GH_c = np.concatenate(GH_c)
+    h_ids = np.concatenate(h_ids)
+    Nh_c = len(h_ids)
+    hpos = -np.ones(ys.Nh, np.int64)
+    hpos[cols_yee] = np.arange(Nh_c)
+
+    # E ordering: regular rows then interface rows
+    n_reg = len(ids_reg)
+    n_if = len(if_ids)
+    e_ids = np.concatenate([ids_reg, if_ids])
+    Ne_c = len(e_ids)
+
+    blocks = problem.get("blocks", []) or []
+
+    def qe_qh(b):
+        return int(b.get("qe", b.get("q"))), int(b.get("qh", b.get("q")))
+
+    red_off, off_e, off_h = [], 0, 0
+    for b in blocks:
+        qe, qh = qe_qh(b)
+        red_off.append((off_e, off_h))
+        off_e += qe * int(b["n_inst"])
+        off_h += qh * int(b["n_inst"])
+    n_red = (off_e, off_h)
+    NE, NH = Ne_c + off_e, Nh_c + off_h
+
+    # ---- K_E -----------------------------------------------------------------
+    Kc = Kinc[rows_yee][:, cols_yee].tocoo()            # regular rows x active H
+    r_, c_, v_ = [Kc.row], [Kc.col], [Kc.data]
+    # map flat H ids -> column (via yee index of the storage position)
+    def hcol(flat_ids):
+        comp = flat_ids // S
+        pos = flat_ids % S
+        out = np.empty(len(flat_ids), np.int64)
+        for c in np.unique(comp):
+            m = comp == c
+            yi = ys.index[int(c)].ravel()[pos[m]]
+            if np.any(yi < 0):
+                raise ValueError("W_if references an eliminated H unknown")
+            out[m] = hpos[yi]
+        if np.any(out < 0):
+            raise ValueError("W_if references an inactive H unknown")
+        return out
+    GE_if = np.zeros(n_if)
+    if n_if:
+        rp = np.asarray(itf["rowptr"], np.int64)
+        cols = hcol(np.asarray(itf["col"], np.int64))
+        vals = np.asarray(itf["val"], np.float64)
+        rr = np.repeat(np.arange(n_if), np.diff(rp))
+        r_.append(n_reg + rr); c_.append(cols); v_.append(vals)
+        GE_if = np.asarray(itf["c"], np.float64)
+        for r in range(n_if):
+            bl, inst, loc = int(itf["block"][r]), int(itf["inst"][r]), int(itf["local"][r])
+            b = blocks[bl]
+            qe, qh = qe_qh(b)
+            o = Nh_c + red_off[bl][1] + inst * qh
+            r_.append(np.full(qh, n_reg + r)); c_.append(o + np.arange(qh))
+            v_.append(np.asarray(b["S_E"], np.float64)[loc])
+    GE_red, GH_red = [], []
+    for bl, b in enumerate(blocks):
+        qe, qh = qe_qh(b)
+        Kt = np.asarray(b["K"], np.float64).reshape(qe, qh)
+        for inst in range(int(b["n_inst"])):
+            oe = red_off[bl][0] + inst * qe
+            oh = red_off[bl][1] + inst * qh
+            rr, cc = np.meshgrid(np.arange(qe), np.arange(qh), indexing="ij")
+            r_.append(Ne_c + oe + rr.ravel()); c_.append(Nh_c + oh + cc.ravel()); v_.append(Kt.ravel())
+            # G_e = (D~_eps/dt)^{-1}: scalar dt (D~ = I) or a diagonal
+            GE_red.append(np.broadcast_to(np.asarray(b["g_e"], np.float64), (qe,)).copy())
+            GH_red.append(np.broadcast_to(np.asarray(b["g_h"], np.float64), (qh,)).copy())
+    KE = sp.csr_matrix((np.concatenate(v_), (np.concatenate(r_), np.concatenate(c_))), shape=(NE, NH))
+
+    # ---- K_H: coarse H rows = K_inc^T over active E (interface E included,
+    # with the incidence weights: surface H rows row-scaled, reading R8) -------
+    e_yee_rows = []
+    for fid in e_ids:
+        c, p = int(fid // S), int(fid % S)
+        e_yee_rows.append(int(ys.index[c].ravel()[p]))
+    e_yee_rows = np.array(e_yee_rows, np.int64)
+    if np.any(e_yee_rows < 0):
+        raise ValueError("an active E unknown lies on a PEC wall")
+    KHc = (Kinc[e_yee_rows][:, cols_yee].T).tocoo()      # Nh_c x Ne_c
+    r_, c_, v_ = [KHc.row], [KHc.col], [KHc.data]
+    if n_if:
+        for r in range(n_if):
+            bl, inst, loc = int(itf["block"][r]), int(itf["inst"][r]), int(itf["local"][r])
+            b = blocks[bl]
+            qe, qh = qe_qh(b)
+            o = red_off[bl][1] + inst * qh
+            r_.append(Nh_c + o + np.arange(qh)); c_.append(np.full(qh, n_reg + r))
+            v_.append(np.asarray(b["S_E"], np.float64)[loc])
+    for bl, b in enumerate(blocks):
+        qe, qh = qe_qh(b)
+        Kt = np.asarray(b["K"], np.float64).reshape(qe, qh)
+        for inst in range(int(b["n_inst"])):
+            oe = red_off[bl][0] + inst * qe
+            oh = red_off[bl][1] + inst * qh
+            rr, cc = np.meshgrid(np.arange(qh), np.arange(qe), indexing="ij")
+            # (K^T)[r, c] = K[c, r]
+            r_.append(Nh_c + oh + rr.ravel()); c_.append(Ne_c + oe + cc.ravel()); v_.append(Kt.T.ravel())
+    KH = sp.csr_matrix((np.concatenate(v_), (np.concatenate(r_), np.concatenate(c_))), shape=(NH, NE))
+
+    GE = np.concatenate([GE_reg, GE_if] + GE_red)
+    GH = np.concatenate([GH_c] + GH_red)
+
+    # ---- sources ---------------------------------------------------------------
+    src = problem.get("sources")
+    epos = {int(v): i for i, v in enumerate(e_ids)}
+    if src is not None and len(src["unknown"]):
+        src_row = np.array([epos[int(u)] for u in src["unknown"]], np.int64)
+        src_coef = np.asarray(src["coef"], np.float64)
+        wave = np.asarray(src["wave"], np.float64)
+    else:
+        src_row, src_coef, wave = np.zeros(0, np.int64), np.zeros(0), np.zeros((0, 0, 1))
+
+    # ---- probes ----------------------------------------------------------------
+    hposd = {int(v): i for i, v in enumerate(h_ids)}
+    probe_rows = []
+    prb = problem.get("probes") or []
+    for p in prb:
+        kind = int(p["kind"])
+        if kind == 0:            # weighted sum of coarse unknowns, all E or all H
+            ids = [int(u) for u in p["unknowns"]]
+            ws = [float(w) for w in p["weights"]]
+            if all((u // S) in ecomps for u in ids):
+                probe_rows.append(("E", {epos[u]: w for u, w in zip(ids, ws)}))
+            elif all((u // S) in hcomps for u in ids):
+                probe_rows.append(("H", {hposd[u]: w for u, w in zip(ids, ws)}))
+            else:
+                raise ValueError("a coarse probe mixes E and H unknowns")
+        else:
+            bl, inst = int(p["block"]), int(p["inst"])
+            qe, qh = qe_qh(blocks[bl])
+            if kind == 1:
+                vrow = np.asarray(p["vrow"], np.float64)[:qe]
+                o = Ne_c + red_off[bl][0] + inst * qe
+                probe_rows.append(("E", {o + i: vrow[i] for i in range(qe) if vrow[i] != 0}))
+            else:
+                vrow = np.asarray(p["vrow"], np.float64)[:qh]
+                o = Nh_c + red_off[bl][1] + inst * qh
+                probe_rows.append(("H", {o + i: vrow[i] for i in range(qh) if vrow[i] != 0}))
+    return HybridRecursion(dim, n, S, e_ids, h_ids, n_red, red_off, KE, KH, GE, GH,
+                           src_row, src_coef, wave, probe_rows)
+
+
+def initial_state(rec: HybridRecursion, problem, member=0):
+    NE, NH = rec.KE.shape
+    E = np.zeros(NE)
+    H = np.zeros(NH)
+    init = problem.get("init")
+    if init:
+        for c, arr in init.items():
+            a = np.asarray(arr, np.float64)
+            a = a.reshape(-1, rec.S)[member] if a.size != rec.S else a.ravel()
+            c = int(c)
+            ids = rec.e_ids if c < 3 else rec.h_ids
+            m = (ids // rec.S) == c
+            tgt = E if c < 3 else H
+            tgt[np.nonzero(m)[0]] = a[ids[m] % rec.S]
+    return E, H
+
+
+def probe_matrices(rec: HybridRecursion):
+    NE, NH = rec.KE.shape
+    P = len(rec.probe_rows)
+    PE = sp.lil_matrix((P, NE))
+    PH = sp.lil_matrix((P, NH))
+    for i, (side, row) in enumerate(rec.probe_rows):
+        tgt = PE if side == "E" else PH
+        for k, w in row.items():
+            tgt[i, k] = w
+    return PE.tocsr(), PH.tocsr()
+
+
+def run(problem, n_steps, member=0, state=None, start_step=0, rec=None):
+    """Advance n_steps from the initial (or given) state for one batch member.
+
+    Returns (E, H, probes[n_steps][n_probe], rec).  Probe sampling: E after the
+    E half (time (n+1) dt), H after the H half."""
+    rec = build(problem) if rec is None else rec
+    E, H = initial_state(rec, problem, member) if state is None else state
+    PE, PH = probe_matrices(rec)
+    probes = np.zeros((n_steps, len(rec.probe_rows)))
+    for s in range(n_steps):
+        step = start_step + s
+        su = None
+        if len(rec.src_row) and step < rec.wave.shape[0]:
+            su = np.zeros(len(E))
+            # E += -coef * J^{n+1/2}   (B holds the sign)
+            np.add.at(su, rec.src_row, -rec.src_coef * rec.wave[step, :, member])
+        E, H = step_leapfrog(E, H, rec.GE, rec.GH, rec.KE, rec.KH, su_E=su)
+        probes[s] = PE @ E + PH @ H
+    return E, H, probes, rec
+
+
+def to_storage(rec: HybridRecursion, E, H):
+    """Coarse parts as per-component storage arrays (flat), reduced parts split."""
+    out = {}
+    Ne_c = len(rec.e_ids)
+    Nh_c = len(rec.h_ids)
+    for ids, vec in ((rec.e_ids, E[:Ne_c]), (rec.h_ids, H[:Nh_c])):
+        comp = ids // rec.S
+        for c in np.unique(comp):
+            a = out.setdefault(int(c), np.zeros(rec.S))
+            m = comp == c
+            a[ids[m] % rec.S] = vec[m]
+    return out, E[Ne_c:], H[Nh_c:]
