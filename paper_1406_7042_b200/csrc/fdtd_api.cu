@@ -1,0 +1,878 @@
+// fdtd_api.cu — the C ABI of include/fdtd.h: validation, upload, step
+// orchestration (eager launches or captured CUDA graphs), probes, state.
+#include "../../include/fdtd.h"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(FDTD_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                             \
+  } while (0)
+
+template <typename T>
+fdtd::Coef<T> make_coef(double c);
+template <>
+fdtd::Coef<float> make_coef<float>(double c) {
+  fdtd::Coef<float> r;
+  r.hi = (float)c;
+  r.lo = (float)(c - (double)r.hi);   // hi/lo split of the fp64 coefficient (R11, F12)
+  return r;
+}
+template <>
+fdtd::Coef<double> make_coef<double>(double c) {
+  fdtd::Coef<double> r;
+  r.hi = c;
+  r.lo = 0.0;
+  return r;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct fdtd_t {
+  virtual ~fdtd_t() {}
+  virtual int step(int64_t n) = 0;
+  virtual int probe(double* out, int64_t cap, int64_t* written) = 0;
+  virtual int get_state(int which, double* out, int64_t n) = 0;
+  virtual int set_state(int which, const double* in, int64_t n) = 0;
+  virtual int sync() = 0;
+  int64_t launches = 0;
+};
+
+namespace {
+
+struct DevMem {
+  void* (*alloc)(size_t, void*) = nullptr;
+  void (*free_)(void*, void*) = nullptr;
+  void* ctx = nullptr;
+  std::vector<void*> owned;
+  ~DevMem() {
+    for (void* p : owned) {
+      if (free_) free_(p, ctx);
+      else cudaFree(p);
+    }
+  }
+  void* get(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    void* p = nullptr;
+    if (alloc) p = alloc(bytes, ctx);
+    else if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
+    if (p) owned.push_back(p);
+    return p;
+  }
+};
+
+template <typename T>
+struct BlockDev {
+  int qe, qh, n_inst, n_if, N;
+  T* K = nullptr;        // [qe][qh]
+  T* Mh = nullptr;       // [qh][qe + n_if] = [K^T | S_E^T]
+  T* SE = nullptr;       // [n_if][qh]
+  T* ge = nullptr;       // [qe]
+  T* gh = nullptr;       // [qh]
+  int64_t xh_off = 0;    // offset of this block's X_h = [e~ ; G] in xh_all ([qe+n_if][N])
+  int64_t h_off = 0;     // offset in h_all ([qh][N])
+  int64_t y_off = 0;     // offset in y_all ([n_if][N])
+};
+
+template <typename T>
+struct Impl : public fdtd_t {
+  // grid
+  int dim = 3, nx = 0, ny = 0, nz = 0, B = 1, px = 0;
+  int64_t S = 0;          // storage indices per component (unpadded)
+  int64_t plane = 0;      // (ny+1)*px
+  int64_t nplanes = 0;    // nz+1 (3-D) or 1 (2-D)
+  int64_t elems = 0;      // device elements per component (plane*nplanes*B)
+  cudaStream_t stream = nullptr;
+  DevMem mem;
+  // fields: F[parity][comp]
+  T* F[2][6] = {{nullptr}};
+  T** dF[2] = {nullptr, nullptr};     // device copies of F[parity] (for pointer-array kernels)
+  // materials
+  bool uniform = true;
+  int n_mat = 0;
+  uint8_t* mat_id = nullptr;
+  fdtd::Coef<T>* tab = nullptr;
+  uint8_t* ifm = nullptr;
+  fdtd::Coef<T> u0{}, u1{};
+  // explicit rows
+  fdtd::RowsE<T> rows{};
+  // blocks
+  std::vector<BlockDev<T>> blocks;
+  T* xh_all = nullptr;
+  T* h_all = nullptr;
+  T* y_all = nullptr;
+  int64_t xh_size = 0, h_size = 0, y_size = 0;
+  int64_t n_gather = 0;
+  int32_t* g_comp = nullptr;
+  int64_t* g_off = nullptr;
+  int64_t* g_dst = nullptr;
+  T** dRED = nullptr;                 // {xh_all, h_all}
+  // probes
+  fdtd::Probes<T> pr{};
+  int n_probe = 0;
+  T* ring = nullptr;
+  int64_t cap = 65536;
+  std::vector<double> host_probes;    // drained samples [step][probe][B]
+  int64_t drained_to = 0;             // absolute step up to which the ring was drained
+  // control
+  int64_t* d_step = nullptr;
+  unsigned long long* d_bad = nullptr;
+  int64_t host_step = 0;              // steps enqueued
+  int check_every = 100;
+  int graph_steps = 32;
+  cudaGraphExec_t graph = nullptr;
+  int64_t graph_kernels = 0;
+  T* staging = nullptr;               // pinned host staging
+  size_t staging_bytes = 0;
+  int kchunk = 16;
+
+  ~Impl() override {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (staging) cudaFreeHost(staging);
+  }
+
+  template <typename U>
+  U* dalloc(int64_t count) {
+    return reinterpret_cast<U*>(mem.get(sizeof(U) * (size_t)count));
+  }
+
+  int64_t dev_off(int64_t s) const {   // storage index -> device storage offset (before *B)
+    int64_t i, j, k;
+    if (dim == 3) {
+      i = s % (nx + 1);
+      j = (s / (nx + 1)) % (ny + 1);
+      k = s / ((int64_t)(nx + 1) * (ny + 1));
+    } else {
+      i = s % (nx + 1);
+      j = s / (nx + 1);
+      k = 0;
+    }
+    return (k * (ny + 1) + j) * px + i;
+  }
+
+  bool is_e(int c) const { return dim == 3 ? (c >= 0 && c <= 2) : c == 2; }
+  bool is_h(int c) const { return dim == 3 ? (c >= 3 && c <= 5) : (c == 3 || c == 4); }
+
+  int create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_interface* itf,
+             const fdtd_reduced_block* bl, int n_blocks, const fdtd_sources* src,
+             const fdtd_probes* probes, const fdtd_exec* ex);
+  int launch_step(int parity, cudaStream_t st, int64_t* count);
+  int step(int64_t n) override;
+  int drain();
+  int probe(double* out, int64_t cap, int64_t* written) override;
+  int get_state(int which, double* out, int64_t n) override;
+  int set_state(int which, const double* in, int64_t n) override;
+  int sync() override;
+  int check_async();
+};
+
+template <typename T>
+int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_interface* itf,
+                    const fdtd_reduced_block* bl, int n_blocks, const fdtd_sources* src,
+                    const fdtd_probes* probes, const fdtd_exec* ex) {
+  dim = g->dim;
+  nx = g->nx; ny = g->ny; nz = (dim == 3) ? g->nz : 0;
+  B = g->batch;
+  if (ex) {
+    stream = reinterpret_cast<cudaStream_t>(ex->stream);
+    mem.alloc = ex->alloc; mem.free_ = ex->free; mem.ctx = ex->alloc_ctx;
+    check_every = ex->check_every < 0 ? 100 : ex->check_every;
+    graph_steps = ex->graph_steps < 0 ? 32 : ex->graph_steps;
+    if (graph_steps % 2) graph_steps += 1;
+    if (ex->probe_capacity > 0) cap = ex->probe_capacity;
+  }
+  px = (B == 1) ? ((nx + 1 + 31) / 32) * 32 : (nx + 1);
+  plane = (int64_t)(ny + 1) * px;
+  nplanes = (dim == 3) ? (nz + 1) : 1;
+  S = (int64_t)(nx + 1) * (ny + 1) * (dim == 3 ? (nz + 1) : 1);
+  elems = plane * nplanes * B;
+  const int ncomp_first = dim == 3 ? 0 : 2, ncomp_last = dim == 3 ? 5 : 4;
+
+  // ---- fields (both parities), zero initial state ----
+  for (int p = 0; p < 2; ++p)
+    for (int c = ncomp_first; c <= ncomp_last; ++c) {
+      F[p][c] = dalloc<T>(elems);
+      if (!F[p][c]) return fail(FDTD_ENOMEM, "field allocation failed (%lld elements)", (long long)elems);
+      CK(cudaMemsetAsync(F[p][c], 0, sizeof(T) * elems, stream));
+    }
+  for (int p = 0; p < 2; ++p) {
+    dF[p] = dalloc<T*>(6);
+    CK(cudaMemcpyAsync(dF[p], F[p], sizeof(T*) * 6, cudaMemcpyHostToDevice, stream));
+  }
+
+  // ---- materials ----
+  std::vector<double> coef;           // [n_mat][6]
+  std::vector<uint8_t> ifmask;
+  std::vector<uint8_t> ids;           // storage-indexed (unpadded), built lazily
+  uniform = (mat == nullptr || mat->n_mat == 0);
+  if (!uniform) {
+    if (mat->n_mat > 256 || !mat->mat_id || !mat->coef || !mat->if_mask)
+      return fail(FDTD_EINVAL, "materials: n_mat must be <= 256 with mat_id/coef/if_mask given");
+    n_mat = mat->n_mat;
+    coef.assign(mat->coef, mat->coef + 6 * n_mat);
+    ifmask.assign(mat->if_mask, mat->if_mask + n_mat);
+    ids.assign(mat->mat_id, mat->mat_id + S);
+    for (int64_t s = 0; s < S; ++s)
+      if (ids[s] >= n_mat) return fail(FDTD_EINVAL, "mat_id[%lld] = %d >= n_mat", (long long)s, ids[s]);
+  } else {
+    const double* uc = mat ? mat->uniform_coef : nullptr;
+    n_mat = 1;
+    coef.assign(6, 0.0);
+    if (uc) for (int c = 0; c < 6; ++c) coef[c] = uc[c];
+    ifmask.assign(1, 0);
+  }
+  auto ensure_table = [&]() {
+    if (uniform) { uniform = false; ids.assign(S, 0); }
+  };
+  auto mat_coef = [&](int64_t s, int c) -> double {
+    return coef[(uniform ? 0 : ids[s]) * 6 + c];
+  };
+  auto storage_ijk = [&](int64_t s, int& i, int& j, int& k) {
+    i = (int)(s % (nx + 1));
+    if (dim == 3) { j = (int)((s / (nx + 1)) % (ny + 1)); k = (int)(s / ((int64_t)(nx + 1) * (ny + 1))); }
+    else { j = (int)(s / (nx + 1)); k = 0; }
+  };
+  auto sidx = [&](int i, int j, int k) -> int64_t {
+    return dim == 3 ? ((int64_t)k * (ny + 1) + j) * (nx + 1) + i : (int64_t)j * (nx + 1) + i;
+  };
+
+  // ---- blocks ----
+  if (n_blocks < 0 || (n_blocks > 0 && !bl)) return fail(FDTD_EINVAL, "blocks: n_blocks/pointer mismatch");
+  blocks.resize(n_blocks);
+  for (int b = 0; b < n_blocks; ++b) {
+    const fdtd_reduced_block& R = bl[b];
+    BlockDev<T>& D = blocks[b];
+    if (R.qe < 1 || R.qh < 1 || R.n_inst < 1 || R.n_if < 0 || !R.K || (R.n_if > 0 && !R.S_E))
+      return fail(FDTD_EINVAL, "block %d: q < 1, n_inst < 1 or missing matrices", b);
+    D.qe = R.qe; D.qh = R.qh; D.n_inst = R.n_inst; D.n_if = R.n_if; D.N = R.n_inst * B;
+    D.xh_off = xh_size; xh_size += (int64_t)(D.qe + D.n_if) * D.N;
+    D.h_off = h_size; h_size += (int64_t)D.qh * D.N;
+    D.y_off = y_size; y_size += (int64_t)D.n_if * D.N;
+    std::vector<T> K((size_t)D.qe * D.qh), Mh((size_t)D.qh * (D.qe + D.n_if)), SE((size_t)D.n_if * D.qh);
+    for (int r = 0; r < D.qe; ++r)
+      for (int c = 0; c < D.qh; ++c) {
+        K[(size_t)r * D.qh + c] = (T)R.K[(size_t)r * D.qh + c];
+        Mh[(size_t)c * (D.qe + D.n_if) + r] = (T)R.K[(size_t)r * D.qh + c];
+      }
+    for (int r = 0; r < D.n_if; ++r)
+      for (int c = 0; c < D.qh; ++c) {
+        SE[(size_t)r * D.qh + c] = (T)R.S_E[(size_t)r * D.qh + c];
+        Mh[(size_t)c * (D.qe + D.n_if) + D.qe + r] = (T)R.S_E[(size_t)r * D.qh + c];
+      }
+    std::vector<T> ge(D.qe), gh(D.qh);
+    for (int r = 0; r < D.qe; ++r) ge[r] = (T)(R.g_e ? R.g_e[r] : R.g_e_scalar);
+    for (int r = 0; r < D.qh; ++r) gh[r] = (T)(R.g_h ? R.g_h[r] : R.g_h_scalar);
+    D.K = dalloc<T>(K.size()); D.Mh = dalloc<T>(Mh.size()); D.SE = dalloc<T>(SE.size());
+    D.ge = dalloc<T>(D.qe); D.gh = dalloc<T>(D.qh);
+    if (!D.K || !D.Mh || !D.SE || !D.ge || !D.gh) return fail(FDTD_ENOMEM, "block %d allocation failed", b);
+    CK(cudaMemcpy(D.K, K.data(), sizeof(T) * K.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(D.Mh, Mh.data(), sizeof(T) * Mh.size(), cudaMemcpyHostToDevice));
+    if (!SE.empty()) CK(cudaMemcpy(D.SE, SE.data(), sizeof(T) * SE.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(D.ge, ge.data(), sizeof(T) * ge.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(D.gh, gh.data(), sizeof(T) * gh.size(), cudaMemcpyHostToDevice));
+  }
+  xh_all = dalloc<T>(xh_size); h_all = dalloc<T>(h_size); y_all = dalloc<T>(y_size);
+  CK(cudaMemsetAsync(xh_all, 0, sizeof(T) * std::max<int64_t>(xh_size, 1), stream));
+  CK(cudaMemsetAsync(h_all, 0, sizeof(T) * std::max<int64_t>(h_size, 1), stream));
+  CK(cudaMemsetAsync(y_all, 0, sizeof(T) * std::max<int64_t>(y_size, 1), stream));
+  dRED = dalloc<T*>(2);
+  {
+    T* red[2] = {xh_all, h_all};
+    CK(cudaMemcpy(dRED, red, sizeof(red), cudaMemcpyHostToDevice));
+  }
+
+  // ---- explicit rows: interface rows, then source rows on regular unknowns ----
+  struct HRow { std::vector<std::pair<int64_t, double>> w; double c = 0; int64_t y = -1; int src = -1; double cs = 0; int comp = 0; int64_t s = 0; };
+  std::vector<HRow> hrows;
+  std::map<int64_t, int> row_of;      // E unknown id -> explicit row
+  std::vector<int32_t> gcomp; std::vector<int64_t> goff, gdst;
+  if (itf && itf->n_rows > 0) {
+    if (!itf->unknown || !itf->c || !itf->rowptr || !itf->block || !itf->inst || !itf->local)
+      return fail(FDTD_EINVAL, "interface: missing arrays");
+    if (uniform) return fail(FDTD_EINVAL, "interface rows need a material table with if_mask bits");
+    for (int64_t r = 0; r < itf->n_rows; ++r) {
+      const int64_t u = itf->unknown[r];
+      const int c = (int)(u / S);
+      const int64_t s = u % S;
+      if (u < 0 || !is_e(c)) return fail(FDTD_ESTAMP, "interface row %lld: %lld is not an E unknown", (long long)r, (long long)u);
+      if (!((ifmask[ids[s]] >> c) & 1))
+        return fail(FDTD_EINVAL, "interface row %lld: if_mask bit not set for its unknown", (long long)r);
+      if (row_of.count(u)) return fail(FDTD_EINVAL, "interface row %lld duplicates an unknown", (long long)r);
+      const int b = itf->block[r], in = itf->inst[r], l = itf->local[r];
+      if (b < 0 || b >= n_blocks || in < 0 || in >= blocks[b].n_inst || l < 0 || l >= blocks[b].n_if)
+        return fail(FDTD_EINVAL, "interface row %lld: block/inst/local out of range", (long long)r);
+      HRow h;
+      h.comp = c; h.s = s; h.c = itf->c[r];
+      for (int64_t k = itf->rowptr[r]; k < itf->rowptr[r + 1]; ++k) {
+        const int64_t hu = itf->col[k];
+        if (hu < 0 || !is_h((int)(hu / S))) return fail(FDTD_ESTAMP, "interface row %lld: column %lld is not an H unknown", (long long)r, (long long)hu);
+        h.w.push_back({hu, itf->val[k]});
+      }
+      const BlockDev<T>& D = blocks[b];
+      h.y = D.y_off + (int64_t)l * D.N + (int64_t)in * B;
+      row_of[u] = (int)hrows.size();
+      hrows.push_back(h);
+      gcomp.push_back(c); goff.push_back(dev_off(s));
+      gdst.push_back(D.xh_off + (int64_t)(D.qe + l) * D.N + (int64_t)in * B);
+    }
+  }
+  int64_t n_src = 0, n_wave = 0;
+  std::vector<T> wave;
+  if (src && src->n_src > 0) {
+    n_src = src->n_src; n_wave = src->n_wave;
+    if (!src->unknown || !src->coef || (n_wave > 0 && !src->wave)) return fail(FDTD_EINVAL, "sources: missing arrays");
+    wave.resize((size_t)(n_wave * n_src * B));
+    for (size_t q = 0; q < wave.size(); ++q) wave[q] = (T)src->wave[q];
+    for (int64_t s_ = 0; s_ < n_src; ++s_) {
+      const int64_t u = src->unknown[s_];
+      const int c = (int)(u / S);
+      const int64_t s = u % S;
+      if (u < 0 || u >= 6 * S || !is_e(c)) return fail(FDTD_ESTAMP, "source %lld: %lld is not an E unknown", (long long)s_, (long long)u);
+      auto it = row_of.find(u);
+      if (it != row_of.end()) {
+        if (hrows[it->second].src >= 0) return fail(FDTD_EINVAL, "two sources on one unknown");
+        hrows[it->second].src = (int)s_; hrows[it->second].cs = src->coef[s_];
+        continue;
+      }
+      const double cb = mat_coef(s, c);
+      int i, j, k;
+      storage_ijk(s, i, j, k);
+      const bool wall = (dim == 3) ? ((c == 0 && (j == 0 || j == ny || k == 0 || k == nz || i >= nx)) ||
+                                      (c == 1 && (i == 0 || i == nx || k == 0 || k == nz || j >= ny)) ||
+                                      (c == 2 && (i == 0 || i == nx || j == 0 || j == ny || k >= nz)))
+                                   : (i == 0 || i == nx || j == 0 || j == ny);
+      if (cb == 0.0 || wall) return fail(FDTD_ESTAMP, "source %lld sits on an inert (PEC / hole) unknown", (long long)s_);
+      HRow h;
+      h.comp = c; h.s = s; h.c = cb; h.src = (int)s_; h.cs = src->coef[s_];
+      // K_inc row (= -curl_H) of the regular stencil, fdtd.h conventions
+      const int64_t Hx = 3 * S, Hy = 4 * S, Hz = 5 * S;
+      if (c == 0) {
+        h.w = {{Hz + sidx(i, j, k), -1.0}, {Hz + sidx(i, j - 1, k), 1.0}, {Hy + sidx(i, j, k), 1.0}, {Hy + sidx(i, j, k - 1), -1.0}};
+      } else if (c == 1) {
+        h.w = {{Hx + sidx(i, j, k), -1.0}, {Hx + sidx(i, j, k - 1), 1.0}, {Hz + sidx(i, j, k), 1.0}, {Hz + sidx(i - 1, j, k), -1.0}};
+      } else {
+        h.w = {{Hy + sidx(i, j, k), -1.0}, {Hy + sidx(i - 1, j, k), 1.0}, {Hx + sidx(i, j, k), 1.0}, {Hx + sidx(i, j - 1, k), -1.0}};
+      }
+      row_of[u] = (int)hrows.size();
+      hrows.push_back(h);
+      // mark the unknown as explicit: new material = old + if bit
+      ensure_table();
+      const int old = ids[s];
+      std::vector<double> nc(coef.begin() + old * 6, coef.begin() + old * 6 + 6);
+      const uint8_t nm = (uint8_t)(ifmask[old] | (1u << c));
+      int found = -1;
+      for (int m = 0; m < (int)ifmask.size(); ++m)
+        if (ifmask[m] == nm && std::equal(nc.begin(), nc.end(), coef.begin() + m * 6)) { found = m; break; }
+      if (found < 0) {
+        if ((int)ifmask.size() >= 256) return fail(FDTD_ENOTSUP, "more than 256 material classes after marking source rows");
+        found = (int)ifmask.size();
+        coef.insert(coef.end(), nc.begin(), nc.end());
+        ifmask.push_back(nm);
+      }
+      ids[s] = (uint8_t)found;
+    }
+  }
+  n_mat = (int)ifmask.size();
+  if (!uniform) {
+    std::vector<uint8_t> padded((size_t)(plane * nplanes), 0);
+    for (int64_t s = 0; s < S; ++s) padded[dev_off(s)] = ids[s];
+    mat_id = dalloc<uint8_t>(padded.size());
+    CK(cudaMemcpy(mat_id, padded.data(), padded.size(), cudaMemcpyHostToDevice));
+    std::vector<fdtd::Coef<T>> tb((size_t)n_mat * 6);
+    for (int m = 0; m < n_mat; ++m)
+      for (int c = 0; c < 6; ++c) tb[(size_t)m * 6 + c] = make_coef<T>(coef[(size_t)m * 6 + c]);
+    tab = dalloc<fdtd::Coef<T>>(tb.size());
+    ifm = dalloc<uint8_t>(n_mat);
+    CK(cudaMemcpy(tab, tb.data(), sizeof(fdtd::Coef<T>) * tb.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ifm, ifmask.data(), n_mat, cudaMemcpyHostToDevice));
+  } else {
+    u0 = make_coef<T>(coef[dim == 3 ? 0 : 2]);
+    u1 = make_coef<T>(coef[3]);
+    for (int c = 1; c < 3; ++c)
+      if (dim == 3 && coef[c] != coef[0]) return fail(FDTD_ENOTSUP, "uniform mode needs equal cb for all E components");
+    for (int c = 4; c < (dim == 3 ? 6 : 5); ++c)
+      if (coef[c] != coef[3]) return fail(FDTD_ENOTSUP, "uniform mode needs equal ch for all H components");
+  }
+  // upload explicit rows
+  {
+    const int64_t nr = (int64_t)hrows.size();
+    rows.n_rows = nr; rows.n_wave = n_wave; rows.n_src = n_src;
+    std::vector<int32_t> ec(nr), hc, srcv(nr);
+    std::vector<int64_t> eo(nr), rp(nr + 1, 0), ho, yo(nr);
+    std::vector<fdtd::Coef<T>> cc(nr);
+    std::vector<T> w, cs(nr);
+    for (int64_t r = 0; r < nr; ++r) {
+      const HRow& h = hrows[r];
+      ec[r] = h.comp; eo[r] = dev_off(h.s); cc[r] = make_coef<T>(h.c);
+      yo[r] = h.y; srcv[r] = h.src; cs[r] = (T)h.cs;
+      for (auto& pw : h.w) {
+        const int hcmp = (int)(pw.first / S);
+        const int64_t hs = pw.first % S;
+        hc.push_back(hcmp); ho.push_back(dev_off(hs)); w.push_back((T)pw.second);
+      }
+      rp[r + 1] = (int64_t)w.size();
+    }
+    auto up = [&](auto* dst, const auto& v) -> int {
+      if (v.empty()) return 0;
+      CK(cudaMemcpy(dst, v.data(), sizeof(v[0]) * v.size(), cudaMemcpyHostToDevice));
+      return 0;
+    };
+    int32_t* d_ec = dalloc<int32_t>(std::max<int64_t>(nr, 1));
+    int64_t* d_eo = dalloc<int64_t>(std::max<int64_t>(nr, 1));
+    fdtd::Coef<T>* d_c = dalloc<fdtd::Coef<T>>(std::max<int64_t>(nr, 1));
+    int64_t* d_rp = dalloc<int64_t>(nr + 1);
+    int32_t* d_hc = dalloc<int32_t>(std::max<size_t>(hc.size(), 1));
+    int64_t* d_ho = dalloc<int64_t>(std::max<size_t>(ho.size(), 1));
+    T* d_w = dalloc<T>(std::max<size_t>(w.size(), 1));
+    int64_t* d_yo = dalloc<int64_t>(std::max<int64_t>(nr, 1));
+    int32_t* d_src = dalloc<int32_t>(std::max<int64_t>(nr, 1));
+    T* d_cs = dalloc<T>(std::max<int64_t>(nr, 1));
+    T* d_wave = dalloc<T>(std::max<size_t>(wave.size(), 1));
+    int e = 0;
+    e |= up(d_ec, ec); e |= up(d_eo, eo); e |= up(d_c, cc); e |= up(d_rp, rp); e |= up(d_hc, hc);
+    e |= up(d_ho, ho); e |= up(d_w, w); e |= up(d_yo, yo); e |= up(d_src, srcv); e |= up(d_cs, cs);
+    e |= up(d_wave, wave);
+    if (e) return e;
+    rows.e_comp = d_ec; rows.e_off = d_eo; rows.c = d_c; rows.rowptr = d_rp; rows.h_comp = d_hc;
+    rows.h_off = d_ho; rows.w = d_w; rows.y_off = d_yo; rows.src = d_src; rows.cs = d_cs; rows.wave = d_wave;
+    n_gather = (int64_t)gcomp.size();
+    g_comp = dalloc<int32_t>(std::max<int64_t>(n_gather, 1));
+    g_off = dalloc<int64_t>(std::max<int64_t>(n_gather, 1));
+    g_dst = dalloc<int64_t>(std::max<int64_t>(n_gather, 1));
+    e |= up(g_comp, gcomp); e |= up(g_off, goff); e |= up(g_dst, gdst);
+    if (e) return e;
+  }
+
+  // ---- probes ----
+  {
+    std::vector<int64_t> rp(1, 0), off;
+    std::vector<int32_t> srcv, strd;
+    std::vector<T> w;
+    n_probe = probes ? (int)probes->n_probe : 0;
+    for (int p = 0; p < n_probe; ++p) {
+      const int kind = probes->kind[p];
+      bool any_e = false, any_h = false;
+      for (int64_t k = probes->rowptr[p]; k < probes->rowptr[p + 1]; ++k) {
+        const int64_t idx = probes->index[k];
+        if (kind == 0) {
+          const int c = (int)(idx / S);
+          if (idx < 0 || idx >= 6 * S || !(is_e(c) || is_h(c))) return fail(FDTD_ESTAMP, "probe %d: bad unknown %lld", p, (long long)idx);
+          any_e |= is_e(c); any_h |= is_h(c);
+          srcv.push_back(c); off.push_back(dev_off(idx % S));
+        } else if (kind == 1 || kind == 2) {
+          const int b = probes->block[p], in = probes->inst[p];
+          if (b < 0 || b >= n_blocks || in < 0 || in >= blocks[b].n_inst) return fail(FDTD_EINVAL, "probe %d: bad block/inst", p);
+          const BlockDev<T>& D = blocks[b];
+          const int q = kind == 1 ? D.qe : D.qh;
+          if (idx < 0 || idx >= q) return fail(FDTD_ESTAMP, "probe %d: reduced index out of range", p);
+          srcv.push_back(kind == 1 ? 6 : 7);
+          off.push_back((kind == 1 ? D.xh_off : D.h_off) + idx * D.N + (int64_t)in * B);
+        } else {
+          return fail(FDTD_EINVAL, "probe %d: unknown kind %d", p, kind);
+        }
+        strd.push_back(1);
+        w.push_back((T)probes->weight[k]);
+      }
+      if (any_e && any_h) return fail(FDTD_EINVAL, "probe %d mixes E and H unknowns", p);
+      rp.push_back((int64_t)w.size());
+    }
+    int64_t* d_rp = dalloc<int64_t>(rp.size());
+    int32_t* d_src = dalloc<int32_t>(std::max<size_t>(srcv.size(), 1));
+    int64_t* d_off = dalloc<int64_t>(std::max<size_t>(off.size(), 1));
+    int32_t* d_st = dalloc<int32_t>(std::max<size_t>(strd.size(), 1));
+    T* d_w = dalloc<T>(std::max<size_t>(w.size(), 1));
+    CK(cudaMemcpy(d_rp, rp.data(), sizeof(int64_t) * rp.size(), cudaMemcpyHostToDevice));
+    if (!srcv.empty()) {
+      CK(cudaMemcpy(d_src, srcv.data(), sizeof(int32_t) * srcv.size(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(d_off, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(d_st, strd.data(), sizeof(int32_t) * strd.size(), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(d_w, w.data(), sizeof(T) * w.size(), cudaMemcpyHostToDevice));
+    }
+    pr.n_probe = n_probe; pr.rowptr = d_rp; pr.src = d_src; pr.off = d_off; pr.stride = d_st; pr.w = d_w;
+    ring = dalloc<T>(std::max<int64_t>(cap * n_probe * B, 1));
+    if (!ring) return fail(FDTD_ENOMEM, "probe ring allocation failed");
+  }
+  d_step = dalloc<int64_t>(1);
+  d_bad = dalloc<unsigned long long>(1);
+  CK(cudaMemsetAsync(d_step, 0, sizeof(int64_t), stream));
+  CK(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), stream));
+  staging_bytes = sizeof(T) * (size_t)std::max<int64_t>(elems, std::max(xh_size, h_size));
+  CK(cudaMallocHost(&staging, staging_bytes));
+  // shared memory opt-in (material table + plane buffers)
+  const size_t smem3 = 2 * 3 * 1024 * sizeof(T) + sizeof(fdtd::MatTable<T>);
+  CK(cudaFuncSetAttribute(fdtd::stencil3d_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  CK(cudaFuncSetAttribute(fdtd::stencil3d_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  CK(cudaFuncSetAttribute(fdtd::stencil2d_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  CK(cudaFuncSetAttribute(fdtd::stencil2d_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  CK(cudaStreamSynchronize(stream));
+  return FDTD_OK;
+}
+
+template <typename T>
+static int launch_gemv(int rows, int cols, int N, const T* A, const T* X, T* out, const T* g, T alpha,
+                       T beta, const int64_t* d_step, int check_every, unsigned long long* bad, cudaStream_t st) {
+  const int threads = 256;
+  const int blocks = (rows * 32 + threads - 1) / threads;
+  if (rows <= 0) return 0;
+  const T gs = g ? (T)0 : (T)1;      // no diagonal given -> unit scale
+  if (N <= 1)
+    fdtd::gemv_rows_kernel<T, 1><<<blocks, threads, 0, st>>>(rows, cols, N, A, X, out, g, gs, alpha, beta, d_step, check_every, bad);
+  else if (N <= 4)
+    fdtd::gemv_rows_kernel<T, 4><<<blocks, threads, 0, st>>>(rows, cols, N, A, X, out, g, gs, alpha, beta, d_step, check_every, bad);
+  else if (N <= 16)
+    fdtd::gemv_rows_kernel<T, 16><<<blocks, threads, 0, st>>>(rows, cols, N, A, X, out, g, gs, alpha, beta, d_step, check_every, bad);
+  else if (N <= 32)
+    fdtd::gemv_rows_kernel<T, 32><<<blocks, threads, 0, st>>>(rows, cols, N, A, X, out, g, gs, alpha, beta, d_step, check_every, bad);
+  else
+    return -1;
+  return 1;
+}
+
+template <typename T>
+int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count) {
+  int64_t n = 0;
+  T* const* E0 = dF[p];
+  T* const* E1 = dF[p ^ 1];
+  // a1 + a3: explicit rows (interface and source rows) into the new buffer
+  if (rows.n_rows > 0) {
+    const int64_t work = rows.n_rows * B;
+    fdtd::rows_e_kernel<T><<<(unsigned)((work + 255) / 256), 256, 0, st>>>(
+        rows, B, (const T* const*)E0, E1, (const T* const*)E0, y_all, d_step);
+    ++n;
+  }
+  // a4: e~ -= G_e K~' h~
+  for (auto& D : blocks) {
+    int r = launch_gemv<T>(D.qe, D.qh, D.N, D.K, h_all + D.h_off, xh_all + D.xh_off, D.ge, (T)-1, (T)1,
+                           d_step, check_every, d_bad, st);
+    if (r < 0) return fail(FDTD_ENOTSUP, "n_inst*batch > 32 per block not supported in this version");
+    n += r;
+  }
+  // a2 + a5: fused coarse stencil
+  const size_t tabsz = uniform ? 0 : sizeof(fdtd::MatTable<T>);
+  if (dim == 3) {
+    int BX, BY;
+    if (B == 1) { BX = 32; BY = 8; }
+    else { BX = B * std::max(2, 128 / B); BY = 8; if (BX * BY > 1024) BY = std::max(2, 1024 / BX); }
+    const int outx = BX / B - 1, outy = BY - 1;
+    dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + outy - 1) / outy, (nz + 1 + kchunk - 1) / kchunk);
+    const size_t sm = 2 * 3 * (size_t)BX * BY * sizeof(T) + tabsz;
+    if (uniform)
+      fdtd::stencil3d_kernel<T, true><<<grid, dim3(BX, BY), sm, st>>>(
+          fdtd::Dims{nx, ny, nz, px, B, plane}, F[p][0], F[p][1], F[p][2], F[p][3], F[p][4], F[p][5],
+          F[p ^ 1][0], F[p ^ 1][1], F[p ^ 1][2], F[p ^ 1][3], F[p ^ 1][4], F[p ^ 1][5], mat_id, tab, ifm, n_mat,
+          u0, u1, kchunk, d_step, check_every, d_bad);
+    else
+      fdtd::stencil3d_kernel<T, false><<<grid, dim3(BX, BY), sm, st>>>(
+          fdtd::Dims{nx, ny, nz, px, B, plane}, F[p][0], F[p][1], F[p][2], F[p][3], F[p][4], F[p][5],
+          F[p ^ 1][0], F[p ^ 1][1], F[p ^ 1][2], F[p ^ 1][3], F[p ^ 1][4], F[p ^ 1][5], mat_id, tab, ifm, n_mat,
+          u0, u1, kchunk, d_step, check_every, d_bad);
+  } else {
+    const int BX = (B == 1) ? 256 : B * std::max(2, 256 / B);
+    const int outx = BX / B - 1;
+    const int jchunk = 16;
+    dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + jchunk - 1) / jchunk, 1);
+    const size_t sm = 2 * (size_t)BX * sizeof(T) + tabsz;
+    if (uniform)
+      fdtd::stencil2d_kernel<T, true><<<grid, BX, sm, st>>>(
+          fdtd::Dims{nx, ny, 0, px, B, plane}, F[p][2], F[p][3], F[p][4], F[p ^ 1][2], F[p ^ 1][3], F[p ^ 1][4],
+          mat_id, tab, ifm, n_mat, u0, u1, jchunk, d_step, check_every, d_bad);
+    else
+      fdtd::stencil2d_kernel<T, false><<<grid, BX, sm, st>>>(
+          fdtd::Dims{nx, ny, 0, px, B, plane}, F[p][2], F[p][3], F[p][4], F[p ^ 1][2], F[p ^ 1][3], F[p ^ 1][4],
+          mat_id, tab, ifm, n_mat, u0, u1, jchunk, d_step, check_every, d_bad);
+  }
+  ++n;
+  // a6: G = E_if^{n+1};  h~ += G_h [K~'^T | S_E^T][e~ ; G];  y = S_E h~
+  if (n_gather > 0) {
+    fdtd::gather_kernel<T><<<(unsigned)((n_gather * B + 255) / 256), 256, 0, st>>>(
+        n_gather, B, g_comp, g_off, g_dst, E1, xh_all);
+    ++n;
+  }
+  for (auto& D : blocks) {
+    n += launch_gemv<T>(D.qh, D.qe + D.n_if, D.N, D.Mh, xh_all + D.xh_off, h_all + D.h_off, D.gh, (T)1, (T)1,
+                        d_step, check_every, d_bad, st);
+    if (D.n_if > 0)
+      n += launch_gemv<T>(D.n_if, D.qh, D.N, D.SE, h_all + D.h_off, y_all + D.y_off, (const T*)nullptr, (T)1,
+                          (T)0, d_step, 0, d_bad, st);
+  }
+  // a7: probes + step counter
+  fdtd::probe_kernel<T><<<1, 256, 0, st>>>(pr, B, (const T* const*)E1, (const T* const*)dRED, ring, cap, d_step);
+  ++n;
+  CK(cudaGetLastError());
+  *count += n;
+  return FDTD_OK;
+}
+
+template <typename T>
+int Impl<T>::drain() {
+  // copy the ring samples of steps [drained_to, host_step) to the host
+  const int64_t from = drained_to, to = host_step;
+  if (to <= from || n_probe == 0) { drained_to = to; return FDTD_OK; }
+  CK(cudaStreamSynchronize(stream));
+  const int64_t per = (int64_t)n_probe * B;
+  std::vector<T> buf((size_t)((to - from) * per));
+  int64_t done = 0;
+  while (done < to - from) {
+    const int64_t s = from + done;
+    const int64_t pos = s % cap;
+    const int64_t len = std::min(cap - pos, (to - from) - done);
+    CK(cudaMemcpy(buf.data() + done * per, ring + pos * per, sizeof(T) * len * per, cudaMemcpyDeviceToHost));
+    done += len;
+  }
+  const size_t old = host_probes.size();
+  host_probes.resize(old + buf.size());
+  for (size_t q = 0; q < buf.size(); ++q) host_probes[old + q] = (double)buf[q];
+  drained_to = to;
+  return FDTD_OK;
+}
+
+template <typename T>
+int Impl<T>::step(int64_t n) {
+  if (n < 0) return fail(FDTD_EINVAL, "negative step count");
+  while (n > 0) {
+    // keep the probe ring from overflowing
+    if (n_probe > 0 && host_step - drained_to >= cap) {
+      int e = drain();
+      if (e) return e;
+    }
+    const int64_t room = n_probe > 0 ? cap - (host_step - drained_to) : n;
+    const int64_t chunk = std::min(n, room);
+    int64_t done = 0;
+    while (done < chunk) {
+      const int64_t left = chunk - done;
+      if (graph_steps > 0 && (host_step & 1) == 0 && left >= graph_steps) {
+        if (!graph) {
+          cudaStream_t cs;
+          CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+          cudaGraph_t gr;
+          CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+          int64_t cnt = 0;
+          int e = FDTD_OK;
+          for (int s = 0; s < graph_steps && e == FDTD_OK; ++s) e = launch_step(s & 1, cs, &cnt);
+          cudaError_t ce = cudaStreamEndCapture(cs, &gr);
+          if (e) { cudaStreamDestroy(cs); return e; }
+          CK(ce);
+          CK(cudaGraphInstantiate(&graph, gr, 0));
+          CK(cudaGraphDestroy(gr));
+          CK(cudaStreamDestroy(cs));
+          graph_kernels = cnt;
+        }
+        CK(cudaGraphLaunch(graph, stream));
+        launches += graph_kernels;
+        host_step += graph_steps;
+        done += graph_steps;
+      } else {
+        int e = launch_step((int)(host_step & 1), stream, &launches);
+        if (e) return e;
+        host_step += 1;
+        done += 1;
+      }
+    }
+    n -= chunk;
+  }
+  return FDTD_OK;
+}
+
+template <typename T>
+int Impl<T>::check_async() {
+  unsigned long long bad = 0;
+  CK(cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost));
+  if (bad != std::numeric_limits<unsigned long long>::max())
+    return fail(FDTD_EDIVERGED, "divergence (non-finite or |x| > 1e100) detected at step %llu", bad);
+  return FDTD_OK;
+}
+
+template <typename T>
+int Impl<T>::sync() {
+  CK(cudaStreamSynchronize(stream));
+  return check_async();
+}
+
+template <typename T>
+int Impl<T>::probe(double* out, int64_t capn, int64_t* written) {
+  int e = drain();
+  if (e) return e;
+  const int64_t need = (int64_t)host_probes.size();
+  if (written) *written = 0;
+  if (need > capn) return fail(FDTD_EINVAL, "probe buffer too small: need %lld doubles", (long long)need);
+  if (need) std::memcpy(out, host_probes.data(), sizeof(double) * need);
+  if (written) *written = need;
+  host_probes.clear();
+  return check_async();
+}
+
+template <typename T>
+int Impl<T>::get_state(int which, double* out, int64_t n) {
+  CK(cudaStreamSynchronize(stream));
+  const int p = (int)(host_step & 1);
+  if (which >= 0 && which <= 5) {
+    if (n != S * B) return fail(FDTD_EINVAL, "get_state: n must be batch*S = %lld", (long long)(S * B));
+    if (!F[p][which]) { std::fill(out, out + n, 0.0); return FDTD_OK; }
+    CK(cudaMemcpy(staging, F[p][which], sizeof(T) * elems, cudaMemcpyDeviceToHost));
+    for (int64_t s = 0; s < S; ++s) {
+      const int64_t o = dev_off(s) * B;
+      for (int b = 0; b < B; ++b) out[(int64_t)b * S + s] = (double)staging[o + b];
+    }
+    return check_async();
+  }
+  if (which == 6 || which == 7) {
+    int64_t tot = 0;
+    for (auto& D : blocks) tot += (int64_t)(which == 6 ? D.qe : D.qh) * D.N;
+    if (n != tot) return fail(FDTD_EINVAL, "get_state: n must be %lld", (long long)tot);
+    int64_t o = 0;
+    for (auto& D : blocks) {
+      const int q = which == 6 ? D.qe : D.qh;
+      const T* src = which == 6 ? xh_all + D.xh_off : h_all + D.h_off;
+      CK(cudaMemcpy(staging, src, sizeof(T) * q * D.N, cudaMemcpyDeviceToHost));
+      for (int in = 0; in < D.n_inst; ++in)
+        for (int b = 0; b < B; ++b)
+          for (int c = 0; c < q; ++c) out[o++] = (double)staging[(int64_t)c * D.N + in * B + b];
+    }
+    return check_async();
+  }
+  if (which == 8) {
+    if (n != 1) return fail(FDTD_EINVAL, "get_state(8): n must be 1");
+    int64_t s = 0;
+    CK(cudaMemcpy(&s, d_step, sizeof(s), cudaMemcpyDeviceToHost));
+    out[0] = (double)s;
+    return FDTD_OK;
+  }
+  return fail(FDTD_EINVAL, "get_state: bad 'which' %d", which);
+}
+
+template <typename T>
+int Impl<T>::set_state(int which, const double* in, int64_t n) {
+  CK(cudaStreamSynchronize(stream));
+  const int p = (int)(host_step & 1);
+  if (which >= 0 && which <= 5) {
+    if (n != S * B) return fail(FDTD_EINVAL, "set_state: n must be batch*S");
+    if (!F[p][which]) return fail(FDTD_EINVAL, "set_state: component %d unused in 2-D", which);
+    std::fill(staging, staging + elems, (T)0);
+    for (int64_t s = 0; s < S; ++s) {
+      const int64_t o = dev_off(s) * B;
+      for (int b = 0; b < B; ++b) staging[o + b] = (T)in[(int64_t)b * S + s];
+    }
+    CK(cudaMemcpy(F[p][which], staging, sizeof(T) * elems, cudaMemcpyHostToDevice));
+    return FDTD_OK;
+  }
+  if (which == 6 || which == 7) {
+    int64_t tot = 0;
+    for (auto& D : blocks) tot += (int64_t)(which == 6 ? D.qe : D.qh) * D.N;
+    if (n != tot) return fail(FDTD_EINVAL, "set_state: n must be %lld", (long long)tot);
+    int64_t o = 0;
+    for (auto& D : blocks) {
+      const int q = which == 6 ? D.qe : D.qh;
+      T* dst = which == 6 ? xh_all + D.xh_off : h_all + D.h_off;
+      for (int in_ = 0; in_ < D.n_inst; ++in_)
+        for (int b = 0; b < B; ++b)
+          for (int c = 0; c < q; ++c) staging[(int64_t)c * D.N + in_ * B + b] = (T)in[o++];
+      CK(cudaMemcpy(dst, staging, sizeof(T) * q * D.N, cudaMemcpyHostToDevice));
+    }
+    // y = S_E h~ must follow h~
+    if (which == 7)
+      for (auto& D : blocks)
+        if (D.n_if > 0)
+          launch_gemv<T>(D.n_if, D.qh, D.N, D.SE, h_all + D.h_off, y_all + D.y_off, (const T*)nullptr, (T)1,
+                         (T)0, d_step, 0, d_bad, stream);
+    CK(cudaStreamSynchronize(stream));
+    return FDTD_OK;
+  }
+  return fail(FDTD_EINVAL, "set_state: bad 'which' %d", which);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int fdtd_create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_interface* iface,
+                const fdtd_reduced_block* blocks, int32_t n_blocks, const fdtd_sources* src,
+                const fdtd_probes* probes, const fdtd_exec* exec, fdtd_t** out) {
+  if (!g || !out) return fail(FDTD_EINVAL, "null grid or output handle");
+  *out = nullptr;
+  if (g->dim != 2 && g->dim != 3) return fail(FDTD_EINVAL, "invalid-grid: dim must be 2 or 3");
+  if (g->nx < 1 || g->ny < 1 || (g->dim == 3 && g->nz < 1) || (g->dim == 2 && g->nz != 1))
+    return fail(FDTD_EINVAL, "invalid-grid: cell counts");
+  if (!(g->dx > 0) || !(g->dy > 0) || (g->dim == 3 && !(g->dz > 0)))
+    return fail(FDTD_EINVAL, "invalid-grid: cell sizes must be > 0");
+  if (g->dx != g->dy || (g->dim == 3 && g->dx != g->dz))
+    return fail(FDTD_ENOTSUP, "this version requires cubic (square) cells");
+  if (g->batch < 1 || g->batch > 512) return fail(FDTD_EINVAL, "batch must be in [1, 512]");
+  if (g->precision != 32 && g->precision != 64) return fail(FDTD_EINVAL, "precision must be 32 or 64");
+  int dev = 0;
+  cudaDeviceProp prop;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess)
+    return fail(FDTD_ECUDA, "no CUDA device");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(FDTD_ENOTSUP, "libfdtd is built for sm_100a; device is sm_%d%d", prop.major, prop.minor);
+  fdtd_t* h = nullptr;
+  int e;
+  if (g->precision == 32) {
+    auto* p = new Impl<float>();
+    e = p->create(g, mat, iface, blocks, n_blocks, src, probes, exec);
+    h = p;
+  } else {
+    auto* p = new Impl<double>();
+    e = p->create(g, mat, iface, blocks, n_blocks, src, probes, exec);
+    h = p;
+  }
+  if (e != FDTD_OK) {
+    delete h;
+    return e;
+  }
+  *out = h;
+  return FDTD_OK;
+}
+
+int fdtd_step(fdtd_t* h, int64_t n) { return h ? h->step(n) : fail(FDTD_EINVAL, "null handle"); }
+int fdtd_probe(fdtd_t* h, double* out, int64_t cap, int64_t* written) {
+  return h ? h->probe(out, cap, written) : fail(FDTD_EINVAL, "null handle");
+}
+int fdtd_get_state(fdtd_t* h, int32_t which, double* out, int64_t n) {
+  return h ? h->get_state(which, out, n) : fail(FDTD_EINVAL, "null handle");
+}
+int fdtd_set_state(fdtd_t* h, int32_t which, const double* in, int64_t n) {
+  return h ? h->set_state(which, in, n) : fail(FDTD_EINVAL, "null handle");
+}
+int fdtd_sync(fdtd_t* h) { return h ? h->sync() : fail(FDTD_EINVAL, "null handle"); }
+int64_t fdtd_launch_count(const fdtd_t* h) { return h ? h->launches : 0; }
+void fdtd_destroy(fdtd_t* h) {
+  if (h) {
+    h->sync();
+    delete h;
+  }
+}
+const char* fdtd_last_error(void) { return g_err.c_str(); }
+int fdtd_version(void) { return FDTD_VERSION; }
+
+}  // extern "C"

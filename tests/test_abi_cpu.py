@@ -1,0 +1,66 @@
+"""Host-side checks of the C ABI (no GPU needed): the library loads, exports
+every symbol include/fdtd.h declares, and validates its arguments."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _lib():
+    from paper_1406_7042_b200 import build, fdtd
+    build.build()
+    return fdtd, fdtd.load_library()
+
+
+def test_header_symbols_exported():
+    fdtd, lib = _lib()
+    hdr = open(os.path.join(ROOT, "include", "fdtd.h")).read()
+    declared = set(re.findall(r"\b(fdtd_[a-z_]+)\s*\(", hdr))
+    assert declared == set(fdtd.EXPORTED_SYMBOLS)
+    for name in declared:
+        assert hasattr(lib, name)
+    assert lib.fdtd_version() == 100
+
+
+def _grid(fdtd, **kw):
+    g = dict(dim=3, nx=4, ny=4, nz=4, dx=1e-3, dy=1e-3, dz=1e-3, batch=1, precision=32, dt=1e-12)
+    g.update(kw)
+    return fdtd.Grid(**g)
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(dim=4), 1), (dict(nx=0), 1), (dict(dx=-1.0), 1), (dict(precision=16), 1),
+    (dict(batch=0), 1), (dict(dim=2, nz=3), 1), (dict(dy=2e-3), 5)])
+def test_create_rejects_invalid_grid(kw, code):
+    fdtd, lib = _lib()
+    g = _grid(fdtd, **kw)
+    h = C.c_void_p()
+    rc = lib.fdtd_create(C.byref(g), None, None, None, 0, None, None, None, C.byref(h))
+    assert rc == code
+    assert lib.fdtd_last_error().decode()
+    assert not h.value
+
+
+def test_create_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    fdtd, lib = _lib()
+    g = _grid(fdtd)
+    h = C.c_void_p()
+    rc = lib.fdtd_create(C.byref(g), None, None, None, 0, None, None, None, C.byref(h))
+    assert rc in (4, 5)      # FDTD_ECUDA / FDTD_ENOTSUP: no silent CPU fallback
+    with pytest.raises(fdtd.FdtdError):
+        fdtd.Sim(dict(dim=3, n=(4, 4, 4), delta=1e-3, dt=1e-12, batch=1, precision=32,
+                      uniform_coef=np.ones(6)))
+
+
+def test_null_handle_calls():
+    fdtd, lib = _lib()
+    assert lib.fdtd_step(None, 1) == 1
+    assert lib.fdtd_sync(None) == 1
+    assert lib.fdtd_launch_count(None) == 0
