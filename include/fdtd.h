@@ -179,6 +179,16 @@ int fdtd_sync(fdtd_t* h);
  * its kernel nodes). */
 int64_t fdtd_launch_count(const fdtd_t* h);
 
+/* Per-phase tracing.  fdtd_profile(h, 1) resets the accumulators and makes the
+ * following fdtd_step calls launch eagerly with CUDA events around each
+ * kernel group (synchronising once per step); fdtd_profile(h, 0) returns to
+ * graph launches.  fdtd_phase_times writes the accumulated device time [ms] of
+ * the phases {explicit E rows, reduced E, coarse stencil, gather, reduced H,
+ * coupling y, probes} into ms[0..6] and, if n > 7, the number of profiled
+ * steps into ms[7]. */
+int fdtd_profile(fdtd_t* h, int32_t enable);
+int fdtd_phase_times(fdtd_t* h, double* ms, int32_t n);
+
 void fdtd_destroy(fdtd_t* h);
 const char* fdtd_last_error(void);
 int fdtd_version(void);

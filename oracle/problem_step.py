@@ -323,3 +323,65 @@ def to_storage(rec: HybridRecursion, E, H):
             m = comp == c
             a[ids[m] % rec.S] = vec[m]
     return out, E[Ne_c:], H[Nh_c:]
+
+
+def sampled_step(problem, arrays, samples, member=0):
+    """One step of (4) for SAMPLED coarse unknowns of a problem without
+    interface rows or sources, straight from the definitions: E^{n+1} at the
+    sampled E unknowns and at every E unknown their H partners need, then
+    H^{n+1} = H^n + ch (K_inc^T E^{n+1}).  ``arrays``: comp -> storage array
+    [B][S] of the state at step n; ``samples``: list of (comp, (i, j, k)).
+    Returns {(comp, idx): value at step n+1}.  For full-size configs the
+    oracle cannot hold (16.8 M cells x 6 unknowns), survey §8(d)."""
+    dim = int(problem["dim"])
+    n = tuple(int(v) for v in problem["n"]) + ((1,) if len(problem["n"]) == 2 else ())
+    shp = yee.storage_shape(dim, n)
+    if problem.get("interface") or problem.get("sources"):
+        raise ValueError("sampled_step covers the pure coarse recursion only")
+    curl_h = yee._CURL_H_3D if dim == 3 else yee._CURL_H_2D
+    mcurl_e = yee._MCURL_E_3D if dim == 3 else yee._MCURL_E_2D
+    ecomps = (0, 1, 2) if dim == 3 else (2,)
+    pec = {c: yee.wall_pec_mask(dim, n, c) & yee.exists_mask(dim, n, c) for c in range(6) if c in
+           (yee.E_COMPS_3D + yee.H_COMPS_3D if dim == 3 else yee.E_COMPS_2D + yee.H_COMPS_2D)}
+    exists = {c: yee.exists_mask(dim, n, c) for c in pec}
+
+    def coef(c, pos):
+        if problem.get("mat_id") is None:
+            return float(problem["uniform_coef"][c])
+        mid = np.asarray(problem["mat_id"]).reshape(shp)
+        return float(np.asarray(problem["mat_coef"])[mid[pos], c])
+
+    def val(c, idx):
+        i, j, k = idx
+        pos = (k, j, i) if dim == 3 else (j, i)
+        if any(p < 0 or p >= s for p, s in zip(pos, shp)):
+            return 0.0, None
+        if not exists[c][pos] or pec[c][pos]:
+            return 0.0, None
+        return float(np.asarray(arrays[c]).reshape(-1, *shp)[member][pos]), pos
+
+    def e_new(c, idx):
+        v, pos = val(c, idx)
+        if pos is None:
+            return 0.0
+        acc = 0.0
+        for (hc, off, sign, _) in curl_h[c]:
+            hv, _ = val(hc, (idx[0] + off[0], idx[1] + off[1], idx[2] + off[2]))
+            acc += sign * hv
+        return v + coef(c, pos) * acc          # E + cb curl H  ==  E - cb K_inc H
+
+    out = {}
+    for (c, idx) in samples:
+        idx = tuple(int(x) for x in idx)
+        if c in ecomps:
+            out[(c, idx)] = e_new(c, idx)
+        else:
+            v, pos = val(c, idx)
+            if pos is None:
+                out[(c, idx)] = 0.0
+                continue
+            acc = 0.0
+            for (ec, off, sign, _) in mcurl_e[c]:
+                acc += sign * e_new(ec, (idx[0] + off[0], idx[1] + off[1], idx[2] + off[2]))
+            out[(c, idx)] = v + coef(c, pos) * acc   # H - ch curl E == H + ch K_inc^T E
+    return out

@@ -65,6 +65,8 @@ struct fdtd_t {
   virtual int get_state(int which, double* out, int64_t n) = 0;
   virtual int set_state(int which, const double* in, int64_t n) = 0;
   virtual int sync() = 0;
+  virtual int set_profile(int on) = 0;
+  virtual int phase_times(double* ms, int n) = 0;
   int64_t launches = 0;
 };
 
@@ -155,10 +157,31 @@ struct Impl : public fdtd_t {
   T* staging = nullptr;               // pinned host staging
   size_t staging_bytes = 0;
   int kchunk = 16;
+  // per-phase tracing (CUDA events around each kernel group, eager launches)
+  static constexpr int NPHASE = 7;       // rows_e, red_e, stencil, gather, red_h, red_y, probe
+  bool prof = false;
+  cudaEvent_t ev[2 * NPHASE] = {};
+  double phase_ms[NPHASE] = {0};
+  int64_t phase_n[NPHASE] = {0};
 
   ~Impl() override {
     if (graph) cudaGraphExecDestroy(graph);
     if (staging) cudaFreeHost(staging);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  int set_profile(int on) override {
+    if (on && !ev[0])
+      for (auto& e : ev) CK(cudaEventCreate(&e));
+    prof = on != 0;
+    for (int i = 0; i < NPHASE; ++i) { phase_ms[i] = 0; phase_n[i] = 0; }
+    return FDTD_OK;
+  }
+  int phase_times(double* ms, int n) override {
+    for (int i = 0; i < n && i < NPHASE; ++i) ms[i] = phase_n[i] ? phase_ms[i] : 0.0;
+    for (int i = NPHASE; i < n; ++i) ms[i] = 0.0;
+    if (n > NPHASE) ms[NPHASE] = (double)(phase_n[2]);
+    return FDTD_OK;
   }
 
   template <typename U>
@@ -186,7 +209,7 @@ struct Impl : public fdtd_t {
   int create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_interface* itf,
              const fdtd_reduced_block* bl, int n_blocks, const fdtd_sources* src,
              const fdtd_probes* probes, const fdtd_exec* ex);
-  int launch_step(int parity, cudaStream_t st, int64_t* count);
+  int launch_step(int parity, cudaStream_t st, int64_t* count, bool profile = false);
   int step(int64_t n) override;
   int drain();
   int probe(double* out, int64_t cap, int64_t* written) override;
@@ -559,25 +582,31 @@ static int launch_gemv(int rows, int cols, int N, const T* A, const T* X, T* out
 }
 
 template <typename T>
-int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count) {
+int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   int64_t n = 0;
+  auto mark = [&](int ph, int edge) { if (profile) cudaEventRecord(ev[2 * ph + edge], st); };
   T* const* E0 = dF[p];
   T* const* E1 = dF[p ^ 1];
   // a1 + a3: explicit rows (interface and source rows) into the new buffer
+  mark(0, 0);
   if (rows.n_rows > 0) {
     const int64_t work = rows.n_rows * B;
     fdtd::rows_e_kernel<T><<<(unsigned)((work + 255) / 256), 256, 0, st>>>(
         rows, B, (const T* const*)E0, E1, (const T* const*)E0, y_all, d_step);
     ++n;
   }
+  mark(0, 1);
   // a4: e~ -= G_e K~' h~
+  mark(1, 0);
   for (auto& D : blocks) {
     int r = launch_gemv<T>(D.qe, D.qh, D.N, D.K, h_all + D.h_off, xh_all + D.xh_off, D.ge, (T)-1, (T)1,
                            d_step, check_every, d_bad, st);
     if (r < 0) return fail(FDTD_ENOTSUP, "n_inst*batch > 32 per block not supported in this version");
     n += r;
   }
+  mark(1, 1);
   // a2 + a5: fused coarse stencil
+  mark(2, 0);
   const size_t tabsz = uniform ? 0 : sizeof(fdtd::MatTable<T>);
   if (dim == 3) {
     int BX, BY;
@@ -612,22 +641,40 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count) {
           mat_id, tab, ifm, n_mat, u0, u1, jchunk, d_step, check_every, d_bad);
   }
   ++n;
+  mark(2, 1);
   // a6: G = E_if^{n+1};  h~ += G_h [K~'^T | S_E^T][e~ ; G];  y = S_E h~
+  mark(3, 0);
   if (n_gather > 0) {
     fdtd::gather_kernel<T><<<(unsigned)((n_gather * B + 255) / 256), 256, 0, st>>>(
         n_gather, B, g_comp, g_off, g_dst, E1, xh_all);
     ++n;
   }
-  for (auto& D : blocks) {
+  mark(3, 1);
+  mark(4, 0);
+  for (auto& D : blocks)
     n += launch_gemv<T>(D.qh, D.qe + D.n_if, D.N, D.Mh, xh_all + D.xh_off, h_all + D.h_off, D.gh, (T)1, (T)1,
                         d_step, check_every, d_bad, st);
+  mark(4, 1);
+  mark(5, 0);
+  for (auto& D : blocks)
     if (D.n_if > 0)
       n += launch_gemv<T>(D.n_if, D.qh, D.N, D.SE, h_all + D.h_off, y_all + D.y_off, (const T*)nullptr, (T)1,
                           (T)0, d_step, 0, d_bad, st);
-  }
+  mark(5, 1);
   // a7: probes + step counter
+  mark(6, 0);
   fdtd::probe_kernel<T><<<1, 256, 0, st>>>(pr, B, (const T* const*)E1, (const T* const*)dRED, ring, cap, d_step);
   ++n;
+  mark(6, 1);
+  if (profile) {
+    CK(cudaEventSynchronize(ev[2 * NPHASE - 1]));
+    for (int ph = 0; ph < NPHASE; ++ph) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev[2 * ph], ev[2 * ph + 1]));
+      phase_ms[ph] += ms;
+      phase_n[ph] += 1;
+    }
+  }
   CK(cudaGetLastError());
   *count += n;
   return FDTD_OK;
@@ -670,7 +717,7 @@ int Impl<T>::step(int64_t n) {
     int64_t done = 0;
     while (done < chunk) {
       const int64_t left = chunk - done;
-      if (graph_steps > 0 && (host_step & 1) == 0 && left >= graph_steps) {
+      if (!prof && graph_steps > 0 && (host_step & 1) == 0 && left >= graph_steps) {
         if (!graph) {
           cudaStream_t cs;
           CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -692,7 +739,7 @@ int Impl<T>::step(int64_t n) {
         host_step += graph_steps;
         done += graph_steps;
       } else {
-        int e = launch_step((int)(host_step & 1), stream, &launches);
+        int e = launch_step((int)(host_step & 1), stream, &launches, prof);
         if (e) return e;
         host_step += 1;
         done += 1;
@@ -866,6 +913,10 @@ int fdtd_set_state(fdtd_t* h, int32_t which, const double* in, int64_t n) {
 }
 int fdtd_sync(fdtd_t* h) { return h ? h->sync() : fail(FDTD_EINVAL, "null handle"); }
 int64_t fdtd_launch_count(const fdtd_t* h) { return h ? h->launches : 0; }
+int fdtd_profile(fdtd_t* h, int32_t enable) { return h ? h->set_profile(enable) : fail(FDTD_EINVAL, "null handle"); }
+int fdtd_phase_times(fdtd_t* h, double* ms, int32_t n) {
+  return h ? h->phase_times(ms, n) : fail(FDTD_EINVAL, "null handle");
+}
 void fdtd_destroy(fdtd_t* h) {
   if (h) {
     h->sync();

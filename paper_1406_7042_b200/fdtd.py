@@ -102,6 +102,10 @@ def load_library(path: str = LIB_PATH):
     lib.fdtd_sync.restype = C.c_int
     lib.fdtd_launch_count.argtypes = [C.c_void_p]
     lib.fdtd_launch_count.restype = C.c_int64
+    lib.fdtd_profile.argtypes = [C.c_void_p, C.c_int32]
+    lib.fdtd_profile.restype = C.c_int
+    lib.fdtd_phase_times.argtypes = [C.c_void_p, _f64p, C.c_int32]
+    lib.fdtd_phase_times.restype = C.c_int
     lib.fdtd_destroy.argtypes = [C.c_void_p]
     lib.fdtd_destroy.restype = None
     lib.fdtd_last_error.argtypes = []
@@ -113,7 +117,9 @@ def load_library(path: str = LIB_PATH):
 
 
 EXPORTED_SYMBOLS = ("fdtd_create", "fdtd_step", "fdtd_probe", "fdtd_get_state", "fdtd_set_state",
-                    "fdtd_sync", "fdtd_launch_count", "fdtd_destroy", "fdtd_last_error", "fdtd_version")
+                    "fdtd_sync", "fdtd_launch_count", "fdtd_profile", "fdtd_phase_times", "fdtd_destroy",
+                    "fdtd_last_error", "fdtd_version")
+PHASES = ("rows_e", "reduced_e", "stencil", "gather", "reduced_h", "coupling_y", "probes")
 
 
 def _check(code):
@@ -299,6 +305,17 @@ class Sim:
     def set_state(self, which, values):
         v = _arr(values, np.float64).ravel()
         _check(self.lib.fdtd_set_state(self.h, int(which), _ptr(v, C.c_double), v.size))
+
+    def profile(self, enable=True):
+        _check(self.lib.fdtd_profile(self.h, int(bool(enable))))
+
+    def phase_times(self):
+        """{phase: accumulated device ms}, plus 'steps' profiled."""
+        out = np.zeros(len(PHASES) + 1)
+        _check(self.lib.fdtd_phase_times(self.h, _ptr(out, C.c_double), len(out)))
+        d = dict(zip(PHASES, out[:len(PHASES)].tolist()))
+        d["steps"] = int(out[-1])
+        return d
 
     def launch_count(self):
         return int(self.lib.fdtd_launch_count(self.h))

@@ -1,0 +1,86 @@
+"""GPU parity on the BASELINE.json configurations, with problems emitted by the
+preprocessing library (the product path) and the oracle stepping the same fp64
+problem description (F13 shared-input rule)."""
+import numpy as np
+import pytest
+
+from oracle import problem_step as ps
+from synth import scenario
+
+from parity import compare, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _prep(which, precision=None, n_steps=None):
+    from paper_1406_7042_b200 import prep
+    scn = scenario(which, precision=precision, n_steps=n_steps)
+    prob, info = prep.build_problem(scn, precision=precision)
+    return scn, prob
+
+
+def test_config1_full_run_fp64():
+    # config 1: 2000 steps, fp64, q = 32 reduced block at 2x fine CFL: <= 1e-12
+    scn, prob = _prep(1)
+    gpu = run_gpu(prob, 2000, precision=64)
+    ora = run_oracle(prob, 2000)
+    es, ep, norm = compare(prob, gpu, ora)
+    assert norm > 0 and es <= 1e-12 and ep <= 1e-12, (es, ep)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_tiny2d_recipe_B(prec):
+    scn, prob = _prep("tiny2d_B", precision=prec)
+    gpu = run_gpu(prob, 300, precision=prec)
+    ora = run_oracle(prob, 300)
+    es, ep, _ = compare(prob, gpu, ora)
+    tol = 1e-12 if prec == 64 else 1e-4
+    assert es <= tol and ep <= tol, (es, ep)
+
+
+def test_config2_full_size_200_steps_fp32():
+    # full 1024^2 grid, q = 256, the launch configuration bench.py times
+    # (CUDA graphs of 32 steps); 200-step CI variant
+    scn, prob = _prep(2, precision=32)
+    gpu = run_gpu(prob, 200, precision=32, graph_steps=32)
+    ora = run_oracle(prob, 200)
+    es, ep, _ = compare(prob, gpu, ora)
+    assert es <= 1e-4 and ep <= 1e-4, (es, ep)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_config3_small_fp(prec):
+    scn, prob = _prep("config3_small", precision=prec)
+    gpu = run_gpu(prob, 200, precision=prec)
+    ora = run_oracle(prob, 200)
+    es, ep, _ = compare(prob, gpu, ora)
+    tol = 1e-12 if prec == 64 else 1e-4
+    assert es <= tol and ep <= tol, (es, ep)
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_config3_full_size_sampled_one_step(prec):
+    # 256^3: the oracle recomputes one step for 400 sampled unknowns from the
+    # GPU state and compares with the GPU's next state, element by element
+    from paper_1406_7042_b200.fdtd import Sim
+    scn, prob = _prep(3, precision=prec)
+    sim = Sim(prob, precision=prec)
+    for c, a in prob["init"].items():
+        sim.set_state(c, a)
+    sim.step(7)
+    st0 = {c: sim.get_state(c) for c in range(6)}
+    sim.step(1)
+    st1 = {c: sim.get_state(c) for c in range(6)}
+    sim.close()
+    rng = np.random.default_rng(0)
+    nx, ny, nz = prob["n"]
+    samples = [(int(rng.integers(0, 6)), (int(rng.integers(0, nx + 1)), int(rng.integers(0, ny + 1)),
+                                          int(rng.integers(0, nz + 1)))) for _ in range(400)]
+    ref = ps.sampled_step(prob, st0, samples)
+    shp = (nz + 1, ny + 1, nx + 1)
+    got = np.array([st1[c].reshape(shp)[idx[2], idx[1], idx[0]] for c, idx in samples])
+    want = np.array([ref[(c, tuple(idx))] for c, idx in samples])
+    scale = np.max(np.abs(want))
+    tol = 1e-13 if prec == 64 else 2e-6
+    assert scale > 0
+    assert np.max(np.abs(got - want)) <= tol * scale
