@@ -183,9 +183,9 @@ int64_t fdtd_launch_count(const fdtd_t* h);
  * following fdtd_step calls launch eagerly with CUDA events around each
  * kernel group (synchronising once per step); fdtd_profile(h, 0) returns to
  * graph launches.  fdtd_phase_times writes the accumulated device time [ms] of
- * the phases {explicit E rows, reduced E, coarse stencil, gather, reduced H,
- * coupling y, probes} into ms[0..6] and, if n > 7, the number of profiled
- * steps into ms[7]. */
+ * the phases {coarse stencil incl. explicit E rows, reduced chain incl.
+ * probes, grid-path reduced kernels (large blocks only)} into ms[0..2] and,
+ * if n > 3, the number of profiled steps into ms[3]. */
 int fdtd_profile(fdtd_t* h, int32_t enable);
 int fdtd_phase_times(fdtd_t* h, double* ms, int32_t n);
 

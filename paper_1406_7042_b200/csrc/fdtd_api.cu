@@ -118,7 +118,6 @@ struct Impl : public fdtd_t {
   DevMem mem;
   // fields: F[parity][comp]
   T* F[2][6] = {{nullptr}};
-  T** dF[2] = {nullptr, nullptr};     // device copies of F[parity] (for pointer-array kernels)
   // materials
   bool uniform = true;
   int n_mat = 0;
@@ -138,7 +137,12 @@ struct Impl : public fdtd_t {
   int32_t* g_comp = nullptr;
   int64_t* g_off = nullptr;
   int64_t* g_dst = nullptr;
-  T** dRED = nullptr;                 // {xh_all, h_all}
+  std::vector<fdtd::RedModel<T>> models;    // device descriptors (host copy)
+  fdtd::RedModel<T>* d_models = nullptr;
+  bool grid_path = false;             // large blocks: grid-wide gemv launches
+  int CL = 8;                         // cluster size of the reduced kernel
+  int NBsel = 1;                      // columns per row template (>= max N)
+  unsigned int* d_done = nullptr;
   // probes
   fdtd::Probes<T> pr{};
   int n_probe = 0;
@@ -158,7 +162,7 @@ struct Impl : public fdtd_t {
   size_t staging_bytes = 0;
   int kchunk = 16;
   // per-phase tracing (CUDA events around each kernel group, eager launches)
-  static constexpr int NPHASE = 7;       // rows_e, red_e, stencil, gather, red_h, red_y, probe
+  static constexpr int NPHASE = 3;       // stencil (+ explicit rows), reduced (+ probes), grid-path extras
   bool prof = false;
   cudaEvent_t ev[2 * NPHASE] = {};
   double phase_ms[NPHASE] = {0};
@@ -180,7 +184,7 @@ struct Impl : public fdtd_t {
   int phase_times(double* ms, int n) override {
     for (int i = 0; i < n && i < NPHASE; ++i) ms[i] = phase_n[i] ? phase_ms[i] : 0.0;
     for (int i = NPHASE; i < n; ++i) ms[i] = 0.0;
-    if (n > NPHASE) ms[NPHASE] = (double)(phase_n[2]);
+    if (n > NPHASE) ms[NPHASE] = (double)(phase_n[0]);
     return FDTD_OK;
   }
 
@@ -248,10 +252,6 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       if (!F[p][c]) return fail(FDTD_ENOMEM, "field allocation failed (%lld elements)", (long long)elems);
       CK(cudaMemsetAsync(F[p][c], 0, sizeof(T) * elems, stream));
     }
-  for (int p = 0; p < 2; ++p) {
-    dF[p] = dalloc<T*>(6);
-    CK(cudaMemcpyAsync(dF[p], F[p], sizeof(T*) * 6, cudaMemcpyHostToDevice, stream));
-  }
 
   // ---- materials ----
   std::vector<double> coef;           // [n_mat][6]
@@ -328,17 +328,12 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   CK(cudaMemsetAsync(xh_all, 0, sizeof(T) * std::max<int64_t>(xh_size, 1), stream));
   CK(cudaMemsetAsync(h_all, 0, sizeof(T) * std::max<int64_t>(h_size, 1), stream));
   CK(cudaMemsetAsync(y_all, 0, sizeof(T) * std::max<int64_t>(y_size, 1), stream));
-  dRED = dalloc<T*>(2);
-  {
-    T* red[2] = {xh_all, h_all};
-    CK(cudaMemcpy(dRED, red, sizeof(red), cudaMemcpyHostToDevice));
-  }
 
   // ---- explicit rows: interface rows, then source rows on regular unknowns ----
   struct HRow { std::vector<std::pair<int64_t, double>> w; double c = 0; int64_t y = -1; int src = -1; double cs = 0; int comp = 0; int64_t s = 0; };
   std::vector<HRow> hrows;
   std::map<int64_t, int> row_of;      // E unknown id -> explicit row
-  std::vector<int32_t> gcomp; std::vector<int64_t> goff, gdst;
+  std::vector<int32_t> gcomp, gblk; std::vector<int64_t> goff, gdst;
   if (itf && itf->n_rows > 0) {
     if (!itf->unknown || !itf->c || !itf->rowptr || !itf->block || !itf->inst || !itf->local)
       return fail(FDTD_EINVAL, "interface: missing arrays");
@@ -365,7 +360,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       h.y = D.y_off + (int64_t)l * D.N + (int64_t)in * B;
       row_of[u] = (int)hrows.size();
       hrows.push_back(h);
-      gcomp.push_back(c); goff.push_back(dev_off(s));
+      gcomp.push_back(c); goff.push_back(dev_off(s)); gblk.push_back(b);
       gdst.push_back(D.xh_off + (int64_t)(D.qe + l) * D.N + (int64_t)in * B);
     }
   }
@@ -488,18 +483,66 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     if (e) return e;
     rows.e_comp = d_ec; rows.e_off = d_eo; rows.c = d_c; rows.rowptr = d_rp; rows.h_comp = d_hc;
     rows.h_off = d_ho; rows.w = d_w; rows.y_off = d_yo; rows.src = d_src; rows.cs = d_cs; rows.wave = d_wave;
+    // dense row maps (storage offset -> explicit row) for the components that have rows
+    for (int c = 0; c < 3; ++c) rows.row_of[c] = nullptr;
+    for (int c = 0; c < 3; ++c) {
+      bool any = false;
+      for (int64_t r = 0; r < nr; ++r) any |= (ec[r] == c);
+      if (!any) continue;
+      std::vector<int32_t> mp((size_t)(plane * nplanes), -1);
+      for (int64_t r = 0; r < nr; ++r)
+        if (ec[r] == c) mp[eo[r]] = (int32_t)r;
+      int32_t* d_mp = dalloc<int32_t>(mp.size());
+      if (!d_mp) return fail(FDTD_ENOMEM, "row map allocation failed");
+      e |= up(d_mp, mp);
+      rows.row_of[c] = d_mp;
+    }
+    if (e) return e;
+    // per-block gather lists (G rows of the reduced chain)
+    std::vector<std::vector<int32_t>> bc(n_blocks);
+    std::vector<std::vector<int64_t>> bo(n_blocks), bd(n_blocks);
+    for (size_t q = 0; q < gcomp.size(); ++q) {
+      bc[gblk[q]].push_back(gcomp[q]); bo[gblk[q]].push_back(goff[q]); bd[gblk[q]].push_back(gdst[q]);
+    }
     n_gather = (int64_t)gcomp.size();
     g_comp = dalloc<int32_t>(std::max<int64_t>(n_gather, 1));
     g_off = dalloc<int64_t>(std::max<int64_t>(n_gather, 1));
     g_dst = dalloc<int64_t>(std::max<int64_t>(n_gather, 1));
     e |= up(g_comp, gcomp); e |= up(g_off, goff); e |= up(g_dst, gdst);
     if (e) return e;
+    // reduced-model descriptors
+    int64_t big = 0;
+    int maxN = 1;
+    for (int b = 0; b < n_blocks; ++b) {
+      BlockDev<T>& D = blocks[b];
+      fdtd::RedModel<T> M{};
+      M.qe = D.qe; M.qh = D.qh; M.n_if = D.n_if; M.N = D.N;
+      M.K = D.K; M.Mh = D.Mh; M.SE = D.SE; M.ge = D.ge; M.gh = D.gh;
+      M.xh = xh_all + D.xh_off; M.h = h_all + D.h_off; M.y = y_all + D.y_off;
+      M.n_g = (int)bc[b].size();
+      int32_t* c1 = dalloc<int32_t>(std::max<size_t>(bc[b].size(), 1));
+      int64_t* o1 = dalloc<int64_t>(std::max<size_t>(bo[b].size(), 1));
+      int64_t* d1 = dalloc<int64_t>(std::max<size_t>(bd[b].size(), 1));
+      for (auto& v : bd[b]) v -= D.xh_off;          // index into this model's xh
+      e |= up(c1, bc[b]); e |= up(o1, bo[b]); e |= up(d1, bd[b]);
+      M.g_comp = c1; M.g_off = o1; M.g_dst = d1;
+      models.push_back(M);
+      big = std::max<int64_t>(big, (int64_t)D.qh * (D.qe + D.n_if));
+      maxN = std::max(maxN, D.N);
+    }
+    if (e) return e;
+    if (maxN > 32) return fail(FDTD_ENOTSUP, "n_inst*batch > 32 per block not supported in this version");
+    NBsel = maxN <= 1 ? 1 : maxN <= 4 ? 4 : maxN <= 16 ? 16 : 32;
+    grid_path = big > (int64_t)4 * 1024 * 1024;      // > 16 MB fp32 of matrices per model
+    d_models = dalloc<fdtd::RedModel<T>>(std::max<size_t>(models.size(), 1));
+    if (!models.empty())
+      CK(cudaMemcpy(d_models, models.data(), sizeof(fdtd::RedModel<T>) * models.size(), cudaMemcpyHostToDevice));
   }
 
   // ---- probes ----
   {
     std::vector<int64_t> rp(1, 0), off;
-    std::vector<int32_t> srcv, strd;
+    std::vector<int32_t> srcv, strd, owner;
     std::vector<T> w;
     n_probe = probes ? (int)probes->n_probe : 0;
     for (int p = 0; p < n_probe; ++p) {
@@ -527,12 +570,15 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
         w.push_back((T)probes->weight[k]);
       }
       if (any_e && any_h) return fail(FDTD_EINVAL, "probe %d mixes E and H unknowns", p);
+      owner.push_back((kind == 0 || grid_path) ? -1 : probes->block[p]);
       rp.push_back((int64_t)w.size());
     }
     int64_t* d_rp = dalloc<int64_t>(rp.size());
     int32_t* d_src = dalloc<int32_t>(std::max<size_t>(srcv.size(), 1));
     int64_t* d_off = dalloc<int64_t>(std::max<size_t>(off.size(), 1));
     int32_t* d_st = dalloc<int32_t>(std::max<size_t>(strd.size(), 1));
+    int32_t* d_ow = dalloc<int32_t>(std::max<size_t>(owner.size(), 1));
+    if (!owner.empty()) CK(cudaMemcpy(d_ow, owner.data(), sizeof(int32_t) * owner.size(), cudaMemcpyHostToDevice));
     T* d_w = dalloc<T>(std::max<size_t>(w.size(), 1));
     CK(cudaMemcpy(d_rp, rp.data(), sizeof(int64_t) * rp.size(), cudaMemcpyHostToDevice));
     if (!srcv.empty()) {
@@ -541,12 +587,14 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       CK(cudaMemcpy(d_st, strd.data(), sizeof(int32_t) * strd.size(), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(d_w, w.data(), sizeof(T) * w.size(), cudaMemcpyHostToDevice));
     }
-    pr.n_probe = n_probe; pr.rowptr = d_rp; pr.src = d_src; pr.off = d_off; pr.stride = d_st; pr.w = d_w;
+    pr.n_probe = n_probe; pr.rowptr = d_rp; pr.src = d_src; pr.off = d_off; pr.w = d_w; pr.owner = d_ow;
     ring = dalloc<T>(std::max<int64_t>(cap * n_probe * B, 1));
     if (!ring) return fail(FDTD_ENOMEM, "probe ring allocation failed");
   }
   d_step = dalloc<int64_t>(1);
   d_bad = dalloc<unsigned long long>(1);
+  d_done = dalloc<unsigned int>(1);
+  CK(cudaMemsetAsync(d_done, 0, sizeof(unsigned int), stream));
   CK(cudaMemsetAsync(d_step, 0, sizeof(int64_t), stream));
   CK(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), stream));
   staging_bytes = sizeof(T) * (size_t)std::max<int64_t>(elems, std::max(xh_size, h_size));
@@ -555,59 +603,56 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   const size_t smem3 = 2 * 3 * 1024 * sizeof(T) + sizeof(fdtd::MatTable<T>);
   CK(cudaFuncSetAttribute(fdtd::stencil3d_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   CK(cudaFuncSetAttribute(fdtd::stencil3d_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
-  CK(cudaFuncSetAttribute(fdtd::stencil2d_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
-  CK(cudaFuncSetAttribute(fdtd::stencil2d_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  CK(cudaFuncSetAttribute(fdtd::stencil2d_tile_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  CK(cudaFuncSetAttribute(fdtd::stencil2d_tile_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   CK(cudaStreamSynchronize(stream));
   return FDTD_OK;
 }
 
 template <typename T>
 static int launch_gemv(int rows, int cols, int N, const T* A, const T* X, T* out, const T* g, T alpha,
-                       T beta, const int64_t* d_step, int check_every, unsigned long long* bad, cudaStream_t st) {
-  const int threads = 256;
-  const int blocks = (rows * 32 + threads - 1) / threads;
+                       bool accumulate, const int64_t* d_step, int check_every, unsigned long long* bad,
+                       cudaStream_t st) {
   if (rows <= 0) return 0;
-  const T gs = g ? (T)0 : (T)1;      // no diagonal given -> unit scale
-  if (N <= 1)
-    fdtd::gemv_rows_kernel<T, 1><<<blocks, threads, 0, st>>>(rows, cols, N, A, X, out, g, gs, alpha, beta, d_step, check_every, bad);
-  else if (N <= 4)
-    fdtd::gemv_rows_kernel<T, 4><<<blocks, threads, 0, st>>>(rows, cols, N, A, X, out, g, gs, alpha, beta, d_step, check_every, bad);
-  else if (N <= 16)
-    fdtd::gemv_rows_kernel<T, 16><<<blocks, threads, 0, st>>>(rows, cols, N, A, X, out, g, gs, alpha, beta, d_step, check_every, bad);
-  else if (N <= 32)
-    fdtd::gemv_rows_kernel<T, 32><<<blocks, threads, 0, st>>>(rows, cols, N, A, X, out, g, gs, alpha, beta, d_step, check_every, bad);
-  else
-    return -1;
+  const int threads = 256;
+  const int blocks = std::min((rows * 32 + threads - 1) / threads, 148 * 8);
+#define FDTD_GEMV(NB) fdtd::gemv_rows_kernel<T, NB><<<blocks, threads, 0, st>>>(rows, cols, N, A, X, out, g, alpha, accumulate, d_step, check_every, bad)
+  if (N <= 1) FDTD_GEMV(1);
+  else if (N <= 4) FDTD_GEMV(4);
+  else if (N <= 16) FDTD_GEMV(16);
+  else if (N <= 32) FDTD_GEMV(32);
+  else return -1;
+#undef FDTD_GEMV
   return 1;
+}
+
+template <typename T, int NB>
+static cudaError_t launch_reduced(const fdtd::RedParams<T>& P, int n_clusters, int CL, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_clusters * CL, 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fdtd::reduced_cluster_kernel<T, NB>, P);
 }
 
 template <typename T>
 int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   int64_t n = 0;
   auto mark = [&](int ph, int edge) { if (profile) cudaEventRecord(ev[2 * ph + edge], st); };
-  T* const* E0 = dF[p];
-  T* const* E1 = dF[p ^ 1];
-  // a1 + a3: explicit rows (interface and source rows) into the new buffer
+  fdtd::Fields<T> F0, F1;
+  for (int c = 0; c < 6; ++c) { F0.f[c] = F[p][c]; F1.f[c] = F[p ^ 1][c]; }
+  // a1-a3 + a5: fused coarse stencil with the explicit rows evaluated in place
   mark(0, 0);
-  if (rows.n_rows > 0) {
-    const int64_t work = rows.n_rows * B;
-    fdtd::rows_e_kernel<T><<<(unsigned)((work + 255) / 256), 256, 0, st>>>(
-        rows, B, (const T* const*)E0, E1, (const T* const*)E0, y_all, d_step);
-    ++n;
-  }
-  mark(0, 1);
-  // a4: e~ -= G_e K~' h~
-  mark(1, 0);
-  for (auto& D : blocks) {
-    int r = launch_gemv<T>(D.qe, D.qh, D.N, D.K, h_all + D.h_off, xh_all + D.xh_off, D.ge, (T)-1, (T)1,
-                           d_step, check_every, d_bad, st);
-    if (r < 0) return fail(FDTD_ENOTSUP, "n_inst*batch > 32 per block not supported in this version");
-    n += r;
-  }
-  mark(1, 1);
-  // a2 + a5: fused coarse stencil
-  mark(2, 0);
   const size_t tabsz = uniform ? 0 : sizeof(fdtd::MatTable<T>);
+  const fdtd::Dims dm{nx, ny, nz, px, B, plane};
   if (dim == 3) {
     int BX, BY;
     if (B == 1) { BX = 32; BY = 8; }
@@ -617,65 +662,82 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
     const size_t sm = 2 * 3 * (size_t)BX * BY * sizeof(T) + tabsz;
     if (uniform)
       fdtd::stencil3d_kernel<T, true><<<grid, dim3(BX, BY), sm, st>>>(
-          fdtd::Dims{nx, ny, nz, px, B, plane}, F[p][0], F[p][1], F[p][2], F[p][3], F[p][4], F[p][5],
-          F[p ^ 1][0], F[p ^ 1][1], F[p ^ 1][2], F[p ^ 1][3], F[p ^ 1][4], F[p ^ 1][5], mat_id, tab, ifm, n_mat,
-          u0, u1, kchunk, d_step, check_every, d_bad);
+          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
     else
       fdtd::stencil3d_kernel<T, false><<<grid, dim3(BX, BY), sm, st>>>(
-          fdtd::Dims{nx, ny, nz, px, B, plane}, F[p][0], F[p][1], F[p][2], F[p][3], F[p][4], F[p][5],
-          F[p ^ 1][0], F[p ^ 1][1], F[p ^ 1][2], F[p ^ 1][3], F[p ^ 1][4], F[p ^ 1][5], mat_id, tab, ifm, n_mat,
-          u0, u1, kchunk, d_step, check_every, d_bad);
+          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
   } else {
-    const int BX = (B == 1) ? 256 : B * std::max(2, 256 / B);
-    const int outx = BX / B - 1;
-    const int jchunk = 16;
-    dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + jchunk - 1) / jchunk, 1);
-    const size_t sm = 2 * (size_t)BX * sizeof(T) + tabsz;
+    int BX = (B == 1) ? 32 : B * std::max(2, 64 / B), BY = 16;
+    if (BX * BY > 1024) BY = std::max(2, 1024 / BX);
+    const int outx = BX / B - 1, outy = BY - 1;
+    dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + outy - 1) / outy, 1);
+    const size_t sm = (size_t)BX * BY * sizeof(T) + tabsz;
     if (uniform)
-      fdtd::stencil2d_kernel<T, true><<<grid, BX, sm, st>>>(
-          fdtd::Dims{nx, ny, 0, px, B, plane}, F[p][2], F[p][3], F[p][4], F[p ^ 1][2], F[p ^ 1][3], F[p ^ 1][4],
-          mat_id, tab, ifm, n_mat, u0, u1, jchunk, d_step, check_every, d_bad);
+      fdtd::stencil2d_tile_kernel<T, true><<<grid, dim3(BX, BY), sm, st>>>(
+          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, d_step, check_every, d_bad);
     else
-      fdtd::stencil2d_kernel<T, false><<<grid, BX, sm, st>>>(
-          fdtd::Dims{nx, ny, 0, px, B, plane}, F[p][2], F[p][3], F[p][4], F[p ^ 1][2], F[p ^ 1][3], F[p ^ 1][4],
-          mat_id, tab, ifm, n_mat, u0, u1, jchunk, d_step, check_every, d_bad);
+      fdtd::stencil2d_tile_kernel<T, false><<<grid, dim3(BX, BY), sm, st>>>(
+          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, d_step, check_every, d_bad);
   }
   ++n;
-  mark(2, 1);
-  // a6: G = E_if^{n+1};  h~ += G_h [K~'^T | S_E^T][e~ ; G];  y = S_E h~
-  mark(3, 0);
-  if (n_gather > 0) {
-    fdtd::gather_kernel<T><<<(unsigned)((n_gather * B + 255) / 256), 256, 0, st>>>(
-        n_gather, B, g_comp, g_off, g_dst, E1, xh_all);
-    ++n;
+  mark(0, 1);
+  // a4, a6 (+ a7): reduced chain, probes, step counter
+  fdtd::RedParams<T> P{};
+  P.n_models = grid_path ? 0 : (int)models.size();
+  P.B = B;
+  P.models = d_models;
+  P.red_base[0] = xh_all;
+  P.red_base[1] = h_all;
+  P.F = F1;
+  P.pr = pr;
+  P.ring = ring;
+  P.cap = cap;
+  P.d_step = d_step;
+  P.done = d_done;
+  P.check_every = check_every;
+  P.bad_step = d_bad;
+  if (grid_path) {
+    mark(2, 0);
+    if (n_gather > 0) {
+      fdtd::gather_kernel<T><<<(unsigned)((n_gather * B + 255) / 256), 256, 0, st>>>(
+          n_gather, B, g_comp, g_off, g_dst, F1, xh_all);
+      ++n;
+    }
+    for (auto& D : blocks) {
+      n += launch_gemv<T>(D.qe, D.qh, D.N, D.K, h_all + D.h_off, xh_all + D.xh_off, D.ge, (T)-1, true,
+                          d_step, check_every, d_bad, st);
+      n += launch_gemv<T>(D.qh, D.qe + D.n_if, D.N, D.Mh, xh_all + D.xh_off, h_all + D.h_off, D.gh, (T)1, true,
+                          d_step, check_every, d_bad, st);
+      if (D.n_if > 0)
+        n += launch_gemv<T>(D.n_if, D.qh, D.N, D.SE, h_all + D.h_off, y_all + D.y_off, (const T*)nullptr,
+                            (T)1, false, d_step, 0, d_bad, st);
+    }
+    mark(2, 1);
   }
-  mark(3, 1);
-  mark(4, 0);
-  for (auto& D : blocks)
-    n += launch_gemv<T>(D.qh, D.qe + D.n_if, D.N, D.Mh, xh_all + D.xh_off, h_all + D.h_off, D.gh, (T)1, (T)1,
-                        d_step, check_every, d_bad, st);
-  mark(4, 1);
-  mark(5, 0);
-  for (auto& D : blocks)
-    if (D.n_if > 0)
-      n += launch_gemv<T>(D.n_if, D.qh, D.N, D.SE, h_all + D.h_off, y_all + D.y_off, (const T*)nullptr, (T)1,
-                          (T)0, d_step, 0, d_bad, st);
-  mark(5, 1);
-  // a7: probes + step counter
-  mark(6, 0);
-  fdtd::probe_kernel<T><<<1, 256, 0, st>>>(pr, B, (const T* const*)E1, (const T* const*)dRED, ring, cap, d_step);
+  mark(1, 0);
+  const int ncl = std::max(1, P.n_models);
+  const int cl = P.n_models > 0 ? CL : 1;
+  cudaError_t le;
+  switch (NBsel) {
+    case 1: le = launch_reduced<T, 1>(P, ncl, cl, st); break;
+    case 4: le = launch_reduced<T, 4>(P, ncl, cl, st); break;
+    case 16: le = launch_reduced<T, 16>(P, ncl, cl, st); break;
+    default: le = launch_reduced<T, 32>(P, ncl, cl, st); break;
+  }
+  if (le != cudaSuccess) return fail(FDTD_ECUDA, "reduced kernel launch: %s", cudaGetErrorString(le));
   ++n;
-  mark(6, 1);
+  mark(1, 1);
+  CK(cudaGetLastError());
   if (profile) {
-    CK(cudaEventSynchronize(ev[2 * NPHASE - 1]));
+    CK(cudaEventSynchronize(ev[3]));
     for (int ph = 0; ph < NPHASE; ++ph) {
+      if (ph == 2 && !grid_path) continue;
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, ev[2 * ph], ev[2 * ph + 1]));
       phase_ms[ph] += ms;
       phase_n[ph] += 1;
     }
   }
-  CK(cudaGetLastError());
   *count += n;
   return FDTD_OK;
 }
@@ -850,7 +912,7 @@ int Impl<T>::set_state(int which, const double* in, int64_t n) {
       for (auto& D : blocks)
         if (D.n_if > 0)
           launch_gemv<T>(D.n_if, D.qh, D.N, D.SE, h_all + D.h_off, y_all + D.y_off, (const T*)nullptr, (T)1,
-                         (T)0, d_step, 0, d_bad, stream);
+                         false, d_step, 0, d_bad, stream);
     CK(cudaStreamSynchronize(stream));
     return FDTD_OK;
   }

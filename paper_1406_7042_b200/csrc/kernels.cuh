@@ -1,23 +1,30 @@
 // kernels.cuh — device kernels of the reduced-hybrid FDTD step (sm_100a).
 //
-// Step n -> n+1 (DESIGN.md §1 rows a1-a7), all on one stream:
-//   rows_e     explicit E rows (interface rows + source rows)     a1, a3
-//   gemv       reduced E half  e~ -= G_e K~' h~                  a4
-//   stencil    fused coarse E->H pass (ping-pong buffers)        a2, a5
-//   gather     E_if -> G                                         a6
-//   gemv       h~ += G_h [K~'^T | S_E^T] [e~ ; G]                a6
-//   gemv       y = S_E h~                                        a6 (for a3 of step n+1)
-//   probes     sample + advance the device step counter          a7
+// One time step n -> n+1 (DESIGN.md §1 rows a1-a7) is two launches:
+//   stencil   fused coarse E->H pass over the grid (ping-pong buffers); the
+//             explicit E rows (interface rows a3, source rows a1) are
+//             evaluated in place by the thread that owns them           a1-a3, a5
+//   reduced   one thread-block cluster per reduced model:
+//               e~ -= G_e K~' h~                                         a4
+//               G = E_if^{n+1} (gather)                                   a6
+//               h~ += G_h [K~'^T | S_E^T] [e~ ; G]                       a6
+//               y = S_E h~   (consumed by the next step's interface rows) a6
+//             + probes, divergence check, device step counter            a7
+// Large reduced blocks (S_E of hundreds of MB) use the grid-wide gemv path
+// instead of a cluster (see fdtd_api.cu).
 //
 // Coarse fields live in "device storage": component arrays indexed
 // ((k*(ny+1) + j)*px + i)*B + b with the batch b innermost and px >= nx+1.
 // E^{n+1} = E^n + cb * curl(H)  ==  E^n - cb * (K_inc H)   (K_inc = -curl)
 // H^{n+1} = H^n - ch * curl(E)  ==  H^n + ch * (K_inc^T E)
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace fdtd {
+
+namespace cg = cooperative_groups;
 
 template <typename T> struct Coef;       // per-material coefficient, hi/lo for fp32 (R11)
 template <> struct Coef<float> {
@@ -44,43 +51,158 @@ struct Dims {
   int64_t plane;                  // (ny+1)*px  (storage indices per k-plane)
 };
 
-__device__ __forceinline__ int64_t didx(const Dims& d, int i, int j, int k) {
-  return ((int64_t)k * (d.ny + 1) + j) * d.px + i;
-}
+template <typename T>
+struct Fields {                   // one parity of the coarse state, by component
+  T* f[6];
+};
 
 __device__ __forceinline__ bool finite_small(double v) {
   return isfinite(v) && fabs(v) <= 1e100;
 }
 
 // ---------------------------------------------------------------------------
-// 3-D fused E->H stencil.  Block (BX, BY) threads covers BX/B cells in x and
-// BY cells in y; it computes E^{n+1} on the whole footprint and H^{n+3/2} on
-// the footprint minus its last x cell and last y row (overlapped tiling: the
-// halo E is recomputed by the neighbouring block, H_old / E_old are read-only
-// so this is race free).  Marches z over [k0, k1).
+// explicit E rows (interface rows of reading R4 and source rows):
+//   E1 = E0 - c (sum_k W_k H0[col_k] + y_r) - cs J[step]
+// row_of[comp][storage offset] gives the row (dense int32 map, -1 elsewhere).
+// ---------------------------------------------------------------------------
+template <typename T>
+struct RowsE {
+  int64_t n_rows;
+  const int32_t* row_of[3];    // per E component, [plane*nplanes] or null
+  const Coef<T>* c;            // [n_rows]
+  const int64_t* rowptr;       // [n_rows+1]
+  const int32_t* h_comp;       // [nnz]
+  const int64_t* h_off;        // [nnz]
+  const T* w;                  // [nnz]
+  const int64_t* y_off;        // [n_rows] offset into y (block base + local*N + inst*B), -1 none
+  const int32_t* src;          // [n_rows] source index or -1
+  const T* cs;                 // [n_rows] source coefficient
+  const T* wave;               // [n_wave][n_src][B]
+  int64_t n_wave, n_src;
+  // list form (for the standalone rows kernel)
+  const int32_t* e_comp;       // [n_rows]
+  const int64_t* e_off;        // [n_rows]
+};
+
+template <typename T>
+__device__ __forceinline__ T eval_row(const RowsE<T>& R, int r, int b, int B, T e0, const Fields<T>& H0,
+                                      const T* __restrict__ y, int64_t step) {
+  T acc = 0;
+  for (int64_t k = R.rowptr[r]; k < R.rowptr[r + 1]; ++k)
+    acc += R.w[k] * H0.f[R.h_comp[k]][R.h_off[k] * B + b];
+  const int64_t yo = R.y_off[r];
+  if (yo >= 0) acc += y[yo + b];
+  T e = e0 - R.c[r].apply(acc);
+  const int s = R.src[r];
+  if (s >= 0 && step < R.n_wave) e -= R.cs[r] * R.wave[(step * R.n_src + s) * B + b];
+  return e;
+}
+
+// ---------------------------------------------------------------------------
+// 2-D (Ez, Hx, Hy) fused E->H stencil, tiled.  Block (BX, BY) threads covers
+// BX/B cells in x and BY rows; every thread computes Ez^{n+1} of its cell, the
+// block keeps them in shared memory and the interior (BX/B-1) x (BY-1) cells
+// update Hx, Hy from their +x / +y neighbours (overlapped tiling: the halo Ez
+// is recomputed by the neighbouring block; old buffers are read-only).
+// Ez += cb ((Hy(i) - Hy(i-1)) - (Hx(j) - Hx(j-1)))
+// Hx -= ch (Ez(j+1) - Ez(j))        Hy += ch (Ez(i+1) - Ez(i))
 // ---------------------------------------------------------------------------
 template <typename T, bool UNIFORM>
 __global__ void __launch_bounds__(1024)
-stencil3d_kernel(Dims d, const T* __restrict__ Ex0, const T* __restrict__ Ey0, const T* __restrict__ Ez0,
-                 const T* __restrict__ Hx0, const T* __restrict__ Hy0, const T* __restrict__ Hz0,
-                 T* __restrict__ Ex1, T* __restrict__ Ey1, T* __restrict__ Ez1,
-                 T* __restrict__ Hx1, T* __restrict__ Hy1, T* __restrict__ Hz1,
-                 const uint8_t* __restrict__ mat_id, const Coef<T>* __restrict__ gtab,
-                 const uint8_t* __restrict__ gifm, int n_mat, Coef<T> u0, Coef<T> u1,
-                 int kchunk, const int64_t* __restrict__ d_step, int check_every,
+stencil2d_tile_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restrict__ mat_id,
+                      const Coef<T>* __restrict__ gtab, const uint8_t* __restrict__ gifm, int n_mat,
+                      Coef<T> u0, Coef<T> u1, RowsE<T> R, const T* __restrict__ y,
+                      const int64_t* __restrict__ d_step, int check_every,
+                      unsigned long long* __restrict__ bad_step) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int BX = blockDim.x, BY = blockDim.y, B = d.B;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  T* sE = reinterpret_cast<T*>(smem_raw);                    // [BY][BX]
+  MatTable<T>* tab = reinterpret_cast<MatTable<T>*>(sE + BX * BY);
+  if (!UNIFORM) {
+    for (int m = ty * BX + tx; m < n_mat; m += BX * BY) {
+      tab->c[m][2] = gtab[m * 6 + 2];
+      tab->c[m][3] = gtab[m * 6 + 3];
+      tab->c[m][4] = gtab[m * 6 + 4];
+      tab->ifm[m] = gifm[m];
+    }
+  }
+  const int outx = BX / B - 1, outy = BY - 1;
+  const int i = blockIdx.x * outx + tx / B;
+  const int b = tx % B;
+  const int j = blockIdx.y * outy + ty;
+  const int nx = d.nx, ny = d.ny;
+  const bool inside = (i <= nx) && (j <= ny);
+  const bool own = inside && (tx / B < outx) && (ty < outy);
+  const int ii = min(i, nx), jj = min(j, ny);
+  const int64_t soff = (int64_t)jj * d.px + ii;            // storage offset
+  const int64_t o = soff * B + b;
+  const int64_t sx = (i > 0) ? B : 0;
+  const int64_t sy = (j > 0) ? (int64_t)d.px * B : 0;
+  const int64_t step = *d_step;
+  __syncthreads();
+  const int m = UNIFORM ? 0 : (int)mat_id[soff];
+  T ez = 0, hx = 0, hy = 0;
+  if (inside) {
+    hx = F0.f[3][o]; hy = F0.f[4][o];
+    const T hx_jm = F0.f[3][o - sy], hy_im = F0.f[4][o - sx];
+    const T ez0 = F0.f[2][o];
+    const Coef<T> c = UNIFORM ? u0 : tab->c[m][2];
+    const T dd = (hy - hy_im) - (hx - hx_jm);
+    const bool act = (i > 0) && (i < nx) && (j > 0) && (j < ny);
+    ez = act ? ez0 + c.apply(dd) : (T)0;
+    if (!UNIFORM && (tab->ifm[m] & 4)) {
+      const int r = R.row_of[2][soff];
+      ez = eval_row(R, r, b, B, ez0, F0, y, step);
+    }
+  }
+  sE[ty * BX + tx] = ez;
+  __syncthreads();
+  if (own) {
+    const T ez_ip = sE[ty * BX + tx + B];
+    const T ez_jp = sE[(ty + 1) * BX + tx];
+    Coef<T> cx, cy;
+    if (UNIFORM) { cx = u1; cy = u1; }
+    else { cx = tab->c[m][3]; cy = tab->c[m][4]; }
+    const T hx1 = (i > 0 && i < nx && j < ny) ? hx - cx.apply(ez_jp - ez) : hx;
+    const T hy1 = (i < nx && j > 0 && j < ny) ? hy + cy.apply(ez_ip - ez) : hy;
+    F1.f[2][o] = ez; F1.f[3][o] = hx1; F1.f[4][o] = hy1;
+    if (check_every > 0 && (step % check_every) == 0 &&
+        !(finite_small(ez) && finite_small(hx1) && finite_small(hy1)))
+      atomicMin(bad_step, (unsigned long long)step);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 3-D fused E->H stencil.  Block (BX, BY) threads covers BX/B cells in x and
+// BY cells in y; it computes E^{n+1} on the whole footprint and H^{n+3/2} on
+// the footprint minus its last x cell and last y row (overlapped tiling), and
+// marches z over [k0, k1).
+// ---------------------------------------------------------------------------
+template <typename T, bool UNIFORM>
+__global__ void __launch_bounds__(1024)
+stencil3d_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restrict__ mat_id,
+                 const Coef<T>* __restrict__ gtab, const uint8_t* __restrict__ gifm, int n_mat,
+                 Coef<T> u0, Coef<T> u1, RowsE<T> R, const T* __restrict__ y, int kchunk,
+                 const int64_t* __restrict__ d_step, int check_every,
                  unsigned long long* __restrict__ bad_step) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int BX = blockDim.x, BY = blockDim.y, B = d.B;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  // shared: E^{n+1} of two planes (3 comps), then the material table
   T* sE = reinterpret_cast<T*>(smem_raw);                       // [2][3][BY][BX]
   MatTable<T>* tab = reinterpret_cast<MatTable<T>*>(sE + 2 * 3 * BX * BY);
   if (!UNIFORM) {
-    for (int m = threadIdx.y * BX + tx; m < n_mat; m += BX * BY) {
+    for (int m = ty * BX + tx; m < n_mat; m += BX * BY) {
       for (int c = 0; c < 6; ++c) tab->c[m][c] = gtab[m * 6 + c];
       tab->ifm[m] = gifm[m];
     }
   }
+  const T* __restrict__ Ex0 = F0.f[0];
+  const T* __restrict__ Ey0 = F0.f[1];
+  const T* __restrict__ Ez0 = F0.f[2];
+  const T* __restrict__ Hx0 = F0.f[3];
+  const T* __restrict__ Hy0 = F0.f[4];
+  const T* __restrict__ Hz0 = F0.f[5];
   const int cells_x = BX / B;
   const int outx = cells_x - 1, outy = BY - 1;
   const int i = blockIdx.x * outx + tx / B;
@@ -91,14 +213,12 @@ stencil3d_kernel(Dims d, const T* __restrict__ Ex0, const T* __restrict__ Ey0, c
   const bool inside = (i <= d.nx) && (j <= d.ny);
   const bool own = inside && (tx / B < outx) && (ty < outy);
   const int nx = d.nx, ny = d.ny, nz = d.nz;
-  // neighbour offsets (device element units), clamped at the low walls where
-  // the partner only feeds an inert (PEC) unknown
   const int64_t sx = (i > 0) ? B : 0;
   const int64_t sy = (j > 0) ? (int64_t)d.px * B : 0;
   const int64_t sz = d.plane * B;
   const int ii = min(i, nx), jj = min(j, ny);
-  const int64_t col = ((int64_t)jj * d.px + ii) * B + b;       // offset within a k-plane
-  // activity masks (outer PEC walls and array extents, fdtd.h conventions)
+  const int64_t scol = (int64_t)jj * d.px + ii;
+  const int64_t col = scol * B + b;
   const bool ax_ij = (i < nx) && (j > 0) && (j < ny);
   const bool ay_ij = (j < ny) && (i > 0) && (i < nx);
   const bool az_ij = (i > 0) && (i < nx) && (j > 0) && (j < ny);
@@ -110,12 +230,8 @@ stencil3d_kernel(Dims d, const T* __restrict__ Ex0, const T* __restrict__ Ey0, c
   bool bad = false;
   __syncthreads();
 
-  // material lookup
-  auto mat_of = [&](int k) -> int { return UNIFORM ? 0 : (int)mat_id[(int64_t)k * d.plane + (int64_t)jj * d.px + ii]; };
-
-  // H^{n+1/2} of the thread's own column at planes k-1 (prev) and k (cur)
+  auto mat_of = [&](int k) -> int { return UNIFORM ? 0 : (int)mat_id[(int64_t)k * d.plane + scol]; };
   T hx_p = 0, hy_p = 0;
-  // compute E^{n+1} at plane k (needs H planes k and k-1)
   auto compute_E = [&](int k, T& hx_c, T& hy_c, T& hz_c, T& ex, T& ey, T& ez) {
     const int64_t o = (int64_t)k * sz + col;
     hx_c = Hx0[o]; hy_c = Hy0[o]; hz_c = Hz0[o];
@@ -134,19 +250,20 @@ stencil3d_kernel(Dims d, const T* __restrict__ Ex0, const T* __restrict__ Ey0, c
     ex = (ax_ij && kin) ? ex0 + cx.apply(dx_) : (T)0;
     ey = (ay_ij && kin) ? ey0 + cy.apply(dy_) : (T)0;
     ez = (az_ij && k < nz) ? ez0 + cz.apply(dz_) : (T)0;
-    if (ifm) {   // explicit rows (interface / sources): value already in the new buffer
-      if (ifm & 1) ex = Ex1[o];
-      if (ifm & 2) ey = Ey1[o];
-      if (ifm & 4) ez = Ez1[o];
+    if (ifm) {   // explicit rows (interface / sources)
+      const int64_t s = (int64_t)k * d.plane + scol;
+      if (ifm & 1) ex = eval_row(R, R.row_of[0][s], b, B, ex0, F0, y, step);
+      if (ifm & 2) ey = eval_row(R, R.row_of[1][s], b, B, ey0, F0, y, step);
+      if (ifm & 4) ez = eval_row(R, R.row_of[2][s], b, B, ez0, F0, y, step);
     }
   };
 
   T* sEx[2] = {sE, sE + 3 * BX * BY};
   const int sidx = ty * BX + tx;
-  T ex_p = 0, ey_p = 0, ez_p = 0;           // E^{n+1} at plane k (own column)
+  T ex_p = 0, ey_p = 0, ez_p = 0;
   T hx_c = 0, hy_c = 0, hz_c = 0;
   if (inside) {
-    if (k0 > 0) {                            // H of plane k0-1 for the first E compute
+    if (k0 > 0) {
       const int64_t o = (int64_t)(k0 - 1) * sz + col;
       hx_p = Hx0[o]; hy_p = Hy0[o];
     }
@@ -158,13 +275,12 @@ stencil3d_kernel(Dims d, const T* __restrict__ Ex0, const T* __restrict__ Ey0, c
   }
   if (own) {
     const int64_t o = (int64_t)k0 * sz + col;
-    Ex1[o] = ex_p; Ey1[o] = ey_p; Ez1[o] = ez_p;
+    F1.f[0][o] = ex_p; F1.f[1][o] = ey_p; F1.f[2][o] = ez_p;
     if (do_check) bad |= !(finite_small(ex_p) && finite_small(ey_p) && finite_small(ez_p));
   }
   for (int k = k0; k < k1; ++k) {
-    // E^{n+1} at plane k+1 (own column); H(k) moves to "prev"
     T ex_n = 0, ey_n = 0, ez_n = 0;
-    T hx_k = hx_c, hy_k = hy_c, hz_k = hz_c;      // H^{n+1/2} at plane k
+    const T hx_k = hx_c, hy_k = hy_c, hz_k = hz_c;
     hx_p = hx_c; hy_p = hy_c;
     if (inside && k + 1 <= nz) compute_E(k + 1, hx_c, hy_c, hz_c, ex_n, ey_n, ez_n);
     T* s1 = sEx[(k + 1) & 1];
@@ -172,7 +288,6 @@ stencil3d_kernel(Dims d, const T* __restrict__ Ex0, const T* __restrict__ Ey0, c
     __syncthreads();
     if (own) {
       const T* s0 = sEx[k & 1];
-      // neighbours at plane k: (i+1, j) and (i, j+1)
       const T ey_ip = s0[BX * BY + sidx + B], ez_ip = s0[2 * BX * BY + sidx + B];
       const T ex_jp = s0[sidx + BX], ez_jp = s0[2 * BX * BY + sidx + BX];
       const int64_t o = (int64_t)k * sz + col;
@@ -185,10 +300,10 @@ stencil3d_kernel(Dims d, const T* __restrict__ Ex0, const T* __restrict__ Ey0, c
       const T hx1 = (hx_ij && k < nz) ? hx_k - cx.apply(dhx) : hx_k;
       const T hy1 = (hy_ij && k < nz) ? hy_k - cy.apply(dhy) : hy_k;
       const T hz1 = (hz_ij && k > 0 && k < nz) ? hz_k - cz.apply(dhz) : hz_k;
-      Hx1[o] = hx1; Hy1[o] = hy1; Hz1[o] = hz1;
+      F1.f[3][o] = hx1; F1.f[4][o] = hy1; F1.f[5][o] = hz1;
       if (k + 1 < k1 && k + 1 <= nz) {
         const int64_t o1 = o + sz;
-        Ex1[o1] = ex_n; Ey1[o1] = ey_n; Ez1[o1] = ez_n;
+        F1.f[0][o1] = ex_n; F1.f[1][o1] = ey_n; F1.f[2][o1] = ez_n;
       }
       if (do_check) bad |= !(finite_small(hx1) && finite_small(hy1) && finite_small(hz1) &&
                              finite_small(ex_n) && finite_small(ey_n) && finite_small(ez_n));
@@ -200,219 +315,180 @@ stencil3d_kernel(Dims d, const T* __restrict__ Ex0, const T* __restrict__ Ey0, c
 }
 
 // ---------------------------------------------------------------------------
-// 2-D (Ez, Hx, Hy) fused stencil: block of BX threads covers BX/B cells in x,
-// marches y over [j0, j1).
-// Ez += cb ((Hy(i) - Hy(i-1)) - (Hx(j) - Hx(j-1)))
-// Hx -= ch (Ez(j+1) - Ez(j))        Hy += ch (Ez(i+1) - Ez(i))
-// ---------------------------------------------------------------------------
-template <typename T, bool UNIFORM>
-__global__ void __launch_bounds__(1024)
-stencil2d_kernel(Dims d, const T* __restrict__ Ez0, const T* __restrict__ Hx0, const T* __restrict__ Hy0,
-                 T* __restrict__ Ez1, T* __restrict__ Hx1, T* __restrict__ Hy1,
-                 const uint8_t* __restrict__ mat_id, const Coef<T>* __restrict__ gtab,
-                 const uint8_t* __restrict__ gifm, int n_mat, Coef<T> u0, Coef<T> u1,
-                 int jchunk, const int64_t* __restrict__ d_step, int check_every,
-                 unsigned long long* __restrict__ bad_step) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int BX = blockDim.x, B = d.B, tx = threadIdx.x;
-  T* sE = reinterpret_cast<T*>(smem_raw);                  // [2][BX]
-  MatTable<T>* tab = reinterpret_cast<MatTable<T>*>(sE + 2 * BX);
-  if (!UNIFORM) {
-    for (int m = tx; m < n_mat; m += BX) {
-      for (int c = 0; c < 6; ++c) tab->c[m][c] = gtab[m * 6 + c];
-      tab->ifm[m] = gifm[m];
-    }
-  }
-  const int outx = BX / B - 1;
-  const int i = blockIdx.x * outx + tx / B;
-  const int b = tx % B;
-  const int j0 = blockIdx.y * jchunk;
-  const int j1 = min(j0 + jchunk, d.ny + 1);
-  const int nx = d.nx, ny = d.ny;
-  const bool inside = i <= nx;
-  const bool own = inside && (tx / B < outx);
-  const int ii = min(i, nx);
-  const int64_t sx = (i > 0) ? B : 0;
-  const int64_t rowst = (int64_t)d.px * B;
-  const int64_t step = *d_step;
-  const bool do_check = check_every > 0 && (step % check_every) == 0;
-  bool bad = false;
-  __syncthreads();
-  auto mat_of = [&](int j) -> int { return UNIFORM ? 0 : (int)mat_id[(int64_t)j * d.px + ii]; };
-  const bool ez_i = (i > 0) && (i < nx);
-  T hx_p = 0;                                    // Hx^{n+1/2}(i, j-1)
-  auto compute_E = [&](int j, T& hx_c, T& hy_c) -> T {
-    const int64_t o = (int64_t)j * rowst + (int64_t)ii * B + b;
-    hx_c = Hx0[o]; hy_c = Hy0[o];
-    const T hy_im = Hy0[o - sx];
-    const T ez0 = Ez0[o];
-    T ez;
-    int m = mat_of(j);
-    Coef<T> c = UNIFORM ? u0 : tab->c[m][2];
-    const T dd = (hy_c - hy_im) - (hx_c - hx_p);
-    ez = (ez_i && j > 0 && j < ny) ? ez0 + c.apply(dd) : (T)0;
-    if (!UNIFORM && (tab->ifm[m] & 4)) ez = Ez1[o];
-    return ez;
-  };
-  T hx_c = 0, hy_c = 0, ez_p = 0;
-  if (inside) {
-    if (j0 > 0) hx_p = Hx0[(int64_t)(j0 - 1) * rowst + (int64_t)ii * B + b];
-    ez_p = compute_E(j0, hx_c, hy_c);
-    if (own) {
-      Ez1[(int64_t)j0 * rowst + (int64_t)ii * B + b] = ez_p;
-      if (do_check) bad |= !finite_small(ez_p);
-    }
-  }
-  for (int j = j0; j < j1; ++j) {
-    const T hx_j = hx_c, hy_j = hy_c;
-    hx_p = hx_c;
-    T ez_n = 0;
-    if (inside && j + 1 <= ny) ez_n = compute_E(j + 1, hx_c, hy_c);
-    sE[(j & 1) * BX + tx] = ez_p;
-    __syncthreads();
-    if (own) {
-      const int64_t o = (int64_t)j * rowst + (int64_t)ii * B + b;
-      const T ez_ip = sE[(j & 1) * BX + tx + B];
-      Coef<T> cx, cy;
-      if (UNIFORM) { cx = u1; cy = u1; }
-      else { const int m = mat_of(j); cx = tab->c[m][3]; cy = tab->c[m][4]; }
-      const T hx1 = (i > 0 && i < nx && j < ny) ? hx_j - cx.apply(ez_n - ez_p) : hx_j;
-      const T hy1 = (i < nx && j > 0 && j < ny) ? hy_j + cy.apply(ez_ip - ez_p) : hy_j;
-      Hx1[o] = hx1; Hy1[o] = hy1;
-      if (j + 1 < j1 && j + 1 <= ny) Ez1[o + rowst] = ez_n;
-      if (do_check) bad |= !(finite_small(hx1) && finite_small(hy1) && finite_small(ez_n));
-    }
-    ez_p = ez_n;
-    __syncthreads();
-  }
-  if (bad) atomicMin(bad_step, (unsigned long long)step);
-}
-
-// ---------------------------------------------------------------------------
-// explicit E rows: E1[u] = E0[u] - c (sum_k W_k H0[col_k] + y) - cs J[step]
-// one thread per (row, member)
+// reduced blocks: one thread-block cluster per model.
 // ---------------------------------------------------------------------------
 template <typename T>
-struct RowsE {
-  int64_t n_rows;
-  const int32_t* e_comp;       // [n_rows]
-  const int64_t* e_off;        // [n_rows] storage offset (device index / B)
-  const Coef<T>* c;            // [n_rows]
-  const int64_t* rowptr;       // [n_rows+1]
-  const int32_t* h_comp;       // [nnz]
-  const int64_t* h_off;        // [nnz]
-  const T* w;                  // [nnz]
-  const int64_t* y_off;        // [n_rows] offset into y (block base + local*N + inst*B), -1 none
-  const int32_t* src;          // [n_rows] source index or -1
-  const T* cs;                 // [n_rows] source coefficient
-  const T* wave;               // [n_wave][n_src][B]
-  int64_t n_wave, n_src;
+struct RedModel {
+  int qe, qh, n_if, N;          // N = n_inst * B columns
+  const T* K;                   // [qe][qh]
+  const T* Mh;                  // [qh][qe + n_if]  = [K^T | S_E^T]
+  const T* SE;                  // [n_if][qh]
+  const T* ge;                  // [qe]
+  const T* gh;                  // [qh]
+  T* xh;                        // [qe + n_if][N]   = [e~ ; G]
+  T* h;                         // [qh][N]
+  T* y;                         // [n_if][N]
+  int n_g;                      // gather entries (interface rows of this model, all instances)
+  const int32_t* g_comp;
+  const int64_t* g_off;
+  const int64_t* g_dst;         // index into xh
 };
 
-template <typename T>
-__global__ void rows_e_kernel(RowsE<T> R, int B, const T* const* E0, T* const* E1, const T* const* H0,
-                              const T* __restrict__ y, const int64_t* __restrict__ d_step) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= R.n_rows * B) return;
-  const int64_t r = t / B;
-  const int b = (int)(t % B);
-  T acc = 0;
-  for (int64_t k = R.rowptr[r]; k < R.rowptr[r + 1]; ++k)
-    acc += R.w[k] * H0[R.h_comp[k]][R.h_off[k] * B + b];
-  const int64_t yo = R.y_off[r];
-  if (yo >= 0) acc += y[yo + b];
-  const int ec = R.e_comp[r];
-  const int64_t eo = R.e_off[r] * B + b;
-  T e = E0[ec][eo] - R.c[r].apply(acc);
-  const int s = R.src[r];
-  const int64_t step = *d_step;
-  if (s >= 0 && step < R.n_wave) e -= R.cs[r] * R.wave[(step * R.n_src + s) * B + b];
-  E1[ec][eo] = e;
-}
-
-// ---------------------------------------------------------------------------
-// small dense products for the reduced blocks:
-//   out[r][n] = beta * out[r][n] + alpha * g[r] * sum_c A[r][c] X[c][n],  n < N
-// one warp per row, A row-major (rows x cols), X [cols][N], N <= NB.
-// ---------------------------------------------------------------------------
-template <typename T, int NB>
-__global__ void gemv_rows_kernel(int rows, int cols, int N, const T* __restrict__ A,
-                                 const T* __restrict__ X, T* __restrict__ out,
-                                 const T* __restrict__ g, T g_scalar, T alpha, T beta,
-                                 const int64_t* __restrict__ d_step, int check_every, unsigned long long* bad_step) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= rows) return;
-  T acc[NB];
-#pragma unroll
-  for (int n = 0; n < NB; ++n) acc[n] = 0;
-  const T* a = A + (int64_t)warp * cols;
-  for (int c = lane; c < cols; c += 32) {
-    const T av = a[c];
-    const T* x = X + (int64_t)c * N;
-#pragma unroll
-    for (int n = 0; n < NB; ++n)
-      if (n < N) acc[n] += av * x[n];
-  }
-#pragma unroll
-  for (int n = 0; n < NB; ++n) {
-    T v = acc[n];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    acc[n] = v;
-  }
-  if (lane < N) {
-    T v = 0;
-#pragma unroll
-    for (int n = 0; n < NB; ++n)
-      if (n == lane) v = acc[n];
-    const T gr = g ? g[warp] : g_scalar;
-    T* o = out + (int64_t)warp * N + lane;
-    const T res = (beta == (T)0 ? (T)0 : beta * *o) + alpha * gr * v;
-    *o = res;
-    if (check_every > 0 && (*d_step % check_every) == 0 && !finite_small((double)res))
-      atomicMin(bad_step, (unsigned long long)*d_step);
-  }
-}
-
-// gather interface E values: G[l][inst*B + b] = E[comp][off*B + b]
-template <typename T>
-__global__ void gather_kernel(int64_t n, int B, const int32_t* __restrict__ comp, const int64_t* __restrict__ off,
-                              const int64_t* __restrict__ dst, T* const* E, T* __restrict__ G) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n * B) return;
-  const int64_t r = t / B;
-  const int b = (int)(t % B);
-  G[dst[r] + b] = E[comp[r]][off[r] * B + b];
-}
-
-// probes: one block; ring[(step % cap)][p][b]; then step += 1
 template <typename T>
 struct Probes {
   int n_probe;
   const int64_t* rowptr;
-  const int32_t* src;        // [terms] 0..5 coarse comp, 6 = e~ buffer, 7 = h~ buffer
-  const int64_t* off;        // [terms] element offset (coarse: storage offset, reduced: base index)
-  const int32_t* stride;     // [terms] multiplier for b (coarse: 1, reduced: 1)
+  const int32_t* src;           // [terms] 0..5 coarse comp, 6 = e~ buffer, 7 = h~ buffer
+  const int64_t* off;           // [terms] coarse: storage offset; reduced: element index
   const T* w;
+  const int32_t* owner;         // [n_probe] model whose cluster samples it (-1: cluster 0)
 };
 
 template <typename T>
-__global__ void probe_kernel(Probes<T> P, int B, const T* const* F, const T* const* RED,
-                             T* __restrict__ ring, int64_t cap, int64_t* d_step) {
-  const int64_t step = *d_step;
-  for (int t = threadIdx.x; t < P.n_probe * B; t += blockDim.x) {
-    const int p = t / B, b = t % B;
-    T acc = 0;
-    for (int64_t k = P.rowptr[p]; k < P.rowptr[p + 1]; ++k) {
-      const int s = P.src[k];
-      const T v = (s < 6) ? F[s][P.off[k] * B + b] : RED[s - 6][P.off[k] + b];
-      acc += P.w[k] * v;
+struct RedParams {
+  int n_models, B;
+  const RedModel<T>* models;
+  const T* red_base[2];         // base pointers of the e~ and h~ buffers (probes)
+  Fields<T> F;                  // coarse fields after the step (new parity)
+  Probes<T> pr;
+  T* ring;
+  int64_t cap;
+  int64_t* d_step;
+  unsigned int* done;
+  int check_every;
+  unsigned long long* bad_step;
+};
+
+// out[r][n] = beta out[r][n] + alpha g[r] sum_c A[r][c] X[c][n] for the rows of
+// this warp set (warp w handles rows w, w + nw, ...)
+template <typename T, int NB>
+__device__ __forceinline__ void warp_rows(int rows, int cols, int N, const T* __restrict__ A,
+                                          const T* __restrict__ X, T* __restrict__ out,
+                                          const T* __restrict__ g, T alpha, bool accumulate,
+                                          int w0, int nw, bool check, bool& bad) {
+  const int lane = threadIdx.x & 31;
+  for (int r = w0; r < rows; r += nw) {
+    T acc[NB];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) acc[n] = 0;
+    const T* a = A + (int64_t)r * cols;
+    for (int c = lane; c < cols; c += 32) {
+      const T av = a[c];
+      const T* x = X + (int64_t)c * N;
+#pragma unroll
+      for (int n = 0; n < NB; ++n)
+        if (n < N) acc[n] += av * x[n];
     }
-    ring[(step % cap) * (int64_t)P.n_probe * B + t] = acc;
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      T v = acc[n];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      acc[n] = v;
+    }
+    if (lane < N) {
+      T v = 0;
+#pragma unroll
+      for (int n = 0; n < NB; ++n)
+        if (n == lane) v = acc[n];
+      const T gr = g ? g[r] : (T)1;
+      T* o = out + (int64_t)r * N + lane;
+      const T res = (accumulate ? *o : (T)0) + alpha * gr * v;
+      *o = res;
+      if (check && !finite_small((double)res)) bad = true;
+    }
   }
+}
+
+template <typename T, int NB>
+__global__ void __launch_bounds__(256)
+reduced_cluster_kernel(RedParams<T> P) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int m = blockIdx.x / CL;
+  const int64_t step = *P.d_step;
+  const bool check = P.check_every > 0 && (step % P.check_every) == 0;
+  bool bad = false;
+  const int warps = blockDim.x >> 5;
+  const int w0 = rank * warps + (threadIdx.x >> 5);
+  const int nw = CL * warps;
+  const bool have = m < P.n_models;
+  RedModel<T> M;
+  if (have) M = P.models[m];
+  // a4: e~ -= G_e K~' h~^{n+1/2};   gather G = E_if^{n+1}
+  if (have) {
+    warp_rows<T, NB>(M.qe, M.qh, M.N, M.K, M.h, M.xh, M.ge, (T)-1, true, w0, nw, check, bad);
+    const int t0 = rank * blockDim.x + threadIdx.x;
+    for (int64_t t = t0; t < (int64_t)M.n_g * P.B; t += (int64_t)CL * blockDim.x) {
+      const int64_t r = t / P.B;
+      const int b = (int)(t % P.B);
+      M.xh[M.g_dst[r] + b] = P.F.f[M.g_comp[r]][M.g_off[r] * P.B + b];
+    }
+  }
+  __threadfence();
+  cl.sync();
+  // a6: h~ += G_h [K~'^T | S_E^T][e~ ; G]
+  if (have) warp_rows<T, NB>(M.qh, M.qe + M.n_if, M.N, M.Mh, M.xh, M.h, M.gh, (T)1, true, w0, nw, check, bad);
+  __threadfence();
+  cl.sync();
+  // y = S_E h~  (interface coupling of the next step)
+  if (have && M.n_if > 0)
+    warp_rows<T, NB>(M.n_if, M.qh, M.N, M.SE, M.h, M.y, (const T*)nullptr, (T)1, false, w0, nw, false, bad);
+  // a7: probes owned by this cluster (reduced states are final after the sync)
+  if (rank == 0) {
+    for (int t = threadIdx.x; t < P.pr.n_probe * P.B; t += blockDim.x) {
+      const int p = t / P.B, b = t % P.B;
+      const int ow = P.pr.owner[p];
+      if (!((ow < 0 && m == 0) || ow == m)) continue;
+      T acc = 0;
+      for (int64_t k = P.pr.rowptr[p]; k < P.pr.rowptr[p + 1]; ++k) {
+        const int s = P.pr.src[k];
+        const T v = (s < 6) ? P.F.f[s][P.pr.off[k] * P.B + b] : P.red_base[s - 6][P.pr.off[k] + b];
+        acc += P.pr.w[k] * v;
+      }
+      P.ring[(step % P.cap) * (int64_t)P.pr.n_probe * P.B + t] = acc;
+    }
+  }
+  if (bad) atomicMin(P.bad_step, (unsigned long long)step);
+  // the last CTA to finish advances the device step counter
   __syncthreads();
-  if (threadIdx.x == 0) *d_step = step + 1;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int prev = atomicAdd(P.done, 1u);
+    if (prev == gridDim.x - 1) {
+      *P.done = 0;
+      __threadfence();
+      *P.d_step = step + 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// grid-wide path for large reduced blocks (S_E of 10^5 x 10^3 and beyond)
+// ---------------------------------------------------------------------------
+template <typename T, int NB>
+__global__ void gemv_rows_kernel(int rows, int cols, int N, const T* __restrict__ A,
+                                 const T* __restrict__ X, T* __restrict__ out,
+                                 const T* __restrict__ g, T alpha, bool accumulate,
+                                 const int64_t* __restrict__ d_step, int check_every,
+                                 unsigned long long* bad_step) {
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  bool bad = false;
+  const bool check = check_every > 0 && (*d_step % check_every) == 0;
+  warp_rows<T, NB>(rows, cols, N, A, X, out, g, alpha, accumulate, w0, nw, check, bad);
+  if (bad) atomicMin(bad_step, (unsigned long long)*d_step);
+}
+
+template <typename T>
+__global__ void gather_kernel(int64_t n, int B, const int32_t* __restrict__ comp, const int64_t* __restrict__ off,
+                              const int64_t* __restrict__ dst, Fields<T> F, T* __restrict__ G) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * B) return;
+  const int64_t r = t / B;
+  const int b = (int)(t % B);
+  G[dst[r] + b] = F.f[comp[r]][off[r] * B + b];
 }
 
 }  // namespace fdtd

@@ -119,7 +119,7 @@ def load_library(path: str = LIB_PATH):
 EXPORTED_SYMBOLS = ("fdtd_create", "fdtd_step", "fdtd_probe", "fdtd_get_state", "fdtd_set_state",
                     "fdtd_sync", "fdtd_launch_count", "fdtd_profile", "fdtd_phase_times", "fdtd_destroy",
                     "fdtd_last_error", "fdtd_version")
-PHASES = ("rows_e", "reduced_e", "stencil", "gather", "reduced_h", "coupling_y", "probes")
+PHASES = ("stencil", "reduced", "reduced_grid")
 
 
 def _check(code):
