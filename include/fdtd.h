@@ -150,6 +150,7 @@ typedef struct fdtd_exec {
   int32_t check_every;      /* divergence check period in steps; 0 = off (default 100 if < 0) */
   int32_t graph_steps;      /* steps per captured CUDA graph (0 = no graphs; default 32 if < 0) */
   int64_t probe_capacity;   /* device probe ring in steps (0 = default 65536)                 */
+  int32_t reduced_form;     /* 0 auto, 1 fused update matrix, 2 leap-frog GEMVs  */
 } fdtd_exec;
 
 /* Validate, deep-copy and upload everything; zero initial state.

@@ -1,5 +1,13 @@
 // fdtd_api.cu — the C ABI of include/fdtd.h: validation, upload, step
 // orchestration (eager launches or captured CUDA graphs), probes, state.
+//
+// Reduced blocks run in one of two forms:
+//  * fused   (small blocks): the three leap-frog half-updates of a step,
+//            h~' = h~ + G_h(K~'^T e~ + S_E^T G), y' = S_E h~', e~'' = e~' - G_e K~' h~'
+//            are composed on the host (fp64) into one update matrix applied by a
+//            single GEMV phase per step (identical in exact arithmetic);
+//  * leapfrog (large blocks, S_E of 10^5 rows): grid-wide GEMV launches in the
+//            paper's order.
 #include "../../include/fdtd.h"
 #include "kernels.cuh"
 
@@ -93,17 +101,21 @@ struct DevMem {
   }
 };
 
+// per reduced model
 template <typename T>
 struct BlockDev {
-  int qe, qh, n_inst, n_if, N;
-  T* K = nullptr;        // [qe][qh]
-  T* Mh = nullptr;       // [qh][qe + n_if] = [K^T | S_E^T]
-  T* SE = nullptr;       // [n_if][qh]
-  T* ge = nullptr;       // [qe]
-  T* gh = nullptr;       // [qh]
-  int64_t xh_off = 0;    // offset of this block's X_h = [e~ ; G] in xh_all ([qe+n_if][N])
-  int64_t h_off = 0;     // offset in h_all ([qh][N])
-  int64_t y_off = 0;     // offset in y_all ([n_if][N])
+  int qe = 0, qh = 0, n_inst = 0, n_if = 0, N = 0;
+  bool fused = false;
+  // host fp64 copies (for the prologue and the fused matrix)
+  std::vector<double> K, SE, ge, gh;
+  // leapfrog path matrices
+  T *K_d = nullptr, *KT_d = nullptr, *SE_d = nullptr, *SET_d = nullptr, *ge_d = nullptr, *gh_d = nullptr;
+  // state offsets (elements) in the concatenated buffers
+  int64_t e_off = 0, h_off = 0, y_off = 0;     // e/h buffers [q][N], y / G [n_if][N]
+  // fused path
+  T* M_d = nullptr;                            // [R_M][C_M]
+  int R_M = 0, C_M = 0;
+  std::vector<int> probe_rows;                 // global probe ids realised as rows of M
 };
 
 template <typename T>
@@ -116,7 +128,6 @@ struct Impl : public fdtd_t {
   int64_t elems = 0;      // device elements per component (plane*nplanes*B)
   cudaStream_t stream = nullptr;
   DevMem mem;
-  // fields: F[parity][comp]
   T* F[2][6] = {{nullptr}};
   // materials
   bool uniform = true;
@@ -127,42 +138,46 @@ struct Impl : public fdtd_t {
   fdtd::Coef<T> u0{}, u1{};
   // explicit rows
   fdtd::RowsE<T> rows{};
-  // blocks
+  // reduced blocks
   std::vector<BlockDev<T>> blocks;
-  T* xh_all = nullptr;
-  T* h_all = nullptr;
+  bool any_fused = false, any_leap = false;
+  T* eb[2] = {nullptr, nullptr};      // e~ (fused: [state, ahead] by parity; leapfrog: eb[0])
+  T* hb[2] = {nullptr, nullptr};      // h~ (fused: by parity; leapfrog: hb[0])
   T* y_all = nullptr;
-  int64_t xh_size = 0, h_size = 0, y_size = 0;
+  T* g_all = nullptr;                 // gathered interface E (leapfrog path)
+  int64_t e_size = 0, h_size = 0, y_size = 0;
+  // gather lists: per block, (comp, storage offset, dst index in [n_if][N])
   int64_t n_gather = 0;
   int32_t* g_comp = nullptr;
   int64_t* g_off = nullptr;
   int64_t* g_dst = nullptr;
-  std::vector<fdtd::RedModel<T>> models;    // device descriptors (host copy)
-  fdtd::RedModel<T>* d_models = nullptr;
-  bool grid_path = false;             // large blocks: grid-wide gemv launches
-  int CL = 8;                         // cluster size of the reduced kernel
-  int NBsel = 1;                      // columns per row template (>= max N)
-  unsigned int* d_done = nullptr;
+  // fused kernel work decomposition
+  fdtd::FusedBlock<T>* d_fblocks = nullptr;
+  int2* d_ctas = nullptr;             // (fused block, first row) per CTA
+  int n_ctas = 0, NBsel = 1, max_cols = 0;
+  size_t fused_smem = 0;
   // probes
   fdtd::Probes<T> pr{};
   int n_probe = 0;
   T* ring = nullptr;
   int64_t cap = 65536;
-  std::vector<double> host_probes;    // drained samples [step][probe][B]
-  int64_t drained_to = 0;             // absolute step up to which the ring was drained
+  std::vector<double> host_probes;
+  int64_t drained_to = 0;
   // control
   int64_t* d_step = nullptr;
   unsigned long long* d_bad = nullptr;
-  int64_t host_step = 0;              // steps enqueued
+  unsigned int* d_done = nullptr;
+  int64_t host_step = 0;
   int check_every = 100;
   int graph_steps = 32;
   cudaGraphExec_t graph = nullptr;
   int64_t graph_kernels = 0;
-  T* staging = nullptr;               // pinned host staging
+  T* staging = nullptr;
   size_t staging_bytes = 0;
   int kchunk = 16;
-  // per-phase tracing (CUDA events around each kernel group, eager launches)
-  static constexpr int NPHASE = 3;       // stencil (+ explicit rows), reduced (+ probes), grid-path extras
+  int reduced_form = 0;
+  // per-phase tracing
+  static constexpr int NPHASE = 3;       // stencil (+ explicit rows), reduced (+ probes), leapfrog GEMVs
   bool prof = false;
   cudaEvent_t ev[2 * NPHASE] = {};
   double phase_ms[NPHASE] = {0};
@@ -184,7 +199,7 @@ struct Impl : public fdtd_t {
   int phase_times(double* ms, int n) override {
     for (int i = 0; i < n && i < NPHASE; ++i) ms[i] = phase_n[i] ? phase_ms[i] : 0.0;
     for (int i = NPHASE; i < n; ++i) ms[i] = 0.0;
-    if (n > NPHASE) ms[NPHASE] = (double)(phase_n[0]);
+    if (n > NPHASE) ms[NPHASE] = (double)phase_n[0];
     return FDTD_OK;
   }
 
@@ -192,15 +207,18 @@ struct Impl : public fdtd_t {
   U* dalloc(int64_t count) {
     return reinterpret_cast<U*>(mem.get(sizeof(U) * (size_t)count));
   }
+  template <typename V>
+  int upload(void* dst, const std::vector<V>& v) {
+    if (!v.empty()) CK(cudaMemcpy(dst, v.data(), sizeof(V) * v.size(), cudaMemcpyHostToDevice));
+    return FDTD_OK;
+  }
 
   int64_t dev_off(int64_t s) const {   // storage index -> device storage offset (before *B)
-    int64_t i, j, k;
+    int64_t i = s % (nx + 1), j, k;
     if (dim == 3) {
-      i = s % (nx + 1);
       j = (s / (nx + 1)) % (ny + 1);
       k = s / ((int64_t)(nx + 1) * (ny + 1));
     } else {
-      i = s % (nx + 1);
       j = s / (nx + 1);
       k = 0;
     }
@@ -210,9 +228,18 @@ struct Impl : public fdtd_t {
   bool is_e(int c) const { return dim == 3 ? (c >= 0 && c <= 2) : c == 2; }
   bool is_h(int c) const { return dim == 3 ? (c >= 3 && c <= 5) : (c == 3 || c == 4); }
 
+  // reduced-state pointers for host access: a fused block keeps
+  // e~ one step ahead, so after s steps e~^s = eb[(s+1)&1], e~^{s+1} = eb[s&1],
+  // h~^{s+1/2} = hb[s&1]; a leap-frog block updates eb[0] / hb[0] in place.
+  T* e_state(const BlockDev<T>& D, int64_t s) const { return (D.fused ? eb[(s + 1) & 1] : eb[0]) + D.e_off; }
+  T* e_ahead(const BlockDev<T>& D, int64_t s) const { return eb[s & 1] + D.e_off; }
+  T* h_state(const BlockDev<T>& D, int64_t s) const { return (D.fused ? hb[s & 1] : hb[0]) + D.h_off; }
+
   int create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_interface* itf,
              const fdtd_reduced_block* bl, int n_blocks, const fdtd_sources* src,
              const fdtd_probes* probes, const fdtd_exec* ex);
+  int build_fused(const fdtd_probes* probes);
+  int prologue(cudaStream_t st);
   int launch_step(int parity, cudaStream_t st, int64_t* count, bool profile = false);
   int step(int64_t n) override;
   int drain();
@@ -222,6 +249,23 @@ struct Impl : public fdtd_t {
   int sync() override;
   int check_async();
 };
+
+template <typename T>
+static int launch_gemv(int rows, int cols, int N, const T* A, const T* X, T* out, const T* g, T alpha,
+                       bool accumulate, const int64_t* d_step, int check_every, unsigned long long* bad,
+                       cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return 0;
+  const int threads = 256;
+  const int blocks = std::min((rows * 32 + threads - 1) / threads, 148 * 16);
+#define FDTD_GEMV(NB) fdtd::gemv_rows_kernel<T, NB><<<blocks, threads, 0, st>>>(rows, cols, N, A, X, out, g, alpha, accumulate, d_step, check_every, bad)
+  if (N <= 1) FDTD_GEMV(1);
+  else if (N <= 4) FDTD_GEMV(4);
+  else if (N <= 16) FDTD_GEMV(16);
+  else if (N <= 32) FDTD_GEMV(32);
+  else return -1;
+#undef FDTD_GEMV
+  return 1;
+}
 
 template <typename T>
 int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_interface* itf,
@@ -237,6 +281,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     graph_steps = ex->graph_steps < 0 ? 32 : ex->graph_steps;
     if (graph_steps % 2) graph_steps += 1;
     if (ex->probe_capacity > 0) cap = ex->probe_capacity;
+    reduced_form = ex->reduced_form;
   }
   px = (B == 1) ? ((nx + 1 + 31) / 32) * 32 : (nx + 1);
   plane = (int64_t)(ny + 1) * px;
@@ -256,7 +301,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   // ---- materials ----
   std::vector<double> coef;           // [n_mat][6]
   std::vector<uint8_t> ifmask;
-  std::vector<uint8_t> ids;           // storage-indexed (unpadded), built lazily
+  std::vector<uint8_t> ids;           // storage-indexed (unpadded)
   uniform = (mat == nullptr || mat->n_mat == 0);
   if (!uniform) {
     if (mat->n_mat > 256 || !mat->mat_id || !mat->coef || !mat->if_mask)
@@ -277,9 +322,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   auto ensure_table = [&]() {
     if (uniform) { uniform = false; ids.assign(S, 0); }
   };
-  auto mat_coef = [&](int64_t s, int c) -> double {
-    return coef[(uniform ? 0 : ids[s]) * 6 + c];
-  };
+  auto mat_coef = [&](int64_t s, int c) -> double { return coef[(uniform ? 0 : ids[s]) * 6 + c]; };
   auto storage_ijk = [&](int64_t s, int& i, int& j, int& k) {
     i = (int)(s % (nx + 1));
     if (dim == 3) { j = (int)((s / (nx + 1)) % (ny + 1)); k = (int)(s / ((int64_t)(nx + 1) * (ny + 1))); }
@@ -289,7 +332,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     return dim == 3 ? ((int64_t)k * (ny + 1) + j) * (nx + 1) + i : (int64_t)j * (nx + 1) + i;
   };
 
-  // ---- blocks ----
+  // ---- reduced blocks ----
   if (n_blocks < 0 || (n_blocks > 0 && !bl)) return fail(FDTD_EINVAL, "blocks: n_blocks/pointer mismatch");
   blocks.resize(n_blocks);
   for (int b = 0; b < n_blocks; ++b) {
@@ -298,36 +341,56 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     if (R.qe < 1 || R.qh < 1 || R.n_inst < 1 || R.n_if < 0 || !R.K || (R.n_if > 0 && !R.S_E))
       return fail(FDTD_EINVAL, "block %d: q < 1, n_inst < 1 or missing matrices", b);
     D.qe = R.qe; D.qh = R.qh; D.n_inst = R.n_inst; D.n_if = R.n_if; D.N = R.n_inst * B;
-    D.xh_off = xh_size; xh_size += (int64_t)(D.qe + D.n_if) * D.N;
+    if (D.N > 32) return fail(FDTD_ENOTSUP, "block %d: n_inst*batch = %d > 32 not supported", b, D.N);
+    D.e_off = e_size; e_size += (int64_t)D.qe * D.N;
     D.h_off = h_size; h_size += (int64_t)D.qh * D.N;
     D.y_off = y_size; y_size += (int64_t)D.n_if * D.N;
-    std::vector<T> K((size_t)D.qe * D.qh), Mh((size_t)D.qh * (D.qe + D.n_if)), SE((size_t)D.n_if * D.qh);
+    D.K.assign(R.K, R.K + (size_t)D.qe * D.qh);
+    if (D.n_if) D.SE.assign(R.S_E, R.S_E + (size_t)D.n_if * D.qh);
+    D.ge.resize(D.qe); D.gh.resize(D.qh);
+    for (int r = 0; r < D.qe; ++r) D.ge[r] = R.g_e ? R.g_e[r] : R.g_e_scalar;
+    for (int r = 0; r < D.qh; ++r) D.gh[r] = R.g_h ? R.g_h[r] : R.g_h_scalar;
+    const int64_t RM = (int64_t)D.qh + D.n_if + D.qe, CM = (int64_t)D.qe + D.n_if + D.qh;
+    D.fused = RM * CM <= (int64_t)6 * 1024 * 1024 && CM * D.N * (int64_t)sizeof(T) <= 160 * 1024;
+    if (reduced_form == 1 && !D.fused) return fail(FDTD_ENOTSUP, "block %d too large for the fused form", b);
+    if (reduced_form == 2) D.fused = false;
+    any_fused |= D.fused;
+    any_leap |= !D.fused;
+    // leapfrog matrices (also used for the prologue gemv e~ -= G_e K~' h~)
+    std::vector<T> K((size_t)D.qe * D.qh), KT((size_t)D.qh * D.qe), SE((size_t)D.n_if * D.qh),
+        SET((size_t)D.qh * D.n_if), ge(D.qe), gh(D.qh);
     for (int r = 0; r < D.qe; ++r)
       for (int c = 0; c < D.qh; ++c) {
-        K[(size_t)r * D.qh + c] = (T)R.K[(size_t)r * D.qh + c];
-        Mh[(size_t)c * (D.qe + D.n_if) + r] = (T)R.K[(size_t)r * D.qh + c];
+        K[(size_t)r * D.qh + c] = (T)D.K[(size_t)r * D.qh + c];
+        KT[(size_t)c * D.qe + r] = (T)D.K[(size_t)r * D.qh + c];
       }
     for (int r = 0; r < D.n_if; ++r)
       for (int c = 0; c < D.qh; ++c) {
-        SE[(size_t)r * D.qh + c] = (T)R.S_E[(size_t)r * D.qh + c];
-        Mh[(size_t)c * (D.qe + D.n_if) + D.qe + r] = (T)R.S_E[(size_t)r * D.qh + c];
+        SE[(size_t)r * D.qh + c] = (T)D.SE[(size_t)r * D.qh + c];
+        SET[(size_t)c * D.n_if + r] = (T)D.SE[(size_t)r * D.qh + c];
       }
-    std::vector<T> ge(D.qe), gh(D.qh);
-    for (int r = 0; r < D.qe; ++r) ge[r] = (T)(R.g_e ? R.g_e[r] : R.g_e_scalar);
-    for (int r = 0; r < D.qh; ++r) gh[r] = (T)(R.g_h ? R.g_h[r] : R.g_h_scalar);
-    D.K = dalloc<T>(K.size()); D.Mh = dalloc<T>(Mh.size()); D.SE = dalloc<T>(SE.size());
-    D.ge = dalloc<T>(D.qe); D.gh = dalloc<T>(D.qh);
-    if (!D.K || !D.Mh || !D.SE || !D.ge || !D.gh) return fail(FDTD_ENOMEM, "block %d allocation failed", b);
-    CK(cudaMemcpy(D.K, K.data(), sizeof(T) * K.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(D.Mh, Mh.data(), sizeof(T) * Mh.size(), cudaMemcpyHostToDevice));
-    if (!SE.empty()) CK(cudaMemcpy(D.SE, SE.data(), sizeof(T) * SE.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(D.ge, ge.data(), sizeof(T) * ge.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(D.gh, gh.data(), sizeof(T) * gh.size(), cudaMemcpyHostToDevice));
+    for (int r = 0; r < D.qe; ++r) ge[r] = (T)D.ge[r];
+    for (int r = 0; r < D.qh; ++r) gh[r] = (T)D.gh[r];
+    D.K_d = dalloc<T>(K.size()); D.ge_d = dalloc<T>(D.qe); D.gh_d = dalloc<T>(D.qh);
+    D.SE_d = dalloc<T>(std::max<size_t>(SE.size(), 1));
+    if (!D.K_d || !D.ge_d || !D.gh_d || !D.SE_d) return fail(FDTD_ENOMEM, "block %d allocation failed", b);
+    if (upload(D.K_d, K) || upload(D.ge_d, ge) || upload(D.gh_d, gh) || upload(D.SE_d, SE)) return FDTD_ECUDA;
+    if (!D.fused) {
+      D.KT_d = dalloc<T>(KT.size()); D.SET_d = dalloc<T>(std::max<size_t>(SET.size(), 1));
+      if (!D.KT_d || !D.SET_d) return fail(FDTD_ENOMEM, "block %d allocation failed", b);
+      if (upload(D.KT_d, KT) || upload(D.SET_d, SET)) return FDTD_ECUDA;
+    }
   }
-  xh_all = dalloc<T>(xh_size); h_all = dalloc<T>(h_size); y_all = dalloc<T>(y_size);
-  CK(cudaMemsetAsync(xh_all, 0, sizeof(T) * std::max<int64_t>(xh_size, 1), stream));
-  CK(cudaMemsetAsync(h_all, 0, sizeof(T) * std::max<int64_t>(h_size, 1), stream));
+  for (int p = 0; p < 2; ++p) {
+    eb[p] = dalloc<T>(std::max<int64_t>(e_size, 1));
+    hb[p] = dalloc<T>(std::max<int64_t>(h_size, 1));
+    CK(cudaMemsetAsync(eb[p], 0, sizeof(T) * std::max<int64_t>(e_size, 1), stream));
+    CK(cudaMemsetAsync(hb[p], 0, sizeof(T) * std::max<int64_t>(h_size, 1), stream));
+  }
+  y_all = dalloc<T>(std::max<int64_t>(y_size, 1));
+  g_all = dalloc<T>(std::max<int64_t>(y_size, 1));
   CK(cudaMemsetAsync(y_all, 0, sizeof(T) * std::max<int64_t>(y_size, 1), stream));
+  CK(cudaMemsetAsync(g_all, 0, sizeof(T) * std::max<int64_t>(y_size, 1), stream));
 
   // ---- explicit rows: interface rows, then source rows on regular unknowns ----
   struct HRow { std::vector<std::pair<int64_t, double>> w; double c = 0; int64_t y = -1; int src = -1; double cs = 0; int comp = 0; int64_t s = 0; };
@@ -361,7 +424,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       row_of[u] = (int)hrows.size();
       hrows.push_back(h);
       gcomp.push_back(c); goff.push_back(dev_off(s)); gblk.push_back(b);
-      gdst.push_back(D.xh_off + (int64_t)(D.qe + l) * D.N + (int64_t)in * B);
+      gdst.push_back((int64_t)l * D.N + (int64_t)in * B);        // within the block's [n_if][N]
     }
   }
   int64_t n_src = 0, n_wave = 0;
@@ -403,7 +466,6 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       }
       row_of[u] = (int)hrows.size();
       hrows.push_back(h);
-      // mark the unknown as explicit: new material = old + if bit
       ensure_table();
       const int old = ids[s];
       std::vector<double> nc(coef.begin() + old * 6, coef.begin() + old * 6 + 6);
@@ -425,14 +487,13 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     std::vector<uint8_t> padded((size_t)(plane * nplanes), 0);
     for (int64_t s = 0; s < S; ++s) padded[dev_off(s)] = ids[s];
     mat_id = dalloc<uint8_t>(padded.size());
-    CK(cudaMemcpy(mat_id, padded.data(), padded.size(), cudaMemcpyHostToDevice));
     std::vector<fdtd::Coef<T>> tb((size_t)n_mat * 6);
     for (int m = 0; m < n_mat; ++m)
       for (int c = 0; c < 6; ++c) tb[(size_t)m * 6 + c] = make_coef<T>(coef[(size_t)m * 6 + c]);
     tab = dalloc<fdtd::Coef<T>>(tb.size());
     ifm = dalloc<uint8_t>(n_mat);
-    CK(cudaMemcpy(tab, tb.data(), sizeof(fdtd::Coef<T>) * tb.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ifm, ifmask.data(), n_mat, cudaMemcpyHostToDevice));
+    if (!mat_id || !tab || !ifm) return fail(FDTD_ENOMEM, "material allocation failed");
+    if (upload(mat_id, padded) || upload(tab, tb) || upload(ifm, ifmask)) return FDTD_ECUDA;
   } else {
     u0 = make_coef<T>(coef[dim == 3 ? 0 : 2]);
     u1 = make_coef<T>(coef[3]);
@@ -454,17 +515,10 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       ec[r] = h.comp; eo[r] = dev_off(h.s); cc[r] = make_coef<T>(h.c);
       yo[r] = h.y; srcv[r] = h.src; cs[r] = (T)h.cs;
       for (auto& pw : h.w) {
-        const int hcmp = (int)(pw.first / S);
-        const int64_t hs = pw.first % S;
-        hc.push_back(hcmp); ho.push_back(dev_off(hs)); w.push_back((T)pw.second);
+        hc.push_back((int)(pw.first / S)); ho.push_back(dev_off(pw.first % S)); w.push_back((T)pw.second);
       }
       rp[r + 1] = (int64_t)w.size();
     }
-    auto up = [&](auto* dst, const auto& v) -> int {
-      if (v.empty()) return 0;
-      CK(cudaMemcpy(dst, v.data(), sizeof(v[0]) * v.size(), cudaMemcpyHostToDevice));
-      return 0;
-    };
     int32_t* d_ec = dalloc<int32_t>(std::max<int64_t>(nr, 1));
     int64_t* d_eo = dalloc<int64_t>(std::max<int64_t>(nr, 1));
     fdtd::Coef<T>* d_c = dalloc<fdtd::Coef<T>>(std::max<int64_t>(nr, 1));
@@ -476,14 +530,12 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     int32_t* d_src = dalloc<int32_t>(std::max<int64_t>(nr, 1));
     T* d_cs = dalloc<T>(std::max<int64_t>(nr, 1));
     T* d_wave = dalloc<T>(std::max<size_t>(wave.size(), 1));
-    int e = 0;
-    e |= up(d_ec, ec); e |= up(d_eo, eo); e |= up(d_c, cc); e |= up(d_rp, rp); e |= up(d_hc, hc);
-    e |= up(d_ho, ho); e |= up(d_w, w); e |= up(d_yo, yo); e |= up(d_src, srcv); e |= up(d_cs, cs);
-    e |= up(d_wave, wave);
-    if (e) return e;
+    if (upload(d_ec, ec) || upload(d_eo, eo) || upload(d_c, cc) || upload(d_rp, rp) || upload(d_hc, hc) ||
+        upload(d_ho, ho) || upload(d_w, w) || upload(d_yo, yo) || upload(d_src, srcv) || upload(d_cs, cs) ||
+        upload(d_wave, wave))
+      return FDTD_ECUDA;
     rows.e_comp = d_ec; rows.e_off = d_eo; rows.c = d_c; rows.rowptr = d_rp; rows.h_comp = d_hc;
     rows.h_off = d_ho; rows.w = d_w; rows.y_off = d_yo; rows.src = d_src; rows.cs = d_cs; rows.wave = d_wave;
-    // dense row maps (storage offset -> explicit row) for the components that have rows
     for (int c = 0; c < 3; ++c) rows.row_of[c] = nullptr;
     for (int c = 0; c < 3; ++c) {
       bool any = false;
@@ -494,102 +546,78 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
         if (ec[r] == c) mp[eo[r]] = (int32_t)r;
       int32_t* d_mp = dalloc<int32_t>(mp.size());
       if (!d_mp) return fail(FDTD_ENOMEM, "row map allocation failed");
-      e |= up(d_mp, mp);
+      if (upload(d_mp, mp)) return FDTD_ECUDA;
       rows.row_of[c] = d_mp;
     }
-    if (e) return e;
-    // per-block gather lists (G rows of the reduced chain)
-    std::vector<std::vector<int32_t>> bc(n_blocks);
-    std::vector<std::vector<int64_t>> bo(n_blocks), bd(n_blocks);
-    for (size_t q = 0; q < gcomp.size(); ++q) {
-      bc[gblk[q]].push_back(gcomp[q]); bo[gblk[q]].push_back(goff[q]); bd[gblk[q]].push_back(gdst[q]);
+    // gather lists (ordered by block), destinations relative to each block's [n_if][N]
+    std::vector<int32_t> gc2;
+    std::vector<int64_t> go2, gd2;
+    for (int b = 0; b < n_blocks; ++b) {
+      blocks[b].probe_rows.clear();
+      for (size_t q = 0; q < gcomp.size(); ++q)
+        if (gblk[q] == b) { gc2.push_back(gcomp[q]); go2.push_back(goff[q]); gd2.push_back(blocks[b].y_off + gdst[q]); }
     }
-    n_gather = (int64_t)gcomp.size();
+    n_gather = (int64_t)gc2.size();
     g_comp = dalloc<int32_t>(std::max<int64_t>(n_gather, 1));
     g_off = dalloc<int64_t>(std::max<int64_t>(n_gather, 1));
     g_dst = dalloc<int64_t>(std::max<int64_t>(n_gather, 1));
-    e |= up(g_comp, gcomp); e |= up(g_off, goff); e |= up(g_dst, gdst);
-    if (e) return e;
-    // reduced-model descriptors
-    int64_t big = 0;
-    int maxN = 1;
-    for (int b = 0; b < n_blocks; ++b) {
-      BlockDev<T>& D = blocks[b];
-      fdtd::RedModel<T> M{};
-      M.qe = D.qe; M.qh = D.qh; M.n_if = D.n_if; M.N = D.N;
-      M.K = D.K; M.Mh = D.Mh; M.SE = D.SE; M.ge = D.ge; M.gh = D.gh;
-      M.xh = xh_all + D.xh_off; M.h = h_all + D.h_off; M.y = y_all + D.y_off;
-      M.n_g = (int)bc[b].size();
-      int32_t* c1 = dalloc<int32_t>(std::max<size_t>(bc[b].size(), 1));
-      int64_t* o1 = dalloc<int64_t>(std::max<size_t>(bo[b].size(), 1));
-      int64_t* d1 = dalloc<int64_t>(std::max<size_t>(bd[b].size(), 1));
-      for (auto& v : bd[b]) v -= D.xh_off;          // index into this model's xh
-      e |= up(c1, bc[b]); e |= up(o1, bo[b]); e |= up(d1, bd[b]);
-      M.g_comp = c1; M.g_off = o1; M.g_dst = d1;
-      models.push_back(M);
-      big = std::max<int64_t>(big, (int64_t)D.qh * (D.qe + D.n_if));
-      maxN = std::max(maxN, D.N);
-    }
-    if (e) return e;
-    if (maxN > 32) return fail(FDTD_ENOTSUP, "n_inst*batch > 32 per block not supported in this version");
-    NBsel = maxN <= 1 ? 1 : maxN <= 4 ? 4 : maxN <= 16 ? 16 : 32;
-    grid_path = big > (int64_t)4 * 1024 * 1024;      // > 16 MB fp32 of matrices per model
-    d_models = dalloc<fdtd::RedModel<T>>(std::max<size_t>(models.size(), 1));
-    if (!models.empty())
-      CK(cudaMemcpy(d_models, models.data(), sizeof(fdtd::RedModel<T>) * models.size(), cudaMemcpyHostToDevice));
+    if (upload(g_comp, gc2) || upload(g_off, go2) || upload(g_dst, gd2)) return FDTD_ECUDA;
   }
 
-  // ---- probes ----
+  // ---- probes: coarse terms and leapfrog-path reduced terms; fused-path
+  // reduced probes become rows of the fused update matrix ----
   {
     std::vector<int64_t> rp(1, 0), off;
-    std::vector<int32_t> srcv, strd, owner;
+    std::vector<int32_t> srcv, owner;
     std::vector<T> w;
     n_probe = probes ? (int)probes->n_probe : 0;
     for (int p = 0; p < n_probe; ++p) {
       const int kind = probes->kind[p];
-      bool any_e = false, any_h = false;
+      bool any_e = false, any_h = false, as_row = false;
+      if (kind == 1 || kind == 2) {
+        const int b = probes->block[p], in = probes->inst[p];
+        if (b < 0 || b >= n_blocks || in < 0 || in >= blocks[b].n_inst) return fail(FDTD_EINVAL, "probe %d: bad block/inst", p);
+        as_row = blocks[b].fused;
+        if (as_row) blocks[b].probe_rows.push_back(p);
+      } else if (kind != 0) {
+        return fail(FDTD_EINVAL, "probe %d: unknown kind %d", p, kind);
+      }
       for (int64_t k = probes->rowptr[p]; k < probes->rowptr[p + 1]; ++k) {
         const int64_t idx = probes->index[k];
         if (kind == 0) {
           const int c = (int)(idx / S);
           if (idx < 0 || idx >= 6 * S || !(is_e(c) || is_h(c))) return fail(FDTD_ESTAMP, "probe %d: bad unknown %lld", p, (long long)idx);
           any_e |= is_e(c); any_h |= is_h(c);
-          srcv.push_back(c); off.push_back(dev_off(idx % S));
-        } else if (kind == 1 || kind == 2) {
-          const int b = probes->block[p], in = probes->inst[p];
-          if (b < 0 || b >= n_blocks || in < 0 || in >= blocks[b].n_inst) return fail(FDTD_EINVAL, "probe %d: bad block/inst", p);
-          const BlockDev<T>& D = blocks[b];
+          srcv.push_back(c); off.push_back(dev_off(idx % S)); w.push_back((T)probes->weight[k]);
+        } else {
+          const BlockDev<T>& D = blocks[probes->block[p]];
           const int q = kind == 1 ? D.qe : D.qh;
           if (idx < 0 || idx >= q) return fail(FDTD_ESTAMP, "probe %d: reduced index out of range", p);
-          srcv.push_back(kind == 1 ? 6 : 7);
-          off.push_back((kind == 1 ? D.xh_off : D.h_off) + idx * D.N + (int64_t)in * B);
-        } else {
-          return fail(FDTD_EINVAL, "probe %d: unknown kind %d", p, kind);
+          if (!as_row) {
+            srcv.push_back(kind == 1 ? 6 : 7);
+            off.push_back((kind == 1 ? D.e_off : D.h_off) + idx * D.N + (int64_t)probes->inst[p] * B);
+            w.push_back((T)probes->weight[k]);
+          }
         }
-        strd.push_back(1);
-        w.push_back((T)probes->weight[k]);
       }
       if (any_e && any_h) return fail(FDTD_EINVAL, "probe %d mixes E and H unknowns", p);
-      owner.push_back((kind == 0 || grid_path) ? -1 : probes->block[p]);
+      owner.push_back(as_row ? -2 : -1);      // -1: sampled by the reduced kernel's CTA 0
       rp.push_back((int64_t)w.size());
     }
     int64_t* d_rp = dalloc<int64_t>(rp.size());
     int32_t* d_src = dalloc<int32_t>(std::max<size_t>(srcv.size(), 1));
     int64_t* d_off = dalloc<int64_t>(std::max<size_t>(off.size(), 1));
-    int32_t* d_st = dalloc<int32_t>(std::max<size_t>(strd.size(), 1));
-    int32_t* d_ow = dalloc<int32_t>(std::max<size_t>(owner.size(), 1));
-    if (!owner.empty()) CK(cudaMemcpy(d_ow, owner.data(), sizeof(int32_t) * owner.size(), cudaMemcpyHostToDevice));
     T* d_w = dalloc<T>(std::max<size_t>(w.size(), 1));
-    CK(cudaMemcpy(d_rp, rp.data(), sizeof(int64_t) * rp.size(), cudaMemcpyHostToDevice));
-    if (!srcv.empty()) {
-      CK(cudaMemcpy(d_src, srcv.data(), sizeof(int32_t) * srcv.size(), cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(d_off, off.data(), sizeof(int64_t) * off.size(), cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(d_st, strd.data(), sizeof(int32_t) * strd.size(), cudaMemcpyHostToDevice));
-      CK(cudaMemcpy(d_w, w.data(), sizeof(T) * w.size(), cudaMemcpyHostToDevice));
-    }
+    int32_t* d_ow = dalloc<int32_t>(std::max<size_t>(owner.size(), 1));
+    if (upload(d_rp, rp) || upload(d_src, srcv) || upload(d_off, off) || upload(d_w, w) || upload(d_ow, owner))
+      return FDTD_ECUDA;
     pr.n_probe = n_probe; pr.rowptr = d_rp; pr.src = d_src; pr.off = d_off; pr.w = d_w; pr.owner = d_ow;
     ring = dalloc<T>(std::max<int64_t>(cap * n_probe * B, 1));
     if (!ring) return fail(FDTD_ENOMEM, "probe ring allocation failed");
+  }
+  if (any_fused) {
+    int e = build_fused(probes);
+    if (e) return e;
   }
   d_step = dalloc<int64_t>(1);
   d_bad = dalloc<unsigned long long>(1);
@@ -597,50 +625,152 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   CK(cudaMemsetAsync(d_done, 0, sizeof(unsigned int), stream));
   CK(cudaMemsetAsync(d_step, 0, sizeof(int64_t), stream));
   CK(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), stream));
-  staging_bytes = sizeof(T) * (size_t)std::max<int64_t>(elems, std::max(xh_size, h_size));
+  staging_bytes = sizeof(T) * (size_t)std::max<int64_t>(elems, std::max(e_size, h_size));
   CK(cudaMallocHost(&staging, staging_bytes));
-  // shared memory opt-in (material table + plane buffers)
   const size_t smem3 = 2 * 3 * 1024 * sizeof(T) + sizeof(fdtd::MatTable<T>);
   CK(cudaFuncSetAttribute(fdtd::stencil3d_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   CK(cudaFuncSetAttribute(fdtd::stencil3d_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
-  CK(cudaFuncSetAttribute(fdtd::stencil2d_tile_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
-  CK(cudaFuncSetAttribute(fdtd::stencil2d_tile_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  CK(cudaFuncSetAttribute(fdtd::stencil2d_rows_kernel<T, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  CK(cudaFuncSetAttribute(fdtd::stencil2d_rows_kernel<T, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  if (fused_smem > 48 * 1024) {
+    CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+    CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+    CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+    CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+  }
   CK(cudaStreamSynchronize(stream));
   return FDTD_OK;
 }
 
+// Compose each small block's step into one update matrix (host, fp64):
+//   columns [e~ (qe) ; G (n_if) ; h~ (qh)],   A1 = G_h K^T,  A2 = G_h S_E^T
+//   rows    h~'  = [ A1          , A2          , I     ]
+//           y'   = [ S_E A1      , S_E A2      , S_E   ]
+//           e~'' = [ I - G_e K A1, -G_e K A2   , -G_e K]
+//           probe rows: E probe [v^T, 0, 0];  H probe v^T [A1, A2, I]
 template <typename T>
-static int launch_gemv(int rows, int cols, int N, const T* A, const T* X, T* out, const T* g, T alpha,
-                       bool accumulate, const int64_t* d_step, int check_every, unsigned long long* bad,
-                       cudaStream_t st) {
-  if (rows <= 0) return 0;
-  const int threads = 256;
-  const int blocks = std::min((rows * 32 + threads - 1) / threads, 148 * 8);
-#define FDTD_GEMV(NB) fdtd::gemv_rows_kernel<T, NB><<<blocks, threads, 0, st>>>(rows, cols, N, A, X, out, g, alpha, accumulate, d_step, check_every, bad)
-  if (N <= 1) FDTD_GEMV(1);
-  else if (N <= 4) FDTD_GEMV(4);
-  else if (N <= 16) FDTD_GEMV(16);
-  else if (N <= 32) FDTD_GEMV(32);
-  else return -1;
-#undef FDTD_GEMV
-  return 1;
+int Impl<T>::build_fused(const fdtd_probes* probes) {
+  std::vector<fdtd::FusedBlock<T>> fb;
+  std::vector<int2> ctas;
+  const int ROWS = 16;                       // rows per CTA (8 warps x 2)
+  int maxN = 1;
+  for (int b = 0; b < (int)blocks.size(); ++b) {
+    BlockDev<T>& D = blocks[b];
+    if (!D.fused) continue;
+    const int qe = D.qe, qh = D.qh, ni = D.n_if;
+    const int CM = qe + ni + qh;
+    const int np = (int)D.probe_rows.size();
+    const int RM = qh + ni + qe + np;
+    std::vector<double> A1((size_t)qh * qe), A2((size_t)qh * ni);
+    for (int r = 0; r < qh; ++r) {
+      for (int c = 0; c < qe; ++c) A1[(size_t)r * qe + c] = D.gh[r] * D.K[(size_t)c * qh + r];
+      for (int c = 0; c < ni; ++c) A2[(size_t)r * ni + c] = D.gh[r] * D.SE[(size_t)c * qh + r];
+    }
+    std::vector<double> M((size_t)RM * CM, 0.0);
+    auto at = [&](int r, int c) -> double& { return M[(size_t)r * CM + c]; };
+    // h~' rows
+    for (int r = 0; r < qh; ++r) {
+      for (int c = 0; c < qe; ++c) at(r, c) = A1[(size_t)r * qe + c];
+      for (int c = 0; c < ni; ++c) at(r, qe + c) = A2[(size_t)r * ni + c];
+      at(r, qe + ni + r) = 1.0;
+    }
+    // y' rows = S_E * (h~' rows)
+    for (int l = 0; l < ni; ++l)
+      for (int k = 0; k < qh; ++k) {
+        const double s = D.SE[(size_t)l * qh + k];
+        if (s == 0.0) continue;
+        for (int c = 0; c < CM; ++c) at(qh + l, c) += s * at(k, c);
+      }
+    // e~'' rows = [I, 0, 0] - G_e K (h~' rows)
+    for (int r = 0; r < qe; ++r) {
+      const int rr = qh + ni + r;
+      at(rr, r) = 1.0;
+      for (int k = 0; k < qh; ++k) {
+        const double s = D.ge[r] * D.K[(size_t)r * qh + k];
+        if (s == 0.0) continue;
+        for (int c = 0; c < CM; ++c) at(rr, c) -= s * at(k, c);
+      }
+    }
+    // probe rows
+    std::vector<int> prow_probe(np), prow_inst(np);
+    for (int q = 0; q < np; ++q) {
+      const int p = D.probe_rows[q];
+      const int rr = qh + ni + qe + q;
+      prow_probe[q] = p;
+      prow_inst[q] = probes->inst[p];
+      for (int64_t k = probes->rowptr[p]; k < probes->rowptr[p + 1]; ++k) {
+        const int idx = (int)probes->index[k];
+        const double wv = probes->weight[k];
+        if (probes->kind[p] == 1) at(rr, idx) += wv;
+        else for (int c = 0; c < CM; ++c) at(rr, c) += wv * at(idx, c);
+      }
+    }
+    std::vector<T> Mt(M.size());
+    for (size_t q = 0; q < M.size(); ++q) Mt[q] = (T)M[q];
+    D.M_d = dalloc<T>(Mt.size());
+    if (!D.M_d || upload(D.M_d, Mt)) return fail(FDTD_ENOMEM, "fused matrix allocation failed");
+    D.R_M = RM; D.C_M = CM;
+    fdtd::FusedBlock<T> f{};
+    f.qe = qe; f.qh = qh; f.n_if = ni; f.N = D.N; f.R = RM; f.C = CM; f.M = D.M_d;
+    f.e_off = D.e_off; f.h_off = D.h_off; f.y_off = D.y_off;
+    f.n_probe_rows = np;
+    int32_t* pp = dalloc<int32_t>(std::max(np, 1));
+    int32_t* pi = dalloc<int32_t>(std::max(np, 1));
+    if (upload(pp, prow_probe) || upload(pi, prow_inst)) return FDTD_ECUDA;
+    f.probe_id = pp; f.probe_inst = pi;
+    // gather entries of this block
+    f.g_begin = 0; f.g_end = 0;
+    fb.push_back(f);
+    for (int r0 = 0; r0 < RM; r0 += ROWS) ctas.push_back(make_int2((int)fb.size() - 1, r0));
+    maxN = std::max(maxN, D.N);
+    max_cols = std::max(max_cols, CM);
+  }
+  // gather ranges (g lists are ordered by block)
+  {
+    std::vector<int64_t> gd_host(n_gather);
+    if (n_gather) CK(cudaMemcpy(gd_host.data(), g_dst, sizeof(int64_t) * n_gather, cudaMemcpyDeviceToHost));
+    int fi = 0;
+    for (int b = 0; b < (int)blocks.size(); ++b) {
+      if (!blocks[b].fused) continue;
+      int64_t lo = -1, hi = -1;
+      for (int64_t q = 0; q < n_gather; ++q) {
+        const int64_t d = gd_host[q];
+        if (d >= blocks[b].y_off && d < blocks[b].y_off + (int64_t)blocks[b].n_if * blocks[b].N) {
+          if (lo < 0) lo = q;
+          hi = q + 1;
+        }
+      }
+      fb[fi].g_begin = lo < 0 ? 0 : lo;
+      fb[fi].g_end = lo < 0 ? 0 : hi;
+      ++fi;
+    }
+  }
+  n_ctas = (int)ctas.size();
+  NBsel = maxN <= 1 ? 1 : maxN <= 4 ? 4 : maxN <= 16 ? 16 : 32;
+  fused_smem = (size_t)max_cols * maxN * sizeof(T);
+  d_fblocks = dalloc<fdtd::FusedBlock<T>>(fb.size());
+  d_ctas = dalloc<int2>(ctas.size());
+  if (!d_fblocks || !d_ctas) return fail(FDTD_ENOMEM, "fused descriptor allocation failed");
+  if (upload(d_fblocks, fb) || upload(d_ctas, ctas)) return FDTD_ECUDA;
+  return FDTD_OK;
 }
 
-template <typename T, int NB>
-static cudaError_t launch_reduced(const fdtd::RedParams<T>& P, int n_clusters, int CL, cudaStream_t st) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_clusters * CL, 1, 1);
-  cfg.blockDim = dim3(256, 1, 1);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CL;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fdtd::reduced_cluster_kernel<T, NB>, P);
+// e~^{s+1} = e~^s - G_e K~' h~^{s+1/2} and y^s = S_E h~^{s+1/2} after the
+// reduced state was (re)set: the fused step consumes e~ one step ahead.
+template <typename T>
+int Impl<T>::prologue(cudaStream_t st) {
+  for (auto& D : blocks) {
+    if (D.n_if > 0)
+      launch_gemv<T>(D.n_if, D.qh, D.N, D.SE_d, h_state(D, host_step), y_all + D.y_off, (const T*)nullptr,
+                     (T)1, false, d_step, 0, d_bad, st);
+    if (!D.fused) continue;
+    CK(cudaMemcpyAsync(e_ahead(D, host_step), e_state(D, host_step), sizeof(T) * D.qe * D.N,
+                       cudaMemcpyDeviceToDevice, st));
+    launch_gemv<T>(D.qe, D.qh, D.N, D.K_d, h_state(D, host_step), e_ahead(D, host_step), D.ge_d,
+                   (T)-1, true, d_step, 0, d_bad, st);
+  }
+  CK(cudaGetLastError());
+  return FDTD_OK;
 }
 
 template <typename T>
@@ -667,27 +797,57 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
       fdtd::stencil3d_kernel<T, false><<<grid, dim3(BX, BY), sm, st>>>(
           dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
   } else {
-    int BX = (B == 1) ? 32 : B * std::max(2, 64 / B), BY = 16;
+    constexpr int CY = 4;
+    int BX = (B == 1) ? 32 : B * std::max(2, 64 / B), BY = 8;
     if (BX * BY > 1024) BY = std::max(2, 1024 / BX);
-    const int outx = BX / B - 1, outy = BY - 1;
+    const int outx = BX / B - 1, outy = BY * CY - 1;
     dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + outy - 1) / outy, 1);
-    const size_t sm = (size_t)BX * BY * sizeof(T) + tabsz;
+    const size_t sm = (size_t)BX * BY * CY * sizeof(T) + tabsz;
     if (uniform)
-      fdtd::stencil2d_tile_kernel<T, true><<<grid, dim3(BX, BY), sm, st>>>(
+      fdtd::stencil2d_rows_kernel<T, true, CY><<<grid, dim3(BX, BY), sm, st>>>(
           dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, d_step, check_every, d_bad);
     else
-      fdtd::stencil2d_tile_kernel<T, false><<<grid, dim3(BX, BY), sm, st>>>(
+      fdtd::stencil2d_rows_kernel<T, false, CY><<<grid, dim3(BX, BY), sm, st>>>(
           dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, d_step, check_every, d_bad);
   }
   ++n;
   mark(0, 1);
-  // a4, a6 (+ a7): reduced chain, probes, step counter
-  fdtd::RedParams<T> P{};
-  P.n_models = grid_path ? 0 : (int)models.size();
+  // leapfrog path for large blocks (grid-wide GEMVs in the paper's order)
+  if (any_leap) {
+    mark(2, 0);
+    if (n_gather > 0) {
+      fdtd::gather_kernel<T><<<(unsigned)((n_gather * B + 255) / 256), 256, 0, st>>>(
+          n_gather, B, g_comp, g_off, g_dst, F1, g_all);
+      ++n;
+    }
+    for (auto& D : blocks) {
+      if (D.fused) continue;
+      T* e = eb[0] + D.e_off;
+      T* h = hb[0] + D.h_off;
+      n += launch_gemv<T>(D.qe, D.qh, D.N, D.K_d, h, e, D.ge_d, (T)-1, true, d_step, check_every, d_bad, st);
+      n += launch_gemv<T>(D.qh, D.qe, D.N, D.KT_d, e, h, D.gh_d, (T)1, true, d_step, check_every, d_bad, st);
+      if (D.n_if > 0) {
+        n += launch_gemv<T>(D.qh, D.n_if, D.N, D.SET_d, g_all + D.y_off, h, D.gh_d, (T)1, true, d_step, check_every,
+                            d_bad, st);
+        n += launch_gemv<T>(D.n_if, D.qh, D.N, D.SE_d, h, y_all + D.y_off, (const T*)nullptr, (T)1, false, d_step,
+                            0, d_bad, st);
+      }
+    }
+    mark(2, 1);
+  }
+  // fused reduced blocks (one GEMV phase) + probes + step counter
+  mark(1, 0);
+  fdtd::FusedParams<T> P{};
+  P.blocks = d_fblocks;
+  P.ctas = d_ctas;
+  P.n_ctas = n_ctas;
   P.B = B;
-  P.models = d_models;
-  P.red_base[0] = xh_all;
-  P.red_base[1] = h_all;
+  P.e_in = eb[p]; P.e_out = eb[p ^ 1];
+  P.h_in = hb[p]; P.h_out = hb[p ^ 1];
+  P.y = y_all;
+  P.g_comp = g_comp; P.g_off = g_off; P.g_dst = g_dst;
+  P.red_base[0] = eb[0];      // leap-frog blocks (fused blocks' probes are matrix rows)
+  P.red_base[1] = hb[0];
   P.F = F1;
   P.pr = pr;
   P.ring = ring;
@@ -696,42 +856,21 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   P.done = d_done;
   P.check_every = check_every;
   P.bad_step = d_bad;
-  if (grid_path) {
-    mark(2, 0);
-    if (n_gather > 0) {
-      fdtd::gather_kernel<T><<<(unsigned)((n_gather * B + 255) / 256), 256, 0, st>>>(
-          n_gather, B, g_comp, g_off, g_dst, F1, xh_all);
-      ++n;
-    }
-    for (auto& D : blocks) {
-      n += launch_gemv<T>(D.qe, D.qh, D.N, D.K, h_all + D.h_off, xh_all + D.xh_off, D.ge, (T)-1, true,
-                          d_step, check_every, d_bad, st);
-      n += launch_gemv<T>(D.qh, D.qe + D.n_if, D.N, D.Mh, xh_all + D.xh_off, h_all + D.h_off, D.gh, (T)1, true,
-                          d_step, check_every, d_bad, st);
-      if (D.n_if > 0)
-        n += launch_gemv<T>(D.n_if, D.qh, D.N, D.SE, h_all + D.h_off, y_all + D.y_off, (const T*)nullptr,
-                            (T)1, false, d_step, 0, d_bad, st);
-    }
-    mark(2, 1);
-  }
-  mark(1, 0);
-  const int ncl = std::max(1, P.n_models);
-  const int cl = P.n_models > 0 ? CL : 1;
-  cudaError_t le;
+  const unsigned grid = (unsigned)std::max(n_ctas, 1);
+  const size_t sm = fused_smem;
   switch (NBsel) {
-    case 1: le = launch_reduced<T, 1>(P, ncl, cl, st); break;
-    case 4: le = launch_reduced<T, 4>(P, ncl, cl, st); break;
-    case 16: le = launch_reduced<T, 16>(P, ncl, cl, st); break;
-    default: le = launch_reduced<T, 32>(P, ncl, cl, st); break;
+    case 1: fdtd::reduced_fused_kernel<T, 1><<<grid, 256, sm, st>>>(P); break;
+    case 4: fdtd::reduced_fused_kernel<T, 4><<<grid, 256, sm, st>>>(P); break;
+    case 16: fdtd::reduced_fused_kernel<T, 16><<<grid, 256, sm, st>>>(P); break;
+    default: fdtd::reduced_fused_kernel<T, 32><<<grid, 256, sm, st>>>(P); break;
   }
-  if (le != cudaSuccess) return fail(FDTD_ECUDA, "reduced kernel launch: %s", cudaGetErrorString(le));
   ++n;
   mark(1, 1);
   CK(cudaGetLastError());
   if (profile) {
     CK(cudaEventSynchronize(ev[3]));
     for (int ph = 0; ph < NPHASE; ++ph) {
-      if (ph == 2 && !grid_path) continue;
+      if (ph == 2 && !any_leap) continue;
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, ev[2 * ph], ev[2 * ph + 1]));
       phase_ms[ph] += ms;
@@ -744,7 +883,6 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
 
 template <typename T>
 int Impl<T>::drain() {
-  // copy the ring samples of steps [drained_to, host_step) to the host
   const int64_t from = drained_to, to = host_step;
   if (to <= from || n_probe == 0) { drained_to = to; return FDTD_OK; }
   CK(cudaStreamSynchronize(stream));
@@ -769,7 +907,6 @@ template <typename T>
 int Impl<T>::step(int64_t n) {
   if (n < 0) return fail(FDTD_EINVAL, "negative step count");
   while (n > 0) {
-    // keep the probe ring from overflowing
     if (n_probe > 0 && host_step - drained_to >= cap) {
       int e = drain();
       if (e) return e;
@@ -861,8 +998,8 @@ int Impl<T>::get_state(int which, double* out, int64_t n) {
     int64_t o = 0;
     for (auto& D : blocks) {
       const int q = which == 6 ? D.qe : D.qh;
-      const T* src = which == 6 ? xh_all + D.xh_off : h_all + D.h_off;
-      CK(cudaMemcpy(staging, src, sizeof(T) * q * D.N, cudaMemcpyDeviceToHost));
+      const T* srcp = which == 6 ? e_state(D, host_step) : h_state(D, host_step);
+      CK(cudaMemcpy(staging, srcp, sizeof(T) * q * D.N, cudaMemcpyDeviceToHost));
       for (int in = 0; in < D.n_inst; ++in)
         for (int b = 0; b < B; ++b)
           for (int c = 0; c < q; ++c) out[o++] = (double)staging[(int64_t)c * D.N + in * B + b];
@@ -901,18 +1038,14 @@ int Impl<T>::set_state(int which, const double* in, int64_t n) {
     int64_t o = 0;
     for (auto& D : blocks) {
       const int q = which == 6 ? D.qe : D.qh;
-      T* dst = which == 6 ? xh_all + D.xh_off : h_all + D.h_off;
+      T* dst = which == 6 ? e_state(D, host_step) : h_state(D, host_step);
       for (int in_ = 0; in_ < D.n_inst; ++in_)
         for (int b = 0; b < B; ++b)
           for (int c = 0; c < q; ++c) staging[(int64_t)c * D.N + in_ * B + b] = (T)in[o++];
       CK(cudaMemcpy(dst, staging, sizeof(T) * q * D.N, cudaMemcpyHostToDevice));
     }
-    // y = S_E h~ must follow h~
-    if (which == 7)
-      for (auto& D : blocks)
-        if (D.n_if > 0)
-          launch_gemv<T>(D.n_if, D.qh, D.N, D.SE, h_all + D.h_off, y_all + D.y_off, (const T*)nullptr, (T)1,
-                         false, d_step, 0, d_bad, stream);
+    int e = prologue(stream);
+    if (e) return e;
     CK(cudaStreamSynchronize(stream));
     return FDTD_OK;
   }

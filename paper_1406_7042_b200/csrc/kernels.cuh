@@ -4,27 +4,22 @@
 //   stencil   fused coarse E->H pass over the grid (ping-pong buffers); the
 //             explicit E rows (interface rows a3, source rows a1) are
 //             evaluated in place by the thread that owns them           a1-a3, a5
-//   reduced   one thread-block cluster per reduced model:
-//               e~ -= G_e K~' h~                                         a4
-//               G = E_if^{n+1} (gather)                                   a6
-//               h~ += G_h [K~'^T | S_E^T] [e~ ; G]                       a6
-//               y = S_E h~   (consumed by the next step's interface rows) a6
+//   reduced   the reduced chain of every small block as ONE GEMV with a
+//             precomposed update matrix (a4, a6: e~, G gather, h~, y),
 //             + probes, divergence check, device step counter            a7
-// Large reduced blocks (S_E of hundreds of MB) use the grid-wide gemv path
-// instead of a cluster (see fdtd_api.cu).
+// Large reduced blocks (S_E of hundreds of MB) run the leap-frog as
+// grid-wide GEMV launches between the two (see fdtd_api.cu).
 //
 // Coarse fields live in "device storage": component arrays indexed
 // ((k*(ny+1) + j)*px + i)*B + b with the batch b innermost and px >= nx+1.
 // E^{n+1} = E^n + cb * curl(H)  ==  E^n - cb * (K_inc H)   (K_inc = -curl)
 // H^{n+1} = H^n - ch * curl(E)  ==  H^n + ch * (K_inc^T E)
 #pragma once
-#include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace fdtd {
 
-namespace cg = cooperative_groups;
 
 template <typename T> struct Coef;       // per-material coefficient, hi/lo for fp32 (R11)
 template <> struct Coef<float> {
@@ -99,17 +94,18 @@ __device__ __forceinline__ T eval_row(const RowsE<T>& R, int r, int b, int B, T 
 }
 
 // ---------------------------------------------------------------------------
-// 2-D (Ez, Hx, Hy) fused E->H stencil, tiled.  Block (BX, BY) threads covers
-// BX/B cells in x and BY rows; every thread computes Ez^{n+1} of its cell, the
-// block keeps them in shared memory and the interior (BX/B-1) x (BY-1) cells
-// update Hx, Hy from their +x / +y neighbours (overlapped tiling: the halo Ez
-// is recomputed by the neighbouring block; old buffers are read-only).
+// 2-D (Ez, Hx, Hy) fused E->H stencil.  Block (BX, BY) threads; each thread owns
+// CY consecutive rows of one column (all its loads are issued before any
+// compute: CY x 5 independent loads in flight per thread).  The block computes
+// Ez^{n+1} on its BX/B x BY*CY footprint and updates Hx, Hy on the footprint
+// minus its last column and row (overlapped tiling: the halo Ez is recomputed
+// by the neighbouring block; the old buffers are read-only, race free).
 // Ez += cb ((Hy(i) - Hy(i-1)) - (Hx(j) - Hx(j-1)))
 // Hx -= ch (Ez(j+1) - Ez(j))        Hy += ch (Ez(i+1) - Ez(i))
 // ---------------------------------------------------------------------------
-template <typename T, bool UNIFORM>
-__global__ void __launch_bounds__(1024)
-stencil2d_tile_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restrict__ mat_id,
+template <typename T, bool UNIFORM, int CY>
+__global__ void __launch_bounds__(256)
+stencil2d_rows_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restrict__ mat_id,
                       const Coef<T>* __restrict__ gtab, const uint8_t* __restrict__ gifm, int n_mat,
                       Coef<T> u0, Coef<T> u1, RowsE<T> R, const T* __restrict__ y,
                       const int64_t* __restrict__ d_step, int check_every,
@@ -117,60 +113,75 @@ stencil2d_tile_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int BX = blockDim.x, BY = blockDim.y, B = d.B;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  T* sE = reinterpret_cast<T*>(smem_raw);                    // [BY][BX]
-  MatTable<T>* tab = reinterpret_cast<MatTable<T>*>(sE + BX * BY);
-  if (!UNIFORM) {
-    for (int m = ty * BX + tx; m < n_mat; m += BX * BY) {
-      tab->c[m][2] = gtab[m * 6 + 2];
-      tab->c[m][3] = gtab[m * 6 + 3];
-      tab->c[m][4] = gtab[m * 6 + 4];
-      tab->ifm[m] = gifm[m];
-    }
-  }
-  const int outx = BX / B - 1, outy = BY - 1;
+  T* sE = reinterpret_cast<T*>(smem_raw);                    // [BY*CY][BX]
+  MatTable<T>* tab = reinterpret_cast<MatTable<T>*>(sE + BX * BY * CY);
+  const T* __restrict__ Ez0 = F0.f[2];
+  const T* __restrict__ Hx0 = F0.f[3];
+  const T* __restrict__ Hy0 = F0.f[4];
+  const int nx = d.nx, ny = d.ny;
+  const int outx = BX / B - 1, outy = BY * CY - 1;
   const int i = blockIdx.x * outx + tx / B;
   const int b = tx % B;
-  const int j = blockIdx.y * outy + ty;
-  const int nx = d.nx, ny = d.ny;
-  const bool inside = (i <= nx) && (j <= ny);
-  const bool own = inside && (tx / B < outx) && (ty < outy);
-  const int ii = min(i, nx), jj = min(j, ny);
-  const int64_t soff = (int64_t)jj * d.px + ii;            // storage offset
-  const int64_t o = soff * B + b;
+  const int jb = blockIdx.y * outy + ty * CY;
+  const int ii = min(i, nx);
   const int64_t sx = (i > 0) ? B : 0;
-  const int64_t sy = (j > 0) ? (int64_t)d.px * B : 0;
+  const int64_t rs = (int64_t)d.px * B;
   const int64_t step = *d_step;
-  __syncthreads();
-  const int m = UNIFORM ? 0 : (int)mat_id[soff];
-  T ez = 0, hx = 0, hy = 0;
-  if (inside) {
-    hx = F0.f[3][o]; hy = F0.f[4][o];
-    const T hx_jm = F0.f[3][o - sy], hy_im = F0.f[4][o - sx];
-    const T ez0 = F0.f[2][o];
-    const Coef<T> c = UNIFORM ? u0 : tab->c[m][2];
-    const T dd = (hy - hy_im) - (hx - hx_jm);
-    const bool act = (i > 0) && (i < nx) && (j > 0) && (j < ny);
-    ez = act ? ez0 + c.apply(dd) : (T)0;
-    if (!UNIFORM && (tab->ifm[m] & 4)) {
-      const int r = R.row_of[2][soff];
-      ez = eval_row(R, r, b, B, ez0, F0, y, step);
+  // issue every load first
+  T hx[CY], hy[CY], hyim[CY], ez0[CY];
+  int m[CY];
+  int64_t o[CY];
+#pragma unroll
+  for (int r = 0; r < CY; ++r) {
+    const int jj = min(jb + r, ny);
+    o[r] = ((int64_t)jj * d.px + ii) * B + b;
+    hx[r] = Hx0[o[r]]; hy[r] = Hy0[o[r]]; hyim[r] = Hy0[o[r] - sx]; ez0[r] = Ez0[o[r]];
+    m[r] = UNIFORM ? 0 : (int)mat_id[(int64_t)jj * d.px + ii];
+  }
+  const T hx_jm = (jb > 0) ? Hx0[o[0] - rs] : (T)0;
+  if (!UNIFORM) {
+    for (int q = ty * BX + tx; q < n_mat; q += BX * BY) {
+      tab->c[q][2] = gtab[q * 6 + 2];
+      tab->c[q][3] = gtab[q * 6 + 3];
+      tab->c[q][4] = gtab[q * 6 + 4];
+      tab->ifm[q] = gifm[q];
     }
   }
-  sE[ty * BX + tx] = ez;
   __syncthreads();
-  if (own) {
-    const T ez_ip = sE[ty * BX + tx + B];
-    const T ez_jp = sE[(ty + 1) * BX + tx];
+  T ez[CY];
+  const bool ci = (i > 0) && (i < nx);
+#pragma unroll
+  for (int r = 0; r < CY; ++r) {
+    const int j = jb + r;
+    const T hxm = (r == 0) ? hx_jm : hx[r - 1];
+    const Coef<T> c = UNIFORM ? u0 : tab->c[m[r]][2];
+    const T dd = (hy[r] - hyim[r]) - (hx[r] - hxm);
+    ez[r] = (ci && j > 0 && j < ny) ? ez0[r] + c.apply(dd) : (T)0;
+    if (!UNIFORM && (tab->ifm[m[r]] & 4) && i <= nx && j <= ny) {
+      const int64_t so = (int64_t)min(j, ny) * d.px + ii;
+      ez[r] = eval_row(R, R.row_of[2][so], b, B, ez0[r], F0, y, step);
+    }
+    sE[(ty * CY + r) * BX + tx] = ez[r];
+  }
+  __syncthreads();
+  const bool colown = (i <= nx) && (tx / B < outx);
+  const bool do_check = check_every > 0 && (step % check_every) == 0;
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < CY; ++r) {
+    const int j = jb + r;
+    if (!colown || j > ny || ty * CY + r >= outy) continue;
+    const T ez_jp = (r + 1 < CY) ? ez[r + 1] : sE[((ty + 1) * CY) * BX + tx];
+    const T ez_ip = sE[(ty * CY + r) * BX + tx + B];
     Coef<T> cx, cy;
     if (UNIFORM) { cx = u1; cy = u1; }
-    else { cx = tab->c[m][3]; cy = tab->c[m][4]; }
-    const T hx1 = (i > 0 && i < nx && j < ny) ? hx - cx.apply(ez_jp - ez) : hx;
-    const T hy1 = (i < nx && j > 0 && j < ny) ? hy + cy.apply(ez_ip - ez) : hy;
-    F1.f[2][o] = ez; F1.f[3][o] = hx1; F1.f[4][o] = hy1;
-    if (check_every > 0 && (step % check_every) == 0 &&
-        !(finite_small(ez) && finite_small(hx1) && finite_small(hy1)))
-      atomicMin(bad_step, (unsigned long long)step);
+    else { cx = tab->c[m[r]][3]; cy = tab->c[m[r]][4]; }
+    const T hx1 = (ci && j < ny) ? hx[r] - cx.apply(ez_jp - ez[r]) : hx[r];
+    const T hy1 = (i < nx && j > 0 && j < ny) ? hy[r] + cy.apply(ez_ip - ez[r]) : hy[r];
+    F1.f[2][o[r]] = ez[r]; F1.f[3][o[r]] = hx1; F1.f[4][o[r]] = hy1;
+    if (do_check) bad |= !(finite_small(ez[r]) && finite_small(hx1) && finite_small(hy1));
   }
+  if (bad) atomicMin(bad_step, (unsigned long long)step);
 }
 
 // ---------------------------------------------------------------------------
@@ -315,25 +326,12 @@ stencil3d_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// reduced blocks: one thread-block cluster per model.
+// reduced blocks.  Small blocks ("fused", see fdtd_api.cu): one GEMV with the
+// precomposed update matrix M per step,
+//   [h~' ; y' ; e~'' ; probe rows] = M [e~ ; G ; h~],
+// spread over many CTAs (16 rows each); every CTA stages the input vector in
+// shared memory ([N][C] so that lanes read consecutive columns).
 // ---------------------------------------------------------------------------
-template <typename T>
-struct RedModel {
-  int qe, qh, n_if, N;          // N = n_inst * B columns
-  const T* K;                   // [qe][qh]
-  const T* Mh;                  // [qh][qe + n_if]  = [K^T | S_E^T]
-  const T* SE;                  // [n_if][qh]
-  const T* ge;                  // [qe]
-  const T* gh;                  // [qh]
-  T* xh;                        // [qe + n_if][N]   = [e~ ; G]
-  T* h;                         // [qh][N]
-  T* y;                         // [n_if][N]
-  int n_g;                      // gather entries (interface rows of this model, all instances)
-  const int32_t* g_comp;
-  const int64_t* g_off;
-  const int64_t* g_dst;         // index into xh
-};
-
 template <typename T>
 struct Probes {
   int n_probe;
@@ -341,15 +339,33 @@ struct Probes {
   const int32_t* src;           // [terms] 0..5 coarse comp, 6 = e~ buffer, 7 = h~ buffer
   const int64_t* off;           // [terms] coarse: storage offset; reduced: element index
   const T* w;
-  const int32_t* owner;         // [n_probe] model whose cluster samples it (-1: cluster 0)
+  const int32_t* owner;         // [n_probe] -1: sampled by CTA 0, -2: a row of a fused matrix
 };
 
 template <typename T>
-struct RedParams {
-  int n_models, B;
-  const RedModel<T>* models;
-  const T* red_base[2];         // base pointers of the e~ and h~ buffers (probes)
-  Fields<T> F;                  // coarse fields after the step (new parity)
+struct FusedBlock {
+  int qe, qh, n_if, N, R, C;
+  const T* M;                   // [R][C]
+  int64_t e_off, h_off, y_off;
+  int n_probe_rows;
+  const int32_t* probe_id;
+  const int32_t* probe_inst;
+  int64_t g_begin, g_end;       // gather entries of this block
+};
+
+template <typename T>
+struct FusedParams {
+  const FusedBlock<T>* blocks;
+  const int2* ctas;             // (block, first row)
+  int n_ctas, B;
+  const T* e_in; T* e_out;      // e~^{n+1} in, e~^{n+2} out
+  const T* h_in; T* h_out;      // h~^{n+1/2} in, h~^{n+3/2} out
+  T* y;
+  const int32_t* g_comp;
+  const int64_t* g_off;
+  const int64_t* g_dst;
+  const T* red_base[2];         // leapfrog-path e~ / h~ buffers (probe terms 6 / 7)
+  Fields<T> F;                  // coarse fields after the step
   Probes<T> pr;
   T* ring;
   int64_t cap;
@@ -359,8 +375,103 @@ struct RedParams {
   unsigned long long* bad_step;
 };
 
-// out[r][n] = beta out[r][n] + alpha g[r] sum_c A[r][c] X[c][n] for the rows of
-// this warp set (warp w handles rows w, w + nw, ...)
+constexpr int FUSED_ROWS = 16;
+
+template <typename T, int NB>
+__global__ void __launch_bounds__(256)
+reduced_fused_kernel(FusedParams<T> P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* X = reinterpret_cast<T*>(smem_raw);
+  const int64_t step = *P.d_step;
+  const bool check = P.check_every > 0 && (step % P.check_every) == 0;
+  bool bad = false;
+  const int B = P.B;
+  if ((int)blockIdx.x < P.n_ctas) {
+    const int2 ct = P.ctas[blockIdx.x];
+    const FusedBlock<T> FB = P.blocks[ct.x];
+    const int C = FB.C, N = FB.N, qe = FB.qe, qh = FB.qh, ni = FB.n_if;
+    // stage X = [e~ ; G ; h~] as [N][C]
+    for (int t = threadIdx.x; t < qe * N; t += blockDim.x) X[(t % N) * C + t / N] = P.e_in[FB.e_off + t];
+    for (int t = threadIdx.x; t < qh * N; t += blockDim.x) X[(t % N) * C + qe + ni + t / N] = P.h_in[FB.h_off + t];
+    for (int t = threadIdx.x; t < ni * N; t += blockDim.x) X[(t % N) * C + qe + t / N] = (T)0;
+    __syncthreads();
+    for (int64_t t = FB.g_begin * B + threadIdx.x; t < FB.g_end * B; t += blockDim.x) {
+      const int64_t q = t / B;
+      const int bb = (int)(t % B);
+      const int64_t dst = P.g_dst[q] - FB.y_off;          // l*N + inst*B
+      const int l = (int)(dst / N), col = (int)(dst % N) + bb;
+      X[col * C + qe + l] = P.F.f[P.g_comp[q]][P.g_off[q] * B + bb];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    const int r1 = min(ct.y + FUSED_ROWS, FB.R);
+    for (int r = ct.y + warp; r < r1; r += nwarp) {
+      T acc[NB];
+#pragma unroll
+      for (int n = 0; n < NB; ++n) acc[n] = 0;
+      const T* a = FB.M + (int64_t)r * C;
+#pragma unroll 4
+      for (int c = lane; c < C; c += 32) {
+        const T av = a[c];
+#pragma unroll
+        for (int n = 0; n < NB; ++n)
+          if (n < N) acc[n] += av * X[n * C + c];
+      }
+#pragma unroll
+      for (int n = 0; n < NB; ++n) {
+        T v = acc[n];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        acc[n] = v;
+      }
+      if (lane < N) {
+        T v = 0;
+#pragma unroll
+        for (int n = 0; n < NB; ++n)
+          if (n == lane) v = acc[n];
+        if (r < qh) P.h_out[FB.h_off + (int64_t)r * N + lane] = v;
+        else if (r < qh + ni) P.y[FB.y_off + (int64_t)(r - qh) * N + lane] = v;
+        else if (r < qh + ni + qe) P.e_out[FB.e_off + (int64_t)(r - qh - ni) * N + lane] = v;
+        else {
+          const int q = r - qh - ni - qe;
+          const int p = FB.probe_id[q], in = FB.probe_inst[q];
+          if (lane >= in * B && lane < in * B + B)
+            P.ring[(step % P.cap) * (int64_t)P.pr.n_probe * B + (int64_t)p * B + (lane - in * B)] = v;
+        }
+        if (check && !finite_small((double)v)) bad = true;
+      }
+    }
+  }
+  // coarse probes and leapfrog-path reduced probes
+  if (blockIdx.x == 0) {
+    for (int t = threadIdx.x; t < P.pr.n_probe * B; t += blockDim.x) {
+      const int p = t / B, bb = t % B;
+      if (P.pr.owner[p] != -1) continue;
+      T acc = 0;
+      for (int64_t k = P.pr.rowptr[p]; k < P.pr.rowptr[p + 1]; ++k) {
+        const int s = P.pr.src[k];
+        const T v = (s < 6) ? P.F.f[s][P.pr.off[k] * B + bb] : P.red_base[s - 6][P.pr.off[k] + bb];
+        acc += P.pr.w[k] * v;
+      }
+      P.ring[(step % P.cap) * (int64_t)P.pr.n_probe * B + t] = acc;
+    }
+  }
+  if (bad) atomicMin(P.bad_step, (unsigned long long)step);
+  // the last CTA to finish advances the device step counter
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int prev = atomicAdd(P.done, 1u);
+    if (prev == gridDim.x - 1) {
+      *P.done = 0;
+      __threadfence();
+      *P.d_step = step + 1;
+    }
+  }
+}
+
+// out[r][n] = (accumulate ? out[r][n] : 0) + alpha g[r] sum_c A[r][c] X[c][n]
+// for the rows of this warp set (warp w handles rows w, w + nw, ...)
 template <typename T, int NB>
 __device__ __forceinline__ void warp_rows(int rows, int cols, int N, const T* __restrict__ A,
                                           const T* __restrict__ X, T* __restrict__ out,
@@ -372,6 +483,7 @@ __device__ __forceinline__ void warp_rows(int rows, int cols, int N, const T* __
 #pragma unroll
     for (int n = 0; n < NB; ++n) acc[n] = 0;
     const T* a = A + (int64_t)r * cols;
+#pragma unroll 4
     for (int c = lane; c < cols; c += 32) {
       const T av = a[c];
       const T* x = X + (int64_t)c * N;
@@ -396,70 +508,6 @@ __device__ __forceinline__ void warp_rows(int rows, int cols, int N, const T* __
       const T res = (accumulate ? *o : (T)0) + alpha * gr * v;
       *o = res;
       if (check && !finite_small((double)res)) bad = true;
-    }
-  }
-}
-
-template <typename T, int NB>
-__global__ void __launch_bounds__(256)
-reduced_cluster_kernel(RedParams<T> P) {
-  cg::cluster_group cl = cg::this_cluster();
-  const int CL = (int)cl.num_blocks();
-  const int rank = (int)cl.block_rank();
-  const int m = blockIdx.x / CL;
-  const int64_t step = *P.d_step;
-  const bool check = P.check_every > 0 && (step % P.check_every) == 0;
-  bool bad = false;
-  const int warps = blockDim.x >> 5;
-  const int w0 = rank * warps + (threadIdx.x >> 5);
-  const int nw = CL * warps;
-  const bool have = m < P.n_models;
-  RedModel<T> M;
-  if (have) M = P.models[m];
-  // a4: e~ -= G_e K~' h~^{n+1/2};   gather G = E_if^{n+1}
-  if (have) {
-    warp_rows<T, NB>(M.qe, M.qh, M.N, M.K, M.h, M.xh, M.ge, (T)-1, true, w0, nw, check, bad);
-    const int t0 = rank * blockDim.x + threadIdx.x;
-    for (int64_t t = t0; t < (int64_t)M.n_g * P.B; t += (int64_t)CL * blockDim.x) {
-      const int64_t r = t / P.B;
-      const int b = (int)(t % P.B);
-      M.xh[M.g_dst[r] + b] = P.F.f[M.g_comp[r]][M.g_off[r] * P.B + b];
-    }
-  }
-  __threadfence();
-  cl.sync();
-  // a6: h~ += G_h [K~'^T | S_E^T][e~ ; G]
-  if (have) warp_rows<T, NB>(M.qh, M.qe + M.n_if, M.N, M.Mh, M.xh, M.h, M.gh, (T)1, true, w0, nw, check, bad);
-  __threadfence();
-  cl.sync();
-  // y = S_E h~  (interface coupling of the next step)
-  if (have && M.n_if > 0)
-    warp_rows<T, NB>(M.n_if, M.qh, M.N, M.SE, M.h, M.y, (const T*)nullptr, (T)1, false, w0, nw, false, bad);
-  // a7: probes owned by this cluster (reduced states are final after the sync)
-  if (rank == 0) {
-    for (int t = threadIdx.x; t < P.pr.n_probe * P.B; t += blockDim.x) {
-      const int p = t / P.B, b = t % P.B;
-      const int ow = P.pr.owner[p];
-      if (!((ow < 0 && m == 0) || ow == m)) continue;
-      T acc = 0;
-      for (int64_t k = P.pr.rowptr[p]; k < P.pr.rowptr[p + 1]; ++k) {
-        const int s = P.pr.src[k];
-        const T v = (s < 6) ? P.F.f[s][P.pr.off[k] * P.B + b] : P.red_base[s - 6][P.pr.off[k] + b];
-        acc += P.pr.w[k] * v;
-      }
-      P.ring[(step % P.cap) * (int64_t)P.pr.n_probe * P.B + t] = acc;
-    }
-  }
-  if (bad) atomicMin(P.bad_step, (unsigned long long)step);
-  // the last CTA to finish advances the device step counter
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned int prev = atomicAdd(P.done, 1u);
-    if (prev == gridDim.x - 1) {
-      *P.done = 0;
-      __threadfence();
-      *P.d_step = step + 1;
     }
   }
 }

@@ -72,7 +72,8 @@ class Probes(C.Structure):
 
 class Exec(C.Structure):
     _fields_ = [("stream", C.c_void_p), ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", C.c_void_p),
-                ("check_every", C.c_int32), ("graph_steps", C.c_int32), ("probe_capacity", C.c_int64)]
+                ("check_every", C.c_int32), ("graph_steps", C.c_int32), ("probe_capacity", C.c_int64),
+                ("reduced_form", C.c_int32)]
 
 
 _lib = None
@@ -148,7 +149,7 @@ class Sim:
     ``precision`` 32/64 overrides problem['precision']."""
 
     def __init__(self, problem, precision=None, stream=None, use_torch_allocator=True,
-                 check_every=100, graph_steps=32, probe_capacity=0):
+                 check_every=100, graph_steps=32, probe_capacity=0, reduced_form="auto"):
         lib = load_library()
         self.lib = lib
         self.problem = problem
@@ -249,6 +250,7 @@ class Sim:
             prb.weight = _ptr(arrs["weight"], C.c_double)
         ex = Exec()
         ex.check_every, ex.graph_steps, ex.probe_capacity = int(check_every), int(graph_steps), int(probe_capacity)
+        ex.reduced_form = {"auto": 0, "fused": 1, "leapfrog": 2}[reduced_form]
         self._torch_cbs = None
         try:
             import torch

@@ -83,15 +83,16 @@ def _enforced_problem(scn, q=24, seed=11):
     return prob
 
 
+@pytest.mark.parametrize("form", ["fused", "leapfrog"])
 @pytest.mark.parametrize("prec", [64, 32])
-def test_hybrid_2d_reduced_enforced(prec):
+def test_hybrid_2d_reduced_enforced(prec, form):
     # q = 24 reduced block above the fine CFL limit (dt = 1.5x fine CFL) after
     # the split enforcement (reading R7)
     scn = scenario("tiny2d", n_steps=400)
     prob = _enforced_problem(scn)
     prob["blocks"][0]["g_e"] = float(scn["dt"])       # D~ = I: scalar G
     prob["blocks"][0]["g_h"] = float(scn["dt"])
-    _check(prob, 400, prec)
+    _check(prob, 400, prec, reduced_form=form)
 
 
 def test_graphs_match_eager_bitwise():
@@ -103,6 +104,38 @@ def test_graphs_match_eager_bitwise():
         assert np.array_equal(a["state"][c], b["state"][c])
     assert np.array_equal(a["red_h"], b["red_h"])
     assert np.array_equal(a["probes"], b["probes"])
+
+
+@pytest.mark.parametrize("form", ["fused", "leapfrog"])
+def test_reduced_probes_and_state_roundtrip(form):
+    # probes on e~ / h~ (Eq. (10) reconstruction rows) and set_state of the
+    # reduced state mid-run
+    scn = scenario("tiny2d", n_steps=120)
+    prob = _enforced_problem(scn)
+    q = prob["blocks"][0]["qe"]
+    rng = np.random.default_rng(3)
+    prob["probes"] = prob["probes"] + [
+        dict(kind=1, block=0, inst=0, vrow=rng.standard_normal(q)),
+        dict(kind=2, block=0, inst=0, vrow=rng.standard_normal(q))]
+    _check(prob, 120, 64, reduced_form=form)
+    from paper_1406_7042_b200.fdtd import Sim
+    from parity import run_oracle
+    ora = run_oracle(prob, 60)
+    sim = Sim(prob, precision=64, reduced_form=form)
+    sim.step(60)
+    e6, h7 = sim.get_state(6), sim.get_state(7)
+    st = {c: sim.get_state(c) for c in (2, 3, 4)}
+    sim.close()
+    sim2 = Sim(prob, precision=64, reduced_form=form)
+    for c, a in st.items():
+        sim2.set_state(c, a)
+    sim2.set_state(6, e6)
+    sim2.set_state(7, h7)
+    sim2.step(60)
+    a = sim2.get_state(7)
+    sim2.close()
+    ref = run_oracle(prob, 120)
+    assert np.linalg.norm(a - ref["red_h"]) <= 1e-11 * np.linalg.norm(ref["red_h"])
 
 
 def test_batch_members_independent():
