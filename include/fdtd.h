@@ -169,7 +169,8 @@ int fdtd_probe(fdtd_t* h, double* out, int64_t cap, int64_t* written);
 
 /* State access (synchronising).  which = 0..5: coarse component c, n = batch*S,
  * layout [batch][S]; which = 6 / 7: all reduced e~ / h~, layout
- * [block][inst][batch][q]; which = 8: the step counter (n = 1). */
+ * [block][inst][batch][q]; which = 8: the step counter n (n = 1; it indexes
+ * the source waveforms, so a restored checkpoint sets it too). */
 int fdtd_get_state(fdtd_t* h, int32_t which, double* out, int64_t n);
 int fdtd_set_state(fdtd_t* h, int32_t which, const double* in, int64_t n);
 

@@ -154,7 +154,8 @@ struct Impl : public fdtd_t {
   // fused kernel work decomposition
   fdtd::FusedBlock<T>* d_fblocks = nullptr;
   int2* d_ctas = nullptr;             // (fused block, first row) per CTA
-  int n_ctas = 0, NBsel = 1, max_cols = 0;
+  int n_ctas = 0, NBsel = 1, max_cols = 0, rows_per_cta = 8;
+  int64_t step_offset = 0;            // device step = host step + offset (set_state(8))
   size_t fused_smem = 0;
   // probes
   fdtd::Probes<T> pr{};
@@ -536,6 +537,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       return FDTD_ECUDA;
     rows.e_comp = d_ec; rows.e_off = d_eo; rows.c = d_c; rows.rowptr = d_rp; rows.h_comp = d_hc;
     rows.h_off = d_ho; rows.w = d_w; rows.y_off = d_yo; rows.src = d_src; rows.cs = d_cs; rows.wave = d_wave;
+    rows.g_out = g_all;
     for (int c = 0; c < 3; ++c) rows.row_of[c] = nullptr;
     for (int c = 0; c < 3; ++c) {
       bool any = false;
@@ -652,7 +654,8 @@ template <typename T>
 int Impl<T>::build_fused(const fdtd_probes* probes) {
   std::vector<fdtd::FusedBlock<T>> fb;
   std::vector<int2> ctas;
-  const int ROWS = 16;                       // rows per CTA (8 warps x 2)
+  const int ROWS = 8;                        // rows per CTA (8 warps x 1)
+  const int PADC = 32 * (16 / (int)sizeof(T));   // lanes x vector width
   int maxN = 1;
   for (int b = 0; b < (int)blocks.size(); ++b) {
     BlockDev<T>& D = blocks[b];
@@ -705,46 +708,27 @@ int Impl<T>::build_fused(const fdtd_probes* probes) {
         else for (int c = 0; c < CM; ++c) at(rr, c) += wv * at(idx, c);
       }
     }
-    std::vector<T> Mt(M.size());
-    for (size_t q = 0; q < M.size(); ++q) Mt[q] = (T)M[q];
+    const int Cp = (CM + PADC - 1) / PADC * PADC;
+    std::vector<T> Mt((size_t)RM * Cp, (T)0);
+    for (int r = 0; r < RM; ++r)
+      for (int c = 0; c < CM; ++c) Mt[(size_t)r * Cp + c] = (T)M[(size_t)r * CM + c];
     D.M_d = dalloc<T>(Mt.size());
     if (!D.M_d || upload(D.M_d, Mt)) return fail(FDTD_ENOMEM, "fused matrix allocation failed");
     D.R_M = RM; D.C_M = CM;
     fdtd::FusedBlock<T> f{};
-    f.qe = qe; f.qh = qh; f.n_if = ni; f.N = D.N; f.R = RM; f.C = CM; f.M = D.M_d;
+    f.qe = qe; f.qh = qh; f.n_if = ni; f.N = D.N; f.R = RM; f.C = CM; f.Cp = Cp; f.M = D.M_d;
     f.e_off = D.e_off; f.h_off = D.h_off; f.y_off = D.y_off;
     f.n_probe_rows = np;
     int32_t* pp = dalloc<int32_t>(std::max(np, 1));
     int32_t* pi = dalloc<int32_t>(std::max(np, 1));
     if (upload(pp, prow_probe) || upload(pi, prow_inst)) return FDTD_ECUDA;
     f.probe_id = pp; f.probe_inst = pi;
-    // gather entries of this block
-    f.g_begin = 0; f.g_end = 0;
     fb.push_back(f);
     for (int r0 = 0; r0 < RM; r0 += ROWS) ctas.push_back(make_int2((int)fb.size() - 1, r0));
     maxN = std::max(maxN, D.N);
-    max_cols = std::max(max_cols, CM);
+    max_cols = std::max(max_cols, Cp);
   }
-  // gather ranges (g lists are ordered by block)
-  {
-    std::vector<int64_t> gd_host(n_gather);
-    if (n_gather) CK(cudaMemcpy(gd_host.data(), g_dst, sizeof(int64_t) * n_gather, cudaMemcpyDeviceToHost));
-    int fi = 0;
-    for (int b = 0; b < (int)blocks.size(); ++b) {
-      if (!blocks[b].fused) continue;
-      int64_t lo = -1, hi = -1;
-      for (int64_t q = 0; q < n_gather; ++q) {
-        const int64_t d = gd_host[q];
-        if (d >= blocks[b].y_off && d < blocks[b].y_off + (int64_t)blocks[b].n_if * blocks[b].N) {
-          if (lo < 0) lo = q;
-          hi = q + 1;
-        }
-      }
-      fb[fi].g_begin = lo < 0 ? 0 : lo;
-      fb[fi].g_end = lo < 0 ? 0 : hi;
-      ++fi;
-    }
-  }
+  rows_per_cta = ROWS;
   n_ctas = (int)ctas.size();
   NBsel = maxN <= 1 ? 1 : maxN <= 4 ? 4 : maxN <= 16 ? 16 : 32;
   fused_smem = (size_t)max_cols * maxN * sizeof(T);
@@ -815,11 +799,6 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   // leapfrog path for large blocks (grid-wide GEMVs in the paper's order)
   if (any_leap) {
     mark(2, 0);
-    if (n_gather > 0) {
-      fdtd::gather_kernel<T><<<(unsigned)((n_gather * B + 255) / 256), 256, 0, st>>>(
-          n_gather, B, g_comp, g_off, g_dst, F1, g_all);
-      ++n;
-    }
     for (auto& D : blocks) {
       if (D.fused) continue;
       T* e = eb[0] + D.e_off;
@@ -845,7 +824,8 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   P.e_in = eb[p]; P.e_out = eb[p ^ 1];
   P.h_in = hb[p]; P.h_out = hb[p ^ 1];
   P.y = y_all;
-  P.g_comp = g_comp; P.g_off = g_off; P.g_dst = g_dst;
+  P.G = g_all;
+  P.rows_per_cta = rows_per_cta;
   P.red_base[0] = eb[0];      // leap-frog blocks (fused blocks' probes are matrix rows)
   P.red_base[1] = hb[0];
   P.F = F1;
@@ -890,7 +870,7 @@ int Impl<T>::drain() {
   std::vector<T> buf((size_t)((to - from) * per));
   int64_t done = 0;
   while (done < to - from) {
-    const int64_t s = from + done;
+    const int64_t s = from + done + step_offset;
     const int64_t pos = s % cap;
     const int64_t len = std::min(cap - pos, (to - from) - done);
     CK(cudaMemcpy(buf.data() + done * per, ring + pos * per, sizeof(T) * len * per, cudaMemcpyDeviceToHost));
@@ -1047,6 +1027,16 @@ int Impl<T>::set_state(int which, const double* in, int64_t n) {
     int e = prologue(stream);
     if (e) return e;
     CK(cudaStreamSynchronize(stream));
+    return FDTD_OK;
+  }
+  if (which == 8) {
+    if (n != 1) return fail(FDTD_EINVAL, "set_state(8): n must be 1");
+    int e = drain();
+    if (e) return e;
+    const int64_t v = (int64_t)in[0];
+    if (v < 0) return fail(FDTD_EINVAL, "set_state(8): negative step");
+    CK(cudaMemcpy(d_step, &v, sizeof(v), cudaMemcpyHostToDevice));
+    step_offset = v - host_step;
     return FDTD_OK;
   }
   return fail(FDTD_EINVAL, "set_state: bad 'which' %d", which);

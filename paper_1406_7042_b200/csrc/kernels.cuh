@@ -74,6 +74,7 @@ struct RowsE {
   const T* cs;                 // [n_rows] source coefficient
   const T* wave;               // [n_wave][n_src][B]
   int64_t n_wave, n_src;
+  T* g_out;                    // interface rows publish E^{n+1} at G[y_off] (reduced-chain input)
   // list form (for the standalone rows kernel)
   const int32_t* e_comp;       // [n_rows]
   const int64_t* e_off;        // [n_rows]
@@ -90,6 +91,7 @@ __device__ __forceinline__ T eval_row(const RowsE<T>& R, int r, int b, int B, T 
   T e = e0 - R.c[r].apply(acc);
   const int s = R.src[r];
   if (s >= 0 && step < R.n_wave) e -= R.cs[r] * R.wave[(step * R.n_src + s) * B + b];
+  if (yo >= 0) R.g_out[yo + b] = e;        // identical value from every thread computing it
   return e;
 }
 
@@ -104,7 +106,7 @@ __device__ __forceinline__ T eval_row(const RowsE<T>& R, int r, int b, int B, T 
 // Hx -= ch (Ez(j+1) - Ez(j))        Hy += ch (Ez(i+1) - Ez(i))
 // ---------------------------------------------------------------------------
 template <typename T, bool UNIFORM, int CY>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 stencil2d_rows_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restrict__ mat_id,
                       const Coef<T>* __restrict__ gtab, const uint8_t* __restrict__ gifm, int n_mat,
                       Coef<T> u0, Coef<T> u1, RowsE<T> R, const T* __restrict__ y,
@@ -344,26 +346,23 @@ struct Probes {
 
 template <typename T>
 struct FusedBlock {
-  int qe, qh, n_if, N, R, C;
-  const T* M;                   // [R][C]
+  int qe, qh, n_if, N, R, C, Cp;   // Cp: padded row pitch (multiple of 32 * VEC)
+  const T* M;                      // [R][Cp]
   int64_t e_off, h_off, y_off;
   int n_probe_rows;
   const int32_t* probe_id;
   const int32_t* probe_inst;
-  int64_t g_begin, g_end;       // gather entries of this block
 };
 
 template <typename T>
 struct FusedParams {
   const FusedBlock<T>* blocks;
   const int2* ctas;             // (block, first row)
-  int n_ctas, B;
+  int n_ctas, B, rows_per_cta;
   const T* e_in; T* e_out;      // e~^{n+1} in, e~^{n+2} out
   const T* h_in; T* h_out;      // h~^{n+1/2} in, h~^{n+3/2} out
   T* y;
-  const int32_t* g_comp;
-  const int64_t* g_off;
-  const int64_t* g_dst;
+  const T* G;                   // E_if^{n+1} published by the stencil ([n_if][N] per block)
   const T* red_base[2];         // leapfrog-path e~ / h~ buffers (probe terms 6 / 7)
   Fields<T> F;                  // coarse fields after the step
   Probes<T> pr;
@@ -375,11 +374,26 @@ struct FusedParams {
   unsigned long long* bad_step;
 };
 
-constexpr int FUSED_ROWS = 16;
+template <typename T> struct Vec;
+template <> struct Vec<float> { using type = float4; static constexpr int n = 4; };
+template <> struct Vec<double> { using type = double2; static constexpr int n = 2; };
+
+template <typename T>
+__device__ __forceinline__ T vdot(const typename Vec<T>::type& a, const typename Vec<T>::type& x);
+template <>
+__device__ __forceinline__ float vdot<float>(const float4& a, const float4& x) {
+  return a.x * x.x + a.y * x.y + a.z * x.z + a.w * x.w;
+}
+template <>
+__device__ __forceinline__ double vdot<double>(const double2& a, const double2& x) {
+  return a.x * x.x + a.y * x.y;
+}
 
 template <typename T, int NB>
 __global__ void __launch_bounds__(256)
 reduced_fused_kernel(FusedParams<T> P) {
+  using V = typename Vec<T>::type;
+  constexpr int VN = Vec<T>::n;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
   const int64_t step = *P.d_step;
@@ -389,33 +403,27 @@ reduced_fused_kernel(FusedParams<T> P) {
   if ((int)blockIdx.x < P.n_ctas) {
     const int2 ct = P.ctas[blockIdx.x];
     const FusedBlock<T> FB = P.blocks[ct.x];
-    const int C = FB.C, N = FB.N, qe = FB.qe, qh = FB.qh, ni = FB.n_if;
-    // stage X = [e~ ; G ; h~] as [N][C]
-    for (int t = threadIdx.x; t < qe * N; t += blockDim.x) X[(t % N) * C + t / N] = P.e_in[FB.e_off + t];
-    for (int t = threadIdx.x; t < qh * N; t += blockDim.x) X[(t % N) * C + qe + ni + t / N] = P.h_in[FB.h_off + t];
-    for (int t = threadIdx.x; t < ni * N; t += blockDim.x) X[(t % N) * C + qe + t / N] = (T)0;
-    __syncthreads();
-    for (int64_t t = FB.g_begin * B + threadIdx.x; t < FB.g_end * B; t += blockDim.x) {
-      const int64_t q = t / B;
-      const int bb = (int)(t % B);
-      const int64_t dst = P.g_dst[q] - FB.y_off;          // l*N + inst*B
-      const int l = (int)(dst / N), col = (int)(dst % N) + bb;
-      X[col * C + qe + l] = P.F.f[P.g_comp[q]][P.g_off[q] * B + bb];
-    }
+    const int C = FB.C, Cp = FB.Cp, N = FB.N, qe = FB.qe, qh = FB.qh, ni = FB.n_if;
+    // stage X = [e~ ; G ; h~ ; 0-padding] as [N][Cp]
+    for (int t = threadIdx.x; t < qe * N; t += blockDim.x) X[(t % N) * Cp + t / N] = P.e_in[FB.e_off + t];
+    for (int t = threadIdx.x; t < ni * N; t += blockDim.x) X[(t % N) * Cp + qe + t / N] = P.G[FB.y_off + t];
+    for (int t = threadIdx.x; t < qh * N; t += blockDim.x) X[(t % N) * Cp + qe + ni + t / N] = P.h_in[FB.h_off + t];
+    for (int t = threadIdx.x; t < (Cp - C) * N; t += blockDim.x) X[(t % N) * Cp + C + t / N] = (T)0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-    const int r1 = min(ct.y + FUSED_ROWS, FB.R);
+    const int r1 = min(ct.y + P.rows_per_cta, FB.R);
     for (int r = ct.y + warp; r < r1; r += nwarp) {
       T acc[NB];
 #pragma unroll
       for (int n = 0; n < NB; ++n) acc[n] = 0;
-      const T* a = FB.M + (int64_t)r * C;
-#pragma unroll 4
-      for (int c = lane; c < C; c += 32) {
-        const T av = a[c];
+      const V* a = reinterpret_cast<const V*>(FB.M + (int64_t)r * Cp);
+      const int nv = Cp / VN;
+#pragma unroll 8
+      for (int c = lane; c < nv; c += 32) {
+        const V av = a[c];
 #pragma unroll
         for (int n = 0; n < NB; ++n)
-          if (n < N) acc[n] += av * X[n * C + c];
+          if (n < N) acc[n] += vdot<T>(av, reinterpret_cast<const V*>(X + n * Cp)[c]);
       }
 #pragma unroll
       for (int n = 0; n < NB; ++n) {

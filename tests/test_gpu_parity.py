@@ -131,6 +131,7 @@ def test_reduced_probes_and_state_roundtrip(form):
         sim2.set_state(c, a)
     sim2.set_state(6, e6)
     sim2.set_state(7, h7)
+    sim2.set_state(8, [60.0])
     sim2.step(60)
     a = sim2.get_state(7)
     sim2.close()
