@@ -175,7 +175,7 @@ struct Impl : public fdtd_t {
   int64_t graph_kernels = 0;
   T* staging = nullptr;
   size_t staging_bytes = 0;
-  int kchunk = 16;
+  int kchunk = 32;
   int reduced_form = 0;
   // per-phase tracing
   static constexpr int NPHASE = 3;       // stencil (+ explicit rows), reduced (+ probes), leapfrog GEMVs
@@ -629,9 +629,10 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   CK(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), stream));
   staging_bytes = sizeof(T) * (size_t)std::max<int64_t>(elems, std::max(e_size, h_size));
   CK(cudaMallocHost(&staging, staging_bytes));
-  const size_t smem3 = 2 * 3 * 1024 * sizeof(T) + sizeof(fdtd::MatTable<T>);
-  CK(cudaFuncSetAttribute(fdtd::stencil3d_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
-  CK(cudaFuncSetAttribute(fdtd::stencil3d_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  const size_t smem3 = (size_t)(3 * 3 * 300 + 3 * 3 * 256 + 2 * 3 * 256) * sizeof(T) * 2 + sizeof(fdtd::MatTable<T>);
+  if (dim == 2 && elems >= ((int64_t)1 << 31)) return fail(FDTD_ENOTSUP, "2-D state too large for 32-bit offsets");
+  CK(cudaFuncSetAttribute(fdtd::stencil3d_pipe_kernel<T, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  CK(cudaFuncSetAttribute(fdtd::stencil3d_pipe_kernel<T, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   CK(cudaFuncSetAttribute(fdtd::stencil2d_rows_kernel<T, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   CK(cudaFuncSetAttribute(fdtd::stencil2d_rows_kernel<T, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   if (fused_smem > 48 * 1024) {
@@ -768,22 +769,23 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   const size_t tabsz = uniform ? 0 : sizeof(fdtd::MatTable<T>);
   const fdtd::Dims dm{nx, ny, nz, px, B, plane};
   if (dim == 3) {
+    constexpr int NS = 3;
     int BX, BY;
     if (B == 1) { BX = 32; BY = 8; }
-    else { BX = B * std::max(2, 128 / B); BY = 8; if (BX * BY > 1024) BY = std::max(2, 1024 / BX); }
+    else { BX = B * std::max(2, 32 / B); BY = std::max(2, 256 / BX); if (BX * BY > 256) BY = 256 / BX; }
     const int outx = BX / B - 1, outy = BY - 1;
     dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + outy - 1) / outy, (nz + 1 + kchunk - 1) / kchunk);
-    const size_t sm = 2 * 3 * (size_t)BX * BY * sizeof(T) + tabsz;
+    const size_t sm = (size_t)(NS * 3 * (BX + B) * (BY + 1) + NS * 3 * BX * BY + 2 * 3 * BX * BY) * sizeof(T) + tabsz;
     if (uniform)
-      fdtd::stencil3d_kernel<T, true><<<grid, dim3(BX, BY), sm, st>>>(
+      fdtd::stencil3d_pipe_kernel<T, true, NS><<<grid, dim3(BX, BY), sm, st>>>(
           dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
     else
-      fdtd::stencil3d_kernel<T, false><<<grid, dim3(BX, BY), sm, st>>>(
+      fdtd::stencil3d_pipe_kernel<T, false, NS><<<grid, dim3(BX, BY), sm, st>>>(
           dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
   } else {
     constexpr int CY = 4;
-    int BX = (B == 1) ? 32 : B * std::max(2, 64 / B), BY = 8;
-    if (BX * BY > 1024) BY = std::max(2, 1024 / BX);
+    int BX = (B == 1) ? 32 : B * std::max(2, 32 / B), BY = 8;
+    if (BX * BY > 256) BY = std::max(1, 256 / BX);
     const int outx = BX / B - 1, outy = BY * CY - 1;
     dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + outy - 1) / outy, 1);
     const size_t sm = (size_t)BX * BY * CY * sizeof(T) + tabsz;

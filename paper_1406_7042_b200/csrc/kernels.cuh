@@ -126,21 +126,21 @@ stencil2d_rows_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
   const int b = tx % B;
   const int jb = blockIdx.y * outy + ty * CY;
   const int ii = min(i, nx);
-  const int64_t sx = (i > 0) ? B : 0;
-  const int64_t rs = (int64_t)d.px * B;
+  // 32-bit element offsets (the host checks the 2-D state fits)
+  const int sx = (i > 0) ? B : 0;
+  const int rs = d.px * B;
   const int64_t step = *d_step;
   // issue every load first
   T hx[CY], hy[CY], hyim[CY], ez0[CY];
   int m[CY];
-  int64_t o[CY];
+  const int o0 = (min(jb, ny) * d.px + ii) * B + b;
 #pragma unroll
   for (int r = 0; r < CY; ++r) {
-    const int jj = min(jb + r, ny);
-    o[r] = ((int64_t)jj * d.px + ii) * B + b;
-    hx[r] = Hx0[o[r]]; hy[r] = Hy0[o[r]]; hyim[r] = Hy0[o[r] - sx]; ez0[r] = Ez0[o[r]];
-    m[r] = UNIFORM ? 0 : (int)mat_id[(int64_t)jj * d.px + ii];
+    const int o = (min(jb + r, ny) * d.px + ii) * B + b;
+    hx[r] = Hx0[o]; hy[r] = Hy0[o]; hyim[r] = Hy0[o - sx]; ez0[r] = Ez0[o];
+    m[r] = UNIFORM ? 0 : (int)mat_id[min(jb + r, ny) * d.px + ii];
   }
-  const T hx_jm = (jb > 0) ? Hx0[o[0] - rs] : (T)0;
+  const T hx_jm = (jb > 0) ? Hx0[o0 - rs] : (T)0;
   if (!UNIFORM) {
     for (int q = ty * BX + tx; q < n_mat; q += BX * BY) {
       tab->c[q][2] = gtab[q * 6 + 2];
@@ -159,10 +159,8 @@ stencil2d_rows_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
     const Coef<T> c = UNIFORM ? u0 : tab->c[m[r]][2];
     const T dd = (hy[r] - hyim[r]) - (hx[r] - hxm);
     ez[r] = (ci && j > 0 && j < ny) ? ez0[r] + c.apply(dd) : (T)0;
-    if (!UNIFORM && (tab->ifm[m[r]] & 4) && i <= nx && j <= ny) {
-      const int64_t so = (int64_t)min(j, ny) * d.px + ii;
-      ez[r] = eval_row(R, R.row_of[2][so], b, B, ez0[r], F0, y, step);
-    }
+    if (!UNIFORM && (tab->ifm[m[r]] & 4) && i <= nx && j <= ny)
+      ez[r] = eval_row(R, R.row_of[2][min(j, ny) * d.px + ii], b, B, ez0[r], F0, y, step);
     sE[(ty * CY + r) * BX + tx] = ez[r];
   }
   __syncthreads();
@@ -180,58 +178,76 @@ stencil2d_rows_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
     else { cx = tab->c[m[r]][3]; cy = tab->c[m[r]][4]; }
     const T hx1 = (ci && j < ny) ? hx[r] - cx.apply(ez_jp - ez[r]) : hx[r];
     const T hy1 = (i < nx && j > 0 && j < ny) ? hy[r] + cy.apply(ez_ip - ez[r]) : hy[r];
-    F1.f[2][o[r]] = ez[r]; F1.f[3][o[r]] = hx1; F1.f[4][o[r]] = hy1;
+    const int o = o0 + r * rs;
+    F1.f[2][o] = ez[r]; F1.f[3][o] = hx1; F1.f[4][o] = hy1;
     if (do_check) bad |= !(finite_small(ez[r]) && finite_small(hx1) && finite_small(hy1));
   }
   if (bad) atomicMin(bad_step, (unsigned long long)step);
 }
 
 // ---------------------------------------------------------------------------
-// 3-D fused E->H stencil.  Block (BX, BY) threads covers BX/B cells in x and
-// BY cells in y; it computes E^{n+1} on the whole footprint and H^{n+3/2} on
-// the footprint minus its last x cell and last y row (overlapped tiling), and
-// marches z over [k0, k1).
+// 3-D fused E->H stencil with a cp.async (LDGSTS) z-plane pipeline.
+// Block (BX, BY) threads covers BX/B cells in x and BY cells in y and marches
+// z over [k0, k1).  Planes of H (with a -x / -y halo) and of E_old stream into
+// an NS-stage shared-memory ring NS-1 planes ahead of use, so every thread
+// keeps ~(NS-1) x 6 words of HBM traffic in flight without registers.  E^{n+1}
+// is computed on the whole footprint (overlapped tiling) and H^{n+3/2} on the
+// footprint minus its last x cell and last y row.
 // ---------------------------------------------------------------------------
-template <typename T, bool UNIFORM>
-__global__ void __launch_bounds__(1024)
-stencil3d_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restrict__ mat_id,
-                 const Coef<T>* __restrict__ gtab, const uint8_t* __restrict__ gifm, int n_mat,
-                 Coef<T> u0, Coef<T> u1, RowsE<T> R, const T* __restrict__ y, int kchunk,
-                 const int64_t* __restrict__ d_step, int check_every,
-                 unsigned long long* __restrict__ bad_step) {
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+template <typename T>
+__device__ __forceinline__ void cp_async(T* dst, const T* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "n"(sizeof(T)), "r"(valid ? (int)sizeof(T) : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <typename T, bool UNIFORM, int NS>
+__global__ void __launch_bounds__(256, 3)
+stencil3d_pipe_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restrict__ mat_id,
+                      const Coef<T>* __restrict__ gtab, const uint8_t* __restrict__ gifm, int n_mat,
+                      Coef<T> u0, Coef<T> u1, RowsE<T> R, const T* __restrict__ y, int kchunk,
+                      const int64_t* __restrict__ d_step, int check_every,
+                      unsigned long long* __restrict__ bad_step) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int BX = blockDim.x, BY = blockDim.y, B = d.B;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  T* sE = reinterpret_cast<T*>(smem_raw);                       // [2][3][BY][BX]
-  MatTable<T>* tab = reinterpret_cast<MatTable<T>*>(sE + 2 * 3 * BX * BY);
+  const int HW = BX + B, HH = BY + 1;                 // H plane with halo
+  const int HP = HW * HH, EP = BX * BY;
+  T* Hs = reinterpret_cast<T*>(smem_raw);            // [NS][3][HH][HW]
+  T* Es = Hs + NS * 3 * HP;                          // [NS][3][BY][BX]
+  T* En = Es + NS * 3 * EP;                          // [2][3][BY][BX]
+  MatTable<T>* tab = reinterpret_cast<MatTable<T>*>(En + 2 * 3 * EP);
   if (!UNIFORM) {
     for (int m = ty * BX + tx; m < n_mat; m += BX * BY) {
       for (int c = 0; c < 6; ++c) tab->c[m][c] = gtab[m * 6 + c];
       tab->ifm[m] = gifm[m];
     }
   }
-  const T* __restrict__ Ex0 = F0.f[0];
-  const T* __restrict__ Ey0 = F0.f[1];
-  const T* __restrict__ Ez0 = F0.f[2];
-  const T* __restrict__ Hx0 = F0.f[3];
-  const T* __restrict__ Hy0 = F0.f[4];
-  const T* __restrict__ Hz0 = F0.f[5];
-  const int cells_x = BX / B;
-  const int outx = cells_x - 1, outy = BY - 1;
+  const int nx = d.nx, ny = d.ny, nz = d.nz;
+  const int outx = BX / B - 1, outy = BY - 1;
   const int i = blockIdx.x * outx + tx / B;
   const int b = tx % B;
   const int j = blockIdx.y * outy + ty;
   const int k0 = blockIdx.z * kchunk;
-  const int k1 = min(k0 + kchunk, d.nz + 1);
-  const bool inside = (i <= d.nx) && (j <= d.ny);
+  const int k1 = min(k0 + kchunk, nz + 1);
+  const int kend = min(k1, nz);                      // last E plane computed
+  const bool inside = (i <= nx) && (j <= ny);
   const bool own = inside && (tx / B < outx) && (ty < outy);
-  const int nx = d.nx, ny = d.ny, nz = d.nz;
-  const int64_t sx = (i > 0) ? B : 0;
-  const int64_t sy = (j > 0) ? (int64_t)d.px * B : 0;
-  const int64_t sz = d.plane * B;
   const int ii = min(i, nx), jj = min(j, ny);
   const int64_t scol = (int64_t)jj * d.px + ii;
   const int64_t col = scol * B + b;
+  const int64_t sz = d.plane * B;
+  const int xi = tx + B, yi = ty + 1;
+  // halo sources: -y row (ty == 0) and -x column (tx < B)
+  const bool hy_halo = (ty == 0), hx_halo = (tx < B);
+  const int64_t col_jm = ((int64_t)max(j - 1, 0) * d.px + ii) * B + b;
+  const int64_t col_im = ((int64_t)jj * d.px + max(i - 1, 0)) * B + b;
+  const bool ok_jm = inside && j > 0, ok_im = inside && i > 0;
   const bool ax_ij = (i < nx) && (j > 0) && (j < ny);
   const bool ay_ij = (j < ny) && (i > 0) && (i < nx);
   const bool az_ij = (i > 0) && (i < nx) && (j > 0) && (j < ny);
@@ -241,89 +257,102 @@ stencil3d_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restrict__
   const int64_t step = *d_step;
   const bool do_check = check_every > 0 && (step % check_every) == 0;
   bool bad = false;
-  __syncthreads();
 
-  auto mat_of = [&](int k) -> int { return UNIFORM ? 0 : (int)mat_id[(int64_t)k * d.plane + scol]; };
-  T hx_p = 0, hy_p = 0;
-  auto compute_E = [&](int k, T& hx_c, T& hy_c, T& hz_c, T& ex, T& ey, T& ez) {
-    const int64_t o = (int64_t)k * sz + col;
-    hx_c = Hx0[o]; hy_c = Hy0[o]; hz_c = Hz0[o];
-    const T hz_jm = Hz0[o - sy], hx_jm = Hx0[o - sy];
-    const T hz_im = Hz0[o - sx], hy_im = Hy0[o - sx];
-    const T ex0 = Ex0[o], ey0 = Ey0[o], ez0 = Ez0[o];
-    const int m = mat_of(k);
-    Coef<T> cx, cy, cz;
-    uint8_t ifm = 0;
-    if (UNIFORM) { cx = u0; cy = u0; cz = u0; }
-    else { cx = tab->c[m][0]; cy = tab->c[m][1]; cz = tab->c[m][2]; ifm = tab->ifm[m]; }
-    const bool kin = (k > 0) && (k < nz);
-    const T dx_ = (hz_c - hz_jm) - (hy_c - hy_p);
-    const T dy_ = (hx_c - hx_p) - (hz_c - hz_im);
-    const T dz_ = (hy_c - hy_im) - (hx_c - hx_jm);
-    ex = (ax_ij && kin) ? ex0 + cx.apply(dx_) : (T)0;
-    ey = (ay_ij && kin) ? ey0 + cy.apply(dy_) : (T)0;
-    ez = (az_ij && k < nz) ? ez0 + cz.apply(dz_) : (T)0;
-    if (ifm) {   // explicit rows (interface / sources)
-      const int64_t s = (int64_t)k * d.plane + scol;
-      if (ifm & 1) ex = eval_row(R, R.row_of[0][s], b, B, ex0, F0, y, step);
-      if (ifm & 2) ey = eval_row(R, R.row_of[1][s], b, B, ey0, F0, y, step);
-      if (ifm & 4) ez = eval_row(R, R.row_of[2][s], b, B, ez0, F0, y, step);
+  auto issue = [&](int k) {
+    const int st = k % NS;
+    T* h = Hs + st * 3 * HP;
+    T* e = Es + st * 3 * EP;
+    const int64_t o = (int64_t)k * sz;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      cp_async(h + c * HP + yi * HW + xi, F0.f[3 + c] + o + col, inside);
+      cp_async(e + c * EP + ty * BX + tx, F0.f[c] + o + col, inside);
+    }
+    if (hy_halo) {     // H at j-1: Hx and Hz are used
+      cp_async(h + 0 * HP + 0 * HW + xi, F0.f[3] + o + col_jm, ok_jm);
+      cp_async(h + 2 * HP + 0 * HW + xi, F0.f[5] + o + col_jm, ok_jm);
+    }
+    if (hx_halo) {     // H at i-1: Hy and Hz are used
+      cp_async(h + 1 * HP + yi * HW + tx, F0.f[4] + o + col_im, ok_im);
+      cp_async(h + 2 * HP + yi * HW + tx, F0.f[5] + o + col_im, ok_im);
     }
   };
-
-  T* sEx[2] = {sE, sE + 3 * BX * BY};
-  const int sidx = ty * BX + tx;
-  T ex_p = 0, ey_p = 0, ez_p = 0;
-  T hx_c = 0, hy_c = 0, hz_c = 0;
-  if (inside) {
-    if (k0 > 0) {
-      const int64_t o = (int64_t)(k0 - 1) * sz + col;
-      hx_p = Hx0[o]; hy_p = Hy0[o];
-    }
-    compute_E(k0, hx_c, hy_c, hz_c, ex_p, ey_p, ez_p);
+  // prologue: planes k0 .. k0+NS-2 in flight; own H of plane k0-1 in registers
+#pragma unroll
+  for (int q = 0; q < NS - 1; ++q) {
+    if (k0 + q <= kend) issue(k0 + q);
+    cp_async_commit();
   }
-  {
-    T* s = sEx[k0 & 1];
-    s[sidx] = ex_p; s[BX * BY + sidx] = ey_p; s[2 * BX * BY + sidx] = ez_p;
+  T hx_p = 0, hy_p = 0;
+  if (inside && k0 > 0) {
+    const int64_t o = (int64_t)(k0 - 1) * sz + col;
+    hx_p = F0.f[3][o]; hy_p = F0.f[4][o];
   }
-  if (own) {
-    const int64_t o = (int64_t)k0 * sz + col;
-    F1.f[0][o] = ex_p; F1.f[1][o] = ey_p; F1.f[2][o] = ez_p;
-    if (do_check) bad |= !(finite_small(ex_p) && finite_small(ey_p) && finite_small(ez_p));
-  }
-  for (int k = k0; k < k1; ++k) {
-    T ex_n = 0, ey_n = 0, ez_n = 0;
-    const T hx_k = hx_c, hy_k = hy_c, hz_k = hz_c;
-    hx_p = hx_c; hy_p = hy_c;
-    if (inside && k + 1 <= nz) compute_E(k + 1, hx_c, hy_c, hz_c, ex_n, ey_n, ez_n);
-    T* s1 = sEx[(k + 1) & 1];
-    s1[sidx] = ex_n; s1[BX * BY + sidx] = ey_n; s1[2 * BX * BY + sidx] = ez_n;
+  __syncthreads();                                   // material table
+  T hxk = 0, hyk = 0, hzk = 0;                       // H_old of the previous plane (own)
+  T exk = 0, eyk = 0, ezk = 0;                       // E_new of the previous plane (own)
+  for (int kk = k0; kk <= kend; ++kk) {
+    if (kk + NS - 1 <= kend) issue(kk + NS - 1);
+    cp_async_commit();
+    cp_async_wait<NS - 1>();
     __syncthreads();
-    if (own) {
-      const T* s0 = sEx[k & 1];
-      const T ey_ip = s0[BX * BY + sidx + B], ez_ip = s0[2 * BX * BY + sidx + B];
-      const T ex_jp = s0[sidx + BX], ez_jp = s0[2 * BX * BY + sidx + BX];
-      const int64_t o = (int64_t)k * sz + col;
-      Coef<T> cx, cy, cz;
-      if (UNIFORM) { cx = u1; cy = u1; cz = u1; }
-      else { const int m = mat_of(k); cx = tab->c[m][3]; cy = tab->c[m][4]; cz = tab->c[m][5]; }
-      const T dhx = (ez_jp - ez_p) - (ey_n - ey_p);
-      const T dhy = (ex_n - ex_p) - (ez_ip - ez_p);
-      const T dhz = (ey_ip - ey_p) - (ex_jp - ex_p);
-      const T hx1 = (hx_ij && k < nz) ? hx_k - cx.apply(dhx) : hx_k;
-      const T hy1 = (hy_ij && k < nz) ? hy_k - cy.apply(dhy) : hy_k;
-      const T hz1 = (hz_ij && k > 0 && k < nz) ? hz_k - cz.apply(dhz) : hz_k;
+    const int st = kk % NS;
+    const T* h = Hs + st * 3 * HP;
+    const T* e = Es + st * 3 * EP;
+    const T hx_c = h[0 * HP + yi * HW + xi], hy_c = h[1 * HP + yi * HW + xi], hz_c = h[2 * HP + yi * HW + xi];
+    const T hz_jm = h[2 * HP + (yi - 1) * HW + xi], hx_jm = h[0 * HP + (yi - 1) * HW + xi];
+    const T hz_im = h[2 * HP + yi * HW + xi - B], hy_im = h[1 * HP + yi * HW + xi - B];
+    const T ex0 = e[0 * EP + ty * BX + tx], ey0 = e[1 * EP + ty * BX + tx], ez0 = e[2 * EP + ty * BX + tx];
+    const int m = UNIFORM ? 0 : (int)mat_id[(int64_t)kk * d.plane + scol];
+    Coef<T> cx, cy, cz;
+    uint8_t ifmk = 0;
+    if (UNIFORM) { cx = u0; cy = u0; cz = u0; }
+    else { cx = tab->c[m][0]; cy = tab->c[m][1]; cz = tab->c[m][2]; ifmk = tab->ifm[m]; }
+    const bool kin = (kk > 0) && (kk < nz);
+    T ex = (ax_ij && kin) ? ex0 + cx.apply((hz_c - hz_jm) - (hy_c - hy_p)) : (T)0;
+    T ey = (ay_ij && kin) ? ey0 + cy.apply((hx_c - hx_p) - (hz_c - hz_im)) : (T)0;
+    T ez = (az_ij && kk < nz) ? ez0 + cz.apply((hy_c - hy_im) - (hx_c - hx_jm)) : (T)0;
+    if (!UNIFORM && ifmk && inside) {
+      const int64_t s = (int64_t)kk * d.plane + scol;
+      if (ifmk & 1) ex = eval_row(R, R.row_of[0][s], b, B, ex0, F0, y, step);
+      if (ifmk & 2) ey = eval_row(R, R.row_of[1][s], b, B, ey0, F0, y, step);
+      if (ifmk & 4) ez = eval_row(R, R.row_of[2][s], b, B, ez0, F0, y, step);
+    }
+    T* en = En + (kk & 1) * 3 * EP;
+    en[0 * EP + ty * BX + tx] = ex; en[1 * EP + ty * BX + tx] = ey; en[2 * EP + ty * BX + tx] = ez;
+    if (own && kk < k1) {
+      const int64_t o = (int64_t)kk * sz + col;
+      F1.f[0][o] = ex; F1.f[1][o] = ey; F1.f[2][o] = ez;
+      if (do_check) bad |= !(finite_small(ex) && finite_small(ey) && finite_small(ez));
+    }
+    __syncthreads();
+    if (kk > k0 && own) {       // H^{n+3/2} of plane kk-1
+      const T* e0 = En + ((kk - 1) & 1) * 3 * EP;
+      const int q = ty * BX + tx;
+      const T ey_ip = e0[1 * EP + q + B], ez_ip = e0[2 * EP + q + B];
+      const T ex_jp = e0[0 * EP + q + BX], ez_jp = e0[2 * EP + q + BX];
+      const int km = kk - 1;
+      Coef<T> hx_, hy_, hz_;
+      if (UNIFORM) { hx_ = u1; hy_ = u1; hz_ = u1; }
+      else { const int mm = (int)mat_id[(int64_t)km * d.plane + scol]; hx_ = tab->c[mm][3]; hy_ = tab->c[mm][4]; hz_ = tab->c[mm][5]; }
+      const T hx1 = (hx_ij && km < nz) ? hxk - hx_.apply((ez_jp - ezk) - (ey - eyk)) : hxk;
+      const T hy1 = (hy_ij && km < nz) ? hyk - hy_.apply((ex - exk) - (ez_ip - ezk)) : hyk;
+      const T hz1 = (hz_ij && km > 0 && km < nz) ? hzk - hz_.apply((ey_ip - eyk) - (ex_jp - exk)) : hzk;
+      const int64_t o = (int64_t)km * sz + col;
       F1.f[3][o] = hx1; F1.f[4][o] = hy1; F1.f[5][o] = hz1;
-      if (k + 1 < k1 && k + 1 <= nz) {
-        const int64_t o1 = o + sz;
-        F1.f[0][o1] = ex_n; F1.f[1][o1] = ey_n; F1.f[2][o1] = ez_n;
-      }
-      if (do_check) bad |= !(finite_small(hx1) && finite_small(hy1) && finite_small(hz1) &&
-                             finite_small(ex_n) && finite_small(ey_n) && finite_small(ez_n));
+      if (do_check) bad |= !(finite_small(hx1) && finite_small(hy1) && finite_small(hz1));
     }
-    ex_p = ex_n; ey_p = ey_n; ez_p = ez_n;
-    __syncthreads();
+    hx_p = hx_c; hy_p = hy_c;
+    hxk = hx_c; hyk = hy_c; hzk = hz_c;
+    exk = ex; eyk = ey; ezk = ez;
   }
+  // last chunk: plane nz of H has no update (Hx, Hy absent, Hz normal to the
+  // PEC wall); the new buffer still needs it
+  if (k1 == nz + 1 && own) {
+    const int64_t o = (int64_t)nz * sz + col;
+    F1.f[3][o] = hxk; F1.f[4][o] = hyk; F1.f[5][o] = hzk;
+  }
+  cp_async_wait<0>();
   if (bad) atomicMin(bad_step, (unsigned long long)step);
 }
 
