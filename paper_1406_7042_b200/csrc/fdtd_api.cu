@@ -12,11 +12,13 @@
 #include "kernels.cuh"
 
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -177,6 +179,10 @@ struct Impl : public fdtd_t {
   size_t staging_bytes = 0;
   int kchunk = 32;
   int reduced_form = 0;
+  // TMA descriptors of the 3-D stencil (per parity of the OLD buffers)
+  bool use_tma = false;
+  fdtd::TmaSet tma[2];
+  int tBX = 32, tBY = 8, tHBX = 36;
   // per-phase tracing
   static constexpr int NPHASE = 3;       // stencil (+ explicit rows), reduced (+ probes), leapfrog GEMVs
   bool prof = false;
@@ -298,6 +304,41 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       if (!F[p][c]) return fail(FDTD_ENOMEM, "field allocation failed (%lld elements)", (long long)elems);
       CK(cudaMemsetAsync(F[p][c], 0, sizeof(T) * elems, stream));
     }
+
+  // ---- TMA tensor maps for the 3-D stencil (B == 1 / aligned batches) ----
+  if (dim == 3) {
+    tBX = (B == 1) ? 32 : B * std::max(2, 32 / B);
+    tBY = (B == 1) ? 8 : std::max(2, 256 / tBX);
+    if (tBX * tBY > 256) tBY = 256 / tBX;
+    const int vec = 16 / (int)sizeof(T);
+    tHBX = ((tBX / B + 1) * B + vec - 1) / vec * vec;
+    const bool aligned = (tBX * (int)sizeof(T)) % 16 == 0 && (px * B * (int)sizeof(T)) % 16 == 0 && tHBX <= 256;
+    if (aligned) {
+      PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+      cudaDriverEntryPointQueryResult qres;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                  &qres) == cudaSuccess && encode && qres == cudaDriverEntryPointSuccess) {
+        use_tma = true;
+        const cuuint64_t gdim[3] = {(cuuint64_t)px * B, (cuuint64_t)ny + 1, (cuuint64_t)nz + 1};
+        const cuuint64_t gstr[2] = {(cuuint64_t)px * B * sizeof(T), (cuuint64_t)px * B * (ny + 1) * sizeof(T)};
+        const cuuint32_t boxH[3] = {(cuuint32_t)tHBX, (cuuint32_t)tBY + 1, 1};
+        const cuuint32_t boxE[3] = {(cuuint32_t)tBX, (cuuint32_t)tBY, 1};
+        const cuuint32_t es[3] = {1, 1, 1};
+        const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+        for (int p = 0; p < 2 && use_tma; ++p)
+          for (int c = 0; c < 3 && use_tma; ++c) {
+            CUresult r1 = encode(&tma[p].h[c], dt, 3, F[p][3 + c], gdim, gstr, boxH, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            CUresult r2 = encode(&tma[p].e[c], dt, 3, F[p][c], gdim, gstr, boxE, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) use_tma = false;
+          }
+      }
+    }
+    if (getenv("FDTD_NO_TMA")) use_tma = false;
+  }
 
   // ---- materials ----
   std::vector<double> coef;           // [n_mat][6]
@@ -633,6 +674,8 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   if (dim == 2 && elems >= ((int64_t)1 << 31)) return fail(FDTD_ENOTSUP, "2-D state too large for 32-bit offsets");
   CK(cudaFuncSetAttribute(fdtd::stencil3d_pipe_kernel<T, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   CK(cudaFuncSetAttribute(fdtd::stencil3d_pipe_kernel<T, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  CK(cudaFuncSetAttribute(fdtd::stencil3d_tma_kernel<T, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3 + 8192));
+  CK(cudaFuncSetAttribute(fdtd::stencil3d_tma_kernel<T, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3 + 8192));
   CK(cudaFuncSetAttribute(fdtd::stencil2d_rows_kernel<T, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   CK(cudaFuncSetAttribute(fdtd::stencil2d_rows_kernel<T, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   if (fused_smem > 48 * 1024) {
@@ -768,7 +811,19 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   mark(0, 0);
   const size_t tabsz = uniform ? 0 : sizeof(fdtd::MatTable<T>);
   const fdtd::Dims dm{nx, ny, nz, px, B, plane};
-  if (dim == 3) {
+  if (dim == 3 && use_tma) {
+    constexpr int NS = 3;
+    const int BX = tBX, BY = tBY;
+    const int outx = BX / B - 1, outy = BY - 1;
+    dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + outy - 1) / outy, (nz + 1 + kchunk - 1) / kchunk);
+    const size_t sm = 128 + (size_t)(NS * 3 * tHBX * (BY + 1) + NS * 3 * BX * BY + 2 * 3 * BX * BY) * sizeof(T) + tabsz;
+    if (uniform)
+      fdtd::stencil3d_tma_kernel<T, true, NS><<<grid, dim3(BX, BY), sm, st>>>(
+          tma[p], tHBX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
+    else
+      fdtd::stencil3d_tma_kernel<T, false, NS><<<grid, dim3(BX, BY), sm, st>>>(
+          tma[p], tHBX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
+  } else if (dim == 3) {
     constexpr int NS = 3;
     int BX, BY;
     if (B == 1) { BX = 32; BY = 8; }

@@ -16,6 +16,7 @@
 // H^{n+1} = H^n - ch * curl(E)  ==  H^n + ch * (K_inc^T E)
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace fdtd {
@@ -353,6 +354,183 @@ stencil3d_pipe_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
     F1.f[3][o] = hxk; F1.f[4][o] = hyk; F1.f[5][o] = hzk;
   }
   cp_async_wait<0>();
+  if (bad) atomicMin(bad_step, (unsigned long long)step);
+}
+
+// ---------------------------------------------------------------------------
+// 3-D fused E->H stencil, TMA version.  Per z-plane one elected thread issues
+// six cp.async.bulk.tensor tile loads (Hx, Hy, Hz with a -x/-y halo, Ex, Ey,
+// Ez) into an NS-stage shared-memory ring, completing on one mbarrier per
+// stage; the 256 threads only compute and store.  Out-of-range box elements
+// (the -1 halo at the low walls, the tail past nx / ny) are zero-filled by
+// the TMA unit.  Same overlapped tiling and z-march as stencil3d_pipe_kernel.
+// ---------------------------------------------------------------------------
+struct TmaSet {
+  CUtensorMap h[3];             // box (HBX, BY+1, 1), start (x0 - B, j0 - 1, k)
+  CUtensorMap e[3];             // box (BX, BY, 1),    start (x0, j0, k)
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename T, bool UNIFORM, int NS>
+__global__ void __launch_bounds__(256, 3)
+stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, Dims d, Fields<T> F0, Fields<T> F1,
+                     const uint8_t* __restrict__ mat_id, const Coef<T>* __restrict__ gtab,
+                     const uint8_t* __restrict__ gifm, int n_mat, Coef<T> u0, Coef<T> u1, RowsE<T> R,
+                     const T* __restrict__ y, int kchunk, const int64_t* __restrict__ d_step,
+                     int check_every, unsigned long long* __restrict__ bad_step) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int BX = blockDim.x, BY = blockDim.y, B = d.B;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int HW = HBX, HH = BY + 1;
+  const int HP = HW * HH, EP = BX * BY;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                // [NS]
+  T* Hs = reinterpret_cast<T*>(smem_raw + 128);                          // [NS][3][HH][HW]
+  T* Es = Hs + NS * 3 * HP;                                               // [NS][3][BY][BX]
+  T* En = Es + NS * 3 * EP;                                               // [2][3][BY][BX]
+  MatTable<T>* tab = reinterpret_cast<MatTable<T>*>(En + 2 * 3 * EP);
+  const bool leader = (tx == 0 && ty == 0);
+  if (leader) {
+    for (int q = 0; q < NS; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (!UNIFORM) {
+    for (int m = ty * BX + tx; m < n_mat; m += BX * BY) {
+      for (int c = 0; c < 6; ++c) tab->c[m][c] = gtab[m * 6 + c];
+      tab->ifm[m] = gifm[m];
+    }
+  }
+  __syncthreads();
+  const int nx = d.nx, ny = d.ny, nz = d.nz;
+  const int outx = BX / B - 1, outy = BY - 1;
+  const int i0 = blockIdx.x * outx, j0 = blockIdx.y * outy;
+  const int i = i0 + tx / B;
+  const int b = tx % B;
+  const int j = j0 + ty;
+  const int k0 = blockIdx.z * kchunk;
+  const int k1 = min(k0 + kchunk, nz + 1);
+  const int kend = min(k1, nz);
+  const bool inside = (i <= nx) && (j <= ny);
+  const bool own = inside && (tx / B < outx) && (ty < outy);
+  const int ii = min(i, nx), jj = min(j, ny);
+  const int64_t scol = (int64_t)jj * d.px + ii;
+  const int64_t col = scol * B + b;
+  const int64_t sz = d.plane * B;
+  const int xi = tx + B, yi = ty + 1;
+  const bool ax_ij = (i < nx) && (j > 0) && (j < ny);
+  const bool ay_ij = (j < ny) && (i > 0) && (i < nx);
+  const bool az_ij = (i > 0) && (i < nx) && (j > 0) && (j < ny);
+  const bool hx_ij = (i > 0) && (i < nx) && (j < ny);
+  const bool hy_ij = (j > 0) && (j < ny) && (i < nx);
+  const bool hz_ij = (i < nx) && (j < ny);
+  const int64_t step = *d_step;
+  const bool do_check = check_every > 0 && (step % check_every) == 0;
+  bool bad = false;
+  const unsigned stage_bytes = (unsigned)((3 * HP + 3 * EP) * sizeof(T));
+  auto issue = [&](int k) {                       // leader only
+    const int st = (k - k0) % NS;
+    T* h = Hs + st * 3 * HP;
+    T* e = Es + st * 3 * EP;
+    mbar_expect_tx(&bars[st], stage_bytes);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      tma_load_3d(h + c * HP, &tm.h[c], (i0 - 1) * B, j0 - 1, k, &bars[st]);
+      tma_load_3d(e + c * EP, &tm.e[c], i0 * B, j0, k, &bars[st]);
+    }
+  };
+  if (leader) {
+#pragma unroll
+    for (int q = 0; q < NS - 1; ++q)
+      if (k0 + q <= kend) issue(k0 + q);
+  }
+  T hx_p = 0, hy_p = 0;
+  if (inside && k0 > 0) {
+    const int64_t o = (int64_t)(k0 - 1) * sz + col;
+    hx_p = F0.f[3][o]; hy_p = F0.f[4][o];
+  }
+  T hxk = 0, hyk = 0, hzk = 0;
+  T exk = 0, eyk = 0, ezk = 0;
+  for (int kk = k0; kk <= kend; ++kk) {
+    if (leader && kk + NS - 1 <= kend) issue(kk + NS - 1);
+    const int st = (kk - k0) % NS;
+    mbar_wait(&bars[st], (unsigned)(((kk - k0) / NS) & 1));
+    const T* h = Hs + st * 3 * HP;
+    const T* e = Es + st * 3 * EP;
+    const T hx_c = h[0 * HP + yi * HW + xi], hy_c = h[1 * HP + yi * HW + xi], hz_c = h[2 * HP + yi * HW + xi];
+    const T hz_jm = h[2 * HP + (yi - 1) * HW + xi], hx_jm = h[0 * HP + (yi - 1) * HW + xi];
+    const T hz_im = h[2 * HP + yi * HW + xi - B], hy_im = h[1 * HP + yi * HW + xi - B];
+    const T ex0 = e[0 * EP + ty * BX + tx], ey0 = e[1 * EP + ty * BX + tx], ez0 = e[2 * EP + ty * BX + tx];
+    const int m = UNIFORM ? 0 : (int)mat_id[(int64_t)kk * d.plane + scol];
+    Coef<T> cx, cy, cz;
+    uint8_t ifmk = 0;
+    if (UNIFORM) { cx = u0; cy = u0; cz = u0; }
+    else { cx = tab->c[m][0]; cy = tab->c[m][1]; cz = tab->c[m][2]; ifmk = tab->ifm[m]; }
+    const bool kin = (kk > 0) && (kk < nz);
+    T ex = (ax_ij && kin) ? ex0 + cx.apply((hz_c - hz_jm) - (hy_c - hy_p)) : (T)0;
+    T ey = (ay_ij && kin) ? ey0 + cy.apply((hx_c - hx_p) - (hz_c - hz_im)) : (T)0;
+    T ez = (az_ij && kk < nz) ? ez0 + cz.apply((hy_c - hy_im) - (hx_c - hx_jm)) : (T)0;
+    if (!UNIFORM && ifmk && inside) {
+      const int64_t s = (int64_t)kk * d.plane + scol;
+      if (ifmk & 1) ex = eval_row(R, R.row_of[0][s], b, B, ex0, F0, y, step);
+      if (ifmk & 2) ey = eval_row(R, R.row_of[1][s], b, B, ey0, F0, y, step);
+      if (ifmk & 4) ez = eval_row(R, R.row_of[2][s], b, B, ez0, F0, y, step);
+    }
+    T* en = En + (kk & 1) * 3 * EP;
+    en[0 * EP + ty * BX + tx] = ex; en[1 * EP + ty * BX + tx] = ey; en[2 * EP + ty * BX + tx] = ez;
+    if (own && kk < k1) {
+      const int64_t o = (int64_t)kk * sz + col;
+      F1.f[0][o] = ex; F1.f[1][o] = ey; F1.f[2][o] = ez;
+      if (do_check) bad |= !(finite_small(ex) && finite_small(ey) && finite_small(ez));
+    }
+    __syncthreads();            // En of plane kk complete; stage st free for reuse after this
+    if (kk > k0 && own) {
+      const T* e0 = En + ((kk - 1) & 1) * 3 * EP;
+      const int q = ty * BX + tx;
+      const T ey_ip = e0[1 * EP + q + B], ez_ip = e0[2 * EP + q + B];
+      const T ex_jp = e0[0 * EP + q + BX], ez_jp = e0[2 * EP + q + BX];
+      const int km = kk - 1;
+      Coef<T> hx_, hy_, hz_;
+      if (UNIFORM) { hx_ = u1; hy_ = u1; hz_ = u1; }
+      else { const int mm = (int)mat_id[(int64_t)km * d.plane + scol]; hx_ = tab->c[mm][3]; hy_ = tab->c[mm][4]; hz_ = tab->c[mm][5]; }
+      const T hx1 = (hx_ij && km < nz) ? hxk - hx_.apply((ez_jp - ezk) - (ey - eyk)) : hxk;
+      const T hy1 = (hy_ij && km < nz) ? hyk - hy_.apply((ex - exk) - (ez_ip - ezk)) : hyk;
+      const T hz1 = (hz_ij && km > 0 && km < nz) ? hzk - hz_.apply((ey_ip - eyk) - (ex_jp - exk)) : hzk;
+      const int64_t o = (int64_t)km * sz + col;
+      F1.f[3][o] = hx1; F1.f[4][o] = hy1; F1.f[5][o] = hz1;
+      if (do_check) bad |= !(finite_small(hx1) && finite_small(hy1) && finite_small(hz1));
+    }
+    hx_p = hx_c; hy_p = hy_c;
+    hxk = hx_c; hyk = hy_c; hzk = hz_c;
+    exk = ex; eyk = ey; ezk = ez;
+  }
+  if (k1 == nz + 1 && own) {
+    const int64_t o = (int64_t)nz * sz + col;
+    F1.f[3][o] = hxk; F1.f[4][o] = hyk; F1.f[5][o] = hzk;
+  }
   if (bad) atomicMin(bad_step, (unsigned long long)step);
 }
 
