@@ -182,7 +182,8 @@ struct Impl : public fdtd_t {
   // TMA descriptors of the 3-D stencil (per parity of the OLD buffers)
   bool use_tma = false;
   fdtd::TmaSet tma[2];
-  int tBX = 32, tBY = 8, tHBX = 36;
+  int tBX = 32, tBY = 8, tHBX = 36, tSX = 4;
+  int64_t guard = 0;                  // elements allocated before each field (TMA halo base)
   // per-phase tracing
   static constexpr int NPHASE = 3;       // stencil (+ explicit rows), reduced (+ probes), leapfrog GEMVs
   bool prof = false;
@@ -290,7 +291,15 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     if (ex->probe_capacity > 0) cap = ex->probe_capacity;
     reduced_form = ex->reduced_form;
   }
-  px = (B == 1) ? ((nx + 1 + 31) / 32) * 32 : (nx + 1);
+  // x pitch: 128 B rows for B == 1; in 3-D keep >= SX spare elements at the end
+  // of each row so the TMA tensor map can start SX elements before a row
+  // (negative box coordinates are not used, see stencil3d_tma_kernel)
+  tSX = std::max(B, 16 / (int)sizeof(T));
+  if (B == 1) px = ((nx + 1 + (dim == 3 ? tSX : 0) + 31) / 32) * 32;
+  else {
+    px = nx + 1 + (dim == 3 ? (tSX + B - 1) / B : 0);
+    while ((px * B * (int)sizeof(T)) % 16) ++px;
+  }
   plane = (int64_t)(ny + 1) * px;
   nplanes = (dim == 3) ? (nz + 1) : 1;
   S = (int64_t)(nx + 1) * (ny + 1) * (dim == 3 ? (nz + 1) : 1);
@@ -298,11 +307,13 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   const int ncomp_first = dim == 3 ? 0 : 2, ncomp_last = dim == 3 ? 5 : 4;
 
   // ---- fields (both parities), zero initial state ----
+  guard = ((int64_t)px * B + tSX + 127) / 128 * 128;
   for (int p = 0; p < 2; ++p)
     for (int c = ncomp_first; c <= ncomp_last; ++c) {
-      F[p][c] = dalloc<T>(elems);
-      if (!F[p][c]) return fail(FDTD_ENOMEM, "field allocation failed (%lld elements)", (long long)elems);
-      CK(cudaMemsetAsync(F[p][c], 0, sizeof(T) * elems, stream));
+      T* base = dalloc<T>(elems + guard);
+      if (!base) return fail(FDTD_ENOMEM, "field allocation failed (%lld elements)", (long long)elems);
+      CK(cudaMemsetAsync(base, 0, sizeof(T) * (elems + guard), stream));
+      F[p][c] = base + guard;
     }
 
   // ---- TMA tensor maps for the 3-D stencil (B == 1 / aligned batches) ----
@@ -312,14 +323,18 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     if (tBX * tBY > 256) tBY = 256 / tBX;
     const int vec = 16 / (int)sizeof(T);
     tHBX = ((tBX / B + 1) * B + vec - 1) / vec * vec;
-    const bool aligned = (tBX * (int)sizeof(T)) % 16 == 0 && (px * B * (int)sizeof(T)) % 16 == 0 && tHBX <= 256;
+    const bool aligned = (tBX * (int)sizeof(T)) % 16 == 0 && (px * B * (int)sizeof(T)) % 16 == 0 && tHBX <= 256 &&
+                         (tSX * (int)sizeof(T)) % 16 == 0;
     if (aligned) {
       PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
       cudaDriverEntryPointQueryResult qres;
       if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
                                   &qres) == cudaSuccess && encode && qres == cudaDriverEntryPointSuccess) {
         use_tma = true;
-        const cuuint64_t gdim[3] = {(cuuint64_t)px * B, (cuuint64_t)ny + 1, (cuuint64_t)nz + 1};
+        // base = field - one row - SX elements: tensor coordinate (x', y', z) is
+        // storage (x' - SX, y' - 1, z); the halo at x = -1 / y = -1 maps to the
+        // spare end-of-row columns / the guard (finite, and only ever selected away)
+        const cuuint64_t gdim[3] = {(cuuint64_t)px * B, (cuuint64_t)ny + 2, (cuuint64_t)nz + 1};
         const cuuint64_t gstr[2] = {(cuuint64_t)px * B * sizeof(T), (cuuint64_t)px * B * (ny + 1) * sizeof(T)};
         const cuuint32_t boxH[3] = {(cuuint32_t)tHBX, (cuuint32_t)tBY + 1, 1};
         const cuuint32_t boxE[3] = {(cuuint32_t)tBX, (cuuint32_t)tBY, 1};
@@ -327,10 +342,12 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
         const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
         for (int p = 0; p < 2 && use_tma; ++p)
           for (int c = 0; c < 3 && use_tma; ++c) {
-            CUresult r1 = encode(&tma[p].h[c], dt, 3, F[p][3 + c], gdim, gstr, boxH, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CUresult r1 = encode(&tma[p].h[c], dt, 3, F[p][3 + c] - (int64_t)px * B - tSX, gdim, gstr, boxH, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE,
                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            CUresult r2 = encode(&tma[p].e[c], dt, 3, F[p][c], gdim, gstr, boxE, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CUresult r2 = encode(&tma[p].e[c], dt, 3, F[p][c] - (int64_t)px * B - tSX, gdim, gstr, boxE, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE,
                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) use_tma = false;
@@ -819,10 +836,10 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
     const size_t sm = 128 + (size_t)(NS * 3 * tHBX * (BY + 1) + NS * 3 * BX * BY + 2 * 3 * BX * BY) * sizeof(T) + tabsz;
     if (uniform)
       fdtd::stencil3d_tma_kernel<T, true, NS><<<grid, dim3(BX, BY), sm, st>>>(
-          tma[p], tHBX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
+          tma[p], tHBX, tSX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
     else
       fdtd::stencil3d_tma_kernel<T, false, NS><<<grid, dim3(BX, BY), sm, st>>>(
-          tma[p], tHBX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
+          tma[p], tHBX, tSX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
   } else if (dim == 3) {
     constexpr int NS = 3;
     int BX, BY;

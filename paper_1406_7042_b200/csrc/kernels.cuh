@@ -361,9 +361,12 @@ stencil3d_pipe_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
 // 3-D fused E->H stencil, TMA version.  Per z-plane one elected thread issues
 // six cp.async.bulk.tensor tile loads (Hx, Hy, Hz with a -x/-y halo, Ex, Ey,
 // Ez) into an NS-stage shared-memory ring, completing on one mbarrier per
-// stage; the 256 threads only compute and store.  Out-of-range box elements
-// (the -1 halo at the low walls, the tail past nx / ny) are zero-filled by
-// the TMA unit.  Same overlapped tiling and z-march as stencil3d_pipe_kernel.
+// stage; the 256 threads only compute and store.  The tensor maps start one
+// row and SX elements before each field (a zeroed guard allocation and spare
+// end-of-row columns), so box coordinates are never negative (negative TMA
+// coordinates raised an illegal-instruction fault on this driver); the tail
+// past nx / ny is zero-filled.  Same overlapped tiling and z-march as
+// stencil3d_pipe_kernel.
 // ---------------------------------------------------------------------------
 struct TmaSet {
   CUtensorMap h[3];             // box (HBX, BY+1, 1), start (x0 - B, j0 - 1, k)
@@ -398,7 +401,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 
 template <typename T, bool UNIFORM, int NS>
 __global__ void __launch_bounds__(256, 3)
-stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, Dims d, Fields<T> F0, Fields<T> F1,
+stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, Dims d, Fields<T> F0, Fields<T> F1,
                      const uint8_t* __restrict__ mat_id, const Coef<T>* __restrict__ gtab,
                      const uint8_t* __restrict__ gifm, int n_mat, Coef<T> u0, Coef<T> u1, RowsE<T> R,
                      const T* __restrict__ y, int kchunk, const int64_t* __restrict__ d_step,
@@ -451,21 +454,24 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, Dims d, Fields<
   const bool do_check = check_every > 0 && (step % check_every) == 0;
   bool bad = false;
   const unsigned stage_bytes = (unsigned)((3 * HP + 3 * EP) * sizeof(T));
-  auto issue = [&](int k) {                       // leader only
-    const int st = (k - k0) % NS;
-    T* h = Hs + st * 3 * HP;
-    T* e = Es + st * 3 * EP;
-    mbar_expect_tx(&bars[st], stage_bytes);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      tma_load_3d(h + c * HP, &tm.h[c], (i0 - 1) * B, j0 - 1, k, &bars[st]);
-      tma_load_3d(e + c * EP, &tm.e[c], i0 * B, j0, k, &bars[st]);
-    }
-  };
+  // the tensor maps are addressed in kernel-parameter space (__grid_constant__):
+  // no lambda / local copy may be taken of them
+#define FDTD_TMA_ISSUE(K)                                                              \
+  do {                                                                                 \
+    const int st_ = ((K) - k0) % NS;                                                   \
+    T* h_ = Hs + st_ * 3 * HP;                                                         \
+    T* e_ = Es + st_ * 3 * EP;                                                         \
+    mbar_expect_tx(&bars[st_], stage_bytes);                                           \
+    tma_load_3d(h_ + 0 * HP, &tm.h[0], (i0 - 1) * B + SX, j0, (K), &bars[st_]);        \
+    tma_load_3d(h_ + 1 * HP, &tm.h[1], (i0 - 1) * B + SX, j0, (K), &bars[st_]);        \
+    tma_load_3d(h_ + 2 * HP, &tm.h[2], (i0 - 1) * B + SX, j0, (K), &bars[st_]);        \
+    tma_load_3d(e_ + 0 * EP, &tm.e[0], i0 * B + SX, j0 + 1, (K), &bars[st_]);          \
+    tma_load_3d(e_ + 1 * EP, &tm.e[1], i0 * B + SX, j0 + 1, (K), &bars[st_]);          \
+    tma_load_3d(e_ + 2 * EP, &tm.e[2], i0 * B + SX, j0 + 1, (K), &bars[st_]);          \
+  } while (0)
   if (leader) {
-#pragma unroll
     for (int q = 0; q < NS - 1; ++q)
-      if (k0 + q <= kend) issue(k0 + q);
+      if (k0 + q <= kend) FDTD_TMA_ISSUE(k0 + q);
   }
   T hx_p = 0, hy_p = 0;
   if (inside && k0 > 0) {
@@ -475,7 +481,7 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, Dims d, Fields<
   T hxk = 0, hyk = 0, hzk = 0;
   T exk = 0, eyk = 0, ezk = 0;
   for (int kk = k0; kk <= kend; ++kk) {
-    if (leader && kk + NS - 1 <= kend) issue(kk + NS - 1);
+    if (leader && kk + NS - 1 <= kend) FDTD_TMA_ISSUE(kk + NS - 1);
     const int st = (kk - k0) % NS;
     mbar_wait(&bars[st], (unsigned)(((kk - k0) / NS) & 1));
     const T* h = Hs + st * 3 * HP;
@@ -532,6 +538,7 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, Dims d, Fields<
     F1.f[3][o] = hxk; F1.f[4][o] = hyk; F1.f[5][o] = hzk;
   }
   if (bad) atomicMin(bad_step, (unsigned long long)step);
+#undef FDTD_TMA_ISSUE
 }
 
 // ---------------------------------------------------------------------------
