@@ -182,7 +182,7 @@ struct Impl : public fdtd_t {
   // TMA descriptors of the 3-D stencil (per parity of the OLD buffers)
   bool use_tma = false;
   fdtd::TmaSet tma[2];
-  int tBX = 32, tBY = 8, tHBX = 36, tSX = 4;
+  int tBX = 32, tBY = 8, tHBX = 36, tSX = 4, tOUTX = 28;
   int64_t guard = 0;                  // elements allocated before each field (TMA halo base)
   // per-phase tracing
   static constexpr int NPHASE = 3;       // stencil (+ explicit rows), reduced (+ probes), leapfrog GEMVs
@@ -322,9 +322,12 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     tBY = (B == 1) ? 8 : std::max(2, 256 / tBX);
     if (tBX * tBY > 256) tBY = 256 / tBX;
     const int vec = 16 / (int)sizeof(T);
-    tHBX = ((tBX / B + 1) * B + vec - 1) / vec * vec;
+    tHBX = tBX + tSX;                                  // H box: SX halo elements + the tile
+    const int al = std::max(1, 16 / (B * (int)sizeof(T)));
+    tOUTX = (tBX / B - 1) / al * al;                   // 16-byte aligned tile origins
+    (void)vec;
     const bool aligned = (tBX * (int)sizeof(T)) % 16 == 0 && (px * B * (int)sizeof(T)) % 16 == 0 && tHBX <= 256 &&
-                         (tSX * (int)sizeof(T)) % 16 == 0;
+                         (tSX * (int)sizeof(T)) % 16 == 0 && tOUTX >= 1 && tSX >= B;
     if (aligned) {
       PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
       cudaDriverEntryPointQueryResult qres;
@@ -831,15 +834,15 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   if (dim == 3 && use_tma) {
     constexpr int NS = 3;
     const int BX = tBX, BY = tBY;
-    const int outx = BX / B - 1, outy = BY - 1;
+    const int outx = tOUTX, outy = BY - 1;
     dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + outy - 1) / outy, (nz + 1 + kchunk - 1) / kchunk);
     const size_t sm = 128 + (size_t)(NS * 3 * tHBX * (BY + 1) + NS * 3 * BX * BY + 2 * 3 * BX * BY) * sizeof(T) + tabsz;
     if (uniform)
       fdtd::stencil3d_tma_kernel<T, true, NS><<<grid, dim3(BX, BY), sm, st>>>(
-          tma[p], tHBX, tSX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
+          tma[p], tHBX, tSX, tOUTX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
     else
       fdtd::stencil3d_tma_kernel<T, false, NS><<<grid, dim3(BX, BY), sm, st>>>(
-          tma[p], tHBX, tSX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
+          tma[p], tHBX, tSX, tOUTX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
   } else if (dim == 3) {
     constexpr int NS = 3;
     int BX, BY;

@@ -362,11 +362,12 @@ stencil3d_pipe_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
 // six cp.async.bulk.tensor tile loads (Hx, Hy, Hz with a -x/-y halo, Ex, Ey,
 // Ez) into an NS-stage shared-memory ring, completing on one mbarrier per
 // stage; the 256 threads only compute and store.  The tensor maps start one
-// row and SX elements before each field (a zeroed guard allocation and spare
-// end-of-row columns), so box coordinates are never negative (negative TMA
-// coordinates raised an illegal-instruction fault on this driver); the tail
-// past nx / ny is zero-filled.  Same overlapped tiling and z-march as
-// stencil3d_pipe_kernel.
+// row and SX elements (16 bytes) before each field (a zeroed guard allocation
+// and spare end-of-row columns), and the tile origins are multiples of 16
+// bytes: box starts are then never negative and always 16-byte aligned (both
+// raised illegal-instruction faults on this driver, tools/dbg/tma_probe*).
+// The tail past nx / ny is zero-filled.  Same overlapped tiling and z-march
+// as stencil3d_pipe_kernel, with the x overlap rounded up to the alignment.
 // ---------------------------------------------------------------------------
 struct TmaSet {
   CUtensorMap h[3];             // box (HBX, BY+1, 1), start (x0 - B, j0 - 1, k)
@@ -401,7 +402,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 
 template <typename T, bool UNIFORM, int NS>
 __global__ void __launch_bounds__(256, 3)
-stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, Dims d, Fields<T> F0, Fields<T> F1,
+stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int outx, Dims d, Fields<T> F0, Fields<T> F1,
                      const uint8_t* __restrict__ mat_id, const Coef<T>* __restrict__ gtab,
                      const uint8_t* __restrict__ gifm, int n_mat, Coef<T> u0, Coef<T> u1, RowsE<T> R,
                      const T* __restrict__ y, int kchunk, const int64_t* __restrict__ d_step,
@@ -429,7 +430,7 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, Dims d,
   }
   __syncthreads();
   const int nx = d.nx, ny = d.ny, nz = d.nz;
-  const int outx = BX / B - 1, outy = BY - 1;
+  const int outy = BY - 1;                  // outx: aligned so box origins are 16-byte aligned
   const int i0 = blockIdx.x * outx, j0 = blockIdx.y * outy;
   const int i = i0 + tx / B;
   const int b = tx % B;
@@ -443,7 +444,7 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, Dims d,
   const int64_t scol = (int64_t)jj * d.px + ii;
   const int64_t col = scol * B + b;
   const int64_t sz = d.plane * B;
-  const int xi = tx + B, yi = ty + 1;
+  const int xi = tx + SX, yi = ty + 1;      // H box starts SX elements before the tile
   const bool ax_ij = (i < nx) && (j > 0) && (j < ny);
   const bool ay_ij = (j < ny) && (i > 0) && (i < nx);
   const bool az_ij = (i > 0) && (i < nx) && (j > 0) && (j < ny);
@@ -462,9 +463,9 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, Dims d,
     T* h_ = Hs + st_ * 3 * HP;                                                         \
     T* e_ = Es + st_ * 3 * EP;                                                         \
     mbar_expect_tx(&bars[st_], stage_bytes);                                           \
-    tma_load_3d(h_ + 0 * HP, &tm.h[0], (i0 - 1) * B + SX, j0, (K), &bars[st_]);        \
-    tma_load_3d(h_ + 1 * HP, &tm.h[1], (i0 - 1) * B + SX, j0, (K), &bars[st_]);        \
-    tma_load_3d(h_ + 2 * HP, &tm.h[2], (i0 - 1) * B + SX, j0, (K), &bars[st_]);        \
+    tma_load_3d(h_ + 0 * HP, &tm.h[0], i0 * B, j0, (K), &bars[st_]);                   \
+    tma_load_3d(h_ + 1 * HP, &tm.h[1], i0 * B, j0, (K), &bars[st_]);                   \
+    tma_load_3d(h_ + 2 * HP, &tm.h[2], i0 * B, j0, (K), &bars[st_]);                   \
     tma_load_3d(e_ + 0 * EP, &tm.e[0], i0 * B + SX, j0 + 1, (K), &bars[st_]);          \
     tma_load_3d(e_ + 1 * EP, &tm.e[1], i0 * B + SX, j0 + 1, (K), &bars[st_]);          \
     tma_load_3d(e_ + 2 * EP, &tm.e[2], i0 * B + SX, j0 + 1, (K), &bars[st_]);          \
