@@ -836,7 +836,9 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
     const int BX = tBX, BY = tBY;
     const int outx = tOUTX, outy = BY - 1;
     dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + outy - 1) / outy, (nz + 1 + kchunk - 1) / kchunk);
-    const size_t sm = 128 + (size_t)(NS * 3 * tHBX * (BY + 1) + NS * 3 * BX * BY + 2 * 3 * BX * BY) * sizeof(T) + tabsz;
+    const int al = 128 / (int)sizeof(T);
+    const size_t HPp = (size_t)(tHBX * (BY + 1) + al - 1) / al * al, EPp = (size_t)(BX * BY + al - 1) / al * al;
+    const size_t sm = 256 + (NS * 3 * HPp + NS * 3 * EPp + 2 * 3 * EPp) * sizeof(T) + tabsz;
     if (uniform)
       fdtd::stencil3d_tma_kernel<T, true, NS><<<grid, dim3(BX, BY), sm, st>>>(
           tma[p], tHBX, tSX, tOUTX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);

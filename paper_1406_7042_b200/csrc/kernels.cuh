@@ -411,9 +411,13 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int out
   const int BX = blockDim.x, BY = blockDim.y, B = d.B;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int HW = HBX, HH = BY + 1;
-  const int HP = HW * HH, EP = BX * BY;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);                // [NS]
-  T* Hs = reinterpret_cast<T*>(smem_raw + 128);                          // [NS][3][HH][HW]
+  // every TMA destination starts on a 128-byte boundary
+  const int al = 128 / (int)sizeof(T);
+  const int HP = (HW * HH + al - 1) / al * al, EP = (BX * BY + al - 1) / al * al;
+  const unsigned base_u = smem_u32(smem_raw);
+  unsigned char* smem_al = smem_raw + ((128u - (base_u & 127u)) & 127u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_al);                 // [NS]
+  T* Hs = reinterpret_cast<T*>(smem_al + 128);                           // [NS][3][HH][HW]
   T* Es = Hs + NS * 3 * HP;                                               // [NS][3][BY][BX]
   T* En = Es + NS * 3 * EP;                                               // [2][3][BY][BX]
   MatTable<T>* tab = reinterpret_cast<MatTable<T>*>(En + 2 * 3 * EP);
