@@ -458,7 +458,8 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int out
   const int64_t step = *d_step;
   const bool do_check = check_every > 0 && (step % check_every) == 0;
   bool bad = false;
-  const unsigned stage_bytes = (unsigned)((3 * HP + 3 * EP) * sizeof(T));
+  // transaction bytes = the boxes actually delivered (not the padded slots)
+  const unsigned stage_bytes = (unsigned)((3 * HW * HH + 3 * BX * BY) * sizeof(T));
   // the tensor maps are addressed in kernel-parameter space (__grid_constant__):
   // no lambda / local copy may be taken of them
 #define FDTD_TMA_ISSUE(K)                                                              \
