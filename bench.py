@@ -34,6 +34,9 @@ WORKLOADS = {
     2: "config2: 2-D Ez/Hx/Hy PEC cavity 1024x1024 cells of 0.5 mm, 32 dielectric inclusions, "
        "64x64-cell box refined 8x -> reduced block q=256 (recipe B), dt = 4x fine CFL, 20000 steps, fp32",
     3: "config3: 3-D PEC cavity 256^3 cells of 1 mm, random initial E, dt = 0.99 CFL, 1000 steps",
+    5: "config5: 3-D microstrip-shaped 400x200x40 cells of 0.25 mm, eps_r 3.38 substrate, PEC strips with "
+       "64 stubs, 64 z-refined (r=10) stub-tip regions reduced to q=128 in 2 shared models (32 instances "
+       "each), dt = 6x fine CFL, 50000 steps, fp32",
 }
 
 
@@ -144,7 +147,7 @@ def run_oracle_sample(prob, seconds=15.0, max_steps=400):
         su = None
         if len(rec.src_row) and done < rec.wave.shape[0]:
             su = np.zeros(len(E))
-            np.add.at(su, rec.src_row, -rec.src_coef * rec.wave[done, :, 0])
+            np.add.at(su, rec.src_row, -rec.src_coef * rec.wave[done, rec.src_col, 0])
         E, H = step_leapfrog(E, H, rec.GE, rec.GH, rec.KE, rec.KH, su_E=su)
         _ = PE @ E + PH @ H
         done += 1

@@ -116,13 +116,18 @@ typedef struct fdtd_reduced_block {
   double g_e_scalar, g_h_scalar;
 } fdtd_reduced_block;
 
-/* Sources J on coarse E unknowns (u^{n+1} = J^{n+1/2}, R2(i)). */
+/* Sources J on coarse E unknowns (u^{n+1} = J^{n+1/2}, R2(i)):
+ * E_u -= coef_u * wave[n][col_u][b].  Sources sharing a time signature (a
+ * current sheet, a gap source) share a waveform column and carry their
+ * spatial amplitude in coef. */
 typedef struct fdtd_sources {
   int64_t n_src;
-  const int64_t* unknown;   /* [n_src] E unknown ids                                */
-  const double* coef;       /* [n_src] E -= coef * J  (coef = dt / eps)             */
-  int64_t n_wave;           /* samples per source; J = 0 for steps >= n_wave         */
-  const double* wave;       /* [n_wave][n_src][batch] J^{n+1/2} for step n           */
+  const int64_t* unknown;   /* [n_src] E unknown ids                                  */
+  const double* coef;       /* [n_src] E -= coef * J  (coef = amplitude * dt / eps)   */
+  const int32_t* column;    /* [n_src] waveform column; NULL -> column s for source s */
+  int64_t n_cols;           /* waveform columns (n_src when column == NULL)           */
+  int64_t n_wave;           /* samples per column; J = 0 for steps >= n_wave           */
+  const double* wave;       /* [n_wave][n_cols][batch] J^{n+1/2} for step n           */
 } fdtd_sources;
 
 /* Probes (Eq. (10) P:170-175 for fine-region reconstruction).  kind 0: sum of

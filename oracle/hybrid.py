@@ -488,3 +488,54 @@ def reduced_system(pr, Kt_rr=None, S_E_if=None):
     De = sp.block_diag([sp.diags(pr["De_c"]), sp.csr_matrix(pr["Dt_e"])]).toarray()
     Dm = sp.block_diag([sp.diags(pr["Dm_c"]), sp.csr_matrix(pr["Dt_m"])]).toarray()
     return De, Dm, K
+
+
+def sheet_pec(sheets, boxes, dim=3):
+    """Predicate for oracle.hybrid.assemble(pec_e_extra=...): an E edge is PEC if
+    it lies in a zero-thickness plate (closed rectangle in a plane z = pos).
+    Plates are given in coarse units; fine edges are tested at their exact
+    rational positions."""
+    def test(key):
+        if key[0] == "c":
+            _, comp, (i, j, k) = key
+            lo, r = (0, 0, 0), (1, 1, 1)
+        else:
+            _, b, comp, (i, j, k) = key
+            lo, r = tuple(boxes[b]["lo"]), tuple(boxes[b]["r"])
+        if comp not in (0, 1):
+            return False
+        x = Fraction(lo[0]) + Fraction(i, r[0])
+        y = Fraction(lo[1]) + Fraction(j, r[1])
+        z = Fraction(lo[2]) + Fraction(k, r[2])
+        for sh in sheets:
+            (x0, y0), (x1, y1) = sh["lo"], sh["hi"]
+            if z != sh["pos"]:
+                continue
+            if comp == 0 and x0 <= x and x + Fraction(1, r[0]) <= x1 and y0 <= y <= y1:
+                return True
+            if comp == 1 and x0 <= x <= x1 and y0 <= y and y + Fraction(1, r[1]) <= y1:
+                return True
+        return False
+    return test
+
+
+def block_pec(boxes):
+    """Predicate for solid PEC blocks given in a box's fine node indices (closed
+    box): an E edge is PEC when both of its end nodes lie in the block."""
+    def test(key):
+        if key[0] != "f":
+            return False
+        _, b, comp, idx = key
+        for blk in boxes[b].get("pec_fine") or []:
+            lo, hi = blk["lo"], blk["hi"]
+            ok = True
+            for a in range(3):
+                lo_a = idx[a]
+                hi_a = idx[a] + (1 if a == comp else 0)
+                if not (lo[a] <= lo_a and hi_a <= hi[a]):
+                    ok = False
+                    break
+            if ok:
+                return True
+        return False
+    return test

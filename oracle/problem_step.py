@@ -51,8 +51,9 @@ class HybridRecursion:
     GH: np.ndarray
     src_row: np.ndarray      # E row of each source
     src_coef: np.ndarray
-    wave: np.ndarray         # [n_wave][n_src][B]
+    wave: np.ndarray         # [n_wave][n_cols][B]
     probe_rows: list         # per probe: (side, sparse row vector over that side)
+    src_col: np.ndarray = None   # waveform column of each source
 
 
 def build(problem) -> HybridRecursion:
@@ -228,8 +229,11 @@ def build(problem) -> HybridRecursion:
         src_row = np.array([epos[int(u)] for u in src["unknown"]], np.int64)
         src_coef = np.asarray(src["coef"], np.float64)
         wave = np.asarray(src["wave"], np.float64)
+        col = src.get("column")
+        src_col = (np.asarray(col, np.int64) if col is not None else np.arange(len(src_row)))
     else:
         src_row, src_coef, wave = np.zeros(0, np.int64), np.zeros(0), np.zeros((0, 0, 1))
+        src_col = np.zeros(0, np.int64)
 
     # ---- probes ----------------------------------------------------------------
     hposd = {int(v): i for i, v in enumerate(h_ids)}
@@ -258,7 +262,7 @@ def build(problem) -> HybridRecursion:
                 o = Nh_c + red_off[bl][1] + inst * qh
                 probe_rows.append(("H", {o + i: vrow[i] for i in range(qh) if vrow[i] != 0}))
     return HybridRecursion(dim, n, S, e_ids, h_ids, n_red, red_off, KE, KH, GE, GH,
-                           src_row, src_coef, wave, probe_rows)
+                           src_row, src_coef, wave, probe_rows, src_col)
 
 
 def initial_state(rec: HybridRecursion, problem, member=0):
@@ -305,7 +309,7 @@ def run(problem, n_steps, member=0, state=None, start_step=0, rec=None):
         if len(rec.src_row) and step < rec.wave.shape[0]:
             su = np.zeros(len(E))
             # E += -coef * J^{n+1/2}   (B holds the sign)
-            np.add.at(su, rec.src_row, -rec.src_coef * rec.wave[step, :, member])
+            np.add.at(su, rec.src_row, -rec.src_coef * rec.wave[step, rec.src_col, member])
         E, H = step_leapfrog(E, H, rec.GE, rec.GH, rec.KE, rec.KH, su_E=su)
         probes[s] = PE @ E + PH @ H
     return E, H, probes, rec

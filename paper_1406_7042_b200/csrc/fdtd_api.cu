@@ -489,12 +489,20 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       gdst.push_back((int64_t)l * D.N + (int64_t)in * B);        // within the block's [n_if][N]
     }
   }
-  int64_t n_src = 0, n_wave = 0;
+  int64_t n_src = 0, n_wave = 0, n_cols = 0;
   std::vector<T> wave;
+  std::vector<int32_t> wcol;
   if (src && src->n_src > 0) {
     n_src = src->n_src; n_wave = src->n_wave;
-    if (!src->unknown || !src->coef || (n_wave > 0 && !src->wave)) return fail(FDTD_EINVAL, "sources: missing arrays");
-    wave.resize((size_t)(n_wave * n_src * B));
+    n_cols = src->column ? src->n_cols : n_src;
+    if (!src->unknown || !src->coef || (n_wave > 0 && !src->wave) || n_cols < 1)
+      return fail(FDTD_EINVAL, "sources: missing arrays");
+    wcol.resize(n_src);
+    for (int64_t q = 0; q < n_src; ++q) {
+      wcol[q] = src->column ? src->column[q] : (int32_t)q;
+      if (wcol[q] < 0 || wcol[q] >= n_cols) return fail(FDTD_EINVAL, "source %lld: waveform column out of range", (long long)q);
+    }
+    wave.resize((size_t)(n_wave * n_cols * B));
     for (size_t q = 0; q < wave.size(); ++q) wave[q] = (T)src->wave[q];
     for (int64_t s_ = 0; s_ < n_src; ++s_) {
       const int64_t u = src->unknown[s_];
@@ -567,7 +575,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   // upload explicit rows
   {
     const int64_t nr = (int64_t)hrows.size();
-    rows.n_rows = nr; rows.n_wave = n_wave; rows.n_src = n_src;
+    rows.n_rows = nr; rows.n_wave = n_wave; rows.n_src = n_cols;     // n_src: waveform columns
     std::vector<int32_t> ec(nr), hc, srcv(nr);
     std::vector<int64_t> eo(nr), rp(nr + 1, 0), ho, yo(nr);
     std::vector<fdtd::Coef<T>> cc(nr);
@@ -575,7 +583,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     for (int64_t r = 0; r < nr; ++r) {
       const HRow& h = hrows[r];
       ec[r] = h.comp; eo[r] = dev_off(h.s); cc[r] = make_coef<T>(h.c);
-      yo[r] = h.y; srcv[r] = h.src; cs[r] = (T)h.cs;
+      yo[r] = h.y; srcv[r] = h.src >= 0 ? wcol[h.src] : -1; cs[r] = (T)h.cs;
       for (auto& pw : h.w) {
         hc.push_back((int)(pw.first / S)); ho.push_back(dev_off(pw.first % S)); w.push_back((T)pw.second);
       }

@@ -71,9 +71,9 @@ struct RowsE {
   const int64_t* h_off;        // [nnz]
   const T* w;                  // [nnz]
   const int64_t* y_off;        // [n_rows] offset into y (block base + local*N + inst*B), -1 none
-  const int32_t* src;          // [n_rows] source index or -1
-  const T* cs;                 // [n_rows] source coefficient
-  const T* wave;               // [n_wave][n_src][B]
+  const int32_t* src;          // [n_rows] waveform column or -1
+  const T* cs;                 // [n_rows] source coefficient (amplitude * dt / eps)
+  const T* wave;               // [n_wave][n_src][B]   (n_src = number of waveform columns)
   int64_t n_wave, n_src;
   T* g_out;                    // interface rows publish E^{n+1} at G[y_off] (reduced-chain input)
   // list form (for the standalone rows kernel)

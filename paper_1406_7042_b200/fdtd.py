@@ -61,8 +61,8 @@ class ReducedBlock(C.Structure):
 
 
 class Sources(C.Structure):
-    _fields_ = [("n_src", C.c_int64), ("unknown", _i64p), ("coef", _f64p), ("n_wave", C.c_int64),
-                ("wave", _f64p)]
+    _fields_ = [("n_src", C.c_int64), ("unknown", _i64p), ("coef", _f64p), ("column", _i32p),
+                ("n_cols", C.c_int64), ("n_wave", C.c_int64), ("wave", _f64p)]
 
 
 class Probes(C.Structure):
@@ -221,6 +221,11 @@ class Sim:
                 wv = np.ascontiguousarray(np.broadcast_to(wv, (wv.shape[0], wv.shape[1], self.B)))
             keep += [u, cf, wv]
             src.n_src, src.unknown, src.coef = len(u), _ptr(u, C.c_int64), _ptr(cf, C.c_double)
+            if s.get("column") is not None:
+                col = _arr(s["column"], np.int32)
+                keep.append(col)
+                src.column = _ptr(col, C.c_int32)
+            src.n_cols = wv.shape[1]
             src.n_wave, src.wave = wv.shape[0], _ptr(wv, C.c_double)
         prb = Probes()
         plist = problem.get("probes") or []

@@ -22,7 +22,7 @@ import scipy.sparse.linalg as spla
 
 from . import fit, reduce
 
-PREP_VERSION = 7
+PREP_VERSION = 8
 CACHE_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))),
                          "cache", "prep")
 
@@ -123,9 +123,32 @@ def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=N
     dt_c = d / (scn["c0"] * math.sqrt(dim))
     alpha = 0.5 * (1.0 - (dt / dt_c) ** 2) if boxes else 0.0
     bas = scn.get("basis") or {}
+    # congruent regions share one reduced model ("model" class): basis,
+    # projection and enforcement run on the first instance; the others must
+    # carry identical local matrices (translated copies)
+    classes = {}
+    for bi, b in enumerate(boxes):
+        classes.setdefault(int(b.get("model", bi)), []).append(bi)
+    class_ids = sorted(classes)
+    box_class = {bi: (ci, classes[c].index(bi)) for ci, c in enumerate(class_ids) for bi in classes[c]}
+    for c in class_ids:
+        first = P.boxes[classes[c][0]]
+        for bi in classes[c][1:]:
+            other = P.boxes[bi]
+            same = (other.Kff.shape == first.Kff.shape and other.Kcf.shape == first.Kcf.shape and
+                    abs(other.Kff - first.Kff).max() <= 1e-12 * abs(first.Kff).max() and
+                    abs(other.Kcf - first.Kcf).max() <= 1e-12 * abs(first.Kcf).max() and
+                    np.allclose(other.De_f, first.De_f, rtol=1e-13) and np.allclose(other.Dm_f, first.Dm_f, rtol=1e-13))
+            if not same:
+                raise ValueError(f"box {bi} is not a translated copy of box {classes[c][0]} (model {c})")
     for bi, part in enumerate(P.boxes):
+        if box_class[bi][1] != 0:
+            continue
         q = int(boxes[bi]["q"])
-        pts = reduce.expansion_points(bas.get("M", 1.1), bas.get("L", 2), bas.get("fmax", 30e9), dt)
+        if bas.get("points") == "zero":
+            pts = [0.0]          # the paper's z = 0 fast path, reading R5(viii)
+        else:
+            pts = reduce.expansion_points(bas.get("M", 1.1), bas.get("L", 2), bas.get("fmax", 30e9), dt)
         t1 = time.time()
         if bas.get("recipe", "A") == "A":
             full = full or hybrid_system(P)
@@ -152,8 +175,9 @@ def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=N
         Kp, SEp, rep = reduce.enforce_block(Kt, SE, De_if, alpha, dt)
         rep.update(t_basis=time.time() - t1, q=q)
         info.setdefault("blocks", []).append(rep)
-        blocks.append(dict(q=q, qe=q, qh=q, n_inst=1, K=Kp, S_E=SEp, g_e=float(dt), g_h=float(dt),
-                           V1=V1, V2=V2, Kt_pre=Kt, S_E_pre=SE, if_ids=part.if_ids))
+        blocks.append(dict(q=q, qe=q, qh=q, n_inst=len(classes[class_ids[box_class[bi][0]]]), K=Kp, S_E=SEp,
+                           g_e=float(dt), g_h=float(dt), V1=V1, V2=V2, Kt_pre=Kt, S_E_pre=SE,
+                           if_ids=part.if_ids))
     if boxes and (check_coarse if check_coarse is not None else 6 * S < 8_000_000):
         full = full or hybrid_system(P)
         sc = coarse_piece_sigma(P, alpha, full)
@@ -171,14 +195,29 @@ def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=N
     # wall-PEC / padding positions carry the regular coefficient: the kernels
     # mask them by index, so only box interiors (holes) need a 0 in the table
     hole = _hole_masks(P)
+    pecx = _pec_extra(scn)
+    if pecx is not None:                   # interior PEC (plates): inert like holes
+        for c in ecomps:
+            hole[c] = hole[c] | pecx(-1, c, shp).ravel()
     for c in ecomps:
         reg = ~hole[c] & ~is_if[c]
         coef[c, reg] = dt / (own_eps.ravel()[reg] * d)          # cb = dt/(eps delta)
         ifm[is_if[c]] |= (1 << c)
     for c in hcomps:
         coef[c, ~hole[c]] = dt / (mu0 * d)                      # ch = dt/(mu delta), R8
+    # distinct (coefficients, interface bits) rows -> material table; per-column
+    # codes first so that 10^7-row grids take seconds
+    codes, vals = [], []
+    for col in list(coef) + [ifm.astype(np.float64)]:
+        u, inv = np.unique(col, return_inverse=True)
+        codes.append(inv.astype(np.int64))
+        vals.append(u)
+    key = np.zeros(S, np.int64)
+    for cd, u in zip(codes, vals):
+        key = key * len(u) + cd
+    ukey, first, mid = np.unique(key, return_index=True, return_inverse=True)
     tab = np.concatenate([coef.T, ifm[:, None].astype(np.float64)], axis=1)
-    uniq, mid = np.unique(tab, axis=0, return_inverse=True)
+    uniq = tab[first]
     if len(uniq) > 256:
         raise RuntimeError(f"{len(uniq)} material classes > 256")
     prob = dict(name=scn.get("name"), dim=dim, n=P.n, delta=d, dt=dt, batch=int(scn.get("batch", 1)),
@@ -194,16 +233,19 @@ def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=N
         Wc = P.W.tocsr()
         blk = np.zeros(len(P.if_ids), np.int32)
         loc = np.zeros(len(P.if_ids), np.int32)
+        ins = np.zeros(len(P.if_ids), np.int32)
         for bi, part in enumerate(P.boxes):
-            blk[part.if_rows] = bi
+            ci, inst = box_class[bi]
+            blk[part.if_rows] = ci
+            ins[part.if_rows] = inst
             loc[part.if_rows] = np.arange(len(part.if_rows))
         cif = np.array([dt / P.De_c[int(f // S)].ravel()[int(f % S)] for f in P.if_ids])
         prob["interface"] = dict(unknown=P.if_ids.astype(np.int64), c=cif, rowptr=Wc.indptr.astype(np.int64),
                                  col=Wc.indices.astype(np.int64), val=Wc.data.copy(), block=blk,
-                                 inst=np.zeros(len(P.if_ids), np.int32), local=loc)
+                                 inst=ins, local=loc)
     else:
         prob["interface"] = None
-    prob["blocks"] = [dict(q=b["q"], qe=b["qe"], qh=b["qh"], n_inst=1, K=b["K"], S_E=b["S_E"],
+    prob["blocks"] = [dict(q=b["q"], qe=b["qe"], qh=b["qh"], n_inst=b["n_inst"], K=b["K"], S_E=b["S_E"],
                            g_e=b["g_e"], g_h=b["g_h"]) for b in blocks]
 
     # ---- sources, probes -----------------------------------------------------------------
@@ -218,8 +260,11 @@ def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=N
                 cf.append(dt / P.De_c[int(c)].ravel()[s] * d)
             else:
                 cf.append(dt / own_eps.ravel()[s])              # G_E * delta = dt/eps
-        prob["sources"] = dict(unknown=np.array(u, np.int64), coef=np.array(cf),
+        amp = np.asarray(src.get("amp", np.ones(len(u))), np.float64)
+        prob["sources"] = dict(unknown=np.array(u, np.int64), coef=np.array(cf) * amp,
                                wave=np.asarray(src["wave"], np.float64))
+        if src.get("column") is not None:
+            prob["sources"]["column"] = np.asarray(src["column"], np.int32)
     else:
         prob["sources"] = None
     prob["probes"] = []
@@ -270,16 +315,60 @@ def _init(scn):
 
 
 def _pec_extra(scn):
+    """Zero-thickness PEC plates (scenario 'pec_sheets', normal axis z): every E
+    edge lying in the plate (closed rectangle) is eliminated, in the coarse grid
+    and in the refined boxes alike (S:137 elimination, R1(ii))."""
     sheets = scn.get("pec_sheets") or []
-    fine_blocks = [(bi, pb) for bi, b in enumerate(scn.get("boxes") or []) for pb in (b.get("pec_fine") or [])]
-    if not sheets and not fine_blocks:
+    boxes = scn.get("boxes") or []
+    blocks_f = {bi: b.get("pec_fine") or [] for bi, b in enumerate(boxes)}
+    if not sheets and not any(blocks_f.values()):
         return None
+    dim = scn["dim"]
+
+    def solid(grid, comp, shape):
+        """solid PEC blocks given in a box's fine node indices (closed): every
+        E edge with both end nodes in the block"""
+        m = np.zeros(shape, bool)
+        if grid < 0 or not blocks_f.get(grid):
+            return m
+        k, j, i = np.indices(shape)
+        ijk = (i, j, k)
+        for blk in blocks_f[grid]:
+            lo, hi = blk["lo"], blk["hi"]
+            inside = np.ones(shape, bool)
+            for a in range(3):
+                if a == comp:
+                    inside &= (ijk[a] >= lo[a]) & (ijk[a] + 1 <= hi[a])
+                else:
+                    inside &= (ijk[a] >= lo[a]) & (ijk[a] <= hi[a])
+            m |= inside
+        return m
 
     def f(grid, comp, shape):
-        # zero-thickness PEC plates in the coarse grid (and their fine copies) and
-        # solid PEC blocks given in fine coordinates: E edges lying in them
         m = np.zeros(shape, bool)
-        if comp >= 3:
+        if comp > 2 or dim != 3:
             return m
+        m |= solid(grid, comp, shape)
+        if comp not in (0, 1) or not sheets:
+            return m
+        if grid < 0:
+            lo, r = (0, 0, 0), (1, 1, 1)
+        else:
+            b = boxes[grid]
+            lo, r = tuple(b["lo"]), tuple(b["r"])
+        k, j, i = np.indices(shape)
+        # integer coarse-unit coordinates scaled by r: X*rx = lo_x*rx + i
+        X = lo[0] * r[0] + i
+        Y = lo[1] * r[1] + j
+        Z = lo[2] * r[2] + k
+        for sh in sheets:
+            if sh["axis"] != 2:
+                raise NotImplementedError("PEC sheets normal to z only")
+            (x0, y0), (x1, y1) = sh["lo"], sh["hi"]
+            onz = Z == sh["pos"] * r[2]
+            if comp == 0:      # Ex edge from X to X+1 (fine units) at Y
+                m |= onz & (X >= x0 * r[0]) & (X + 1 <= x1 * r[0]) & (Y >= y0 * r[1]) & (Y <= y1 * r[1])
+            else:              # Ey edge from Y to Y+1 at X
+                m |= onz & (X >= x0 * r[0]) & (X <= x1 * r[0]) & (Y >= y0 * r[1]) & (Y + 1 <= y1 * r[1])
         return m
     return f

@@ -81,7 +81,7 @@ class Fit:
     K: tuple = None                                # COO (e_comp, e_flat, h_comp, h_flat, val)
 
 
-def build_fit(dim, n, h, dom, eps_cell, mu_cell, pec):
+def build_fit(dim, n, h, dom, eps_cell, mu_cell, pec, need_K=True):
     """dom: bool cells [nz][ny][nx]; eps_cell/mu_cell: absolute eps/mu per cell;
     pec: comp -> bool storage mask of PEC-eliminated unknowns."""
     n = tuple(int(v) for v in n)
@@ -104,6 +104,9 @@ def build_fit(dim, n, h, dom, eps_cell, mu_cell, pec):
         F.cnt[c] = np.where(act, cnt, 0)
         F.D[c] = np.where(act, mu_cell[own] * (vol / h[a]) * Lt, 0.0)
         F.active[c] = act
+    if not need_K:
+        F.K = tuple(np.zeros(0, t) for t in (np.int8, np.int64, np.int8, np.int64, np.float64))
+        return F
     # K entries, face by face
     S = int(np.prod(sshape(n, dim)))
     ec_l, ef_l, hc_l, hf_l, v_l = [], [], [], [], []
@@ -233,7 +236,7 @@ def assemble(dim, n, delta, eps_r, boxes, eps0, mu0, pec_extra=None):
         for c in pec:
             pec[c] = pec[c] | pec_extra(-1, c, shp)
     hz = delta if dim == 3 else 1.0
-    coarse = build_fit(dim, n, (delta, delta, hz), dom, eps, mu, pec)
+    coarse = build_fit(dim, n, (delta, delta, hz), dom, eps, mu, pec, need_K=bool(boxes))
     ecomps, hcomps = comps_of(dim)
     De_c = {c: coarse.D[c] / scale for c in ecomps}
     Dm_c = {c: coarse.D[c] / scale for c in hcomps}

@@ -38,18 +38,27 @@ class ShiftedSolver:
     A11 = (z-1) De/dt, A12 = K, A21 = -z K^T, A22 = (z-1) Dm/dt."""
 
     def __init__(self, De, Dm, K, dt, z):
-        self.z, self.dt = z, dt
-        self.K = K.tocsr().astype(np.complex128)
-        self.KT = K.T.tocsr().astype(np.complex128)
-        self.a11 = (z - 1.0) * De / dt
-        self.a22 = (z - 1.0) * Dm / dt
-        # Schur complement A11 - A12 A22^-1 A21 = A11 + z K A22^-1 K^T
-        Sc = sp.diags(self.a11) + z * (self.K @ sp.diags(1.0 / self.a22) @ self.KT)
-        self.lu = spla.splu(Sc.tocsc())
+        z = complex(z)
+        self.real = z.imag == 0.0
+        self.z = z.real if self.real else z
+        self.dt = dt
+        dtype = np.float64 if self.real else np.complex128
+        self.K = K.tocsr().astype(dtype)
+        self.KT = K.T.tocsr().astype(dtype)
+        self.a11 = (self.z - 1.0) * De / dt
+        self.a22 = (self.z - 1.0) * Dm / dt
+        if self.z == 0:
+            # the z = 0 fast path of P:371: R - F is block upper triangular,
+            # so the solve is a back substitution (no factorisation)
+            self.lu = None
+        else:
+            # Schur complement A11 - A12 A22^-1 A21 = A11 + z K A22^-1 K^T
+            Sc = sp.diags(self.a11) + self.z * (self.K @ sp.diags(1.0 / self.a22) @ self.KT)
+            self.lu = spla.splu(Sc.tocsc())
 
     def solve(self, b1, b2):
         rhs = b1 - self.K @ (b2 / self.a22[:, None])
-        x1 = self.lu.solve(rhs)
+        x1 = rhs / self.a11[:, None] if self.lu is None else self.lu.solve(rhs)
         x2 = (b2 + self.z * (self.KT @ x1)) / self.a22[:, None]
         return x1, x2
 
@@ -105,7 +114,7 @@ class _Basis:
         return self.Vt[:self.k].T
 
 
-def krylov_basis(De, Dm, K, dt, B, keep_e, keep_h, q, points, max_iter=None):
+def krylov_basis(De, Dm, K, dt, B, keep_e, keep_h, q, points, max_iter=None, window_bytes=4e9):
     """Multi-point block Arnoldi on (R+F)/(R-F) of the lossless system (De, Dm, K)
     started at A(z)^{-1} B; the rows keep_e / keep_h of each realified Krylov
     block feed the V1 / V2 pools (round-robin over the points, R5(iv)).
@@ -117,16 +126,29 @@ def krylov_basis(De, Dm, K, dt, B, keep_e, keep_h, q, points, max_iter=None):
     solvers = [ShiftedSolver(De, Dm, K, dt, z) for z in points]
     cap = 2 * max_iter * B.shape[1] // max(len(points), 1) + 4 * B.shape[1]
     cap = min(cap, 4 * q + 4 * B.shape[1])
+    # large systems keep only a window of recent Krylov blocks per point for
+    # the re-orthogonalisation (partial reorthogonalisation); the V pools are
+    # always fully orthogonalised
+    if (Ne + Nh) * cap * 16 > window_bytes:
+        cap = max(4 * B.shape[1], int(window_bytes // ((Ne + Nh) * 16)) // B.shape[1] * B.shape[1])
+        windowed = True
+    else:
+        windowed = False
     Qs, nxt = [], []
     for s in solvers:
-        x1, x2 = s.solve(B[:Ne].astype(np.complex128), B[Ne:].astype(np.complex128))
-        Qs.append(_Basis(Ne + Nh, cap, np.complex128, 1e-10))
+        dt_ = np.float64 if s.real else np.complex128
+        x1, x2 = s.solve(B[:Ne].astype(dt_), B[Ne:].astype(dt_))
+        Qs.append(_Basis(Ne + Nh, cap, dt_, 1e-10))
         nxt.append(np.vstack([x1, x2]))
     it = 0
     while not (P1.k >= q and P2.k >= q) and it < max_iter:
         progressed = False
         for pi, s in enumerate(solvers):
             Q, X = Qs[pi], nxt[pi]
+            if windowed and Q.k + X.shape[1] > Q.Vt.shape[0]:
+                keep = Q.Vt.shape[0] // 2               # slide the window
+                Q.Vt[:keep] = Q.Vt[Q.k - keep:Q.k]
+                Q.k = keep
             if X.shape[1] == 0 or Q.k >= Q.Vt.shape[0]:
                 continue
             idx = Q.add(X)
@@ -135,7 +157,7 @@ def krylov_basis(De, Dm, K, dt, B, keep_e, keep_h, q, points, max_iter=None):
                 continue
             progressed = True
             Wb = Q.Vt[idx].T
-            real = np.hstack([Wb.real, Wb.imag]) if abs(s.z.imag) > 0 else Wb.real
+            real = Wb if s.real else np.hstack([Wb.real, Wb.imag])
             P1.add(real[:Ne][keep_e], q)
             P2.add(real[Ne:][keep_h], q)
             # next block: A^{-1} (R+F) W,   (R+F) = [[De/dt, 0], [-K^T, Dm/dt]]

@@ -7,7 +7,8 @@ A scenario is a plain dict (all geometry in coarse cell units):
   boxes: [dict(lo, hi, r, q, model, pec_fine)]  refined regions
   pec_sheets: [dict(axis, plane, lo, hi)]        zero-thickness PEC plates
   dt [s], n_steps, precision (32|64), batch B,
-  sources: dict(comp [ns], idx [ns, 3], wave [n_steps][ns][B])  J^{n+1/2}
+  sources: dict(comp [ns], idx [ns, 3], wave [n_steps][n_cols][B], optional
+           column [ns] (shared waveform columns) and amp [ns])     J^{n+1/2}
   probes: [dict(terms=[(comp, (i, j, k), weight), ...])]
   init: None | {comp: array [B][storage]}
   basis: dict(recipe, L, M, fmax, p, seed)
@@ -184,6 +185,107 @@ def cavity3d_random(name, config_id, nx, ny, nz, delta, dt_factor, n_steps, prec
 
 
 # ---------------------------------------------------------------------------
+# 3-D rectangular waveguide with a thin refined iris (config 4 and a variant)
+# ---------------------------------------------------------------------------
+
+def waveguide3d(name, config_id, nx, ny, nz, delta, slab, rx, iris_cells, aperture_y, q, batch,
+                src_x, probe, dt_factor, n_steps, precision, seed=None):
+    """PEC-walled guide, coarse x-cells [slab[0], slab[1])
+    refined r_x over the full cross-section (tensor-graded, conformal in y, z),
+    a PEC iris of iris_cells fine cells at the slab centre with a centred
+    aperture of aperture_y cells (full height); B excitations: a Jz sheet with
+    the TE10 profile sin(pi y / b) at x = src_x, modulated Gaussians with seeded
+    centre frequencies f_c ~ U[0.5, 2] x the TE10 cutoff c/(2b), -20 dB at
+    +-f_c/4; one Ez probe per member."""
+    rng = np.random.default_rng(SEED0 + config_id if seed is None else seed)
+    nfx = (slab[1] - slab[0]) * rx
+    fx0 = nfx // 2 - iris_cells // 2
+    a0 = (ny - aperture_y) // 2
+    a1 = a0 + aperture_y
+    iris = [dict(lo=(fx0, 0, 0), hi=(fx0 + iris_cells, a0, nz)),
+            dict(lo=(fx0, a1, 0), hi=(fx0 + iris_cells, ny, nz))]
+    boxes = [dict(lo=(slab[0], 0, 0), hi=(slab[1], ny, nz), r=(rx, 1, 1), q=q, model=0, pec_fine=iris)]
+    fcut = C0 / (2 * ny * delta)
+    fc = rng.uniform(0.5, 2.0, size=batch) * fcut
+    dt = dt_factor * cfl_coarse(3, delta)
+    t = _times(dt, n_steps)
+    wave = np.zeros((n_steps, 1, batch))
+    for b in range(batch):
+        wave[:, 0, b] = _mod_gauss(t, fc[b], gaussian_tau(fc[b] / 4.0))
+    idx = [(src_x, j, k) for j in range(1, ny) for k in range(nz)]
+    amp = np.array([math.sin(math.pi * j / ny) for (_, j, _) in idx])
+    sources = dict(comp=np.full(len(idx), 2), idx=np.array(idx), column=np.zeros(len(idx), np.int32),
+                   amp=amp, wave=wave)
+    probes = [dict(terms=[(2, probe, 1.0)])]
+    basis = dict(recipe="B", points="zero", p=8, seed=SEED0 + config_id)
+    return dict(name=name, config_id=config_id, dim=3, n=(nx, ny, nz), delta=delta, eps0=EPS0, mu0=MU0,
+                c0=C0, eps_r=np.ones((nz, ny, nx)), boxes=boxes, pec_sheets=[], dt=dt, dt_factor=dt_factor,
+                n_steps=n_steps, precision=precision, batch=batch, sources=sources, probes=probes,
+                init=None, basis=basis, fc=fc)
+
+
+# ---------------------------------------------------------------------------
+# 3-D microstrip-filter-shaped domain (config 5 and a small variant)
+# ---------------------------------------------------------------------------
+
+def _stub_positions(rng, n, lo, hi, width, spacing):
+    """n stub x-starts in [lo, hi - width] with pairwise spacing >= spacing:
+    the slack beyond the minimum spacing is split at random (seeded)."""
+    span = (hi - width) - lo
+    slack = span - (n - 1) * spacing
+    if slack < 0:
+        raise ValueError("stubs do not fit")
+    cuts = np.sort(rng.integers(0, slack + 1, size=n))
+    return [int(lo + q * spacing + c) for q, c in enumerate(cuts)]
+
+
+def microstrip3d(name, config_id, nx, ny, nz, delta, n_stub_side, line_x, line_w, sub_k, eps_sub,
+                 stub_w, stub_len, region_xy, region_z, rz, q, dt_factor, n_steps, precision,
+                 f20db=30e9, seed=None, spacing=10):
+    """PEC box, substrate eps_r in z-cells [0, sub_k),
+    zero-thickness PEC strips at z = sub_k (a through-line of width line_w,
+    y-centred, x in [line_x[0], line_x[1]], and n_stub_side open stubs of width
+    stub_w on each side), one refined region (r_z) around every stub tip.
+    Regions of one side are exact translated copies -> two shared models."""
+    rng = np.random.default_rng(SEED0 + config_id if seed is None else seed)
+    eps = np.ones((nz, ny, nx))
+    eps[:sub_k] = eps_sub
+    y0 = (ny - line_w) // 2
+    y1 = y0 + line_w
+    zs = sub_k
+    sheets = [dict(axis=2, pos=zs, lo=(line_x[0], y0), hi=(line_x[1], y1))]
+    boxes = []
+    for side, model in ((+1, 0), (-1, 1)):
+        xs = _stub_positions(rng, n_stub_side, line_x[0] + 4, line_x[1] - 4, stub_w, spacing)
+        lens = rng.integers(stub_len[0], stub_len[1] + 1, size=n_stub_side)
+        for sx, L in zip(xs, lens):
+            L = int(L)
+            if side > 0:
+                tip = y1 + L
+                sheets.append(dict(axis=2, pos=zs, lo=(sx, y1), hi=(sx + stub_w, tip)))
+            else:
+                tip = y0 - L
+                sheets.append(dict(axis=2, pos=zs, lo=(sx, tip), hi=(sx + stub_w, y0)))
+            bx0 = sx - (region_xy - stub_w) // 2
+            by0 = tip - region_xy // 2
+            boxes.append(dict(lo=(bx0, by0, region_z[0]), hi=(bx0 + region_xy, by0 + region_xy, region_z[1]),
+                              r=(1, 1, rz), q=q, model=model, pec_fine=[]))
+    dt = dt_factor * cfl_coarse(3, delta)
+    t = _times(dt, n_steps)
+    w = _gauss(t, gaussian_tau(f20db))
+    src_idx = [(line_x[0], j, k) for j in range(y0, y1) for k in range(0, zs)]
+    sources = dict(comp=np.full(len(src_idx), 2), idx=np.array(src_idx),
+                   column=np.zeros(len(src_idx), np.int32), wave=w.reshape(n_steps, 1, 1))
+    jc = (y0 + y1) // 2
+    probes = [dict(terms=[(2, (xp, jc, k), delta) for k in range(zs)]) for xp in (line_x[0], line_x[1])]
+    basis = dict(recipe="B", L=2, M=1.1, fmax=f20db, p=4, seed=SEED0 + config_id)
+    return dict(name=name, config_id=config_id, dim=3, n=(nx, ny, nz), delta=delta, eps0=EPS0, mu0=MU0,
+                c0=C0, eps_r=eps, boxes=boxes, pec_sheets=sheets, dt=dt, dt_factor=dt_factor,
+                n_steps=n_steps, precision=precision, batch=1, sources=sources, probes=probes,
+                init=None, basis=basis)
+
+
+# ---------------------------------------------------------------------------
 # registry
 # ---------------------------------------------------------------------------
 
@@ -212,11 +314,24 @@ def scenario(which, precision=None, n_steps=None, **kw):
                      n_rect=0, n_probes=1, pulse="gauss_deriv", f20db=30e9)
     elif which == "tiny3d":
         s = cavity3d_random("tiny3d", 103, 37, 21, 13, 1e-3, 0.99, 100, precision or 64)
+    elif which == 4:
+        s = waveguide3d("config4", 4, 512, 128, 128, 0.5e-3, (255, 257), 10, 2, 48, 1024, 16, 32,
+                        (480, 64, 64), 0.8, 10000, precision or 32)
+    elif which == "tiny4":
+        s = waveguide3d("tiny4", 104, 48, 12, 10, 0.5e-3, (23, 25), 4, 2, 4, 24, 4, 5, (40, 6, 5),
+                        0.8, 300, precision or 64)
+    elif which == 5:
+        s = microstrip3d("config5", 5, 400, 200, 40, 0.25e-3, 32, (20, 380), 9, 4, 3.38, 4, (10, 60),
+                         8, (3, 5), 10, 128, 0.6, 50000, precision or 32)
+    elif which == "tiny5":
+        # config-5 structure on a small domain: 2 stubs per side, r_z = 4, q = 16
+        s = microstrip3d("tiny5", 105, 60, 48, 10, 0.25e-3, 2, (6, 54), 5, 3, 3.38, 3, (6, 12),
+                         6, (2, 4), 4, 16, 0.6, 300, precision or 64, spacing=12)
     elif which == "config3_small":
         s = cavity3d_random("config3_small", 3, 64, 48, 40, 1e-3, 0.99, 200, precision or 32)
     else:
         raise KeyError(which)
-    if precision is not None and which not in (3, "tiny3d", "config3_small"):
+    if precision is not None and which not in (3, "tiny3d", "config3_small", 4, "tiny4", 5, "tiny5"):
         s["precision"] = precision
     if n_steps is not None and n_steps != s["n_steps"]:
         s["n_steps"] = n_steps

@@ -84,3 +84,41 @@ def test_config3_full_size_sampled_one_step(prec):
     tol = 1e-13 if prec == 64 else 2e-6
     assert scale > 0
     assert np.max(np.abs(got - want)) <= tol * scale
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_tiny5_shared_models_pec_plates(prec):
+    # config-5 structure: z-refined regions around stub tips, PEC plates through
+    # the regions, two shared models with two instances each
+    scn, prob = _prep("tiny5", precision=prec)
+    assert [b["n_inst"] for b in prob["blocks"]] == [2, 2]
+    gpu = run_gpu(prob, 300, precision=prec)
+    ora = run_oracle(prob, 300)
+    es, ep, _ = compare(prob, gpu, ora)
+    tol = 1e-12 if prec == 64 else 1e-4
+    assert es <= tol and ep <= tol, (es, ep)
+
+
+def test_config5_full_size_fp32_short_run():
+    # full 400x200x40 grid, 64 regions in two 32-instance models (N = 32 GEMM
+    # columns), the launch configuration bench.py --config 5 times
+    scn, prob = _prep(5, precision=32)
+    n = 24
+    gpu = run_gpu(prob, n, precision=32, graph_steps=8)
+    ora = run_oracle(prob, n)
+    es, ep, _ = compare(prob, gpu, ora)
+    assert es <= 1e-4 and ep <= 1e-4, (es, ep)
+
+
+@pytest.mark.parametrize("form", ["fused", "leapfrog"])
+@pytest.mark.parametrize("prec", [64, 32])
+def test_tiny4_batched_iris_guide(prec, form):
+    # config-4 structure: x-graded refined slab with a PEC iris, B = 4
+    # excitations of a TE10 sheet source, z = 0 Krylov basis (reading R5(viii))
+    scn, prob = _prep("tiny4", precision=prec)
+    gpu = run_gpu(prob, 300, precision=prec, reduced_form=form)
+    tol = 1e-12 if prec == 64 else 1e-4
+    for m in (0, 3):
+        ora = run_oracle(prob, 300, member=m)
+        es, ep, _ = compare(prob, gpu, ora, member=m)
+        assert es <= tol and ep <= tol, (m, es, ep)

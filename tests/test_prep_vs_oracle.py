@@ -86,3 +86,85 @@ def test_prep_hybrid_equals_oracle(name, dim, n, boxes):
     rng = np.random.default_rng(0)
     eps = rng.uniform(1, 3, (n[2], n[1], n[0]) if dim == 3 else (n[1], n[0]))
     check(dim, n, eps, boxes)
+
+
+def test_prep_hybrid_with_pec_sheets_equals_oracle():
+    # config-5-like: PEC plates crossing refined regions (z-refined), two
+    # shared models; the oracle eliminates the plate edges independently
+    from oracle.hybrid import sheet_pec
+    from paper_1406_7042_b200.prep import _pec_extra
+    scn = scenario("tiny5")
+    P = fit.assemble(3, scn["n"], scn["delta"], scn["eps_r"], scn["boxes"], scn["eps0"], scn["mu0"],
+                     pec_extra=_pec_extra(scn))
+    ob = [hy.Box(tuple(b["lo"]), tuple(b["hi"]), tuple(b["r"])) for b in scn["boxes"]]
+    O = hy.assemble(3, scn["n"], scn["delta"], scn["eps_r"], ob, scn["eps0"], scn["mu0"],
+                    pec_e_extra=sheet_pec(scn["pec_sheets"], scn["boxes"]))
+    S = P.S
+    shp = fit.sshape(P.n, 3)
+
+    def cflat(key):
+        _, c, (i, j, k) = key
+        return c * S + int(np.ravel_multi_index((k, j, i), shp))
+    surf = sorted(cflat(O.e_keys[r]) for r in np.nonzero(O.e_tag == 1)[0])
+    assert np.array_equal(np.array(surf), P.if_ids)
+    # the plate edges are gone in both
+    pecx = _pec_extra(scn)
+    n_pec = sum(int(pecx(-1, c, shp).sum()) for c in (0, 1))
+    assert n_pec > 0
+    Kc = O.K.tocsr()
+    for q, fid in enumerate(P.if_ids[::7]):
+        c, s_ = int(fid // S), int(fid % S)
+        k, j, i = np.unravel_index(s_, shp)
+        r = O.e_index[("c", c, (int(i), int(j), int(k)))]
+        assert abs(P.De_c[c].ravel()[s_] - O.De[r]) <= 1e-13 * O.De[r]
+        row = Kc[r]
+        ref = {cflat(O.h_keys[cc]): v for cc, v in zip(row.indices, row.data) if O.h_keys[cc][0] == "c"}
+        qq = int(np.searchsorted(P.if_ids, fid))
+        prow = P.W[qq]
+        got = {int(cc): v for cc, v in zip(prow.indices, prow.data)}
+        assert set(ref) == set(got)
+        assert all(abs(ref[kk] - got[kk]) <= 1e-13 * abs(ref[kk]) for kk in ref)
+    for bi, part in enumerate(P.boxes):
+        nf = part.fine.n
+        shf = fit.sshape(nf, 3)
+        Sf = int(np.prod(shf))
+
+        def fflat(key):
+            _, b, c, (i, j, k) = key
+            return c * Sf + int(np.ravel_multi_index((k, j, i), shf))
+        oe = {fflat(O.e_keys[r]): r for r in np.nonzero((O.e_tag == 2) & (O.e_box == bi))[0]}
+        assert set(oe) == set(part.e_int.tolist())
+        pe = np.array([oe[v] for v in part.e_int])
+        oh = {fflat(O.h_keys[r]): r for r in np.nonzero((O.h_tag == 2) & (O.h_box == bi))[0]}
+        ph_ = np.array([oh[v] for v in part.h_int])
+        assert abs(O.K[pe][:, ph_] - part.Kff).max() <= 1e-13 * abs(part.Kff).max()
+
+
+def test_prep_hybrid_with_solid_pec_iris_equals_oracle():
+    # config-4-like: x-graded slab over the full cross-section with a solid
+    # PEC iris inside the refined region
+    from oracle.hybrid import block_pec
+    from paper_1406_7042_b200.prep import _pec_extra
+    scn = scenario("tiny4")
+    P = fit.assemble(3, scn["n"], scn["delta"], scn["eps_r"], scn["boxes"], scn["eps0"], scn["mu0"],
+                     pec_extra=_pec_extra(scn))
+    ob = [hy.Box(tuple(b["lo"]), tuple(b["hi"]), tuple(b["r"])) for b in scn["boxes"]]
+    O = hy.assemble(3, scn["n"], scn["delta"], scn["eps_r"], ob, scn["eps0"], scn["mu0"],
+                    pec_e_extra=block_pec(scn["boxes"]))
+    part = P.boxes[0]
+    nf = part.fine.n
+    shf = fit.sshape(nf, 3)
+    Sf = int(np.prod(shf))
+
+    def fflat(key):
+        _, b, c, (i, j, k) = key
+        return c * Sf + int(np.ravel_multi_index((k, j, i), shf))
+    oe = {fflat(O.e_keys[r]): r for r in np.nonzero(O.e_tag == 2)[0]}
+    assert set(oe) == set(part.e_int.tolist())
+    oh = {fflat(O.h_keys[r]): r for r in np.nonzero(O.h_tag == 2)[0]}
+    pe = np.array([oe[v] for v in part.e_int]); ph_ = np.array([oh[v] for v in part.h_int])
+    assert abs(O.K[pe][:, ph_] - part.Kff).max() <= 1e-13 * abs(part.Kff).max()
+    assert np.allclose(O.De[pe], part.De_f, rtol=1e-13)
+    # the iris removed fine E unknowns
+    P0 = fit.assemble(3, scn["n"], scn["delta"], scn["eps_r"], scn["boxes"], scn["eps0"], scn["mu0"])
+    assert len(P0.boxes[0].e_int) > len(part.e_int)
