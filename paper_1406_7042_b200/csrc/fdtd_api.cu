@@ -110,8 +110,11 @@ struct BlockDev {
   bool fused = false;
   // host fp64 copies (for the prologue and the fused matrix)
   std::vector<double> K, SE, ge, gh;
-  // leapfrog path matrices
+  // unpadded matrices (fused blocks: prologue GEMVs) and padded-row copies
+  // (leap-frog blocks: 16-byte vector loads)
   T *K_d = nullptr, *KT_d = nullptr, *SE_d = nullptr, *SET_d = nullptr, *ge_d = nullptr, *gh_d = nullptr;
+  T *Kp_d = nullptr, *KTp_d = nullptr, *SEp_d = nullptr, *Tv_d = nullptr;
+  int Kph = 0, Kpe = 0;                        // padded row pitches (multiples of 32 * VEC)
   // state offsets (elements) in the concatenated buffers
   int64_t e_off = 0, h_off = 0, y_off = 0;     // e/h buffers [q][N], y / G [n_if][N]
   // fused path
@@ -276,6 +279,36 @@ static int launch_gemv(int rows, int cols, int N, const T* A, const T* X, T* out
 }
 
 template <typename T>
+static int launch_rowblock(int rows, int K, int Kp, int N, const T* A, const T* X, T* out, const T* g, T alpha,
+                           bool acc, const int64_t* d_step, int check_every, unsigned long long* bad,
+                           cudaStream_t st) {
+  if (rows <= 0) return 0;
+  const size_t sm = (size_t)Kp * N * sizeof(T);
+  const int blocks = std::min((rows + 7) / 8, 148 * 2);
+#define FDTD_RB(NB) fdtd::rowblock_gemv_kernel<T, NB><<<blocks, 256, sm, st>>>(rows, K, Kp, N, A, X, out, g, alpha, acc, d_step, check_every, bad)
+  if (N <= 1) FDTD_RB(1);
+  else if (N <= 4) FDTD_RB(4);
+  else if (N <= 16) FDTD_RB(16);
+  else FDTD_RB(32);
+#undef FDTD_RB
+  return 1;
+}
+
+template <typename T>
+static int launch_colsum(int rows, int cols, int Kp, int N, const T* A, const T* X, T* out, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return 0;
+  const int cpt = std::min((cols + 255) / 256, 4);
+  const int ytiles = (cols + 256 * cpt - 1) / (256 * cpt);
+  const dim3 blocks(std::max(1, std::min(rows, 148 * 4 / ytiles)), ytiles);
+#define FDTD_CS(NB, CPT) fdtd::colsum_gemv_kernel<T, NB, CPT><<<blocks, 256, 0, st>>>(rows, cols, Kp, N, A, X, out)
+  if (N <= 4) { if (cpt <= 1) FDTD_CS(4, 1); else if (cpt <= 2) FDTD_CS(4, 2); else FDTD_CS(4, 4); }
+  else if (N <= 16) { if (cpt <= 1) FDTD_CS(16, 1); else if (cpt <= 2) FDTD_CS(16, 2); else FDTD_CS(16, 4); }
+  else { if (cpt <= 1) FDTD_CS(32, 1); else if (cpt <= 2) FDTD_CS(32, 2); else FDTD_CS(32, 4); }
+#undef FDTD_CS
+  return 1;
+}
+
+template <typename T>
 int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_interface* itf,
                     const fdtd_reduced_block* bl, int n_blocks, const fdtd_sources* src,
                     const fdtd_probes* probes, const fdtd_exec* ex) {
@@ -433,14 +466,28 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       }
     for (int r = 0; r < D.qe; ++r) ge[r] = (T)D.ge[r];
     for (int r = 0; r < D.qh; ++r) gh[r] = (T)D.gh[r];
-    D.K_d = dalloc<T>(K.size()); D.ge_d = dalloc<T>(D.qe); D.gh_d = dalloc<T>(D.qh);
-    D.SE_d = dalloc<T>(std::max<size_t>(SE.size(), 1));
-    if (!D.K_d || !D.ge_d || !D.gh_d || !D.SE_d) return fail(FDTD_ENOMEM, "block %d allocation failed", b);
-    if (upload(D.K_d, K) || upload(D.ge_d, ge) || upload(D.gh_d, gh) || upload(D.SE_d, SE)) return FDTD_ECUDA;
-    if (!D.fused) {
-      D.KT_d = dalloc<T>(KT.size()); D.SET_d = dalloc<T>(std::max<size_t>(SET.size(), 1));
-      if (!D.KT_d || !D.SET_d) return fail(FDTD_ENOMEM, "block %d allocation failed", b);
-      if (upload(D.KT_d, KT) || upload(D.SET_d, SET)) return FDTD_ECUDA;
+    D.ge_d = dalloc<T>(D.qe); D.gh_d = dalloc<T>(D.qh);
+    if (!D.ge_d || !D.gh_d || upload(D.ge_d, ge) || upload(D.gh_d, gh)) return fail(FDTD_ENOMEM, "block %d allocation failed", b);
+    if (D.fused) {
+      D.K_d = dalloc<T>(K.size());
+      D.SE_d = dalloc<T>(std::max<size_t>(SE.size(), 1));
+      if (!D.K_d || !D.SE_d) return fail(FDTD_ENOMEM, "block %d allocation failed", b);
+      if (upload(D.K_d, K) || upload(D.SE_d, SE)) return FDTD_ECUDA;
+    } else {
+      const int PADC = 32 * (16 / (int)sizeof(T));
+      D.Kph = (D.qh + PADC - 1) / PADC * PADC;
+      D.Kpe = (D.qe + PADC - 1) / PADC * PADC;
+      std::vector<T> Kp((size_t)D.qe * D.Kph, (T)0), KTp((size_t)D.qh * D.Kpe, (T)0), SEp((size_t)D.n_if * D.Kph, (T)0);
+      for (int r = 0; r < D.qe; ++r)
+        for (int c = 0; c < D.qh; ++c) Kp[(size_t)r * D.Kph + c] = K[(size_t)r * D.qh + c];
+      for (int r = 0; r < D.qh; ++r)
+        for (int c = 0; c < D.qe; ++c) KTp[(size_t)r * D.Kpe + c] = KT[(size_t)r * D.qe + c];
+      for (int r = 0; r < D.n_if; ++r)
+        for (int c = 0; c < D.qh; ++c) SEp[(size_t)r * D.Kph + c] = SE[(size_t)r * D.qh + c];
+      D.Kp_d = dalloc<T>(Kp.size()); D.KTp_d = dalloc<T>(KTp.size());
+      D.SEp_d = dalloc<T>(std::max<size_t>(SEp.size(), 1)); D.Tv_d = dalloc<T>((size_t)D.qh * D.N);
+      if (!D.Kp_d || !D.KTp_d || !D.SEp_d || !D.Tv_d) return fail(FDTD_ENOMEM, "block %d allocation failed", b);
+      if (upload(D.Kp_d, Kp) || upload(D.KTp_d, KTp) || upload(D.SEp_d, SEp)) return FDTD_ECUDA;
     }
   }
   for (int p = 0; p < 2; ++p) {
@@ -706,6 +753,16 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   CK(cudaFuncSetAttribute(fdtd::stencil3d_tma_kernel<T, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3 + 8192));
   CK(cudaFuncSetAttribute(fdtd::stencil2d_rows_kernel<T, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   CK(cudaFuncSetAttribute(fdtd::stencil2d_rows_kernel<T, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
+  {
+    const int big = 200 * 1024;
+    CK(cudaFuncSetAttribute(fdtd::rowblock_gemv_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(fdtd::rowblock_gemv_kernel<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(fdtd::rowblock_gemv_kernel<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(fdtd::rowblock_gemv_kernel<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    for (auto& D : blocks)
+      if (!D.fused && (size_t)std::max(D.Kph, D.Kpe) * D.N * sizeof(T) > (size_t)big)
+        return fail(FDTD_ENOTSUP, "reduced block too large for the staged leap-frog GEMV (q x N)");
+  }
   if (fused_smem > 48 * 1024) {
     CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
     CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
@@ -816,10 +873,15 @@ int Impl<T>::build_fused(const fdtd_probes* probes) {
 template <typename T>
 int Impl<T>::prologue(cudaStream_t st) {
   for (auto& D : blocks) {
+    if (!D.fused) {
+      if (D.n_if > 0)
+        launch_rowblock<T>(D.n_if, D.qh, D.Kph, D.N, D.SEp_d, h_state(D, host_step), y_all + D.y_off,
+                           (const T*)nullptr, (T)1, false, d_step, 0, d_bad, st);
+      continue;
+    }
     if (D.n_if > 0)
       launch_gemv<T>(D.n_if, D.qh, D.N, D.SE_d, h_state(D, host_step), y_all + D.y_off, (const T*)nullptr,
                      (T)1, false, d_step, 0, d_bad, st);
-    if (!D.fused) continue;
     CK(cudaMemcpyAsync(e_ahead(D, host_step), e_state(D, host_step), sizeof(T) * D.qe * D.N,
                        cudaMemcpyDeviceToDevice, st));
     launch_gemv<T>(D.qe, D.qh, D.N, D.K_d, h_state(D, host_step), e_ahead(D, host_step), D.ge_d,
@@ -846,7 +908,7 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
     dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + outy - 1) / outy, (nz + 1 + kchunk - 1) / kchunk);
     const int al = 128 / (int)sizeof(T);
     const size_t HPp = (size_t)(tHBX * (BY + 1) + al - 1) / al * al, EPp = (size_t)(BX * BY + al - 1) / al * al;
-    const size_t sm = 256 + (NS * 3 * HPp + NS * 3 * EPp + 2 * 3 * EPp) * sizeof(T) + tabsz;
+    const size_t sm = 256 + (NS * 3 * HPp + NS * 3 * EPp + 3 * 3 * EPp) * sizeof(T) + tabsz;
     if (uniform)
       fdtd::stencil3d_tma_kernel<T, true, NS><<<grid, dim3(BX, BY), sm, st>>>(
           tma[p], tHBX, tSX, tOUTX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
@@ -890,14 +952,17 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
       if (D.fused) continue;
       T* e = eb[0] + D.e_off;
       T* h = hb[0] + D.h_off;
-      n += launch_gemv<T>(D.qe, D.qh, D.N, D.K_d, h, e, D.ge_d, (T)-1, true, d_step, check_every, d_bad, st);
-      n += launch_gemv<T>(D.qh, D.qe, D.N, D.KT_d, e, h, D.gh_d, (T)1, true, d_step, check_every, d_bad, st);
-      if (D.n_if > 0) {
-        n += launch_gemv<T>(D.qh, D.n_if, D.N, D.SET_d, g_all + D.y_off, h, D.gh_d, (T)1, true, d_step, check_every,
-                            d_bad, st);
-        n += launch_gemv<T>(D.n_if, D.qh, D.N, D.SE_d, h, y_all + D.y_off, (const T*)nullptr, (T)1, false, d_step,
-                            0, d_bad, st);
-      }
+      // a4: e~ -= G_e K~' h~^{n+1/2}
+      n += launch_rowblock<T>(D.qe, D.qh, D.Kph, D.N, D.Kp_d, h, e, D.ge_d, (T)-1, true, d_step, check_every, d_bad, st);
+      // a6: T = K~'^T e~ + S_E^T G ; h~ += G_h T ; y = S_E h~
+      n += launch_rowblock<T>(D.qh, D.qe, D.Kpe, D.N, D.KTp_d, e, D.Tv_d, (const T*)nullptr, (T)1, false, d_step, 0,
+                              d_bad, st);
+      if (D.n_if > 0) n += launch_colsum<T>(D.n_if, D.qh, D.Kph, D.N, D.SEp_d, g_all + D.y_off, D.Tv_d, st);
+      fdtd::axpy_diag_kernel<T><<<(D.qh * D.N + 255) / 256, 256, 0, st>>>(D.qh, D.N, D.gh_d, D.Tv_d, h);
+      ++n;
+      if (D.n_if > 0)
+        n += launch_rowblock<T>(D.n_if, D.qh, D.Kph, D.N, D.SEp_d, h, y_all + D.y_off, (const T*)nullptr, (T)1, false,
+                                d_step, check_every, d_bad, st);
     }
     mark(2, 1);
   }

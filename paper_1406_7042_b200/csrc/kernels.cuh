@@ -419,8 +419,11 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int out
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_al);                 // [NS]
   T* Hs = reinterpret_cast<T*>(smem_al + 128);                           // [NS][3][HH][HW]
   T* Es = Hs + NS * 3 * HP;                                               // [NS][3][BY][BX]
-  T* En = Es + NS * 3 * EP;                                               // [2][3][BY][BX]
-  MatTable<T>* tab = reinterpret_cast<MatTable<T>*>(En + 2 * 3 * EP);
+  // E^{n+1} planes: three buffers, because no CTA barrier separates iteration
+  // kk's H update (reads plane kk-1, rows ty+1 written by another warp) from
+  // iteration kk+1's stores -- only the mbarrier wait, which is per thread
+  T* En = Es + NS * 3 * EP;                                               // [3][3][BY][BX]
+  MatTable<T>* tab = reinterpret_cast<MatTable<T>*>(En + 3 * 3 * EP);
   const bool leader = (tx == 0 && ty == 0);
   if (leader) {
     for (int q = 0; q < NS; ++q) mbar_init(&bars[q], 1);
@@ -511,7 +514,7 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int out
       if (ifmk & 2) ey = eval_row(R, R.row_of[1][s], b, B, ey0, F0, y, step);
       if (ifmk & 4) ez = eval_row(R, R.row_of[2][s], b, B, ez0, F0, y, step);
     }
-    T* en = En + (kk & 1) * 3 * EP;
+    T* en = En + (kk % 3) * 3 * EP;
     en[0 * EP + ty * BX + tx] = ex; en[1 * EP + ty * BX + tx] = ey; en[2 * EP + ty * BX + tx] = ez;
     if (own && kk < k1) {
       const int64_t o = (int64_t)kk * sz + col;
@@ -520,7 +523,7 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int out
     }
     __syncthreads();            // En of plane kk complete; stage st free for reuse after this
     if (kk > k0 && own) {
-      const T* e0 = En + ((kk - 1) & 1) * 3 * EP;
+      const T* e0 = En + ((kk + 2) % 3) * 3 * EP;   // plane kk-1
       const int q = ty * BX + tx;
       const T ey_ip = e0[1 * EP + q + B], ez_ip = e0[2 * EP + q + B];
       const T ex_jp = e0[0 * EP + q + BX], ez_jp = e0[2 * EP + q + BX];
@@ -755,6 +758,116 @@ __global__ void gemv_rows_kernel(int rows, int cols, int N, const T* __restrict_
   const bool check = check_every > 0 && (*d_step % check_every) == 0;
   warp_rows<T, NB>(rows, cols, N, A, X, out, g, alpha, accumulate, w0, nw, check, bad);
   if (bad) atomicMin(bad_step, (unsigned long long)*d_step);
+}
+
+// ---------------------------------------------------------------------------
+// leap-frog path for large reduced blocks (config 4: S_E = 65,024 x 1,024,
+// N = 16 columns).  Two streaming kernels, HBM-bound on the matrix:
+//  * rowblock_gemv: out[r][n] = (acc ? out : 0) + alpha g[r] sum_c A[r][c] X[c][n]
+//    persistent CTAs; X staged once per CTA in shared memory as [N][K]; A rows
+//    streamed with 16-byte loads (requires K % (32 * VEC) == 0 -> padded rows)
+//  * colsum_gemv: out[c][n] += sum_r A[r][c] X[r][n] over a contiguous row chunk
+//    per CTA (A row-major is read once, coalesced); partial sums in registers,
+//    then one atomicAdd per (c, n) per CTA.
+// ---------------------------------------------------------------------------
+template <typename T, int NB>
+__global__ void __launch_bounds__(256)
+rowblock_gemv_kernel(int rows, int K, int Kp, int N, const T* __restrict__ A, const T* __restrict__ X,
+                     T* __restrict__ out, const T* __restrict__ g, T alpha, bool accumulate,
+                     const int64_t* __restrict__ d_step, int check_every, unsigned long long* bad_step) {
+  using V = typename Vec<T>::type;
+  constexpr int VN = Vec<T>::n;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Xs = reinterpret_cast<T*>(smem_raw);                   // [N][Kp]
+  for (int t = threadIdx.x; t < Kp * N; t += blockDim.x) {
+    const int n = t / Kp, c = t % Kp;
+    Xs[t] = (c < K) ? X[(int64_t)c * N + n] : (T)0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const bool check = check_every > 0 && (*d_step % check_every) == 0;
+  bool bad = false;
+  const int nv = Kp / VN;
+  for (int r = w0; r < rows; r += nw) {
+    T acc[NB];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) acc[n] = 0;
+    const V* a = reinterpret_cast<const V*>(A + (int64_t)r * Kp);
+#pragma unroll 4
+    for (int c = lane; c < nv; c += 32) {
+      const V av = a[c];
+#pragma unroll
+      for (int n = 0; n < NB; ++n)
+        if (n < N) acc[n] += vdot<T>(av, reinterpret_cast<const V*>(Xs + n * Kp)[c]);
+    }
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      T v = acc[n];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      acc[n] = v;
+    }
+    if (lane < N) {
+      T v = 0;
+#pragma unroll
+      for (int n = 0; n < NB; ++n)
+        if (n == lane) v = acc[n];
+      const T gr = g ? g[r] : (T)1;
+      T* o = out + (int64_t)r * N + lane;
+      const T res = (accumulate ? *o : (T)0) + alpha * gr * v;
+      *o = res;
+      if (check && !finite_small((double)res)) bad = true;
+    }
+  }
+  if (bad) atomicMin(bad_step, (unsigned long long)*d_step);
+}
+
+template <typename T, int NB, int CPT>
+__global__ void __launch_bounds__(256)
+colsum_gemv_kernel(int rows, int cols, int Kp, int N, const T* __restrict__ A, const T* __restrict__ X,
+                   T* __restrict__ out) {
+  // thread t owns columns c = c0 + t + 256 * u (u < CPT), c0 = 256 * CPT * blockIdx.y;
+  // rows [r0, r1) of this CTA
+  const int c0 = 256 * CPT * blockIdx.y;
+  const int chunk = (rows + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * chunk, r1 = min(rows, r0 + chunk);
+  T acc[CPT][NB];
+#pragma unroll
+  for (int u = 0; u < CPT; ++u)
+#pragma unroll
+    for (int n = 0; n < NB; ++n) acc[u][n] = 0;
+  for (int r = r0; r < r1; ++r) {
+    T xv[NB];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) xv[n] = (n < N) ? X[(int64_t)r * N + n] : (T)0;
+    const T* a = A + (int64_t)r * Kp;
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) {
+      const int c = c0 + threadIdx.x + 256 * u;
+      const T av = (c < cols) ? a[c] : (T)0;
+#pragma unroll
+      for (int n = 0; n < NB; ++n) acc[u][n] += av * xv[n];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < CPT; ++u) {
+    const int c = c0 + threadIdx.x + 256 * u;
+    if (c >= cols) continue;
+#pragma unroll
+    for (int n = 0; n < NB; ++n)
+      if (n < N) atomicAdd(out + (int64_t)c * N + n, acc[u][n]);
+  }
+}
+
+// h~ += G_h * T   (T = K~'^T e~ + S_E^T G accumulated by the two kernels above)
+template <typename T>
+__global__ void axpy_diag_kernel(int rows, int N, const T* __restrict__ g, const T* __restrict__ Tv,
+                                 T* __restrict__ h) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows * N) return;
+  h[t] += g[t / N] * Tv[t];
 }
 
 template <typename T>

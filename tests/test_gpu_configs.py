@@ -122,3 +122,35 @@ def test_tiny4_batched_iris_guide(prec, form):
         ora = run_oracle(prob, 300, member=m)
         es, ep, _ = compare(prob, gpu, ora, member=m)
         assert es <= tol and ep <= tol, (m, es, ep)
+
+
+def test_tma_stencil_bitwise_equals_cp_async_stencil(monkeypatch):
+    # the TMA and the cp.async 3-D stencils do the same arithmetic: from random
+    # states they must agree bit for bit (regression: a cross-warp race on the
+    # E-plane buffers of the TMA kernel showed up as whole wrong tile rows)
+    from paper_1406_7042_b200.fdtd import Sim
+    scn, prob = _prep("tiny5", precision=64)
+    prob = dict(prob, init={})
+    nx, ny, nz = prob["n"]
+    S = (nx + 1) * (ny + 1) * (nz + 1)
+    rng = np.random.default_rng(0)
+
+    def run(no_tma, state):
+        if no_tma:
+            monkeypatch.setenv("FDTD_NO_TMA", "1")
+        else:
+            monkeypatch.delenv("FDTD_NO_TMA", raising=False)
+        sim = Sim(prob, precision=64, graph_steps=0)
+        for c in range(6):
+            sim.set_state(c, state[c])
+        sim.step(3)
+        sim.sync()
+        out = [sim.get_state(c) for c in range(6)]
+        sim.close()
+        return out
+
+    for _ in range(12):
+        state = [rng.standard_normal((1, S)) for _ in range(6)]
+        a, b = run(True, state), run(False, state)
+        for c in range(6):
+            assert np.array_equal(a[c], b[c]), c
