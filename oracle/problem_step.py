@@ -389,3 +389,162 @@ def sampled_step(problem, arrays, samples, member=0):
                 acc += sign * e_new(ec, (idx[0] + off[0], idx[1] + off[1], idx[2] + off[2]))
             out[(c, idx)] = v + coef(c, pos) * acc   # H - ch curl E == H + ch K_inc^T E
     return out
+
+
+def sampled_hybrid_step(problem, arrays, red_e, red_h, samples, member=0, step=0):
+    """One step of the hybrid recursion (4)/(12) (the same update as ``run``,
+    ``step_leapfrog``: E' = E - G_E (K_E H) + s, H' = H + G_H (K_H E')) for
+    full-size problems the matrix form cannot hold (config 4: 8.5 M cells and a
+    65,024 x 1,024 S_E), evaluated unknown by unknown from the problem
+    description:
+
+      * every interface row r (block b, instance i, local l):
+            E_if' = E_if - c_r (sum_k w_rk H[col_rk] + S_E[l] . h~_{b,i}) + s_r
+      * every reduced block/instance:
+            e~' = e~ - g_e (K~ h~)
+            h~' = h~ + g_h (K~^T e~' + sum_{rows r of (b, i)} S_E[l_r] E_if'[r])
+      * the SAMPLED coarse unknowns: E' = E + cb curl H (+ source) on regular
+        rows (only active H: ch != 0), H' = H + ch (K_inc^T E') with E' from
+        the two rules above.
+
+    ``arrays``: comp -> [B][S] (or [S]) storage arrays of E^n, H^{n+1/2};
+    ``red_e`` / ``red_h``: one member's reduced states, [block][inst][q] order;
+    ``step``: the source waveform index of this step.  Returns
+    (coarse {(comp, idx): value}, E_if' in interface-row order, e~', h~')."""
+    dim = int(problem["dim"])
+    n = tuple(int(v) for v in problem["n"]) + ((1,) if len(problem["n"]) == 2 else ())
+    shp = yee.storage_shape(dim, n)
+    S = int(np.prod(shp))
+    curl_h = yee._CURL_H_3D if dim == 3 else yee._CURL_H_2D
+    mcurl_e = yee._MCURL_E_3D if dim == 3 else yee._MCURL_E_2D
+    ecomps = (0, 1, 2) if dim == 3 else (2,)
+    comps = (yee.E_COMPS_3D + yee.H_COMPS_3D) if dim == 3 else (yee.E_COMPS_2D + yee.H_COMPS_2D)
+    live = {c: yee.exists_mask(dim, n, c) & ~yee.wall_pec_mask(dim, n, c) for c in comps}
+    mid = np.asarray(problem["mat_id"]).reshape(shp)
+    mcoef = np.asarray(problem["mat_coef"], np.float64)
+    itf = problem["interface"]
+    blocks = problem.get("blocks") or []
+
+    def pos_of(idx):
+        i, j, k = idx
+        return (k, j, i) if dim == 3 else (j, i)
+
+    def inside(pos):
+        return all(0 <= p < s for p, s in zip(pos, shp))
+
+    def coef(c, pos):
+        return float(mcoef[mid[pos], c])
+
+    def raw(c, pos):
+        a = np.asarray(arrays[c])
+        return float(a.reshape(-1, *shp)[member if a.size != S else 0][pos])
+
+    def h_val(c, idx):                      # active coarse H (K_E columns)
+        pos = pos_of(idx)
+        if not inside(pos) or not live[c][pos] or coef(c, pos) == 0.0:
+            return 0.0
+        return raw(c, pos)
+
+    def flat(pos):
+        return int(np.ravel_multi_index(pos, shp))
+
+    # sources: unknown -> list of (coef, column)
+    src = problem.get("sources")
+    srcs = {}
+    if src is not None and len(src["unknown"]):
+        cols = src.get("column")
+        for q, u in enumerate(np.asarray(src["unknown"], np.int64)):
+            srcs.setdefault(int(u), []).append(
+                (float(np.asarray(src["coef"])[q]), int(cols[q]) if cols is not None else q))
+        wave = np.asarray(src["wave"], np.float64)
+    else:
+        wave = np.zeros((0, 0, 1))
+
+    def s_term(u):
+        v = 0.0
+        for cf, col in srcs.get(u, ()):
+            if step < wave.shape[0]:
+                v -= cf * wave[step, col, member]
+        return v
+
+    # reduced states per (block, instance)
+    def split(vec, side):
+        out, o = {}, 0
+        for bl, b in enumerate(blocks):
+            q = int(b.get("qe" if side == "e" else "qh", b.get("q")))
+            for i in range(int(b["n_inst"])):
+                out[(bl, i)] = np.asarray(vec[o:o + q], np.float64)
+                o += q
+        return out
+    e_red, h_red = split(red_e, "e"), split(red_h, "h")
+
+    # interface rows
+    unk = np.asarray(itf["unknown"], np.int64)
+    rp = np.asarray(itf["rowptr"], np.int64)
+    colv = np.asarray(itf["col"], np.int64)
+    valv = np.asarray(itf["val"], np.float64)
+    cr = np.asarray(itf["c"], np.float64)
+    blk, ins, loc = (np.asarray(itf[k], np.int64) for k in ("block", "inst", "local"))
+    SE = [np.asarray(b["S_E"]) for b in blocks]
+    Eif = np.empty(len(unk))
+    row_of = {}
+    for r in range(len(unk)):
+        u = int(unk[r])
+        c, p = u // S, u % S
+        pos = np.unravel_index(p, shp)
+        acc = 0.0
+        for k in range(rp[r], rp[r + 1]):
+            hc, hp = int(colv[k] // S), int(colv[k] % S)
+            acc += valv[k] * raw(hc, np.unravel_index(hp, shp))
+        acc += float(np.dot(SE[blk[r]][loc[r]].astype(np.float64), h_red[(int(blk[r]), int(ins[r]))]))
+        Eif[r] = raw(c, pos) - cr[r] * acc + s_term(u)
+        row_of[u] = r
+
+    # reduced update
+    e_new_red, h_new_red = {}, {}
+    for bl, b in enumerate(blocks):
+        qe = int(b.get("qe", b.get("q")))
+        qh = int(b.get("qh", b.get("q")))
+        K = np.asarray(b["K"], np.float64).reshape(qe, qh)
+        ge = np.broadcast_to(np.asarray(b["g_e"], np.float64), (qe,))
+        gh = np.broadcast_to(np.asarray(b["g_h"], np.float64), (qh,))
+        for i in range(int(b["n_inst"])):
+            e1 = e_red[(bl, i)] - ge * (K @ h_red[(bl, i)])
+            rows = np.nonzero((blk == bl) & (ins == i))[0]
+            t = K.T @ e1
+            if len(rows):
+                t = t + SE[bl][loc[rows]].astype(np.float64).T @ Eif[rows]
+            e_new_red[(bl, i)] = e1
+            h_new_red[(bl, i)] = h_red[(bl, i)] + gh * t
+
+    def e_new(c, idx):
+        pos = pos_of(idx)
+        if not inside(pos) or not live[c][pos]:
+            return 0.0
+        u = c * S + flat(pos)
+        if u in row_of:
+            return float(Eif[row_of[u]])
+        cb = coef(c, pos)
+        if cb == 0.0:
+            return raw(c, pos)                 # inert (hole / PEC plate): unchanged
+        acc = 0.0
+        for (hc, off, sign, _) in curl_h[c]:
+            acc += sign * h_val(hc, (idx[0] + off[0], idx[1] + off[1], idx[2] + off[2]))
+        return raw(c, pos) + cb * acc + s_term(u)
+
+    out = {}
+    for (c, idx) in samples:
+        idx = tuple(int(x) for x in idx)
+        if c in ecomps:
+            out[(c, idx)] = e_new(c, idx)
+            continue
+        pos = pos_of(idx)
+        if not inside(pos) or not live[c][pos] or coef(c, pos) == 0.0:
+            out[(c, idx)] = raw(c, pos) if inside(pos) else 0.0
+            continue
+        acc = 0.0
+        for (ec, off, sign, _) in mcurl_e[c]:
+            acc += sign * e_new(ec, (idx[0] + off[0], idx[1] + off[1], idx[2] + off[2]))
+        out[(c, idx)] = raw(c, pos) + coef(c, pos) * acc
+    flat_red = lambda d: np.concatenate([d[k] for k in sorted(d)]) if d else np.zeros(0)
+    return out, Eif, flat_red(e_new_red), flat_red(h_new_red)

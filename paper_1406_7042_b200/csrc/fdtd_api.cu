@@ -157,9 +157,14 @@ struct Impl : public fdtd_t {
   int64_t* g_off = nullptr;
   int64_t* g_dst = nullptr;
   // fused kernel work decomposition
-  fdtd::FusedBlock<T>* d_fblocks = nullptr;
-  int2* d_ctas = nullptr;             // (fused block, first row) per CTA
+  std::vector<fdtd::FusedBlock<T>> fblocks;   // descriptors (copied into the kernel parameters)
+  std::vector<int> tile0;                     // first tile of each fused block
   int n_ctas = 0, NBsel = 1, max_cols = 0, rows_per_cta = 8;
+  bool fused_gemm = false;
+  int NPsel = 32;
+  static constexpr int GEMM_KS = 4;
+  // rows per thread of the GEMM kernel: 64-row tiles for NP <= 16, 32 for NP = 32
+  static constexpr int gemm_rpw(int np) { return np == 32 ? 4 : np / 4; }
   int64_t step_offset = 0;            // device step = host step + offset (set_state(8))
   size_t fused_smem = 0;
   // probes
@@ -180,7 +185,14 @@ struct Impl : public fdtd_t {
   int64_t graph_kernels = 0;
   T* staging = nullptr;
   size_t staging_bytes = 0;
-  int kchunk = 32;
+  int kchunk_max = 32;         // z-planes per CTA of the 3-D stencils (upper bound)
+  // z-chunk: at most kchunk_max planes, at least ~2 waves of CTAs (148 SMs x 3
+  // resident), chunks balanced (config 5: 41 planes -> 3 x 14, not 32 + 9)
+  int zchunk(int gxy) const {
+    int nch = std::max((nz + 1 + kchunk_max - 1) / kchunk_max, (2 * 148 * 3 + gxy - 1) / gxy);
+    nch = std::max(1, std::min(nch, (nz + 1 + 7) / 8));
+    return (nz + 1 + nch - 1) / nch;
+  }
   int reduced_form = 0;
   // TMA descriptors of the 3-D stencil (per parity of the OLD buffers)
   bool use_tma = false;
@@ -391,6 +403,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       }
     }
     if (getenv("FDTD_NO_TMA")) use_tma = false;
+    if (const char* e = getenv("FDTD_KCHUNK")) kchunk_max = std::max(1, atoi(e));
   }
 
   // ---- materials ----
@@ -737,11 +750,11 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     int e = build_fused(probes);
     if (e) return e;
   }
-  d_step = dalloc<int64_t>(1);
+  d_step = dalloc<int64_t>(2);     // step counter, one slot per step parity
   d_bad = dalloc<unsigned long long>(1);
   d_done = dalloc<unsigned int>(1);
   CK(cudaMemsetAsync(d_done, 0, sizeof(unsigned int), stream));
-  CK(cudaMemsetAsync(d_step, 0, sizeof(int64_t), stream));
+  CK(cudaMemsetAsync(d_step, 0, 2 * sizeof(int64_t), stream));
   CK(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), stream));
   staging_bytes = sizeof(T) * (size_t)std::max<int64_t>(elems, std::max(e_size, h_size));
   CK(cudaMallocHost(&staging, staging_bytes));
@@ -763,7 +776,13 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       if (!D.fused && (size_t)std::max(D.Kph, D.Kpe) * D.N * sizeof(T) > (size_t)big)
         return fail(FDTD_ENOTSUP, "reduced block too large for the staged leap-frog GEMV (q x N)");
   }
-  if (fused_smem > 48 * 1024) {
+  if (fused_gemm && fused_smem > 48 * 1024) {
+    CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 4, gemm_rpw(4), GEMM_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+    CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 8, gemm_rpw(8), GEMM_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+    CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 16, gemm_rpw(16), GEMM_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+    CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), GEMM_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+  }
+  if (!fused_gemm && fused_smem > 48 * 1024) {
     CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
     CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
     CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
@@ -783,9 +802,25 @@ template <typename T>
 int Impl<T>::build_fused(const fdtd_probes* probes) {
   std::vector<fdtd::FusedBlock<T>> fb;
   std::vector<int2> ctas;
-  const int ROWS = 8;                        // rows per CTA (8 warps x 1)
   const int PADC = 32 * (16 / (int)sizeof(T));   // lanes x vector width
-  int maxN = 1;
+  int maxN = 1, maxCp = 0;
+  for (auto& D : blocks)
+    if (D.fused) {
+      maxN = std::max(maxN, D.N);
+      maxCp = std::max(maxCp, (D.qe + D.n_if + D.qh + PADC - 1) / PADC * PADC);
+    }
+  NPsel = maxN <= 4 ? 4 : maxN <= 8 ? 8 : maxN <= 16 ? 16 : 32;
+  // batched blocks (N >= 4 columns) take the cluster-split SIMT GEMM kernel,
+  // single-column ones the warp-per-row GEMV kernel (FDTD_FUSED=gemv|gemm
+  // overrides); the GEMM kernel's shared memory must fit
+  {
+    const int TRg = 8 * (32 / NPsel) * gemm_rpw(NPsel);
+    const size_t need = (size_t)(TRg * NPsel + maxCp / GEMM_KS * NPsel + TRg * (maxCp / GEMM_KS + 16 / sizeof(T))) * sizeof(T);
+    fused_gemm = maxN >= 4;
+    if (const char* e = getenv("FDTD_FUSED")) fused_gemm = std::string(e) == "gemm";
+    if (need > 200 * 1024) fused_gemm = false;
+  }
+  const int ROWS = fused_gemm ? 8 * (32 / NPsel) * gemm_rpw(NPsel) : 8;   // rows per tile / CTA
   for (int b = 0; b < (int)blocks.size(); ++b) {
     BlockDev<T>& D = blocks[b];
     if (!D.fused) continue;
@@ -838,7 +873,8 @@ int Impl<T>::build_fused(const fdtd_probes* probes) {
       }
     }
     const int Cp = (CM + PADC - 1) / PADC * PADC;
-    std::vector<T> Mt((size_t)RM * Cp, (T)0);
+    const int RMp = (RM + ROWS - 1) / ROWS * ROWS;      // zero rows up to a whole tile
+    std::vector<T> Mt((size_t)RMp * Cp, (T)0);
     for (int r = 0; r < RM; ++r)
       for (int c = 0; c < CM; ++c) Mt[(size_t)r * Cp + c] = (T)M[(size_t)r * CM + c];
     D.M_d = dalloc<T>(Mt.size());
@@ -860,11 +896,20 @@ int Impl<T>::build_fused(const fdtd_probes* probes) {
   rows_per_cta = ROWS;
   n_ctas = (int)ctas.size();
   NBsel = maxN <= 1 ? 1 : maxN <= 4 ? 4 : maxN <= 16 ? 16 : 32;
-  fused_smem = (size_t)max_cols * maxN * sizeof(T);
-  d_fblocks = dalloc<fdtd::FusedBlock<T>>(fb.size());
-  d_ctas = dalloc<int2>(ctas.size());
-  if (!d_fblocks || !d_ctas) return fail(FDTD_ENOMEM, "fused descriptor allocation failed");
-  if (upload(d_fblocks, fb) || upload(d_ctas, ctas)) return FDTD_ECUDA;
+  fused_smem = fused_gemm ? (size_t)(ROWS * NPsel + max_cols / GEMM_KS * NPsel +
+                                     ROWS * (max_cols / GEMM_KS + 16 / sizeof(T))) * sizeof(T)
+                          : (size_t)max_cols * maxN * sizeof(T);
+  if (fused_smem > 200 * 1024)
+    return fail(FDTD_ENOTSUP, "fused reduced kernel needs %zu bytes of shared memory (> 200 KB)", fused_smem);
+  if ((int)fb.size() > fdtd::kMaxFusedBlocks)
+    return fail(FDTD_ENOTSUP, "more than %d fused reduced blocks (model classes)", fdtd::kMaxFusedBlocks);
+  fblocks = fb;
+  tile0.assign(1, 0);
+  for (size_t b = 0; b < fb.size(); ++b) {
+    int nt = 0;
+    for (auto& c : ctas) nt += (c.x == (int)b);
+    tile0.push_back(tile0.back() + nt);
+  }
   return FDTD_OK;
 }
 
@@ -894,6 +939,7 @@ int Impl<T>::prologue(cudaStream_t st) {
 template <typename T>
 int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   int64_t n = 0;
+  const int64_t* ds = d_step + p;          // this step's counter slot (the fused kernel writes the other)
   auto mark = [&](int ph, int edge) { if (profile) cudaEventRecord(ev[2 * ph + edge], st); };
   fdtd::Fields<T> F0, F1;
   for (int c = 0; c < 6; ++c) { F0.f[c] = F[p][c]; F1.f[c] = F[p ^ 1][c]; }
@@ -905,30 +951,32 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
     constexpr int NS = 3;
     const int BX = tBX, BY = tBY;
     const int outx = tOUTX, outy = BY - 1;
+    const int kchunk = zchunk(((nx + 1 + outx - 1) / outx) * ((ny + 1 + outy - 1) / outy));
     dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + outy - 1) / outy, (nz + 1 + kchunk - 1) / kchunk);
     const int al = 128 / (int)sizeof(T);
     const size_t HPp = (size_t)(tHBX * (BY + 1) + al - 1) / al * al, EPp = (size_t)(BX * BY + al - 1) / al * al;
     const size_t sm = 256 + (NS * 3 * HPp + NS * 3 * EPp + 3 * 3 * EPp) * sizeof(T) + tabsz;
     if (uniform)
       fdtd::stencil3d_tma_kernel<T, true, NS><<<grid, dim3(BX, BY), sm, st>>>(
-          tma[p], tHBX, tSX, tOUTX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
+          tma[p], tHBX, tSX, tOUTX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, ds, check_every, d_bad);
     else
       fdtd::stencil3d_tma_kernel<T, false, NS><<<grid, dim3(BX, BY), sm, st>>>(
-          tma[p], tHBX, tSX, tOUTX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
+          tma[p], tHBX, tSX, tOUTX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, ds, check_every, d_bad);
   } else if (dim == 3) {
     constexpr int NS = 3;
     int BX, BY;
     if (B == 1) { BX = 32; BY = 8; }
     else { BX = B * std::max(2, 32 / B); BY = std::max(2, 256 / BX); if (BX * BY > 256) BY = 256 / BX; }
     const int outx = BX / B - 1, outy = BY - 1;
+    const int kchunk = zchunk(((nx + 1 + outx - 1) / outx) * ((ny + 1 + outy - 1) / outy));
     dim3 grid((nx + 1 + outx - 1) / outx, (ny + 1 + outy - 1) / outy, (nz + 1 + kchunk - 1) / kchunk);
     const size_t sm = (size_t)(NS * 3 * (BX + B) * (BY + 1) + NS * 3 * BX * BY + 2 * 3 * BX * BY) * sizeof(T) + tabsz;
     if (uniform)
       fdtd::stencil3d_pipe_kernel<T, true, NS><<<grid, dim3(BX, BY), sm, st>>>(
-          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
+          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, ds, check_every, d_bad);
     else
       fdtd::stencil3d_pipe_kernel<T, false, NS><<<grid, dim3(BX, BY), sm, st>>>(
-          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, d_step, check_every, d_bad);
+          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, ds, check_every, d_bad);
   } else {
     constexpr int CY = 4;
     int BX = (B == 1) ? 32 : B * std::max(2, 32 / B), BY = 8;
@@ -938,10 +986,10 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
     const size_t sm = (size_t)BX * BY * CY * sizeof(T) + tabsz;
     if (uniform)
       fdtd::stencil2d_rows_kernel<T, true, CY><<<grid, dim3(BX, BY), sm, st>>>(
-          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, d_step, check_every, d_bad);
+          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad);
     else
       fdtd::stencil2d_rows_kernel<T, false, CY><<<grid, dim3(BX, BY), sm, st>>>(
-          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, d_step, check_every, d_bad);
+          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad);
   }
   ++n;
   mark(0, 1);
@@ -953,24 +1001,25 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
       T* e = eb[0] + D.e_off;
       T* h = hb[0] + D.h_off;
       // a4: e~ -= G_e K~' h~^{n+1/2}
-      n += launch_rowblock<T>(D.qe, D.qh, D.Kph, D.N, D.Kp_d, h, e, D.ge_d, (T)-1, true, d_step, check_every, d_bad, st);
+      n += launch_rowblock<T>(D.qe, D.qh, D.Kph, D.N, D.Kp_d, h, e, D.ge_d, (T)-1, true, ds, check_every, d_bad, st);
       // a6: T = K~'^T e~ + S_E^T G ; h~ += G_h T ; y = S_E h~
-      n += launch_rowblock<T>(D.qh, D.qe, D.Kpe, D.N, D.KTp_d, e, D.Tv_d, (const T*)nullptr, (T)1, false, d_step, 0,
+      n += launch_rowblock<T>(D.qh, D.qe, D.Kpe, D.N, D.KTp_d, e, D.Tv_d, (const T*)nullptr, (T)1, false, ds, 0,
                               d_bad, st);
       if (D.n_if > 0) n += launch_colsum<T>(D.n_if, D.qh, D.Kph, D.N, D.SEp_d, g_all + D.y_off, D.Tv_d, st);
       fdtd::axpy_diag_kernel<T><<<(D.qh * D.N + 255) / 256, 256, 0, st>>>(D.qh, D.N, D.gh_d, D.Tv_d, h);
       ++n;
       if (D.n_if > 0)
         n += launch_rowblock<T>(D.n_if, D.qh, D.Kph, D.N, D.SEp_d, h, y_all + D.y_off, (const T*)nullptr, (T)1, false,
-                                d_step, check_every, d_bad, st);
+                                ds, check_every, d_bad, st);
     }
     mark(2, 1);
   }
   // fused reduced blocks (one GEMV phase) + probes + step counter
   mark(1, 0);
   fdtd::FusedParams<T> P{};
-  P.blocks = d_fblocks;
-  P.ctas = d_ctas;
+  for (size_t b = 0; b < fblocks.size(); ++b) P.fb[b] = fblocks[b];
+  for (size_t b = 0; b < tile0.size(); ++b) P.tile0[b] = tile0[b];
+  P.nfb = (int)fblocks.size();
   P.n_ctas = n_ctas;
   P.B = B;
   P.e_in = eb[p]; P.e_out = eb[p ^ 1];
@@ -984,17 +1033,27 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   P.pr = pr;
   P.ring = ring;
   P.cap = cap;
-  P.d_step = d_step;
-  P.done = d_done;
+  P.d_step = d_step + p;
+  P.d_step_next = d_step + (p ^ 1);
   P.check_every = check_every;
   P.bad_step = d_bad;
-  const unsigned grid = (unsigned)std::max(n_ctas, 1);
   const size_t sm = fused_smem;
+  if (fused_gemm) {
+    const unsigned grid = (unsigned)(std::max(n_ctas, 1) * GEMM_KS);
+    switch (NPsel) {
+      case 4: fdtd::reduced_gemm_kernel<T, 4, gemm_rpw(4), GEMM_KS><<<grid, 256, sm, st>>>(P); break;
+      case 8: fdtd::reduced_gemm_kernel<T, 8, gemm_rpw(8), GEMM_KS><<<grid, 256, sm, st>>>(P); break;
+      case 16: fdtd::reduced_gemm_kernel<T, 16, gemm_rpw(16), GEMM_KS><<<grid, 256, sm, st>>>(P); break;
+      default: fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), GEMM_KS><<<grid, 256, sm, st>>>(P); break;
+    }
+  } else {
+  const unsigned grid = (unsigned)std::max(n_ctas, 1);
   switch (NBsel) {
     case 1: fdtd::reduced_fused_kernel<T, 1><<<grid, 256, sm, st>>>(P); break;
     case 4: fdtd::reduced_fused_kernel<T, 4><<<grid, 256, sm, st>>>(P); break;
     case 16: fdtd::reduced_fused_kernel<T, 16><<<grid, 256, sm, st>>>(P); break;
     default: fdtd::reduced_fused_kernel<T, 32><<<grid, 256, sm, st>>>(P); break;
+  }
   }
   ++n;
   mark(1, 1);
@@ -1141,7 +1200,7 @@ int Impl<T>::get_state(int which, double* out, int64_t n) {
   if (which == 8) {
     if (n != 1) return fail(FDTD_EINVAL, "get_state(8): n must be 1");
     int64_t s = 0;
-    CK(cudaMemcpy(&s, d_step, sizeof(s), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&s, d_step + (host_step & 1), sizeof(s), cudaMemcpyDeviceToHost));
     out[0] = (double)s;
     return FDTD_OK;
   }
@@ -1187,7 +1246,7 @@ int Impl<T>::set_state(int which, const double* in, int64_t n) {
     if (e) return e;
     const int64_t v = (int64_t)in[0];
     if (v < 0) return fail(FDTD_EINVAL, "set_state(8): negative step");
-    CK(cudaMemcpy(d_step, &v, sizeof(v), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_step + (host_step & 1), &v, sizeof(v), cudaMemcpyHostToDevice));
     step_offset = v - host_step;
     return FDTD_OK;
   }

@@ -206,6 +206,11 @@ __device__ __forceinline__ void cp_async(T* dst, const T* src, bool valid) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+// 16-byte global -> shared copy; zero-fills when !valid
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0));
+}
 
 template <typename T, bool UNIFORM, int NS>
 __global__ void __launch_bounds__(256, 3)
@@ -292,6 +297,7 @@ stencil3d_pipe_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
   __syncthreads();                                   // material table
   T hxk = 0, hyk = 0, hzk = 0;                       // H_old of the previous plane (own)
   T exk = 0, eyk = 0, ezk = 0;                       // E_new of the previous plane (own)
+  int m_next = UNIFORM ? 0 : (int)__ldg(mat_id + (int64_t)k0 * d.plane + scol), m_prev = 0;
   for (int kk = k0; kk <= kend; ++kk) {
     if (kk + NS - 1 <= kend) issue(kk + NS - 1);
     cp_async_commit();
@@ -304,7 +310,8 @@ stencil3d_pipe_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
     const T hz_jm = h[2 * HP + (yi - 1) * HW + xi], hx_jm = h[0 * HP + (yi - 1) * HW + xi];
     const T hz_im = h[2 * HP + yi * HW + xi - B], hy_im = h[1 * HP + yi * HW + xi - B];
     const T ex0 = e[0 * EP + ty * BX + tx], ey0 = e[1 * EP + ty * BX + tx], ez0 = e[2 * EP + ty * BX + tx];
-    const int m = UNIFORM ? 0 : (int)mat_id[(int64_t)kk * d.plane + scol];
+    const int m = m_next;                                   // material of plane kk (prefetched)
+    if (!UNIFORM && kk + 1 <= kend) m_next = (int)__ldg(mat_id + (int64_t)(kk + 1) * d.plane + scol);
     Coef<T> cx, cy, cz;
     uint8_t ifmk = 0;
     if (UNIFORM) { cx = u0; cy = u0; cz = u0; }
@@ -335,7 +342,7 @@ stencil3d_pipe_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
       const int km = kk - 1;
       Coef<T> hx_, hy_, hz_;
       if (UNIFORM) { hx_ = u1; hy_ = u1; hz_ = u1; }
-      else { const int mm = (int)mat_id[(int64_t)km * d.plane + scol]; hx_ = tab->c[mm][3]; hy_ = tab->c[mm][4]; hz_ = tab->c[mm][5]; }
+      else { hx_ = tab->c[m_prev][3]; hy_ = tab->c[m_prev][4]; hz_ = tab->c[m_prev][5]; }   // plane kk-1
       const T hx1 = (hx_ij && km < nz) ? hxk - hx_.apply((ez_jp - ezk) - (ey - eyk)) : hxk;
       const T hy1 = (hy_ij && km < nz) ? hyk - hy_.apply((ex - exk) - (ez_ip - ezk)) : hyk;
       const T hz1 = (hz_ij && km > 0 && km < nz) ? hzk - hz_.apply((ey_ip - eyk) - (ex_jp - exk)) : hzk;
@@ -346,6 +353,7 @@ stencil3d_pipe_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
     hx_p = hx_c; hy_p = hy_c;
     hxk = hx_c; hyk = hy_c; hzk = hz_c;
     exk = ex; eyk = ey; ezk = ez;
+    m_prev = m;
   }
   // last chunk: plane nz of H has no update (Hx, Hy absent, Hz normal to the
   // PEC wall); the new buffer still needs it
@@ -489,6 +497,7 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int out
   }
   T hxk = 0, hyk = 0, hzk = 0;
   T exk = 0, eyk = 0, ezk = 0;
+  int m_next = UNIFORM ? 0 : (int)__ldg(mat_id + (int64_t)k0 * d.plane + scol), m_prev = 0;
   for (int kk = k0; kk <= kend; ++kk) {
     if (leader && kk + NS - 1 <= kend) FDTD_TMA_ISSUE(kk + NS - 1);
     const int st = (kk - k0) % NS;
@@ -499,7 +508,8 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int out
     const T hz_jm = h[2 * HP + (yi - 1) * HW + xi], hx_jm = h[0 * HP + (yi - 1) * HW + xi];
     const T hz_im = h[2 * HP + yi * HW + xi - B], hy_im = h[1 * HP + yi * HW + xi - B];
     const T ex0 = e[0 * EP + ty * BX + tx], ey0 = e[1 * EP + ty * BX + tx], ez0 = e[2 * EP + ty * BX + tx];
-    const int m = UNIFORM ? 0 : (int)mat_id[(int64_t)kk * d.plane + scol];
+    const int m = m_next;                                   // material of plane kk (prefetched)
+    if (!UNIFORM && kk + 1 <= kend) m_next = (int)__ldg(mat_id + (int64_t)(kk + 1) * d.plane + scol);
     Coef<T> cx, cy, cz;
     uint8_t ifmk = 0;
     if (UNIFORM) { cx = u0; cy = u0; cz = u0; }
@@ -530,7 +540,7 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int out
       const int km = kk - 1;
       Coef<T> hx_, hy_, hz_;
       if (UNIFORM) { hx_ = u1; hy_ = u1; hz_ = u1; }
-      else { const int mm = (int)mat_id[(int64_t)km * d.plane + scol]; hx_ = tab->c[mm][3]; hy_ = tab->c[mm][4]; hz_ = tab->c[mm][5]; }
+      else { hx_ = tab->c[m_prev][3]; hy_ = tab->c[m_prev][4]; hz_ = tab->c[m_prev][5]; }   // plane kk-1
       const T hx1 = (hx_ij && km < nz) ? hxk - hx_.apply((ez_jp - ezk) - (ey - eyk)) : hxk;
       const T hy1 = (hy_ij && km < nz) ? hyk - hy_.apply((ex - exk) - (ez_ip - ezk)) : hyk;
       const T hz1 = (hz_ij && km > 0 && km < nz) ? hzk - hz_.apply((ey_ip - eyk) - (ex_jp - exk)) : hzk;
@@ -541,6 +551,7 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int out
     hx_p = hx_c; hy_p = hy_c;
     hxk = hx_c; hyk = hy_c; hzk = hz_c;
     exk = ex; eyk = ey; ezk = ez;
+    m_prev = m;
   }
   if (k1 == nz + 1 && own) {
     const int64_t o = (int64_t)nz * sz + col;
@@ -577,10 +588,14 @@ struct FusedBlock {
   const int32_t* probe_inst;
 };
 
+constexpr int kMaxFusedBlocks = 8;
 template <typename T>
 struct FusedParams {
-  const FusedBlock<T>* blocks;
-  const int2* ctas;             // (block, first row)
+  // block descriptors live in the kernel parameters (__grid_constant__): the
+  // CTA -> (block, first row) map is arithmetic, no dependent global loads
+  FusedBlock<T> fb[kMaxFusedBlocks];
+  int tile0[kMaxFusedBlocks + 1];   // first tile (CTA / cluster) of each block
+  int nfb;
   int n_ctas, B, rows_per_cta;
   const T* e_in; T* e_out;      // e~^{n+1} in, e~^{n+2} out
   const T* h_in; T* h_out;      // h~^{n+1/2} in, h~^{n+3/2} out
@@ -591,11 +606,19 @@ struct FusedParams {
   Probes<T> pr;
   T* ring;
   int64_t cap;
-  int64_t* d_step;
-  unsigned int* done;
+  const int64_t* d_step;        // this step's counter slot
+  int64_t* d_step_next;         // the other parity's slot: <- step + 1
   int check_every;
   unsigned long long* bad_step;
 };
+
+template <typename T>
+__device__ __forceinline__ int2 fused_tile(const FusedParams<T>& P, int tile) {
+  int b = 0;
+#pragma unroll 1
+  while (b + 1 < P.nfb && tile >= P.tile0[b + 1]) ++b;
+  return make_int2(b, (tile - P.tile0[b]) * P.rows_per_cta);
+}
 
 template <typename T> struct Vec;
 template <> struct Vec<float> { using type = float4; static constexpr int n = 4; };
@@ -612,9 +635,66 @@ __device__ __forceinline__ double vdot<double>(const double2& a, const double2& 
   return a.x * x.x + a.y * x.y;
 }
 
+template <typename T>
+__device__ __forceinline__ T vdot_reg(const typename Vec<T>::type& a, const T* x);
+template <>
+__device__ __forceinline__ float vdot_reg<float>(const float4& a, const float* x) {
+  return a.x * x[0] + a.y * x[1] + a.z * x[2] + a.w * x[3];
+}
+template <>
+__device__ __forceinline__ double vdot_reg<double>(const double2& a, const double* x) {
+  return a.x * x[0] + a.y * x[1];
+}
+// load a word of CTA `rank`'s shared memory (same offset) through the cluster
+template <typename T>
+__device__ __forceinline__ T dsmem_load(unsigned local_addr, unsigned rank);
+template <>
+__device__ __forceinline__ float dsmem_load<float>(unsigned local_addr, unsigned rank) {
+  unsigned remote;
+  float v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local_addr), "r"(rank));
+  asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(remote) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ double dsmem_load<double>(unsigned local_addr, unsigned rank) {
+  unsigned remote;
+  double v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local_addr), "r"(rank));
+  asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(v) : "r"(remote) : "memory");
+  return v;
+}
+
+// coarse probes, leapfrog-path reduced probes, divergence flag and the device
+// step counter (advanced by the last CTA to finish) -- shared by both fused
+// reduced kernels
+template <typename T>
+__device__ __forceinline__ void fused_tail(const FusedParams<T>& P, int64_t step, bool bad) {
+  const int B = P.B;
+  // coarse probes and leapfrog-path reduced probes
+  if (blockIdx.x == 0) {
+    for (int t = threadIdx.x; t < P.pr.n_probe * B; t += blockDim.x) {
+      const int p = t / B, bb = t % B;
+      if (P.pr.owner[p] != -1) continue;
+      T acc = 0;
+      for (int64_t k = P.pr.rowptr[p]; k < P.pr.rowptr[p + 1]; ++k) {
+        const int s = P.pr.src[k];
+        const T v = (s < 6) ? P.F.f[s][P.pr.off[k] * B + bb] : P.red_base[s - 6][P.pr.off[k] + bb];
+        acc += P.pr.w[k] * v;
+      }
+      P.ring[(step % P.cap) * (int64_t)P.pr.n_probe * B + t] = acc;
+    }
+  }
+  if (bad) atomicMin(P.bad_step, (unsigned long long)step);
+  // the step counter lives in two slots by step parity: this kernel reads slot
+  // p and publishes step + 1 in slot p^1, which only the next step reads (no
+  // grid-wide completion counter needed)
+  if (blockIdx.x == 0 && threadIdx.x == 0) *P.d_step_next = step + 1;
+}
+
 template <typename T, int NB>
 __global__ void __launch_bounds__(256)
-reduced_fused_kernel(FusedParams<T> P) {
+reduced_fused_kernel(const __grid_constant__ FusedParams<T> P) {
   using V = typename Vec<T>::type;
   constexpr int VN = Vec<T>::n;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -624,8 +704,8 @@ reduced_fused_kernel(FusedParams<T> P) {
   bool bad = false;
   const int B = P.B;
   if ((int)blockIdx.x < P.n_ctas) {
-    const int2 ct = P.ctas[blockIdx.x];
-    const FusedBlock<T> FB = P.blocks[ct.x];
+    const int2 ct = fused_tile(P, (int)blockIdx.x);
+    const FusedBlock<T>& FB = P.fb[ct.x];
     const int C = FB.C, Cp = FB.Cp, N = FB.N, qe = FB.qe, qh = FB.qh, ni = FB.n_if;
     // stage X = [e~ ; G ; h~ ; 0-padding] as [N][Cp]
     for (int t = threadIdx.x; t < qe * N; t += blockDim.x) X[(t % N) * Cp + t / N] = P.e_in[FB.e_off + t];
@@ -673,32 +753,132 @@ reduced_fused_kernel(FusedParams<T> P) {
       }
     }
   }
-  // coarse probes and leapfrog-path reduced probes
-  if (blockIdx.x == 0) {
-    for (int t = threadIdx.x; t < P.pr.n_probe * B; t += blockDim.x) {
-      const int p = t / B, bb = t % B;
-      if (P.pr.owner[p] != -1) continue;
-      T acc = 0;
-      for (int64_t k = P.pr.rowptr[p]; k < P.pr.rowptr[p + 1]; ++k) {
-        const int s = P.pr.src[k];
-        const T v = (s < 6) ? P.F.f[s][P.pr.off[k] * B + bb] : P.red_base[s - 6][P.pr.off[k] + bb];
-        acc += P.pr.w[k] * v;
+  fused_tail(P, step, bad);
+}
+
+// ---------------------------------------------------------------------------
+// Batched reduced blocks (N = instances x batch >= 4 columns): the same fused
+// update [h~' ; y' ; e~'' ; probe rows] = M [e~ ; G ; h~] as a register-tiled
+// SIMT GEMM.  A cluster of KS CTAs shares one tile of TR rows: CTA `rank`
+// contracts the K-slice [rank*Cp/KS, (rank+1)*Cp/KS) -- its slice of X staged
+// in shared memory as [k][NP] (the natural [q][N] layout of the states: a
+// straight copy, lanes read consecutive words) -- and the KS partial tiles are
+// summed in a fixed order through distributed shared memory (deterministic).
+// Lane = (row group, column n): M is read with 16-byte broadcast loads (every
+// lane of a row group reads the same row), X with conflict-free 4-byte loads.
+// ---------------------------------------------------------------------------
+template <typename T, int NP, int RPW, int KS>
+__global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(256)
+reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
+  using V = typename Vec<T>::type;
+  constexpr int VN = Vec<T>::n;
+  constexpr int GPW = 32 / NP;                 // row groups per warp
+  constexpr int TR = 8 * GPW * RPW;            // rows per tile
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Ps = reinterpret_cast<T*>(smem_raw);      // [TR][NP] partial tile
+  T* Xs = Ps + TR * NP;                        // [kc][NP] slice of [e~ ; G ; h~]
+  const int64_t step = *P.d_step;
+  const bool check = P.check_every > 0 && (step % P.check_every) == 0;
+  bool bad = false;
+  const int B = P.B;
+  unsigned rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+  const int tile = blockIdx.x / KS;
+  const bool active = tile < P.n_ctas;
+  int2 ct = make_int2(0, 0);
+  if (active) {
+    ct = fused_tile(P, tile);
+    const FusedBlock<T>& FB = P.fb[ct.x];
+    const int N = FB.N, C = FB.C, qe = FB.qe, ni = FB.n_if;
+    const int kc = FB.Cp / KS, k_lo = (int)rank * kc;
+    T* Ms = Xs + kc * NP;                      // [TR][kc + VN] slice of M (padded pitch)
+    const int mp = kc + VN;
+    // M slice: 16-byte cp.async, all in flight at once
+    for (int t = threadIdx.x; t < TR * (kc / VN); t += blockDim.x) {
+      const int u = t / (kc / VN), v = t % (kc / VN);
+      cp_async16(Ms + u * mp + v * VN, FB.M + (int64_t)(ct.y + u) * FB.Cp + k_lo + v * VN, true);
+    }
+    if (N == NP && N % VN == 0) {
+      // X slice, straight 16-byte copies (every k-row is N contiguous words)
+      for (int t = threadIdx.x; t < kc * (NP / VN); t += blockDim.x) {
+        const int kk = t / (NP / VN), n = (t % (NP / VN)) * VN, k = k_lo + kk;
+        const T* src = P.e_in;                 // any valid address when zero-filled
+        if (k < qe) src = P.e_in + FB.e_off + (int64_t)k * N + n;
+        else if (k < qe + ni) src = P.G + FB.y_off + (int64_t)(k - qe) * N + n;
+        else if (k < C) src = P.h_in + FB.h_off + (int64_t)(k - qe - ni) * N + n;
+        cp_async16(Xs + kk * NP + n, src, k < C);
       }
-      P.ring[(step % P.cap) * (int64_t)P.pr.n_probe * B + t] = acc;
+    } else {
+      for (int t0 = threadIdx.x; t0 < kc * NP; t0 += 8 * 256) {
+        T v[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const int t = t0 + w * 256, kk = t / NP, n = t % NP, k = k_lo + kk;
+          v[w] = 0;
+          if (t < kc * NP && n < N && k < C) {
+            if (k < qe) v[w] = P.e_in[FB.e_off + (int64_t)k * N + n];
+            else if (k < qe + ni) v[w] = P.G[FB.y_off + (int64_t)(k - qe) * N + n];
+            else v[w] = P.h_in[FB.h_off + (int64_t)(k - qe - ni) * N + n];
+          }
+        }
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+          if (t0 + w * 256 < kc * NP) Xs[t0 + w * 256] = v[w];
+      }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int n = lane % NP, g = lane / NP;
+    const int rl0 = (warp * GPW + g) * RPW;
+    T acc[RPW];
+#pragma unroll
+    for (int u = 0; u < RPW; ++u) acc[u] = 0;
+    const int nv = kc / VN;
+#pragma unroll 4
+    for (int kv = 0; kv < nv; ++kv) {
+      T x[VN];
+#pragma unroll
+      for (int j = 0; j < VN; ++j) x[j] = Xs[(kv * VN + j) * NP + n];
+#pragma unroll
+      for (int u = 0; u < RPW; ++u) {
+        const V m = *reinterpret_cast<const V*>(Ms + (rl0 + u) * mp + kv * VN);
+        acc[u] += vdot_reg<T>(m, x);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RPW; ++u) Ps[(rl0 + u) * NP + n] = acc[u];
+  }
+  // all partial tiles of the cluster written
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (active) {
+    const FusedBlock<T>& FB = P.fb[ct.x];
+    const int N = FB.N, qe = FB.qe, qh = FB.qh, ni = FB.n_if;
+    constexpr int RPR = TR / KS;               // rows reduced by this rank
+    const unsigned ps_local = smem_u32(Ps);
+    for (int t = threadIdx.x; t < RPR * NP; t += blockDim.x) {
+      const int rl = (int)rank * RPR + t / NP, n = t % NP;
+      const int r = ct.y + rl;
+      T v = 0;
+#pragma unroll
+      for (int q = 0; q < KS; ++q) v += dsmem_load<T>(ps_local + (unsigned)((rl * NP + n) * sizeof(T)), (unsigned)q);
+      if (r >= FB.R || n >= N) continue;
+      if (r < qh) P.h_out[FB.h_off + (int64_t)r * N + n] = v;
+      else if (r < qh + ni) P.y[FB.y_off + (int64_t)(r - qh) * N + n] = v;
+      else if (r < qh + ni + qe) P.e_out[FB.e_off + (int64_t)(r - qh - ni) * N + n] = v;
+      else {
+        const int q = r - qh - ni - qe;
+        const int p = FB.probe_id[q], in = FB.probe_inst[q];
+        if (n >= in * B && n < in * B + B)
+          P.ring[(step % P.cap) * (int64_t)P.pr.n_probe * B + (int64_t)p * B + (n - in * B)] = v;
+      }
+      if (check && !finite_small((double)v)) bad = true;
     }
   }
-  if (bad) atomicMin(P.bad_step, (unsigned long long)step);
-  // the last CTA to finish advances the device step counter
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned int prev = atomicAdd(P.done, 1u);
-    if (prev == gridDim.x - 1) {
-      *P.done = 0;
-      __threadfence();
-      *P.d_step = step + 1;
-    }
-  }
+  // no CTA leaves (releasing its shared memory) before every rank has read it
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  fused_tail(P, step, bad);
 }
 
 // out[r][n] = (accumulate ? out[r][n] : 0) + alpha g[r] sum_c A[r][c] X[c][n]

@@ -22,7 +22,11 @@ import scipy.sparse.linalg as spla
 
 from . import fit, reduce
 
-PREP_VERSION = 8
+PREP_VERSION = 9
+# dense reduced matrices above this many entries are stored rounded to fp32
+# (reading R13: config 4's S_E is 65,024 x 1,024; both the GPU and
+# the oracle consume the same rounded values)
+BIG_DENSE = 1 << 25
 CACHE_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))),
                          "cache", "prep")
 
@@ -173,6 +177,8 @@ def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=N
         Kt, SE = reduce.project(V1, V2, part.Kff, part.Kcf)
         De_if = np.array([P.De_c[int(f // S)].ravel()[int(f % S)] for f in part.if_ids])
         Kp, SEp, rep = reduce.enforce_block(Kt, SE, De_if, alpha, dt)
+        if SEp.size > BIG_DENSE:
+            SEp = SEp.astype(np.float32)
         rep.update(t_basis=time.time() - t1, q=q)
         info.setdefault("blocks", []).append(rep)
         blocks.append(dict(q=q, qe=q, qh=q, n_inst=len(classes[class_ids[box_class[bi][0]]]), K=Kp, S_E=SEp,
@@ -277,7 +283,9 @@ def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=N
     # the problem description: the GPU never needs V beyond probe rows)
     info["basis_blocks"] = [dict(V1=b["V1"] if b["V1"].size < 4_000_000 else None,
                                  V2=b["V2"] if b["V2"].size < 4_000_000 else None,
-                                 Kt_pre=b["Kt_pre"], S_E_pre=b["S_E_pre"], if_ids=b["if_ids"])
+                                 Kt_pre=b["Kt_pre"],
+                                 S_E_pre=b["S_E_pre"] if b["S_E_pre"].size <= BIG_DENSE else None,
+                                 if_ids=b["if_ids"])
                             for b in blocks]
     if cache:
         os.makedirs(CACHE_DIR, exist_ok=True)

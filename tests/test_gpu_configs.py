@@ -86,10 +86,13 @@ def test_config3_full_size_sampled_one_step(prec):
     assert np.max(np.abs(got - want)) <= tol * scale
 
 
+@pytest.mark.parametrize("kernel", ["gemv", "gemm"])
 @pytest.mark.parametrize("prec", [64, 32])
-def test_tiny5_shared_models_pec_plates(prec):
+def test_tiny5_shared_models_pec_plates(prec, kernel, monkeypatch):
     # config-5 structure: z-refined regions around stub tips, PEC plates through
-    # the regions, two shared models with two instances each
+    # the regions, two shared models with two instances each (N = 2 columns:
+    # both fused kernels)
+    monkeypatch.setenv("FDTD_FUSED", kernel)
     scn, prob = _prep("tiny5", precision=prec)
     assert [b["n_inst"] for b in prob["blocks"]] == [2, 2]
     gpu = run_gpu(prob, 300, precision=prec)
@@ -110,11 +113,16 @@ def test_config5_full_size_fp32_short_run():
     assert es <= 1e-4 and ep <= 1e-4, (es, ep)
 
 
-@pytest.mark.parametrize("form", ["fused", "leapfrog"])
+@pytest.mark.parametrize("form", ["fused", "fused-gemv", "leapfrog"])
 @pytest.mark.parametrize("prec", [64, 32])
-def test_tiny4_batched_iris_guide(prec, form):
+def test_tiny4_batched_iris_guide(prec, form, monkeypatch):
     # config-4 structure: x-graded refined slab with a PEC iris, B = 4
-    # excitations of a TE10 sheet source, z = 0 Krylov basis (reading R5(viii))
+    # excitations of a TE10 sheet source, z = 0 Krylov basis (reading R5(viii));
+    # "fused" takes the cluster-split GEMM kernel (N = 4), "fused-gemv" forces
+    # the warp-per-row kernel
+    if form == "fused-gemv":
+        monkeypatch.setenv("FDTD_FUSED", "gemv")
+        form = "fused"
     scn, prob = _prep("tiny4", precision=prec)
     gpu = run_gpu(prob, 300, precision=prec, reduced_form=form)
     tol = 1e-12 if prec == 64 else 1e-4
@@ -154,3 +162,69 @@ def test_tma_stencil_bitwise_equals_cp_async_stencil(monkeypatch):
         a, b = run(True, state), run(False, state)
         for c in range(6):
             assert np.array_equal(a[c], b[c]), c
+
+
+def _gpu_red_order(vec_by_member, problem):
+    """[B][q_total] per-member reduced vectors -> the binding's set_state order
+    [block][inst][B][q]."""
+    B = vec_by_member.shape[0]
+    out, o = [], 0
+    for b in problem["blocks"]:
+        q = int(b.get("qe", b.get("q")))
+        for i in range(int(b["n_inst"])):
+            out.append(vec_by_member[:, o:o + q].ravel())
+            o += q
+    return np.concatenate(out)
+
+
+def test_config4_full_size_sampled_one_step():
+    # config 4 at full size (512 x 128 x 128, q = 1024 block with 65,024
+    # interface rows, B = 16, leap-frog reduced path) in the launch
+    # configuration bench.py times: one step from a seeded random state
+    # (active unknowns of a window around the refined slab and the source
+    # plane), against the unknown-by-unknown oracle (sampled_hybrid_step,
+    # pinned in test_oracle_sampled.py) for two members
+    from paper_1406_7042_b200.fdtd import Sim
+    from sampled_state import random_state
+    scn, prob = _prep(4, precision=32)
+    prob = dict(prob, init={})
+    nx, ny, nz = prob["n"]
+    px = nx + 1
+    win = lambda idx: ((idx % px >= 240) & (idx % px <= 272)) | ((idx % px >= 28) & (idx % px <= 36))
+    arrays, red_e, red_h = random_state(prob, seed=4, window=win)
+    step = 60
+    sim = Sim(prob, precision=32, graph_steps=0)
+    assert sim.B == 16
+    for c in range(6):
+        sim.set_state(c, arrays[c])
+    sim.set_state(6, _gpu_red_order(red_e, prob))
+    sim.set_state(7, _gpu_red_order(red_h, prob))
+    sim.set_state(8, [float(step)])
+    sim.step(1)
+    sim.sync()
+    got = {c: sim.get_state(c) for c in range(6)}
+    ge, gh = sim.get_state(6), sim.get_state(7)
+    sim.close()
+    S = (nx + 1) * (ny + 1) * (nz + 1)
+    rng = np.random.default_rng(2)
+    samples = []
+    for c in range(6):
+        for _ in range(60):
+            samples.append((c, (int(rng.integers(240, 273)), int(rng.integers(0, ny + 1)), int(rng.integers(0, nz + 1)))))
+        for _ in range(20):
+            samples.append((c, (int(rng.integers(28, 37)), int(rng.integers(0, ny + 1)), int(rng.integers(0, nz + 1)))))
+    ifu = np.asarray(prob["interface"]["unknown"], np.int64)
+    from parity import reduced_member, block_shapes
+    for m in (0, 11):
+        out, Eif, e1, h1 = ps.sampled_hybrid_step(prob, arrays, red_e[m], red_h[m], samples, member=m, step=step)
+        scale = max(abs(v) for v in out.values())
+        for (c, (i, j, k)), want in out.items():
+            g = got[c][m][(k * (ny + 1) + j) * (nx + 1) + i]
+            assert abs(g - want) <= 2e-5 * scale, (m, c, (i, j, k), g, want)
+        gif = np.array([got[int(u // S)][m][int(u % S)] for u in ifu])
+        assert np.abs(gif - Eif).max() <= 2e-5 * np.abs(Eif).max()
+        sh = block_shapes(prob)
+        gre = reduced_member(ge, sh, 16, m, "e")
+        grh = reduced_member(gh, sh, 16, m, "h")
+        assert np.abs(gre - e1).max() <= 2e-5 * np.abs(e1).max()
+        assert np.abs(grh - h1).max() <= 2e-5 * np.abs(h1).max()
