@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libfdtd.so")
 SOURCES = ["fdtd_api.cu"]
-HEADERS = ["kernels.cuh", os.path.join("..", "..", "include", "fdtd.h")]
+HEADERS = ["kernels.cuh", "persist2d.cuh", os.path.join("..", "..", "include", "fdtd.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]

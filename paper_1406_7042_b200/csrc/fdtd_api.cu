@@ -10,6 +10,7 @@
 //            paper's order.
 #include "../../include/fdtd.h"
 #include "kernels.cuh"
+#include "persist2d.cuh"
 
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -261,6 +262,24 @@ struct Impl : public fdtd_t {
   int create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_interface* itf,
              const fdtd_reduced_block* bl, int n_blocks, const fdtd_sources* src,
              const fdtd_probes* probes, const fdtd_exec* ex);
+  // ---- persistent 2-D path (persist2d.cuh) ----
+  struct XRow { int comp; int64_t s; double c; std::vector<std::pair<int64_t, double>> w; int64_t y; int src_col; double cs; };
+  std::vector<XRow> xrows;                          // explicit rows (host copy)
+  std::vector<int32_t> hpr_src, hpr_owner;          // coarse probes (host copy)
+  std::vector<int64_t> hpr_off, hpr_rp;
+  std::vector<double> hpr_w;
+  bool persist = false;
+  int p_maxrows = 0;
+  int pTX = 0, pTY = 0, pntx = 0, pnty = 0, p_nif_tiles = 0, p_nred = 0, p_Rtot = 0, p_rpc = 0, p_Cmax = 0;
+  int p_row0[fdtd::kMaxFusedBlocks + 1] = {};
+  size_t p_smem = 0;
+  fdtd::P2Rows<T> p_rows{};
+  fdtd::P2Probes<T> p_probes{};
+  T *p_ezL = nullptr, *p_ezB = nullptr, *p_hyR = nullptr, *p_hxT = nullptr;
+  unsigned* p_flags = nullptr;                      // fE[nT] fH[nT] gready reddone abort
+  uint8_t* p_tile_if = nullptr;
+  int setup_persist();
+  int launch_persist(int64_t n, int64_t* count);
   int build_fused(const fdtd_probes* probes);
   int prologue(cudaStream_t st);
   int launch_step(int parity, cudaStream_t st, int64_t* count, bool profile = false);
@@ -632,6 +651,8 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     for (int c = 4; c < (dim == 3 ? 6 : 5); ++c)
       if (coef[c] != coef[3]) return fail(FDTD_ENOTSUP, "uniform mode needs equal ch for all H components");
   }
+  for (const auto& h : hrows)
+    xrows.push_back(XRow{h.comp, h.s, h.c, h.w, h.y, h.src >= 0 ? wcol[h.src] : -1, h.cs});
   // upload explicit rows
   {
     const int64_t nr = (int64_t)hrows.size();
@@ -743,6 +764,8 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     if (upload(d_rp, rp) || upload(d_src, srcv) || upload(d_off, off) || upload(d_w, w) || upload(d_ow, owner))
       return FDTD_ECUDA;
     pr.n_probe = n_probe; pr.rowptr = d_rp; pr.src = d_src; pr.off = d_off; pr.w = d_w; pr.owner = d_ow;
+    hpr_src = srcv; hpr_owner = owner; hpr_off = off; hpr_rp = rp;
+    for (auto v : w) hpr_w.push_back((double)v);
     ring = dalloc<T>(std::max<int64_t>(cap * n_probe * B, 1));
     if (!ring) return fail(FDTD_ENOMEM, "probe ring allocation failed");
   }
@@ -788,7 +811,271 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
     CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
   }
+  {
+    int e = setup_persist();
+    if (e) return e;
+  }
   CK(cudaStreamSynchronize(stream));
+  return FDTD_OK;
+}
+
+// Persistent 2-D path (persist2d.cuh): eligible when the problem is 2-D,
+// single-member, every reduced block fused with one column, every explicit row
+// references only the four H neighbours of its own cell, every coarse probe
+// lies in one tile, and all tiles fit co-resident.  Otherwise the per-step
+// kernels run (same results, bit for bit).
+template <typename T>
+int Impl<T>::setup_persist() {
+  persist = false;
+  auto why_not = [&](int code) {
+    if (getenv("FDTD_VERBOSE")) fprintf(stderr, "fdtd: persistent 2-D path not used (reason %d)\n", code);
+    return FDTD_OK;
+  };
+  if (const char* e = getenv("FDTD_PERSIST"))
+    if (std::string(e) == "0") return why_not(1);
+  if (dim != 2 || B != 1 || any_leap) return why_not(2);
+  for (auto& D : blocks)
+    if (!D.fused || D.N != 1) return why_not(3);
+  for (size_t q = 0; q < hpr_owner.size(); ++q) {
+    if (hpr_owner[q] != -1) continue;
+    for (int64_t k = hpr_rp[q]; k < hpr_rp[q + 1]; ++k)
+      if (hpr_src[k] < 2 || hpr_src[k] > 4) return why_not(4);
+  }
+  int dev = 0, nsm = 0, coop = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  if (!coop) return why_not(5);
+  // reduced rows
+  int Rtot = 0, Cmax = 0, nfb = 0;
+  for (size_t b = 0; b < fblocks.size(); ++b) {
+    p_row0[b] = Rtot;
+    const int RMp = fblocks[b].R;
+    Rtot += RMp;
+    Cmax = std::max(Cmax, fblocks[b].Cp);
+    ++nfb;
+  }
+  p_row0[nfb] = Rtot;
+  // tiles cover cells i < nx, j < ny (the last storage column / row is constant)
+  const int TX = (nx <= 32) ? 32 : 64;
+  const int ntx = (nx + TX - 1) / TX;
+  int TY = 0, nty = 0, rpc = 0, nT = 0, nR = 0;
+  size_t smem = 0;
+  for (int cand : {64, 96, 128, 32}) {
+    const int ty = (ny <= 32) ? 32 : cand;
+    const int nt_y = (ny + ty - 1) / ty;
+    const int nt = ntx * nt_y;
+    int maxrows = 0;
+    {
+      std::vector<int> cnt(ntx * nt_y, 0);
+      for (const auto& x : xrows) {
+        const int i = (int)(x.s % (nx + 1)), j = (int)(x.s / (nx + 1));
+        if (i < nx && j < ny) maxrows = std::max(maxrows, ++cnt[(j / ty) * ntx + i / TX]);
+      }
+    }
+    const size_t tile_sm = sizeof(T) * ((size_t)3 * TX * ty + 2 * TX + 2 * ty) +
+                           3 * fdtd::MAX_MAT * sizeof(fdtd::Coef<T>) + fdtd::MAX_MAT +
+                           ((size_t)TX * ty + 15) / 16 * 16 + (2 * sizeof(T) * (size_t)maxrows + 15) / 16 * 16 +
+                           sizeof(fdtd::P2Row<T>) * (size_t)maxrows + 64;
+    if (tile_sm > 220 * 1024) continue;
+    CK(cudaFuncSetAttribute(fdtd::persist2d_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sm));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdtd::persist2d_kernel<T>, 512, tile_sm));
+    const int capacity = per_sm * nsm;
+    int nr = 0, r = 0;
+    size_t sm = tile_sm;
+    if (Rtot > 0) {
+      nr = std::min(capacity - nt, std::max(1, (Rtot + 7) / 8));
+      if (nr < 1) continue;
+      r = (Rtot + nr - 1) / nr;
+      sm = std::max(tile_sm, sizeof(T) * (size_t)(1 + r) * Cmax + 64);
+      if (sm > 220 * 1024) continue;
+      CK(cudaFuncSetAttribute(fdtd::persist2d_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdtd::persist2d_kernel<T>, 512, sm));
+      nr = (Rtot + r - 1) / r;
+      if (per_sm * nsm < nt + nr) continue;
+    }
+    TY = ty; nty = nt_y; nT = nt; nR = nr; rpc = r; smem = sm; p_maxrows = maxrows;
+    break;
+  }
+  auto storage_ijk = [&](int64_t s_, int& i, int& j, int& k) {   // 2-D storage index
+    i = (int)(s_ % (nx + 1)); j = (int)(s_ / (nx + 1)); k = 0;
+  };
+  // explicit rows -> tiles, with the H terms as local slots
+  std::vector<std::vector<int>> by_tile(nT);
+  std::vector<int32_t> li(xrows.size());
+  std::vector<int8_t> nterm(xrows.size()), slot(4 * xrows.size(), 0);
+  std::vector<T> wv(4 * xrows.size(), (T)0);
+  for (size_t r = 0; r < xrows.size(); ++r) {
+    const XRow& x = xrows[r];
+    if (x.comp != 2 || x.w.size() > 4) return why_not(7);
+    int i, j, k;
+    storage_ijk(x.s, i, j, k);
+    if (i >= nx || j >= ny) return why_not(11);
+    for (size_t q = 0; q < x.w.size(); ++q) {
+      const int hc = (int)(x.w[q].first / S);
+      int hi, hj, hk;
+      storage_ijk(x.w[q].first % S, hi, hj, hk);
+      int sl = -1;
+      if (hc == 4 && hi == i && hj == j) sl = 0;
+      else if (hc == 4 && hi == i - 1 && hj == j) sl = 1;
+      else if (hc == 3 && hi == i && hj == j) sl = 2;
+      else if (hc == 3 && hi == i && hj == j - 1) sl = 3;
+      if (sl < 0) return why_not(8);
+      slot[4 * r + q] = (int8_t)sl;
+      wv[4 * r + q] = (T)x.w[q].second;
+    }
+    nterm[r] = (int8_t)x.w.size();
+    li[r] = (j % TY) * TX + (i % TX);
+    by_tile[(j / TY) * ntx + (i / TX)].push_back((int)r);
+  }
+  std::vector<int32_t> tptr(1, 0), rli, rsrc;
+  std::vector<int8_t> rnt, rsl;
+  std::vector<T> rw, rcs;
+  std::vector<fdtd::Coef<T>> rc;
+  std::vector<int64_t> ryo;
+  std::vector<uint8_t> tif(nT, 0);
+  int nif_tiles = 0;
+  for (int t = 0; t < nT; ++t) {
+    for (int r : by_tile[t]) {
+      const XRow& x = xrows[r];
+      rli.push_back(li[r]); rnt.push_back(nterm[r]);
+      for (int q = 0; q < 4; ++q) { rsl.push_back(slot[4 * r + q]); rw.push_back(wv[4 * r + q]); }
+      rc.push_back(make_coef<T>(x.c)); ryo.push_back(x.y); rsrc.push_back(x.src_col); rcs.push_back((T)x.cs);
+      if (x.y >= 0) tif[t] = 1;
+    }
+    tptr.push_back((int32_t)rli.size());
+    nif_tiles += tif[t];
+  }
+  // coarse probes -> tiles
+  std::vector<std::vector<int>> pb_tile(nT);
+  for (size_t q = 0; q < hpr_owner.size(); ++q) {
+    if (hpr_owner[q] != -1) continue;
+    int tt = -1;
+    for (int64_t k = hpr_rp[q]; k < hpr_rp[q + 1]; ++k) {
+      const int i = (int)(hpr_off[k] % px), j = (int)(hpr_off[k] / px);
+      if (i >= nx || j >= ny) return why_not(12);
+      const int t = (j / TY) * ntx + (i / TX);
+      if (tt >= 0 && t != tt) return why_not(9);
+      tt = t;
+    }
+    if (tt >= 0) pb_tile[tt].push_back((int)q);
+  }
+  std::vector<int32_t> pptr(1, 0), ppid, ptp(1, 0), pli;
+  std::vector<int8_t> pcomp;
+  std::vector<T> pw;
+  for (int t = 0; t < nT; ++t) {
+    for (int q : pb_tile[t]) {
+      ppid.push_back(q);
+      for (int64_t k = hpr_rp[q]; k < hpr_rp[q + 1]; ++k) {
+        const int i = (int)(hpr_off[k] % px), j = (int)(hpr_off[k] / px);
+        pli.push_back((j % TY) * TX + (i % TX));
+        pcomp.push_back((int8_t)(hpr_src[k] - 2));
+        pw.push_back((T)hpr_w[k]);
+      }
+      ptp.push_back((int32_t)pli.size());
+    }
+    pptr.push_back((int32_t)ppid.size());
+  }
+  // device copies
+  auto up = [&](auto& vec, auto*& dptr) -> int {
+    using E = typename std::remove_reference<decltype(vec)>::type::value_type;
+    E* d = dalloc<E>(std::max<size_t>(vec.size(), 1));
+    if (!d) return fail(FDTD_ENOMEM, "persistent-path allocation failed");
+    if (!vec.empty() && upload(d, vec)) return FDTD_ECUDA;
+    dptr = d;
+    return FDTD_OK;
+  };
+  const int32_t *d_tptr, *d_li, *d_src, *d_pptr, *d_ppid, *d_ptp, *d_pli;
+  const int8_t *d_nt, *d_sl, *d_pcomp;
+  const T *d_w, *d_cs, *d_pw;
+  const fdtd::Coef<T>* d_c;
+  const int64_t* d_yo;
+  const uint8_t* d_tif;
+  int e = FDTD_OK;
+#define FDTD_UP(v, d) do { auto* tmp_ = (decltype(v.data()))nullptr; e = up(v, tmp_); if (e) return e; d = tmp_; } while (0)
+  FDTD_UP(tptr, d_tptr); FDTD_UP(rli, d_li); FDTD_UP(rsrc, d_src); FDTD_UP(pptr, d_pptr); FDTD_UP(ppid, d_ppid);
+  FDTD_UP(ptp, d_ptp); FDTD_UP(pli, d_pli); FDTD_UP(rnt, d_nt); FDTD_UP(rsl, d_sl); FDTD_UP(pcomp, d_pcomp);
+  FDTD_UP(rw, d_w); FDTD_UP(rcs, d_cs); FDTD_UP(pw, d_pw); FDTD_UP(rc, d_c); FDTD_UP(ryo, d_yo); FDTD_UP(tif, d_tif);
+#undef FDTD_UP
+  p_rows = fdtd::P2Rows<T>{d_tptr, d_li, d_c, d_nt, d_sl, d_w, d_yo, d_src, d_cs, rows.wave, rows.n_wave, rows.n_src};
+  p_probes = fdtd::P2Probes<T>{d_pptr, d_ppid, d_ptp, d_pli, d_pcomp, d_pw};
+  p_tile_if = const_cast<uint8_t*>(d_tif);
+  p_ezL = dalloc<T>((size_t)2 * nT * TY); p_hyR = dalloc<T>((size_t)2 * nT * TY);
+  p_ezB = dalloc<T>((size_t)2 * nT * TX); p_hxT = dalloc<T>((size_t)2 * nT * TX);
+  p_flags = dalloc<unsigned>((size_t)2 * nT + 3);
+  if (!p_ezL || !p_hyR || !p_ezB || !p_hxT || !p_flags) return fail(FDTD_ENOMEM, "persistent-path allocation failed");
+  CK(cudaMemsetAsync(p_flags, 0, sizeof(unsigned) * (2 * nT + 3), stream));
+  pTX = TX; pTY = TY; pntx = ntx; pnty = nty; p_rpc = rpc; p_Rtot = Rtot; p_Cmax = Cmax; p_smem = smem;
+  p_nif_tiles = nif_tiles;
+  p_nred = nR;
+  persist = true;
+  if (getenv("FDTD_VERBOSE")) {
+    fprintf(stderr, "fdtd: persistent 2-D path: %d x %d tiles of %d x %d, %d reduced CTAs x %d rows, smem %zu, "
+            "maxrows %d (P2Row %zu B), interface tiles %d\n", ntx, nty, TX, TY, nR, rpc, smem, p_maxrows,
+            sizeof(fdtd::P2Row<T>), nif_tiles);
+    for (int t = 0; t < nT; ++t)
+      if (tptr[t + 1] > tptr[t]) fprintf(stderr, "  tile %d: rows %d..%d\n", t, tptr[t], tptr[t + 1]);
+  }
+  return FDTD_OK;
+}
+
+template <typename T>
+int Impl<T>::launch_persist(int64_t n, int64_t* count) {
+  const int nT = pntx * pnty;
+  const int p0 = (int)(host_step & 1), p1 = (int)((host_step + n) & 1);
+  fdtd::Persist2D<T> P{};
+  P.nx = nx; P.ny = ny; P.px = px; P.TX = pTX; P.TY = pTY; P.ntx = pntx; P.nty = pnty;
+  P.Fin[0] = F[p0][2]; P.Fin[1] = F[p0][3]; P.Fin[2] = F[p0][4];
+  P.Fout[0] = F[p1][2]; P.Fout[1] = F[p1][3]; P.Fout[2] = F[p1][4];
+  P.mat_id = uniform ? nullptr : mat_id;
+  P.gtab = tab; P.gifm = ifm; P.n_mat = n_mat; P.u0 = u0; P.u1 = u1;
+  P.R = p_rows; P.PR = p_probes;
+  P.ezL = p_ezL; P.ezB = p_ezB; P.hyR = p_hyR; P.hxT = p_hxT;
+  P.fE = p_flags; P.fH = p_flags + nT; P.gready = p_flags + 2 * nT; P.reddone = p_flags + 2 * nT + 1;
+  P.abort_flag = reinterpret_cast<int*>(p_flags + 2 * nT + 2);
+  P.tile_if = p_tile_if; P.n_if_tiles = p_nif_tiles; P.n_red_ctas = p_nred;
+  for (size_t b = 0; b < fblocks.size(); ++b) P.fb[b] = fblocks[b];
+  for (size_t b = 0; b <= fblocks.size(); ++b) P.row0[b] = p_row0[b];
+  P.nfb = (int)fblocks.size(); P.Rtot = p_Rtot; P.rpc = p_rpc; P.Cmax = p_Cmax;
+  P.eb[0] = eb[0]; P.eb[1] = eb[1]; P.hb[0] = hb[0]; P.hb[1] = hb[1]; P.y = y_all; P.G = g_all;
+  P.ring = ring; P.cap = cap; P.n_probe = n_probe;
+  P.step0 = host_step + step_offset; P.p0 = p0; P.nsteps = (int)n;
+  P.d_step_out = d_step + p1;
+  P.check_every = check_every; P.bad_step = d_bad; P.maxrows = p_maxrows;
+  CK(cudaMemsetAsync(p_flags, 0, sizeof(unsigned) * (2 * nT + 3), stream));
+  static unsigned long long* dbg = nullptr;
+  if (getenv("FDTD_P2DBG")) {
+    if (!dbg) CK(cudaMalloc(&dbg, 3 * 8 * 8 * sizeof(unsigned long long)));
+    CK(cudaMemset(dbg, 0, 3 * 8 * 8 * sizeof(unsigned long long)));
+    P.dbg = dbg;
+    int ti = 0;
+    std::vector<uint8_t> tif(nT);
+    CK(cudaMemcpy(tif.data(), p_tile_if, nT, cudaMemcpyDeviceToHost));
+    for (int q = 0; q < nT; ++q) if (tif[q]) { ti = q; break; }
+    P.dbg_tile_if = ti;
+  }
+  void* args[] = {&P};
+  CK(cudaLaunchCooperativeKernel((const void*)fdtd::persist2d_kernel<T>, dim3(nT + p_nred), dim3(512), args, p_smem,
+                                 stream));
+  *count += 1;
+  if (P.dbg && n >= 108) {
+    std::vector<unsigned long long> h(3 * 8 * 8);
+    CK(cudaStreamSynchronize(stream));
+    CK(cudaMemcpy(h.data(), P.dbg, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    const unsigned long long t0 = h[0];
+    for (int sl = 0; sl < 3; ++sl) {
+      fprintf(stderr, "slot %d (%s):\n", sl, sl == 0 ? "tile 0" : sl == 1 ? "interface tile" : "reduced CTA 0");
+      for (int st = 0; st < 8; ++st) {
+        fprintf(stderr, "  step %d:", 100 + st);
+        for (int k = 0; k < 5; ++k) {
+          const unsigned long long v = h[(sl * 8 + st) * 8 + k];
+          fprintf(stderr, " %8.3f", v ? (double)(v - t0) * 1e-3 : -1.0);
+        }
+        fprintf(stderr, "\n");
+      }
+    }
+  }
   return FDTD_OK;
 }
 
@@ -1105,6 +1392,12 @@ int Impl<T>::step(int64_t n) {
     const int64_t room = n_probe > 0 ? cap - (host_step - drained_to) : n;
     const int64_t chunk = std::min(n, room);
     int64_t done = 0;
+    if (persist && !prof && graph_steps > 0 && chunk > 0) {
+      int e = launch_persist(chunk, &launches);
+      if (e) return e;
+      host_step += chunk;
+      done = chunk;
+    }
     while (done < chunk) {
       const int64_t left = chunk - done;
       if (!prof && graph_steps > 0 && (host_step & 1) == 0 && left >= graph_steps) {
@@ -1143,6 +1436,11 @@ int Impl<T>::step(int64_t n) {
 template <typename T>
 int Impl<T>::check_async() {
   unsigned long long bad = 0;
+  if (persist) {
+    int ab = 0;
+    CK(cudaMemcpy(&ab, p_flags + 2 * pntx * pnty + 2, sizeof(ab), cudaMemcpyDeviceToHost));
+    if (ab) return fail(FDTD_ECUDA, "persistent 2-D kernel: inter-CTA wait timed out (watchdog)");
+  }
   CK(cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost));
   if (bad != std::numeric_limits<unsigned long long>::max())
     return fail(FDTD_EDIVERGED, "divergence (non-finite or |x| > 1e100) detected at step %llu", bad);

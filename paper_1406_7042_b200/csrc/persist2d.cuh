@@ -1,0 +1,500 @@
+// persist2d.cuh — persistent, on-chip-resident 2-D hybrid step (sm_100a).
+//
+// The whole time march of a 2-D problem (Ez, Hx, Hy coarse grid + fused
+// single-column reduced blocks) in ONE cooperative launch.  Each CTA owns a
+// TX x TY tile of the coarse grid and keeps its three fields in shared memory
+// for the whole launch (config 2: 1025^2 x 3 fp32 = 12.6 MB spread over 289
+// CTAs, 48 KB each) -- no per-step HBM/L2 round trip of the state (DESIGN.md
+// §5.4).  Per step (paper eq. (4)/(12) order, rows a1-a7 of DESIGN.md §1):
+//
+//   E phase  Ez^{n+1} on the tile; the left column of Hy / bottom row of Hx it
+//            needs come from the neighbours' published H halos of step n-1;
+//            explicit rows (interface rows with the reduced coupling y = S_E
+//            h~, source rows) are evaluated in place and interface rows
+//            publish E_if^{n+1} into G.
+//   H phase  Hx, Hy on the tile; the right column / top row of Ez come from
+//            the neighbours' published E halos of step n.
+//   reduced  every CTA keeps a few rows of the fused update matrix M
+//            resident in shared memory and computes them once all interface
+//            tiles published G: [h~' ; y' ; e~'' ; probe rows] = M [e~ ; G ; h~].
+//
+// Synchronisation is point to point through monotonic per-tile flags (fE, fH:
+// phases completed) and two counters (gready: interface tiles that published
+// G, reddone: CTAs that finished their reduced rows); halos are double
+// buffered by step parity, which makes every write-after-read safe (the
+// argument is in DESIGN.md §5.4).  Cross-CTA data is read with ld.global.cg
+// (L2, never a stale L1 line).  Every wait is bounded: after ~1 s of spinning
+// the CTA raises `abort` and all CTAs leave; the host reports the error.
+//
+// The arithmetic of every update is the same expression, in the same order,
+// as stencil2d_rows_kernel / eval_row / reduced_fused_kernel: the persistent
+// and the per-step paths agree bit for bit (tests/test_gpu_parity.py).
+#pragma once
+
+namespace fdtd {
+
+template <typename T>
+struct P2Rows {                 // explicit rows grouped by tile (CSR over tiles)
+  const int32_t* tile_ptr;      // [nT+1]
+  const int32_t* li;            // local cell index jl * TX + il
+  const Coef<T>* c;
+  const int8_t* nterm;          // H terms (<= 4), in the problem's CSR order
+  const int8_t* slot;           // [4]: 0 Hy(i,j) 1 Hy(i-1,j) 2 Hx(i,j) 3 Hx(i,j-1)
+  const T* w;                   // [4]
+  const int64_t* yo;            // y / G index, -1 none
+  const int32_t* src;           // waveform column, -1 none
+  const T* cs;
+  const T* wave;                // [n_wave][n_cols]
+  int64_t n_wave, n_cols;
+};
+
+template <typename T>
+struct P2Row {                  // one explicit row, cached in shared memory
+  Coef<T> c;
+  T w[4];
+  T cs;
+  int64_t yo;
+  int32_t li, src;
+  int8_t nterm, slot[4];
+};
+
+template <typename T>
+struct P2Probes {               // coarse probes whose terms all lie in one tile
+  const int32_t* tile_ptr;      // [nT+1] over probes
+  const int32_t* pid;
+  const int32_t* term_ptr;      // [np+1]
+  const int32_t* term_li;
+  const int8_t* term_comp;      // 0 Ez, 1 Hx, 2 Hy
+  const T* term_w;
+};
+
+template <typename T>
+struct Persist2D {
+  int nx, ny, px, TX, TY, ntx, nty;
+  const T* Fin[3];              // Ez, Hx, Hy at the start (storage layout, pitch px)
+  T* Fout[3];
+  const uint8_t* mat_id;        // padded storage-indexed material ids (or null: uniform)
+  const Coef<T>* gtab;          // [n_mat][6]
+  const uint8_t* gifm;
+  int n_mat;
+  Coef<T> u0, u1;
+  P2Rows<T> R;
+  P2Probes<T> PR;
+  T* ezL; T* ezB; T* hyR; T* hxT;         // halos [2][nT][TY] / [2][nT][TX]
+  unsigned* fE; unsigned* fH;             // [nT] phases completed
+  unsigned* gready; unsigned* reddone; int* abort_flag;
+  const uint8_t* tile_if;                 // tile has interface rows
+  int n_if_tiles, n_red_ctas;
+  // reduced (fused, N = 1)
+  FusedBlock<T> fb[kMaxFusedBlocks];
+  int row0[kMaxFusedBlocks + 1];          // first global row of each block
+  int nfb, Rtot, rpc, Cmax;           // rpc: rows per reduced CTA (CTAs nT .. nT+n_red_ctas-1)
+  T* eb[2]; T* hb[2]; T* y; T* G;
+  T* ring; int64_t cap; int n_probe;
+  int64_t step0; int p0; int nsteps;
+  int64_t* d_step_out;
+  int check_every;
+  int maxrows;                  // explicit rows of the fullest tile
+  unsigned long long* bad_step;
+  unsigned long long* dbg;      // optional phase timestamps (FDTD_P2DBG), [cta slot][step][8]
+  int dbg_tile_if;              // which tile to trace besides tile 0
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define P2_STAMP(slot, k)                                                                    \
+  do {                                                                                       \
+    if (P.dbg && threadIdx.x == 0 && ls >= 100 && ls < 108)                                  \
+      P.dbg[((slot) * 8 + (ls - 100)) * 8 + (k)] = gtimer();                                 \
+  } while (0)
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// thread 0 spins until *flag >= target; false on abort / timeout (~1 s of
+// SM clock).  No back-off: the flags are the step's critical path.
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ bool p2_wait(const unsigned* flag, unsigned target, int* abort_flag) {
+  // relaxed polling (no L1 invalidation per poll), one acquire fence on success
+  if (ld_relaxed_u32(flag) < target) {
+    const long long t0 = clock64();
+    unsigned it = 0;
+    while (ld_relaxed_u32(flag) < target) {
+      if ((++it & 63u) == 0) {
+        if (*reinterpret_cast<volatile int*>(abort_flag)) return false;
+        if (clock64() - t0 > 2000000000LL) { atomicExch(abort_flag, 1); return false; }
+      }
+    }
+  }
+  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+  return true;
+}
+
+template <typename T>
+__device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, int& s_abort) {
+  const int TX = P.TX, TY = P.TY, TT = TX * TY;
+  const int nT = P.ntx * P.nty;
+  const int t = blockIdx.x;
+  const int tx_ = t % P.ntx, ty_ = t / P.ntx;
+  const int i0 = tx_ * TX, j0 = ty_ * TY;
+  const int left = tx_ > 0 ? t - 1 : -1, right = tx_ + 1 < P.ntx ? t + 1 : -1;
+  const int bottom = ty_ > 0 ? t - P.ntx : -1, top = ty_ + 1 < P.nty ? t + P.ntx : -1;
+  const int nx = P.nx, ny = P.ny, px = P.px;
+  const bool uniform = (P.mat_id == nullptr);
+  T* sEz = reinterpret_cast<T*>(smem_raw);
+  T* sHx = sEz + TT;
+  T* sHy = sHx + TT;
+  T* hL = sHy + TT;                  // Hy(i0-1, j)
+  T* hB = hL + TY;                   // Hx(i, j0-1)
+  T* eR = hB + TX;                   // Ez(i0+TX, j)
+  T* eT = eR + TY;                   // Ez(i, j0+TY)
+  Coef<T>* cE = reinterpret_cast<Coef<T>*>(eT + TX);
+  Coef<T>* cHx = cE + MAX_MAT;
+  Coef<T>* cHy = cHx + MAX_MAT;
+  uint8_t* ifm = reinterpret_cast<uint8_t*>(cHy + MAX_MAT);
+  uint8_t* smat = ifm + MAX_MAT;     // [TT]
+  T* yv = reinterpret_cast<T*>(smat + ((TT + 15) / 16) * 16);   // [max rows per tile] prefetched y (+ source)
+  P2Row<T>* rs = reinterpret_cast<P2Row<T>*>(yv + ((2 * P.maxrows * (int)sizeof(T) + 15) / 16) * 16 / (int)sizeof(T));
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lx = tid & 31, ly = tid >> 5, NLY = nthr >> 5;
+  // the tile covers cells i < nx, j < ny: the last storage column / row (PEC
+  // wall Ez = 0, H never updated) is constant and written back by CTA 0
+  for (int jl = ly; jl < TY; jl += NLY)
+    for (int il = lx; il < TX; il += 32) {
+      const int i = i0 + il, j = j0 + jl;
+      const int c = jl * TX + il;
+      T ez = 0, hx = 0, hy = 0;
+      uint8_t m = 0;
+      if (i < nx && j < ny) {
+        const int64_t o = (int64_t)j * px + i;
+        ez = P.Fin[0][o]; hx = P.Fin[1][o]; hy = P.Fin[2][o];
+        if (!uniform) m = P.mat_id[o];
+      }
+      sEz[c] = ez; sHx[c] = hx; sHy[c] = hy; smat[c] = m;
+    }
+  if (!uniform) {
+    for (int q = tid; q < P.n_mat; q += nthr) {
+      cE[q] = P.gtab[q * 6 + 2]; cHx[q] = P.gtab[q * 6 + 3]; cHy[q] = P.gtab[q * 6 + 4];
+      ifm[q] = P.gifm[q];
+    }
+  }
+  const int rows_lo = P.R.tile_ptr[t], rows_hi = P.R.tile_ptr[t + 1];
+  for (int r = rows_lo + tid; r < rows_hi; r += nthr) {
+    P2Row<T> x;
+    x.c = P.R.c[r]; x.cs = P.R.cs[r]; x.yo = P.R.yo[r]; x.li = P.R.li[r]; x.src = P.R.src[r];
+    x.nterm = P.R.nterm[r];
+    for (int k = 0; k < 4; ++k) { x.w[k] = P.R.w[4 * r + k]; x.slot[k] = P.R.slot[4 * r + k]; }
+    rs[r - rows_lo] = x;
+  }
+  __syncthreads();
+  const bool has_if = P.tile_if[t] != 0;
+  const int pr_lo = P.PR.tile_ptr[t], pr_hi = P.PR.tile_ptr[t + 1];
+  bool bad = false;
+  long long first_bad = -1;
+  const int dslot = (t == 0) ? 0 : (t == P.dbg_tile_if ? 1 : -1);
+  for (int ls = 0; ls < P.nsteps; ++ls) {
+    const int64_t step = P.step0 + ls;
+    const bool do_check = P.check_every > 0 && (step % P.check_every) == 0;
+    if (dslot >= 0) P2_STAMP(dslot, 0);
+    // ------------------------------------------------------------- E phase
+    // (a) interior cells need no halo: computed before waiting for neighbours
+    auto e_cell = [&](int il, int jl) {
+      const int i = i0 + il, j = j0 + jl;
+      const int c = jl * TX + il;
+      const int m = smat[c];
+      if (!uniform && (ifm[m] & 4)) return;                // explicit row below
+      const T hy = sHy[c], hx = sHx[c];
+      const T hyim = (il > 0) ? sHy[c - 1] : hL[jl];
+      const T hxm = (jl > 0) ? sHx[c - TX] : hB[il];
+      const Coef<T> cc = uniform ? P.u0 : cE[m];
+      const T dd = (hy - hyim) - (hx - hxm);
+      sEz[c] = (i > 0 && j > 0) ? sEz[c] + cc.apply(dd) : (T)0;
+    };
+    for (int jl = 1 + ly; jl < TY; jl += NLY) {
+      if (j0 + jl >= ny) break;
+      for (int il = 1 + lx; il < TX; il += 32) {
+        if (i0 + il >= nx) break;
+        e_cell(il, jl);
+      }
+    }
+    // (b) wait for the left / bottom H halos (and, on interface tiles, for the
+    //     reduced update of the previous step), then fetch halos and y together
+    if (ls > 0) {
+      if (tid == 0) {
+        bool ok = true;
+        if (left >= 0) ok = p2_wait(P.fH + left, (unsigned)ls, P.abort_flag);
+        if (ok && bottom >= 0) ok = p2_wait(P.fH + bottom, (unsigned)ls, P.abort_flag);
+        if (ok && has_if) ok = p2_wait(P.reddone, (unsigned)(P.n_red_ctas * ls), P.abort_flag);
+        if (!ok) s_abort = 1;
+      }
+      __syncthreads();
+      if (s_abort) break;
+    }
+    if (dslot >= 0) P2_STAMP(dslot, 1);
+    {
+      const int hb_ = (ls - 1) & 1;
+      for (int jl = tid; jl < TY; jl += nthr) {
+        T v = 0;
+        if (left >= 0) v = (ls == 0) ? ((j0 + jl < ny) ? P.Fin[2][(int64_t)(j0 + jl) * px + i0 - 1] : (T)0)
+                                     : __ldcg(P.hyR + ((int64_t)hb_ * nT + left) * TY + jl);
+        hL[jl] = v;
+      }
+      for (int il = tid; il < TX; il += nthr) {
+        T v = 0;
+        if (bottom >= 0) v = (ls == 0) ? ((i0 + il < nx) ? P.Fin[1][(int64_t)(j0 - 1) * px + i0 + il] : (T)0)
+                                       : __ldcg(P.hxT + ((int64_t)hb_ * nT + bottom) * TX + il);
+        hB[il] = v;
+      }
+      for (int r = tid; r < rows_hi - rows_lo; r += nthr) {
+        const int64_t yo = rs[r].yo;
+        const int sc = rs[r].src;
+        yv[r] = (yo >= 0) ? __ldcg(P.y + yo) : (T)0;
+        if (sc >= 0) yv[P.maxrows + r] = (step < P.R.n_wave) ? P.R.wave[step * P.R.n_cols + sc] : (T)0;
+      }
+    }
+    __syncthreads();
+    // (c) first column and first row
+    for (int q = tid; q < TX + TY - 1; q += nthr) {
+      const int il = q < TX ? q : 0, jl = q < TX ? 0 : q - TX + 1;
+      if (i0 + il >= nx || j0 + jl >= ny) continue;
+      e_cell(il, jl);
+    }
+    // (d) explicit rows (eval_row: acc in the problem's order, then y, then source)
+    for (int r = tid; r < rows_hi - rows_lo; r += nthr) {
+      const P2Row<T>& x = rs[r];
+      const int c = x.li;
+      const int il = c % TX, jl = c / TX;
+      T acc = 0;
+      for (int k = 0; k < x.nterm; ++k) {
+        const int sl = x.slot[k];
+        T hv;
+        if (sl == 0) hv = sHy[c];
+        else if (sl == 1) hv = (il > 0) ? sHy[c - 1] : hL[jl];
+        else if (sl == 2) hv = sHx[c];
+        else hv = (jl > 0) ? sHx[c - TX] : hB[il];
+        acc += x.w[k] * hv;
+      }
+      if (x.yo >= 0) acc += yv[r];
+      T e = sEz[c] - x.c.apply(acc);
+      if (x.src >= 0 && step < P.R.n_wave) e -= x.cs * yv[P.maxrows + r];
+      sEz[c] = e;
+      if (x.yo >= 0) __stcg(P.G + x.yo, e);
+    }
+    __syncthreads();
+    {
+      const int eb_ = ls & 1;
+      for (int jl = tid; jl < TY; jl += nthr) __stcg(P.ezL + ((int64_t)eb_ * nT + t) * TY + jl, sEz[jl * TX]);
+      for (int il = tid; il < TX; il += nthr) __stcg(P.ezB + ((int64_t)eb_ * nT + t) * TX + il, sEz[il]);
+    }
+    __syncthreads();
+    if (dslot >= 0) P2_STAMP(dslot, 2);
+    if (tid == 0) {
+      __threadfence();
+      st_release_u32(P.fE + t, (unsigned)(ls + 1));
+      if (has_if) atomicAdd(P.gready, 1u);
+    }
+    // ------------------------------------------------------------- H phase
+    auto h_cell = [&](int il, int jl) {
+      const int i = i0 + il;
+      const int c = jl * TX + il;
+      const T ez = sEz[c];
+      const T ez_jp = (jl + 1 < TY) ? sEz[c + TX] : eT[il];
+      const T ez_ip = (il + 1 < TX) ? sEz[c + 1] : eR[jl];
+      Coef<T> cx, cy;
+      if (uniform) { cx = P.u1; cy = P.u1; }
+      else { const int m = smat[c]; cx = cHx[m]; cy = cHy[m]; }
+      const T hx = sHx[c], hy = sHy[c];
+      const T hx1 = (i > 0) ? hx - cx.apply(ez_jp - ez) : hx;
+      const T hy1 = (j0 + jl > 0) ? hy + cy.apply(ez_ip - ez) : hy;
+      sHx[c] = hx1; sHy[c] = hy1;
+      if (do_check && !(finite_small(ez) && finite_small(hx1) && finite_small(hy1))) bad = true;
+    };
+    // (a) interior: no E halo needed
+    for (int jl = ly; jl < TY - 1; jl += NLY) {
+      if (j0 + jl >= ny) break;
+      for (int il = lx; il < TX - 1; il += 32) {
+        if (i0 + il >= nx) break;
+        h_cell(il, jl);
+      }
+    }
+    // (b) right / top E halos
+    if (tid == 0) {
+      bool ok = true;
+      if (right >= 0) ok = p2_wait(P.fE + right, (unsigned)(ls + 1), P.abort_flag);
+      if (ok && top >= 0) ok = p2_wait(P.fE + top, (unsigned)(ls + 1), P.abort_flag);
+      if (!ok) s_abort = 1;
+    }
+    __syncthreads();
+    if (s_abort) break;
+    if (dslot >= 0) P2_STAMP(dslot, 3);
+    {
+      const int eb_ = ls & 1;
+      for (int jl = tid; jl < TY; jl += nthr)
+        eR[jl] = (right >= 0) ? __ldcg(P.ezL + ((int64_t)eb_ * nT + right) * TY + jl) : (T)0;
+      for (int il = tid; il < TX; il += nthr)
+        eT[il] = (top >= 0) ? __ldcg(P.ezB + ((int64_t)eb_ * nT + top) * TX + il) : (T)0;
+    }
+    __syncthreads();
+    // (c) last column and last row
+    for (int q = tid; q < TX + TY - 1; q += nthr) {
+      const int il = q < TX ? q : TX - 1, jl = q < TX ? TY - 1 : q - TX;
+      if (i0 + il >= nx || j0 + jl >= ny) continue;
+      h_cell(il, jl);
+    }
+    if (bad && first_bad < 0) first_bad = step;
+    __syncthreads();
+    {
+      const int hb_ = ls & 1;
+      for (int jl = tid; jl < TY; jl += nthr) __stcg(P.hyR + ((int64_t)hb_ * nT + t) * TY + jl, sHy[jl * TX + TX - 1]);
+      for (int il = tid; il < TX; il += nthr) __stcg(P.hxT + ((int64_t)hb_ * nT + t) * TX + il, sHx[(TY - 1) * TX + il]);
+    }
+    // coarse probes owned by this tile (fields after the step)
+    for (int q = pr_lo + tid; q < pr_hi; q += nthr) {
+      T acc = 0;
+      for (int k = P.PR.term_ptr[q]; k < P.PR.term_ptr[q + 1]; ++k) {
+        const int c = P.PR.term_li[k], cp = P.PR.term_comp[k];
+        const T v = cp == 0 ? sEz[c] : (cp == 1 ? sHx[c] : sHy[c]);
+        acc += P.PR.term_w[k] * v;
+      }
+      P.ring[(step % P.cap) * (int64_t)P.n_probe + P.PR.pid[q]] = acc;
+    }
+    __syncthreads();
+    if (dslot >= 0) P2_STAMP(dslot, 4);
+    if (tid == 0) { __threadfence(); st_release_u32(P.fH + t, (unsigned)(ls + 1)); }
+  }
+  __syncthreads();
+  if (!s_abort) {
+    for (int jl = ly; jl < TY; jl += NLY)
+      for (int il = lx; il < TX; il += 32) {
+        const int i = i0 + il, j = j0 + jl;
+        if (i >= nx || j >= ny) continue;
+        const int64_t o = (int64_t)j * px + i;
+        const int c = jl * TX + il;
+        P.Fout[0][o] = sEz[c]; P.Fout[1][o] = sHx[c]; P.Fout[2][o] = sHy[c];
+      }
+    if (t == 0) {
+      // constant last column i = nx and row j = ny: Ez = 0 (wall) once stepped, H unchanged
+      for (int q = tid; q < (ny + 1) + nx; q += nthr) {
+        const int i = q <= ny ? nx : q - (ny + 1), j = q <= ny ? q : ny;
+        const int64_t o = (int64_t)j * px + i;
+        P.Fout[0][o] = P.nsteps > 0 ? (T)0 : P.Fin[0][o];
+        P.Fout[1][o] = P.Fin[1][o]; P.Fout[2][o] = P.Fin[2][o];
+      }
+      if (tid == 0) *P.d_step_out = P.step0 + P.nsteps;
+    }
+  }
+  if (first_bad >= 0) atomicMin(P.bad_step, (unsigned long long)first_bad);
+}
+
+// dedicated reduced CTAs: rows [r_lo, r_hi) of the fused update matrices,
+// resident in shared memory for the whole launch
+template <typename T>
+__device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw, int& s_abort) {
+  using V = typename Vec<T>::type;
+  constexpr int VN = Vec<T>::n;
+  const int rc = blockIdx.x - P.ntx * P.nty;
+  T* Xs = reinterpret_cast<T*>(smem_raw);       // [Cmax]
+  T* Ms = Xs + P.Cmax;                          // [rpc][Cmax]
+  const int tid = threadIdx.x, nthr = blockDim.x, lx = tid & 31;
+  const int r_lo = min(rc * P.rpc, P.Rtot), r_hi = min(r_lo + P.rpc, P.Rtot);
+  for (int g = r_lo; g < r_hi; ++g) {
+    int b = 0;
+    while (b + 1 < P.nfb && g >= P.row0[b + 1]) ++b;
+    const FusedBlock<T>& FB = P.fb[b];
+    const T* src = FB.M + (int64_t)(g - P.row0[b]) * FB.Cp;
+    for (int c = tid; c < P.Cmax; c += nthr) Ms[(g - r_lo) * P.Cmax + c] = (c < FB.Cp) ? src[c] : (T)0;
+  }
+  __syncthreads();
+  long long first_bad = -1;
+  for (int ls = 0; ls < P.nsteps; ++ls) {
+    const int64_t step = P.step0 + ls;
+    const int p = (P.p0 + ls) & 1;
+    const bool do_check = P.check_every > 0 && (step % P.check_every) == 0;
+    if (rc == 0) P2_STAMP(2, 0);
+    // inputs e~, h~ of this step: every reduced CTA finished the previous one
+    if (tid == 0 && ls > 0 && !p2_wait(P.reddone, (unsigned)(P.n_red_ctas * ls), P.abort_flag)) s_abort = 1;
+    __syncthreads();
+    if (s_abort) break;
+    int g = r_lo;
+    bool waited = false;
+    while (g < r_hi) {
+      int b = 0;
+      while (b + 1 < P.nfb && g >= P.row0[b + 1]) ++b;
+      const FusedBlock<T>& FB = P.fb[b];
+      const int g_end = min(r_hi, P.row0[b + 1]);
+      const int qe = FB.qe, ni = FB.n_if, qh = FB.qh, C = FB.C;
+      const T* e_in = P.eb[p];
+      const T* h_in = P.hb[p];
+      for (int c = tid; c < FB.Cp; c += nthr) {
+        if (c >= qe && c < qe + ni) continue;
+        T v = 0;
+        if (c < qe) v = __ldcg(e_in + FB.e_off + c);
+        else if (c < C) v = __ldcg(h_in + FB.h_off + (c - qe - ni));
+        Xs[c] = v;
+      }
+      if (!waited) {
+        if (rc == 0) P2_STAMP(2, 1);
+        if (tid == 0 && !p2_wait(P.gready, (unsigned)(P.n_if_tiles * (ls + 1)), P.abort_flag)) s_abort = 1;
+        __syncthreads();
+        if (s_abort) break;
+        waited = true;
+        if (rc == 0) P2_STAMP(2, 2);
+      }
+      for (int c = qe + tid; c < qe + ni; c += nthr) Xs[c] = __ldcg(P.G + FB.y_off + (c - qe));
+      __syncthreads();
+      const int warp = tid >> 5, nw = nthr >> 5;
+      for (int gg = g + warp; gg < g_end; gg += nw) {
+        const int r = gg - P.row0[b];
+        const V* a = reinterpret_cast<const V*>(Ms + (gg - r_lo) * P.Cmax);
+        T acc = 0;
+        const int nv = FB.Cp / VN;
+#pragma unroll 8
+        for (int cc = lx; cc < nv; cc += 32) acc += vdot<T>(a[cc], reinterpret_cast<const V*>(Xs)[cc]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lx == 0) {
+          if (r < qh) __stcg(P.hb[p ^ 1] + FB.h_off + r, acc);
+          else if (r < qh + ni) __stcg(P.y + FB.y_off + (r - qh), acc);
+          else if (r < qh + ni + qe) __stcg(P.eb[p ^ 1] + FB.e_off + (r - qh - ni), acc);
+          else {
+            const int q = r - qh - ni - qe;
+            P.ring[(step % P.cap) * (int64_t)P.n_probe + FB.probe_id[q]] = acc;
+          }
+          if (do_check && !finite_small((double)acc) && first_bad < 0) first_bad = step;
+        }
+      }
+      __syncthreads();
+      g = g_end;
+    }
+    if (s_abort) break;
+    if (rc == 0) P2_STAMP(2, 3);
+    if (tid == 0) { __threadfence(); atomicAdd(P.reddone, 1u); }
+  }
+  if (first_bad >= 0) atomicMin(P.bad_step, (unsigned long long)first_bad);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512, 2)
+persist2d_kernel(const __grid_constant__ Persist2D<T> P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_abort;
+  if (threadIdx.x == 0) s_abort = 0;
+  __syncthreads();
+  if ((int)blockIdx.x < P.ntx * P.nty) persist2d_tile<T>(P, smem_raw, s_abort);
+  else persist2d_reduced<T>(P, smem_raw, s_abort);
+}
+
+}  // namespace fdtd

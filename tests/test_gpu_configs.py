@@ -228,3 +228,23 @@ def test_config4_full_size_sampled_one_step():
         grh = reduced_member(gh, sh, 16, m, "h")
         assert np.abs(gre - e1).max() <= 2e-5 * np.abs(e1).max()
         assert np.abs(grh - h1).max() <= 2e-5 * np.abs(h1).max()
+
+
+@pytest.mark.parametrize("which,prec", [("tiny2d_B", 32), ("tiny2d_B", 64), (1, 64), (2, 32)])
+def test_persistent_2d_bitwise_equals_per_step_kernels(which, prec, monkeypatch):
+    # the persistent on-chip-resident 2-D kernel (one cooperative launch per
+    # step() call) against the per-step stencil + fused-reduced kernels: same
+    # arithmetic, so states, reduced states and probe series agree bit for bit,
+    # across several launches (ragged chunks)
+    scn, prob = _prep(which, precision=prec)
+    n = 150
+    chunks = [37, 1, 64, 48]
+    monkeypatch.setenv("FDTD_PERSIST", "0")
+    a = run_gpu(prob, n, precision=prec, chunks=chunks)
+    monkeypatch.delenv("FDTD_PERSIST")
+    b = run_gpu(prob, n, precision=prec, chunks=chunks)
+    assert b["launches"] == len(chunks), "persistent path not taken"
+    for c in a["state"]:
+        assert np.array_equal(a["state"][c], b["state"][c]), c
+    assert np.array_equal(a["red_e"], b["red_e"]) and np.array_equal(a["red_h"], b["red_h"])
+    assert np.array_equal(a["probes"], b["probes"])
