@@ -186,6 +186,16 @@ int fdtd_sync(fdtd_t* h);
  * its kernel nodes). */
 int64_t fdtd_launch_count(const fdtd_t* h);
 
+/* Which kernel paths fdtd_step takes (bit mask, fixed at fdtd_create):
+ *   1  persistent on-chip-resident 2-D kernel (one cooperative launch per
+ *      fdtd_step call; 2-D, batch 1, fused single-column reduced blocks)
+ *   2  TMA 3-D stencil (else the cp.async one, in 3-D)
+ *   4  cluster-split GEMM kernel for fused reduced blocks (else warp-per-row)
+ *   8  leap-frog GEMV path for at least one large reduced block
+ * Environment overrides (testing): FDTD_PERSIST=0, FDTD_NO_TMA,
+ * FDTD_FUSED=gemv|gemm, FDTD_KCHUNK=<planes>. */
+int32_t fdtd_path(const fdtd_t* h);
+
 /* Per-phase tracing.  fdtd_profile(h, 1) resets the accumulators and makes the
  * following fdtd_step calls launch eagerly with CUDA events around each
  * kernel group (synchronising once per step); fdtd_profile(h, 0) returns to

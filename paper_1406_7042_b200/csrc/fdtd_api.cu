@@ -79,6 +79,7 @@ struct fdtd_t {
   virtual int set_profile(int on) = 0;
   virtual int phase_times(double* ms, int n) = 0;
   int64_t launches = 0;
+  int32_t path_bits = 0;
 };
 
 namespace {
@@ -815,6 +816,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     int e = setup_persist();
     if (e) return e;
   }
+  path_bits = (persist ? 1 : 0) | (use_tma ? 2 : 0) | (fused_gemm ? 4 : 0) | (any_leap ? 8 : 0);
   CK(cudaStreamSynchronize(stream));
   return FDTD_OK;
 }
@@ -1607,6 +1609,7 @@ int fdtd_set_state(fdtd_t* h, int32_t which, const double* in, int64_t n) {
 }
 int fdtd_sync(fdtd_t* h) { return h ? h->sync() : fail(FDTD_EINVAL, "null handle"); }
 int64_t fdtd_launch_count(const fdtd_t* h) { return h ? h->launches : 0; }
+int32_t fdtd_path(const fdtd_t* h) { return h ? h->path_bits : 0; }
 int fdtd_profile(fdtd_t* h, int32_t enable) { return h ? h->set_profile(enable) : fail(FDTD_EINVAL, "null handle"); }
 int fdtd_phase_times(fdtd_t* h, double* ms, int32_t n) {
   return h ? h->phase_times(ms, n) : fail(FDTD_EINVAL, "null handle");

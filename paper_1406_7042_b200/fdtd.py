@@ -103,6 +103,8 @@ def load_library(path: str = LIB_PATH):
     lib.fdtd_sync.restype = C.c_int
     lib.fdtd_launch_count.argtypes = [C.c_void_p]
     lib.fdtd_launch_count.restype = C.c_int64
+    lib.fdtd_path.argtypes = [C.c_void_p]
+    lib.fdtd_path.restype = C.c_int32
     lib.fdtd_profile.argtypes = [C.c_void_p, C.c_int32]
     lib.fdtd_profile.restype = C.c_int
     lib.fdtd_phase_times.argtypes = [C.c_void_p, _f64p, C.c_int32]
@@ -118,7 +120,7 @@ def load_library(path: str = LIB_PATH):
 
 
 EXPORTED_SYMBOLS = ("fdtd_create", "fdtd_step", "fdtd_probe", "fdtd_get_state", "fdtd_set_state",
-                    "fdtd_sync", "fdtd_launch_count", "fdtd_profile", "fdtd_phase_times", "fdtd_destroy",
+                    "fdtd_sync", "fdtd_launch_count", "fdtd_path", "fdtd_profile", "fdtd_phase_times", "fdtd_destroy",
                     "fdtd_last_error", "fdtd_version")
 PHASES = ("stencil", "reduced", "reduced_grid")
 
@@ -326,6 +328,13 @@ class Sim:
 
     def launch_count(self):
         return int(self.lib.fdtd_launch_count(self.h))
+
+    PATH_BITS = {1: "persistent2d", 2: "tma3d", 4: "fused_gemm", 8: "leapfrog"}
+
+    def path(self):
+        """Kernel paths taken by step() (fdtd_path bit mask) as a list of names."""
+        m = int(self.lib.fdtd_path(self.h))
+        return [nm for bit, nm in self.PATH_BITS.items() if m & bit]
 
     def close(self):
         if getattr(self, "h", None):
