@@ -200,6 +200,8 @@ struct Impl : public fdtd_t {
   bool use_tma = false;
   fdtd::TmaSet tma[2];
   int tBX = 32, tBY = 8, tHBX = 36, tSX = 4, tOUTX = 28;
+  int tW = 1;                   // members per thread in the TMA stencil (16 bytes when the batch allows)
+  static constexpr int kW = 16 / (int)sizeof(T);
   int64_t guard = 0;                  // elements allocated before each field (TMA halo base)
   // per-phase tracing
   static constexpr int NPHASE = 3;       // stencil (+ explicit rows), reduced (+ probes), leapfrog GEMVs
@@ -386,6 +388,10 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     tBX = (B == 1) ? 32 : B * std::max(2, 32 / B);
     tBY = (B == 1) ? 8 : std::max(2, 256 / tBX);
     if (tBX * tBY > 256) tBY = 256 / tBX;
+    if (B > 1 && B % kW == 0 && 32 * kW >= 2 * B && !getenv("FDTD_NO_VEC")) {
+      // batched: each thread owns 16 bytes of members, 32 threads per row
+      tW = kW; tBX = 32 * kW; tBY = 8;
+    }
     const int vec = 16 / (int)sizeof(T);
     tHBX = tBX + tSX;                                  // H box: SX halo elements + the tile
     const int al = std::max(1, 16 / (B * (int)sizeof(T)));
@@ -788,6 +794,14 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   CK(cudaFuncSetAttribute(fdtd::stencil3d_pipe_kernel<T, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   CK(cudaFuncSetAttribute(fdtd::stencil3d_tma_kernel<T, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3 + 8192));
   CK(cudaFuncSetAttribute(fdtd::stencil3d_tma_kernel<T, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3 + 8192));
+  {
+    const int smv = (int)(sizeof(T) * (3 * 3 * (size_t)(tHBX * (tBY + 1) + 32) + 6 * 3 * (size_t)(tBX * tBY + 32)) +
+                          sizeof(fdtd::MatTable<T>) + 512);
+    CK(cudaFuncSetAttribute(fdtd::stencil3d_tma_vec_kernel<T, false, 3, kW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            std::max(smv, 48 * 1024)));
+    CK(cudaFuncSetAttribute(fdtd::stencil3d_tma_vec_kernel<T, true, 3, kW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            std::max(smv, 48 * 1024)));
+  }
   CK(cudaFuncSetAttribute(fdtd::stencil2d_rows_kernel<T, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   CK(cudaFuncSetAttribute(fdtd::stencil2d_rows_kernel<T, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   {
@@ -1245,7 +1259,14 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
     const int al = 128 / (int)sizeof(T);
     const size_t HPp = (size_t)(tHBX * (BY + 1) + al - 1) / al * al, EPp = (size_t)(BX * BY + al - 1) / al * al;
     const size_t sm = 256 + (NS * 3 * HPp + NS * 3 * EPp + 3 * 3 * EPp) * sizeof(T) + tabsz;
-    if (uniform)
+    if (tW > 1) {
+      if (uniform)
+        fdtd::stencil3d_tma_vec_kernel<T, true, NS, kW><<<grid, dim3(BX / kW, BY), sm, st>>>(
+            tma[p], tHBX, tSX, tOUTX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, ds, check_every, d_bad);
+      else
+        fdtd::stencil3d_tma_vec_kernel<T, false, NS, kW><<<grid, dim3(BX / kW, BY), sm, st>>>(
+            tma[p], tHBX, tSX, tOUTX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, ds, check_every, d_bad);
+    } else if (uniform)
       fdtd::stencil3d_tma_kernel<T, true, NS><<<grid, dim3(BX, BY), sm, st>>>(
           tma[p], tHBX, tSX, tOUTX, dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, kchunk, ds, check_every, d_bad);
     else

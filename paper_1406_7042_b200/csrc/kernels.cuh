@@ -16,6 +16,7 @@
 // H^{n+1} = H^n - ch * curl(E)  ==  H^n + ch * (K_inc^T E)
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -556,6 +557,212 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int out
   if (k1 == nz + 1 && own) {
     const int64_t o = (int64_t)nz * sz + col;
     F1.f[3][o] = hxk; F1.f[4][o] = hyk; F1.f[5][o] = hzk;
+  }
+  if (bad) atomicMin(bad_step, (unsigned long long)step);
+#undef FDTD_TMA_ISSUE
+}
+
+// ---------------------------------------------------------------------------
+// Batched 3-D stencil (B >= 2 members innermost): the TMA kernel with each
+// thread owning W = 16 bytes of members of one cell (float4 / double2), so a
+// 32-thread row covers 32*W elements = 32*W/B cells instead of 2 (B = 16,
+// W = 4: 8 cells, x overlap 8/7 instead of 2/1).  Same plane march, ring,
+// mbarriers, overlapped tiling and arithmetic (per member, in the same order)
+// as stencil3d_tma_kernel.
+// ---------------------------------------------------------------------------
+template <typename T, int W>
+struct LV {
+  T v[W];
+};
+template <typename T, int W>
+__device__ __forceinline__ LV<T, W> lv_ld(const T* p) {
+  LV<T, W> r;
+  if constexpr (sizeof(T) * W == 16) {
+    using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    const V x = *reinterpret_cast<const V*>(p);
+    if constexpr (W == 4) { r.v[0] = x.x; r.v[1] = x.y; r.v[2] = x.z; r.v[3] = x.w; }
+    else { r.v[0] = x.x; r.v[1] = x.y; }
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) r.v[w] = p[w];
+  }
+  return r;
+}
+template <typename T, int W>
+__device__ __forceinline__ void lv_st(T* p, const LV<T, W>& r) {
+  if constexpr (sizeof(T) * W == 16) {
+    using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    V x;
+    if constexpr (W == 4) { x.x = r.v[0]; x.y = r.v[1]; x.z = r.v[2]; x.w = r.v[3]; }
+    else { x.x = r.v[0]; x.y = r.v[1]; }
+    *reinterpret_cast<V*>(p) = x;
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) p[w] = r.v[w];
+  }
+}
+
+template <typename T, bool UNIFORM, int NS, int W>
+__global__ void __launch_bounds__(256, 2)
+stencil3d_tma_vec_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int outx, Dims d, Fields<T> F0,
+                         Fields<T> F1, const uint8_t* __restrict__ mat_id, const Coef<T>* __restrict__ gtab,
+                         const uint8_t* __restrict__ gifm, int n_mat, Coef<T> u0, Coef<T> u1, RowsE<T> R,
+                         const T* __restrict__ y, int kchunk, const int64_t* __restrict__ d_step,
+                         int check_every, unsigned long long* __restrict__ bad_step) {
+  using L = LV<T, W>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int BX = blockDim.x * W, BY = blockDim.y, B = d.B;   // BX: elements per tile row
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int HW = HBX, HH = BY + 1;
+  const int al = 128 / (int)sizeof(T);
+  const int HP = (HW * HH + al - 1) / al * al, EP = (BX * BY + al - 1) / al * al;
+  const unsigned base_u = smem_u32(smem_raw);
+  unsigned char* smem_al = smem_raw + ((128u - (base_u & 127u)) & 127u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_al);
+  T* Hs = reinterpret_cast<T*>(smem_al + 128);
+  T* Es = Hs + NS * 3 * HP;
+  T* En = Es + NS * 3 * EP;                  // [3][3][BY][BX] (three buffers, see the scalar kernel)
+  MatTable<T>* tab = reinterpret_cast<MatTable<T>*>(En + 3 * 3 * EP);
+  const bool leader = (tx == 0 && ty == 0);
+  if (leader) {
+    for (int q = 0; q < NS; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (!UNIFORM) {
+    for (int m = ty * blockDim.x + tx; m < n_mat; m += blockDim.x * BY) {
+      for (int c = 0; c < 6; ++c) tab->c[m][c] = gtab[m * 6 + c];
+      tab->ifm[m] = gifm[m];
+    }
+  }
+  __syncthreads();
+  const int nx = d.nx, ny = d.ny, nz = d.nz;
+  const int outy = BY - 1;
+  const int i0 = blockIdx.x * outx, j0 = blockIdx.y * outy;
+  const int xe = tx * W;                     // first element of this thread in the tile row
+  const int i = i0 + xe / B;
+  const int b = xe % B;
+  const int j = j0 + ty;
+  const int k0 = blockIdx.z * kchunk;
+  const int k1 = min(k0 + kchunk, nz + 1);
+  const int kend = min(k1, nz);
+  const bool inside = (i <= nx) && (j <= ny);
+  const bool own = inside && (xe / B < outx) && (ty < outy);
+  const int ii = min(i, nx), jj = min(j, ny);
+  const int64_t scol = (int64_t)jj * d.px + ii;
+  const int64_t col = scol * B + b;
+  const int64_t sz = d.plane * B;
+  const int xi = xe + SX, yi = ty + 1;
+  const bool ax_ij = (i < nx) && (j > 0) && (j < ny);
+  const bool ay_ij = (j < ny) && (i > 0) && (i < nx);
+  const bool az_ij = (i > 0) && (i < nx) && (j > 0) && (j < ny);
+  const bool hx_ij = (i > 0) && (i < nx) && (j < ny);
+  const bool hy_ij = (j > 0) && (j < ny) && (i < nx);
+  const bool hz_ij = (i < nx) && (j < ny);
+  const int64_t step = *d_step;
+  const bool do_check = check_every > 0 && (step % check_every) == 0;
+  bool bad = false;
+  const unsigned stage_bytes = (unsigned)((3 * HW * HH + 3 * BX * BY) * sizeof(T));
+#define FDTD_TMA_ISSUE(K)                                                              \
+  do {                                                                                 \
+    const int st_ = ((K) - k0) % NS;                                                   \
+    T* h_ = Hs + st_ * 3 * HP;                                                         \
+    T* e_ = Es + st_ * 3 * EP;                                                         \
+    mbar_expect_tx(&bars[st_], stage_bytes);                                           \
+    tma_load_3d(h_ + 0 * HP, &tm.h[0], i0 * B, j0, (K), &bars[st_]);                   \
+    tma_load_3d(h_ + 1 * HP, &tm.h[1], i0 * B, j0, (K), &bars[st_]);                   \
+    tma_load_3d(h_ + 2 * HP, &tm.h[2], i0 * B, j0, (K), &bars[st_]);                   \
+    tma_load_3d(e_ + 0 * EP, &tm.e[0], i0 * B + SX, j0 + 1, (K), &bars[st_]);          \
+    tma_load_3d(e_ + 1 * EP, &tm.e[1], i0 * B + SX, j0 + 1, (K), &bars[st_]);          \
+    tma_load_3d(e_ + 2 * EP, &tm.e[2], i0 * B + SX, j0 + 1, (K), &bars[st_]);          \
+  } while (0)
+  if (leader) {
+    for (int q = 0; q < NS - 1; ++q)
+      if (k0 + q <= kend) FDTD_TMA_ISSUE(k0 + q);
+  }
+  L hx_p{}, hy_p{};
+  if (inside && k0 > 0) {
+    const int64_t o = (int64_t)(k0 - 1) * sz + col;
+    hx_p = lv_ld<T, W>(F0.f[3] + o); hy_p = lv_ld<T, W>(F0.f[4] + o);
+  }
+  L hxk{}, hyk{}, hzk{}, exk{}, eyk{}, ezk{};
+  int m_next = UNIFORM ? 0 : (int)__ldg(mat_id + (int64_t)k0 * d.plane + scol), m_prev = 0;
+  for (int kk = k0; kk <= kend; ++kk) {
+    if (leader && kk + NS - 1 <= kend) FDTD_TMA_ISSUE(kk + NS - 1);
+    const int st = (kk - k0) % NS;
+    mbar_wait(&bars[st], (unsigned)(((kk - k0) / NS) & 1));
+    const T* h = Hs + st * 3 * HP;
+    const T* e = Es + st * 3 * EP;
+    const L hx_c = lv_ld<T, W>(h + 0 * HP + yi * HW + xi), hy_c = lv_ld<T, W>(h + 1 * HP + yi * HW + xi);
+    const L hz_c = lv_ld<T, W>(h + 2 * HP + yi * HW + xi);
+    const L hz_jm = lv_ld<T, W>(h + 2 * HP + (yi - 1) * HW + xi), hx_jm = lv_ld<T, W>(h + 0 * HP + (yi - 1) * HW + xi);
+    const L hz_im = lv_ld<T, W>(h + 2 * HP + yi * HW + xi - B), hy_im = lv_ld<T, W>(h + 1 * HP + yi * HW + xi - B);
+    const L ex0 = lv_ld<T, W>(e + 0 * EP + ty * BX + xe), ey0 = lv_ld<T, W>(e + 1 * EP + ty * BX + xe);
+    const L ez0 = lv_ld<T, W>(e + 2 * EP + ty * BX + xe);
+    const int m = m_next;
+    if (!UNIFORM && kk + 1 <= kend) m_next = (int)__ldg(mat_id + (int64_t)(kk + 1) * d.plane + scol);
+    Coef<T> cx, cy, cz;
+    uint8_t ifmk = 0;
+    if (UNIFORM) { cx = u0; cy = u0; cz = u0; }
+    else { cx = tab->c[m][0]; cy = tab->c[m][1]; cz = tab->c[m][2]; ifmk = tab->ifm[m]; }
+    const bool kin = (kk > 0) && (kk < nz);
+    L ex, ey, ez;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      ex.v[w] = (ax_ij && kin) ? ex0.v[w] + cx.apply((hz_c.v[w] - hz_jm.v[w]) - (hy_c.v[w] - hy_p.v[w])) : (T)0;
+      ey.v[w] = (ay_ij && kin) ? ey0.v[w] + cy.apply((hx_c.v[w] - hx_p.v[w]) - (hz_c.v[w] - hz_im.v[w])) : (T)0;
+      ez.v[w] = (az_ij && kk < nz) ? ez0.v[w] + cz.apply((hy_c.v[w] - hy_im.v[w]) - (hx_c.v[w] - hx_jm.v[w])) : (T)0;
+    }
+    if (!UNIFORM && ifmk && inside) {
+      const int64_t s = (int64_t)kk * d.plane + scol;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        if (ifmk & 1) ex.v[w] = eval_row(R, R.row_of[0][s], b + w, B, ex0.v[w], F0, y, step);
+        if (ifmk & 2) ey.v[w] = eval_row(R, R.row_of[1][s], b + w, B, ey0.v[w], F0, y, step);
+        if (ifmk & 4) ez.v[w] = eval_row(R, R.row_of[2][s], b + w, B, ez0.v[w], F0, y, step);
+      }
+    }
+    T* en = En + (kk % 3) * 3 * EP;
+    lv_st<T, W>(en + 0 * EP + ty * BX + xe, ex); lv_st<T, W>(en + 1 * EP + ty * BX + xe, ey);
+    lv_st<T, W>(en + 2 * EP + ty * BX + xe, ez);
+    if (own && kk < k1) {
+      const int64_t o = (int64_t)kk * sz + col;
+      lv_st<T, W>(F1.f[0] + o, ex); lv_st<T, W>(F1.f[1] + o, ey); lv_st<T, W>(F1.f[2] + o, ez);
+      if (do_check)
+#pragma unroll
+        for (int w = 0; w < W; ++w) bad |= !(finite_small(ex.v[w]) && finite_small(ey.v[w]) && finite_small(ez.v[w]));
+    }
+    __syncthreads();
+    if (kk > k0 && own) {
+      const T* e0 = En + ((kk + 2) % 3) * 3 * EP;   // plane kk-1
+      const int q = ty * BX + xe;
+      const L ey_ip = lv_ld<T, W>(e0 + 1 * EP + q + B), ez_ip = lv_ld<T, W>(e0 + 2 * EP + q + B);
+      const L ex_jp = lv_ld<T, W>(e0 + 0 * EP + q + BX), ez_jp = lv_ld<T, W>(e0 + 2 * EP + q + BX);
+      const int km = kk - 1;
+      Coef<T> hx_, hy_, hz_;
+      if (UNIFORM) { hx_ = u1; hy_ = u1; hz_ = u1; }
+      else { hx_ = tab->c[m_prev][3]; hy_ = tab->c[m_prev][4]; hz_ = tab->c[m_prev][5]; }
+      L hx1, hy1, hz1;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        hx1.v[w] = (hx_ij && km < nz) ? hxk.v[w] - hx_.apply((ez_jp.v[w] - ezk.v[w]) - (ey.v[w] - eyk.v[w])) : hxk.v[w];
+        hy1.v[w] = (hy_ij && km < nz) ? hyk.v[w] - hy_.apply((ex.v[w] - exk.v[w]) - (ez_ip.v[w] - ezk.v[w])) : hyk.v[w];
+        hz1.v[w] = (hz_ij && km > 0 && km < nz) ? hzk.v[w] - hz_.apply((ey_ip.v[w] - eyk.v[w]) - (ex_jp.v[w] - exk.v[w]))
+                                                 : hzk.v[w];
+      }
+      const int64_t o = (int64_t)km * sz + col;
+      lv_st<T, W>(F1.f[3] + o, hx1); lv_st<T, W>(F1.f[4] + o, hy1); lv_st<T, W>(F1.f[5] + o, hz1);
+      if (do_check)
+#pragma unroll
+        for (int w = 0; w < W; ++w) bad |= !(finite_small(hx1.v[w]) && finite_small(hy1.v[w]) && finite_small(hz1.v[w]));
+    }
+    hx_p = hx_c; hy_p = hy_c;
+    hxk = hx_c; hyk = hy_c; hzk = hz_c;
+    exk = ex; eyk = ey; ezk = ez;
+    m_prev = m;
+  }
+  if (k1 == nz + 1 && own) {
+    const int64_t o = (int64_t)nz * sz + col;
+    lv_st<T, W>(F1.f[3] + o, hxk); lv_st<T, W>(F1.f[4] + o, hyk); lv_st<T, W>(F1.f[5] + o, hzk);
   }
   if (bad) atomicMin(bad_step, (unsigned long long)step);
 #undef FDTD_TMA_ISSUE

@@ -248,3 +248,37 @@ def test_persistent_2d_bitwise_equals_per_step_kernels(which, prec, monkeypatch)
         assert np.array_equal(a["state"][c], b["state"][c]), c
     assert np.array_equal(a["red_e"], b["red_e"]) and np.array_equal(a["red_h"], b["red_h"])
     assert np.array_equal(a["probes"], b["probes"])
+
+
+@pytest.mark.parametrize("prec", [32, 64])
+def test_batched_vec_stencil_bitwise_equals_scalar_tma(prec, monkeypatch):
+    # B = 4: the batched TMA stencil (16 bytes of members per thread) against
+    # the scalar TMA stencil, from random states incl. the interface rows:
+    # per-member arithmetic in the same order -> bit for bit
+    from paper_1406_7042_b200.fdtd import Sim
+    scn, prob = _prep("tiny4", precision=prec)
+    prob = dict(prob, init={})
+    nx, ny, nz = prob["n"]
+    S = (nx + 1) * (ny + 1) * (nz + 1)
+    rng = np.random.default_rng(1)
+
+    def run(no_vec, state):
+        if no_vec:
+            monkeypatch.setenv("FDTD_NO_VEC", "1")
+        else:
+            monkeypatch.delenv("FDTD_NO_VEC", raising=False)
+        sim = Sim(prob, precision=prec, graph_steps=0)
+        for c in range(6):
+            sim.set_state(c, state[c])
+        sim.step(5)
+        sim.sync()
+        out = [sim.get_state(c) for c in range(7)]
+        sim.close()
+        return out
+
+    from sampled_state import random_state
+    arrays, _, _ = random_state(prob, seed=3)
+    state = [arrays[c] for c in range(6)]
+    a, b = run(True, state), run(False, state)
+    for c in range(7):
+        assert np.array_equal(a[c], b[c]), c
