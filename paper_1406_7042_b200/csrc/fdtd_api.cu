@@ -116,6 +116,8 @@ struct BlockDev {
   // (leap-frog blocks: 16-byte vector loads)
   T *K_d = nullptr, *KT_d = nullptr, *SE_d = nullptr, *SET_d = nullptr, *ge_d = nullptr, *gh_d = nullptr;
   T *Kp_d = nullptr, *KTp_d = nullptr, *SEp_d = nullptr, *Tv_d = nullptr;
+  T* part_d = nullptr;                         // [splits][qh][N] S_E^T G partial sums (fp32 GEMM path)
+  int splits = 0;                              // > 0: tall-skinny fp32 GEMM kernels for the S_E products
   int Kph = 0, Kpe = 0;                        // padded row pitches (multiples of 32 * VEC)
   // state offsets (elements) in the concatenated buffers
   int64_t e_off = 0, h_off = 0, y_off = 0;     // e/h buffers [q][N], y / G [n_if][N]
@@ -342,6 +344,36 @@ static int launch_colsum(int rows, int cols, int Kp, int N, const T* A, const T*
   return 1;
 }
 
+static int gemm_nn_smem(int NQ, int Kp) {
+  const int TR = 4 * 256 / NQ, KC = NQ >= 4 ? 32 : 16;
+  return (int)(sizeof(float) * ((size_t)Kp * 4 * NQ + 3 * (size_t)TR * (KC + 4)));
+}
+static int gemm_tn_smem(int NQ) {
+  const int TC = 4 * 256 / NQ;
+  return (int)(sizeof(float) * 3 * 16 * ((size_t)TC + 4 * NQ));
+}
+// y = S_E h~ (rows = n_if) and S_E^T G partials for the fp32 GEMM path
+static int launch_gemm_nn(int rows, int K, int Kp, int N, const float* A, const float* X, float* out, const float* g,
+                          float alpha, bool acc, const int64_t* d_step, int check_every, unsigned long long* bad,
+                          cudaStream_t st) {
+  const int NQ = N / 4;
+  const int grid = std::min(148, std::max(1, rows / 64));
+  const int sm = gemm_nn_smem(NQ, Kp);
+#define FDTD_GNN(Q) fdtd::gemm_nn_f32_kernel<Q><<<grid, 256, sm, st>>>(rows, K, Kp, A, X, out, g, alpha, acc, d_step, check_every, bad)
+  if (NQ == 2) FDTD_GNN(2); else if (NQ == 4) FDTD_GNN(4); else FDTD_GNN(8);
+#undef FDTD_GNN
+  return 1;
+}
+static int launch_gemm_tn(int rows, int cols, int Kp, int N, int splits, const float* A, const float* G, float* part,
+                          cudaStream_t st) {
+  const int NQ = N / 4, TC = 4 * 256 / NQ;
+  const dim3 grid((cols + TC - 1) / TC, splits);
+  const int sm = gemm_tn_smem(NQ);
+#define FDTD_GTN(Q) fdtd::gemm_tn_f32_partial_kernel<Q><<<grid, 256, sm, st>>>(rows, cols, Kp, A, G, part)
+  if (NQ == 2) FDTD_GTN(2); else if (NQ == 4) FDTD_GTN(4); else FDTD_GTN(8);
+#undef FDTD_GTN
+  return 1;
+}
 template <typename T>
 int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_interface* itf,
                     const fdtd_reduced_block* bl, int n_blocks, const fdtd_sources* src,
@@ -527,6 +559,14 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       D.SEp_d = dalloc<T>(std::max<size_t>(SEp.size(), 1)); D.Tv_d = dalloc<T>((size_t)D.qh * D.N);
       if (!D.Kp_d || !D.KTp_d || !D.SEp_d || !D.Tv_d) return fail(FDTD_ENOMEM, "block %d allocation failed", b);
       if (upload(D.Kp_d, Kp) || upload(D.KTp_d, KTp) || upload(D.SEp_d, SEp)) return FDTD_ECUDA;
+      if (sizeof(T) == 4 && (D.N == 8 || D.N == 16 || D.N == 32) &&
+          (D.n_if >= 148 * 64 || getenv("FDTD_FORCE_SKINNY")) && !getenv("FDTD_NO_SKINNY")) {
+        const int TC = 4 * 256 / (D.N / 4);
+        const int ctile = (D.qh + TC - 1) / TC;
+        D.splits = std::max(1, std::min(2 * 148 / ctile, D.n_if / 64));
+        D.part_d = dalloc<T>((size_t)D.splits * D.qh * D.N);
+        if (!D.part_d) return fail(FDTD_ENOMEM, "block %d: partial-sum workspace allocation failed", b);
+      }
     }
   }
   for (int p = 0; p < 2; ++p) {
@@ -813,6 +853,22 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     for (auto& D : blocks)
       if (!D.fused && (size_t)std::max(D.Kph, D.Kpe) * D.N * sizeof(T) > (size_t)big)
         return fail(FDTD_ENOTSUP, "reduced block too large for the staged leap-frog GEMV (q x N)");
+    for (auto& D : blocks) {
+      if (!D.splits) continue;
+      const int NQ = D.N / 4;
+      const int sn = gemm_nn_smem(NQ, D.Kph), stn = gemm_tn_smem(NQ);
+      if (sn > 220 * 1024) { D.splits = 0; continue; }
+      if (NQ == 2) {
+        CK(cudaFuncSetAttribute(fdtd::gemm_nn_f32_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sn));
+        CK(cudaFuncSetAttribute(fdtd::gemm_tn_f32_partial_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, stn));
+      } else if (NQ == 4) {
+        CK(cudaFuncSetAttribute(fdtd::gemm_nn_f32_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sn));
+        CK(cudaFuncSetAttribute(fdtd::gemm_tn_f32_partial_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, stn));
+      } else {
+        CK(cudaFuncSetAttribute(fdtd::gemm_nn_f32_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sn));
+        CK(cudaFuncSetAttribute(fdtd::gemm_tn_f32_partial_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, stn));
+      }
+    }
   }
   if (fused_gemm && fused_smem > 48 * 1024) {
     CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 4, gemm_rpw(4), GEMM_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
@@ -1315,6 +1371,20 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
       // a6: T = K~'^T e~ + S_E^T G ; h~ += G_h T ; y = S_E h~
       n += launch_rowblock<T>(D.qh, D.qe, D.Kpe, D.N, D.KTp_d, e, D.Tv_d, (const T*)nullptr, (T)1, false, ds, 0,
                               d_bad, st);
+      if constexpr (sizeof(T) == 4) {
+        if (D.splits > 0) {
+          // S_E^T G: split-K partials, then h~ += G_h (T + sum of partials) in a fixed order;
+          // y = S_E h~: tall-skinny GEMM
+          n += launch_gemm_tn(D.n_if, D.qh, D.Kph, D.N, D.splits, (const float*)D.SEp_d,
+                              (const float*)(g_all + D.y_off), (float*)D.part_d, st);
+          fdtd::reduce_axpy_f32_kernel<<<(D.qh * D.N + 255) / 256, 256, 0, st>>>(
+              D.qh, D.N, D.splits, (const float*)D.part_d, (const float*)D.Tv_d, (const float*)D.gh_d, (float*)h);
+          ++n;
+          n += launch_gemm_nn(D.n_if, D.qh, D.Kph, D.N, (const float*)D.SEp_d, (const float*)h,
+                              (float*)(y_all + D.y_off), nullptr, 1.f, false, ds, check_every, d_bad, st);
+          continue;
+        }
+      }
       if (D.n_if > 0) n += launch_colsum<T>(D.n_if, D.qh, D.Kph, D.N, D.SEp_d, g_all + D.y_off, D.Tv_d, st);
       fdtd::axpy_diag_kernel<T><<<(D.qh * D.N + 255) / 256, 256, 0, st>>>(D.qh, D.N, D.gh_d, D.Tv_d, h);
       ++n;

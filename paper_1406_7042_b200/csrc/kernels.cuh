@@ -1257,6 +1257,201 @@ __global__ void axpy_diag_kernel(int rows, int N, const T* __restrict__ g, const
   h[t] += g[t / N] * Tv[t];
 }
 
+// ---------------------------------------------------------------------------
+// Leap-frog path, fp32 tall-skinny GEMMs (config 4: S_E 65,024 x 1,024, N = 16).
+// Register-tiled SIMT: every thread owns a 4 x 4 (rows x columns) tile of the
+// output; operands staged in shared memory by 16-byte cp.async in a 3-stage
+// ring; inner step = 8 LDS.128 for 64 FMA.  HBM-bound on A (each element read
+// once per product), FMA work 2 R K N per product.
+//
+// gemm_nn: out[r][n] = (acc ? out[r][n] : 0) + alpha g[r] sum_k A[r][k] X[k][n]
+//   A row-major with pitch Kp (multiple of 32), X [K][N] (N = 4 NQ) staged once
+//   per CTA; each CTA owns a contiguous, balanced range of rows.
+// ---------------------------------------------------------------------------
+template <int NQ>
+__global__ void __launch_bounds__(256, 1)
+gemm_nn_f32_kernel(int rows, int K, int Kp, const float* __restrict__ A, const float* __restrict__ X,
+                   float* __restrict__ out, const float* __restrict__ g, float alpha, bool accumulate,
+                   const int64_t* __restrict__ d_step, int check_every, unsigned long long* bad_step) {
+  constexpr int N = 4 * NQ;
+  constexpr int RQ = 256 / NQ;                 // row quads per tile
+  constexpr int TR = 4 * RQ;                   // rows per tile
+  constexpr int KC = NQ >= 4 ? 32 : 16, KCP = KC + 4, NS = 3;
+  extern __shared__ __align__(16) float smf[];
+  float* Xs = smf;                             // [Kp][N]
+  float* As = Xs + (size_t)Kp * N;             // [NS][TR][KCP]
+  const int tid = threadIdx.x;
+  const int cq = tid % NQ, rq = tid / NQ;
+  for (int t = tid; t < Kp * NQ; t += 256) {
+    const int k = t / NQ, c = (t % NQ) * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (k < K) v = *reinterpret_cast<const float4*>(X + (int64_t)k * N + c);
+    *reinterpret_cast<float4*>(Xs + (int64_t)k * N + c) = v;
+  }
+  const int r_begin = (int)((int64_t)rows * blockIdx.x / gridDim.x);
+  const int r_end = (int)((int64_t)rows * (blockIdx.x + 1) / gridDim.x);
+  const int nkc = (K + KC - 1) / KC;
+  const int ntile = (r_end - r_begin + TR - 1) / TR;
+  const int total = ntile * nkc;
+  const bool check = check_every > 0 && (*d_step % check_every) == 0;
+  bool bad = false;
+  auto issue = [&](int it) {
+    if (it < total) {
+      const int tile = it / nkc, kc = it % nkc;
+      const int r0 = r_begin + tile * TR, k0 = kc * KC;
+      float* dst = As + (size_t)(it % NS) * TR * KCP;
+      for (int q = tid; q < TR * (KC / 4); q += 256) {
+        const int rr = q / (KC / 4), c4 = (q % (KC / 4)) * 4;
+        const int r = r0 + rr;
+        const bool ok = r < r_end && k0 + c4 < Kp;
+        cp_async16(dst + rr * KCP + c4, A + (int64_t)(ok ? r : r_begin) * Kp + (ok ? k0 + c4 : 0), ok);
+      }
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  issue(1);
+  float acc[4][4];
+  for (int it = 0; it < total; ++it) {
+    const int tile = it / nkc, kc = it % nkc;
+    if (kc == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
+    }
+    issue(it + 2);
+    cp_async_wait<2>();
+    __syncthreads();
+    const float* a = As + (size_t)(it % NS) * TR * KCP + (rq * 4) * KCP;
+    const float* x = Xs + (int64_t)(kc * KC) * N + cq * 4;
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      float4 a4[4], x4[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a4[i] = *reinterpret_cast<const float4*>(a + i * KCP + kk);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) x4[j] = *reinterpret_cast<const float4*>(x + (kk + j) * N);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float av[4] = {a4[i].x, a4[i].y, a4[i].z, a4[i].w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[i][0] += av[j] * x4[j].x;
+          acc[i][1] += av[j] * x4[j].y;
+          acc[i][2] += av[j] * x4[j].z;
+          acc[i][3] += av[j] * x4[j].w;
+        }
+      }
+    }
+    if (kc == nkc - 1) {
+      const int r0 = r_begin + tile * TR + rq * 4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = r0 + i;
+        if (r >= r_end) continue;
+        const float gr = g ? g[r] : 1.f;
+        float4* o = reinterpret_cast<float4*>(out + (int64_t)r * N + cq * 4);
+        float4 v = accumulate ? *o : make_float4(0.f, 0.f, 0.f, 0.f);
+        v.x += alpha * gr * acc[i][0]; v.y += alpha * gr * acc[i][1];
+        v.z += alpha * gr * acc[i][2]; v.w += alpha * gr * acc[i][3];
+        *o = v;
+        if (check) bad |= !(finite_small(v.x) && finite_small(v.y) && finite_small(v.z) && finite_small(v.w));
+      }
+    }
+    __syncthreads();                           // stage it % NS is refilled by issue(it + 3)
+  }
+  cp_async_wait<0>();
+  if (bad) atomicMin(bad_step, (unsigned long long)*d_step);
+}
+
+// gemm_tn partial: part[s][c][n] = sum_{r in split s} A[r][c] G[r][n]
+//   grid (column tiles of TC = 4 * 256 / NQ columns, splits); the splits are
+//   summed in a fixed order by reduce_axpy_f32_kernel (deterministic).
+template <int NQ>
+__global__ void __launch_bounds__(256, 2)
+gemm_tn_f32_partial_kernel(int rows, int cols, int Kp, const float* __restrict__ A, const float* __restrict__ G,
+                           float* __restrict__ part) {
+  constexpr int N = 4 * NQ;
+  constexpr int CQ = 256 / NQ;                 // column quads per tile
+  constexpr int TC = 4 * CQ;
+  constexpr int RC = 16, NS = 3;
+  extern __shared__ __align__(16) float smf[];
+  float* As = smf;                             // [NS][RC][TC]
+  float* Gs = As + NS * RC * TC;               // [NS][RC][N]
+  const int tid = threadIdx.x;
+  const int nq = tid % NQ, cq = tid / NQ;
+  const int c0 = blockIdx.x * TC;
+  const int r_begin = (int)((int64_t)rows * blockIdx.y / gridDim.y);
+  const int r_end = (int)((int64_t)rows * (blockIdx.y + 1) / gridDim.y);
+  const int nch = (r_end - r_begin + RC - 1) / RC;
+  auto issue = [&](int ch) {
+    if (ch < nch) {
+      const int r0 = r_begin + ch * RC;
+      float* da = As + (size_t)(ch % NS) * RC * TC;
+      float* dg = Gs + (size_t)(ch % NS) * RC * N;
+      for (int q = tid; q < RC * (TC / 4); q += 256) {
+        const int rr = q / (TC / 4), c4 = (q % (TC / 4)) * 4;
+        const int r = r0 + rr;
+        const bool ok = r < r_end && c0 + c4 < Kp;
+        cp_async16(da + rr * TC + c4, A + (int64_t)(ok ? r : r_begin) * Kp + (ok ? c0 + c4 : 0), ok);
+      }
+      for (int q = tid; q < RC * NQ; q += 256) {
+        const int rr = q / NQ, n4 = (q % NQ) * 4;
+        const int r = r0 + rr;
+        const bool ok = r < r_end;
+        cp_async16(dg + rr * N + n4, G + (int64_t)(ok ? r : r_begin) * N + n4, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  issue(1);
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
+  for (int ch = 0; ch < nch; ++ch) {
+    issue(ch + 2);
+    cp_async_wait<2>();
+    __syncthreads();
+    const float* a = As + (size_t)(ch % NS) * RC * TC + cq * 4;
+    const float* gg = Gs + (size_t)(ch % NS) * RC * N + nq * 4;
+#pragma unroll
+    for (int rr = 0; rr < RC; ++rr) {
+      const float4 a4 = *reinterpret_cast<const float4*>(a + rr * TC);
+      const float4 g4 = *reinterpret_cast<const float4*>(gg + rr * N);
+      const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i][0] += av[i] * g4.x; acc[i][1] += av[i] * g4.y;
+        acc[i][2] += av[i] * g4.z; acc[i][3] += av[i] * g4.w;
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = c0 + cq * 4 + i;
+    if (c >= cols) continue;
+    *reinterpret_cast<float4*>(part + ((int64_t)blockIdx.y * cols + c) * N + nq * 4) =
+        make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+  }
+}
+
+// h~[c][n] += g_h[c] (T[c][n] + sum_s part[s][c][n])   (splits in order)
+__global__ void reduce_axpy_f32_kernel(int cols, int N, int splits, const float* __restrict__ part,
+                                       const float* __restrict__ Tv, const float* __restrict__ gh,
+                                       float* __restrict__ h) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cols * N) return;
+  float v = Tv[t];
+  for (int s2 = 0; s2 < splits; ++s2) v += part[(int64_t)s2 * cols * N + t];
+  h[t] += gh[t / N] * v;
+}
+
 template <typename T>
 __global__ void gather_kernel(int64_t n, int B, const int32_t* __restrict__ comp, const int64_t* __restrict__ off,
                               const int64_t* __restrict__ dst, Fields<T> F, T* __restrict__ G) {

@@ -282,3 +282,23 @@ def test_batched_vec_stencil_bitwise_equals_scalar_tma(prec, monkeypatch):
     a, b = run(True, state), run(False, state)
     for c in range(7):
         assert np.array_equal(a[c], b[c]), c
+
+
+@pytest.mark.parametrize("skinny", ["force", "off"])
+def test_tiny4_batch8_leapfrog_skinny_gemm(skinny, monkeypatch):
+    # the fp32 tall-skinny GEMM kernels of the leap-frog path (config 4's
+    # S_E products, N in {8, 16, 32}) on the small iris guide with B = 8
+    # members (waveforms duplicated with distinct amplitudes), against the
+    # oracle for two members; "off" runs the GEMV kernels on the same problem
+    scn, prob = _prep("tiny4", precision=32)
+    w = np.asarray(prob["sources"]["wave"])
+    prob = dict(prob, sources=dict(prob["sources"], wave=np.concatenate([w, -0.7 * w], axis=2)), batch=8)
+    if skinny == "force":
+        monkeypatch.setenv("FDTD_FORCE_SKINNY", "1")
+    else:
+        monkeypatch.setenv("FDTD_NO_SKINNY", "1")
+    gpu = run_gpu(prob, 300, precision=32, reduced_form="leapfrog")
+    for m in (1, 6):
+        ora = run_oracle(prob, 300, member=m)
+        es, ep, _ = compare(prob, gpu, ora, member=m)
+        assert es <= 1e-4 and ep <= 1e-4, (m, es, ep)
