@@ -175,7 +175,9 @@ int fdtd_probe(fdtd_t* h, double* out, int64_t cap, int64_t* written);
 /* State access (synchronising).  which = 0..5: coarse component c, n = batch*S,
  * layout [batch][S]; which = 6 / 7: all reduced e~ / h~, layout
  * [block][inst][batch][q]; which = 8: the step counter n (n = 1; it indexes
- * the source waveforms, so a restored checkpoint sets it too). */
+ * the source waveforms, so a restored checkpoint sets it too).  In 3-D,
+ * fdtd_set_state stores E entries that are not unknowns (E tangential to the
+ * PEC walls, Eq. (3) with PEC elimination) as 0 whatever `in` holds. */
 int fdtd_get_state(fdtd_t* h, int32_t which, double* out, int64_t n);
 int fdtd_set_state(fdtd_t* h, int32_t which, const double* in, int64_t n);
 
@@ -192,8 +194,10 @@ int64_t fdtd_launch_count(const fdtd_t* h);
  *   2  TMA 3-D stencil (else the cp.async one, in 3-D)
  *   4  cluster-split GEMM kernel for fused reduced blocks (else warp-per-row)
  *   8  leap-frog GEMV path for at least one large reduced block
+ *  16  the 3-D tile stencil (W elements per thread, NS-plane TMA ring; with bit 2)
  * Environment overrides (testing): FDTD_PERSIST=0, FDTD_NO_TMA,
- * FDTD_FUSED=gemv|gemm, FDTD_KCHUNK=<planes>. */
+ * FDTD_FUSED=gemv|gemm, FDTD_KCHUNK=<planes>, FDTD_STENCIL_OLD=1 (the
+ * reference TMA stencils instead of the tile stencil), FDTD_TILE=<W>,<NS>. */
 int32_t fdtd_path(const fdtd_t* h);
 
 /* Per-phase tracing.  fdtd_profile(h, 1) resets the accumulators and makes the

@@ -1,19 +1,22 @@
 """Compile libfdtd.so for sm_100a, in-tree (the .so travels with the repo
-snapshot to the GPU box)."""
+snapshot to the GPU box).  The translation units compile in parallel."""
 from __future__ import annotations
 
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libfdtd.so")
-SOURCES = ["fdtd_api.cu"]
-HEADERS = ["kernels.cuh", "persist2d.cuh", os.path.join("..", "..", "include", "fdtd.h")]
+OBJDIR = os.path.join(HERE, "csrc", "obj")
+SOURCES = ["fdtd_api.cu", "stencil3d.cu"]
+HEADERS = ["kernels.cuh", "persist2d.cuh", "stencil3d.cuh", "stencil3d_launch.h",
+           os.path.join("..", "..", "include", "fdtd.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared"]
+              "-Xcompiler", "-fPIC"]
 
 
 def _nvcc():
@@ -31,15 +34,24 @@ def needs_build():
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
-        return OUT
-    cmd = [_nvcc()] + NVCC_FLAGS + ["-o", OUT] + [os.path.join(CSRC, s) for s in SOURCES]
+def _run(cmd, verbose):
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
+
+
+def build(force=False, verbose=False):
+    if not force and not needs_build():
+        return OUT
+    os.makedirs(OBJDIR, exist_ok=True)
+    nv = _nvcc()
+    objs = [os.path.join(OBJDIR, os.path.splitext(s)[0] + ".o") for s in SOURCES]
+    cmds = [[nv] + NVCC_FLAGS + ["-c", os.path.join(CSRC, s), "-o", o] for s, o in zip(SOURCES, objs)]
+    with ThreadPoolExecutor(len(cmds)) as ex:
+        list(ex.map(lambda c: _run(c, verbose), cmds))
+    _run([nv, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT] + objs, verbose)
     return OUT
 
 

@@ -11,6 +11,7 @@
 #include "../../include/fdtd.h"
 #include "kernels.cuh"
 #include "persist2d.cuh"
+#include "stencil3d_launch.h"
 
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -203,6 +204,11 @@ struct Impl : public fdtd_t {
   fdtd::TmaSet tma[2];
   int tBX = 32, tBY = 8, tHBX = 36, tSX = 4, tOUTX = 28;
   int tW = 1;                   // members per thread in the TMA stencil (16 bytes when the batch allows)
+  bool use_tile = false;        // the tile stencil (stencil3d.cuh) is the 3-D path
+  fdtd::TileCfg tcfg;
+  fdtd::TileSplit tsplit;
+  int tile_grid = 0;
+  size_t tile_smem = 0;
   static constexpr int kW = 16 / (int)sizeof(T);
   int64_t guard = 0;                  // elements allocated before each field (TMA halo base)
   // per-phase tracing
@@ -282,6 +288,8 @@ struct Impl : public fdtd_t {
   fdtd::P2Probes<T> p_probes{};
   T *p_ezL = nullptr, *p_ezB = nullptr, *p_hyR = nullptr, *p_hxT = nullptr;
   unsigned* p_flags = nullptr;                      // fE[nT] fH[nT] gready reddone abort
+  unsigned long long* p_ll = nullptr;               // fp32 flag-in-data exchange buffers (persist2d.cuh)
+  size_t p_ll_words = 0;
   uint8_t* p_tile_if = nullptr;
   int setup_persist();
   int launch_persist(int64_t n, int64_t* count);
@@ -424,6 +432,20 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       // batched: each thread owns 16 bytes of members, 32 threads per row
       tW = kW; tBX = 32 * kW; tBY = 8;
     }
+    // the tile stencil (default): batch 1 with W x cells per thread, or a
+    // batch of 16 members with 16 bytes per thread; 32-bit element offsets
+    {
+      fdtd::TileCfg c;
+      c.BY = 8;
+      if (B == 1) { c.MB = 0; c.W = 2; c.NS = sizeof(T) == 4 ? 6 : 3; }
+      else { c.MB = B; c.W = kW; c.NS = 3; }
+      if (const char* e = getenv("FDTD_TILE")) sscanf(e, "%d,%d", &c.W, &c.NS);
+      const int64_t span = (int64_t)px * B * (ny + 1) * (nz + 1) + (int64_t)px * B + 64;
+      if (fdtd::tile_supported<T>(c) && span < ((int64_t)1 << 31) && !getenv("FDTD_STENCIL_OLD")) {
+        use_tile = true; tcfg = c;
+        tW = c.W; tBX = 32 * c.W; tBY = c.BY;
+      }
+    }
     const int vec = 16 / (int)sizeof(T);
     tHBX = tBX + tSX;                                  // H box: SX halo elements + the tile
     const int al = std::max(1, 16 / (B * (int)sizeof(T)));
@@ -461,6 +483,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       }
     }
     if (getenv("FDTD_NO_TMA")) use_tma = false;
+    if (!use_tma) use_tile = false;
     if (const char* e = getenv("FDTD_KCHUNK")) kchunk_max = std::max(1, atoi(e));
   }
 
@@ -834,6 +857,48 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   CK(cudaFuncSetAttribute(fdtd::stencil3d_pipe_kernel<T, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   CK(cudaFuncSetAttribute(fdtd::stencil3d_tma_kernel<T, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3 + 8192));
   CK(cudaFuncSetAttribute(fdtd::stencil3d_tma_kernel<T, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3 + 8192));
+  if (use_tile) {
+    const size_t ttab = uniform ? 0 : ((size_t)n_mat * (6 * sizeof(fdtd::Coef<T>) + 1) + 15) / 16 * 16;
+    tile_smem = fdtd::tile_smem_bytes(tcfg, tHBX, (int)sizeof(T), ttab) + 128;
+    if (tile_smem > 227 * 1024) return fail(FDTD_ENOTSUP, "tile stencil: %zu bytes of shared memory", tile_smem);
+    CK(fdtd::tile_prepare<T>(tcfg, tile_smem));
+    // persistent grid: every resident CTA slot, each a balanced range of column-planes
+    const int outy = tBY - 1;
+    tsplit.ntx = (nx + 1 + tOUTX - 1) / tOUTX;
+    tsplit.outx = tOUTX; tsplit.outy = outy; tsplit.nzp = nz + 1;
+    tsplit.ncols = tsplit.ntx * ((ny + 1 + outy - 1) / outy);
+    int sms = 148;
+    {
+      int dev = 0;
+      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int per_sm = std::max(1, fdtd::tile_blocks_per_sm<T>(tcfg, uniform, tile_smem));
+    int G = per_sm * sms;
+    if (const char* e = getenv("FDTD_TILE_GRID")) G = std::max(1, atoi(e));
+    // z-chunking: minimise the planes of the busiest CTA slot, counting the
+    // two extra planes (lead H plane, trailing plane) each item loads
+    {
+      const int nzp = nz + 1;
+      double best = 1e300;
+      int best_kc = nzp;
+      for (int nch = 1; nch <= nzp; ++nch) {
+        const int kc = (nzp + nch - 1) / nch;
+        if (kc < 4 && nch > 1) break;
+        const int nch_eff = (nzp + kc - 1) / kc;
+        const int64_t items = (int64_t)tsplit.ncols * nch_eff;
+        const int64_t rounds = (items + G - 1) / G;
+        const double cost = (double)rounds * (kc + (nch_eff > 1 ? 2 : 1));
+        if (cost < best * 0.999) { best = cost; best_kc = kc; }
+      }
+      if (const char* e = getenv("FDTD_TILE_KC")) best_kc = std::max(1, atoi(e));
+      tsplit.kc = best_kc;
+      tsplit.nitems = tsplit.ncols * ((nzp + best_kc - 1) / best_kc);
+    }
+    tile_grid = std::min(tsplit.nitems, G);
+    if (getenv("FDTD_VERBOSE"))
+      fprintf(stderr, "fdtd: tile stencil W=%d NS=%d MB=%d smem=%zu per_sm=%d grid=%d items=%d (cols %d x kc %d)\n",
+              tcfg.W, tcfg.NS, tcfg.MB, tile_smem, per_sm, tile_grid, tsplit.nitems, tsplit.ncols, tsplit.kc);
+  }
   {
     const int smv = (int)(sizeof(T) * (3 * 3 * (size_t)(tHBX * (tBY + 1) + 32) + 6 * 3 * (size_t)(tBX * tBY + 32)) +
                           sizeof(fdtd::MatTable<T>) + 512);
@@ -886,7 +951,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     int e = setup_persist();
     if (e) return e;
   }
-  path_bits = (persist ? 1 : 0) | (use_tma ? 2 : 0) | (fused_gemm ? 4 : 0) | (any_leap ? 8 : 0);
+  path_bits = (persist ? 1 : 0) | (use_tma ? 2 : 0) | (fused_gemm ? 4 : 0) | (any_leap ? 8 : 0) | (use_tile ? 16 : 0);
   CK(cudaStreamSynchronize(stream));
   return FDTD_OK;
 }
@@ -1076,6 +1141,12 @@ int Impl<T>::setup_persist() {
   p_ezL = dalloc<T>((size_t)2 * nT * TY); p_hyR = dalloc<T>((size_t)2 * nT * TY);
   p_ezB = dalloc<T>((size_t)2 * nT * TX); p_hxT = dalloc<T>((size_t)2 * nT * TX);
   p_flags = dalloc<unsigned>((size_t)2 * nT + 3);
+  if (sizeof(T) == 4) {
+    p_ll_words = (size_t)2 * nT * (2 * TY + 2 * TX) + 2 * (size_t)(2 * std::max<int64_t>(y_size, 1) +
+                                                                   std::max<int64_t>(e_size, 1) + std::max<int64_t>(h_size, 1));
+    p_ll = dalloc<unsigned long long>(p_ll_words);
+    if (!p_ll) return fail(FDTD_ENOMEM, "persistent-path allocation failed");
+  }
   if (!p_ezL || !p_hyR || !p_ezB || !p_hxT || !p_flags) return fail(FDTD_ENOMEM, "persistent-path allocation failed");
   CK(cudaMemsetAsync(p_flags, 0, sizeof(unsigned) * (2 * nT + 3), stream));
   pTX = TX; pTY = TY; pntx = ntx; pnty = nty; p_rpc = rpc; p_Rtot = Rtot; p_Cmax = Cmax; p_smem = smem;
@@ -1116,6 +1187,20 @@ int Impl<T>::launch_persist(int64_t n, int64_t* count) {
   P.d_step_out = d_step + p1;
   P.check_every = check_every; P.bad_step = d_bad; P.maxrows = p_maxrows;
   CK(cudaMemsetAsync(p_flags, 0, sizeof(unsigned) * (2 * nT + 3), stream));
+  if (p_ll) {
+    // tagged words carry the local step + 1: zero them so no stale word matches
+    CK(cudaMemsetAsync(p_ll, 0, sizeof(unsigned long long) * p_ll_words, stream));
+    unsigned long long* q = p_ll;
+    P.lezL = q; q += (size_t)2 * nT * pTY;
+    P.lhyR = q; q += (size_t)2 * nT * pTY;
+    P.lezB = q; q += (size_t)2 * nT * pTX;
+    P.lhxT = q; q += (size_t)2 * nT * pTX;
+    P.ysz = std::max<int64_t>(y_size, 1); P.esz = std::max<int64_t>(e_size, 1); P.hsz = std::max<int64_t>(h_size, 1);
+    P.lG = q; q += 2 * P.ysz;
+    P.ly = q; q += 2 * P.ysz;
+    P.leb = q; q += 2 * P.esz;
+    P.lhb = q; q += 2 * P.hsz;
+  }
   static unsigned long long* dbg = nullptr;
   if (getenv("FDTD_P2DBG")) {
     if (!dbg) CK(cudaMalloc(&dbg, 3 * 8 * 8 * sizeof(unsigned long long)));
@@ -1306,7 +1391,10 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   mark(0, 0);
   const size_t tabsz = uniform ? 0 : sizeof(fdtd::MatTable<T>);
   const fdtd::Dims dm{nx, ny, nz, px, B, plane};
-  if (dim == 3 && use_tma) {
+  if (dim == 3 && use_tile) {
+    CK(fdtd::tile_launch<T>(tcfg, uniform, tile_grid, tile_smem, st, tma[p], tsplit, dm, F0, F1, mat_id, tab,
+                            ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad));
+  } else if (dim == 3 && use_tma) {
     constexpr int NS = 3;
     const int BX = tBX, BY = tBY;
     const int outx = tOUTX, outy = BY - 1;
@@ -1606,7 +1694,16 @@ int Impl<T>::set_state(int which, const double* in, int64_t n) {
     if (n != S * B) return fail(FDTD_EINVAL, "set_state: n must be batch*S");
     if (!F[p][which]) return fail(FDTD_EINVAL, "set_state: component %d unused in 2-D", which);
     std::fill(staging, staging + elems, (T)0);
+    // 3-D E entries that are not unknowns (tangential E on the PEC walls) are
+    // stored as 0: the stencil keeps their old value (stencil3d.cuh)
+    const bool mask_e = dim == 3 && which <= 2;
     for (int64_t s = 0; s < S; ++s) {
+      if (mask_e) {
+        const int64_t i = s % (nx + 1), j = (s / (nx + 1)) % (ny + 1), k = s / ((int64_t)(nx + 1) * (ny + 1));
+        const bool xi = i > 0 && i < nx, yi = j > 0 && j < ny, zi = k > 0 && k < nz;
+        const bool unk = which == 0 ? (i < nx && yi && zi) : which == 1 ? (xi && j < ny && zi) : (xi && yi && k < nz);
+        if (!unk) continue;
+      }
       const int64_t o = dev_off(s) * B;
       for (int b = 0; b < B; ++b) staging[o + b] = (T)in[(int64_t)b * S + s];
     }

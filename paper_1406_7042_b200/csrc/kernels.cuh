@@ -1442,7 +1442,7 @@ gemm_tn_f32_partial_kernel(int rows, int cols, int Kp, const float* __restrict__
 }
 
 // h~[c][n] += g_h[c] (T[c][n] + sum_s part[s][c][n])   (splits in order)
-__global__ void reduce_axpy_f32_kernel(int cols, int N, int splits, const float* __restrict__ part,
+static __global__ void reduce_axpy_f32_kernel(int cols, int N, int splits, const float* __restrict__ part,
                                        const float* __restrict__ Tv, const float* __restrict__ gh,
                                        float* __restrict__ h) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;

@@ -98,7 +98,42 @@ struct Persist2D {
   unsigned long long* bad_step;
   unsigned long long* dbg;      // optional phase timestamps (FDTD_P2DBG), [cta slot][step][8]
   int dbg_tile_if;              // which tile to trace besides tile 0
+  // fp32: flag-in-data ("LL") exchange buffers, each word = (step tag << 32) | value bits,
+  // double buffered by local step parity; they replace the per-tile flags and counters
+  unsigned long long *lezL, *lezB, *lhyR, *lhxT;   // halos [2][nT][TY] / [2][nT][TX]
+  unsigned long long *lG, *ly;                     // [2][y_size]
+  unsigned long long *leb, *lhb;                   // [2][e_size] / [2][h_size]
+  int64_t ysz, esz, hsz;
 };
+
+// LL words: a 64-bit relaxed store/load is single-copy atomic, so a reader that
+// sees the expected tag also sees the value stored with it; no fence, no flag
+__device__ __forceinline__ void ll_st(unsigned long long* p, float v, unsigned tag) {
+  const unsigned long long w = ((unsigned long long)tag << 32) | (unsigned long long)__float_as_uint(v);
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;\n" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ unsigned long long ll_raw(const unsigned long long* p) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+// spin until the word carries `tag`; false on abort / timeout (~1 s of SM clock)
+__device__ __forceinline__ bool ll_ld(const unsigned long long* p, unsigned tag, float& v, int* abort_flag) {
+  unsigned long long w = ll_raw(p);
+  if ((unsigned)(w >> 32) != tag) {
+    const long long t0 = clock64();
+    unsigned it = 0;
+    do {
+      w = ll_raw(p);
+      if ((++it & 63u) == 0) {
+        if (*reinterpret_cast<volatile int*>(abort_flag)) return false;
+        if (clock64() - t0 > 2000000000LL) { atomicExch(abort_flag, 1); return false; }
+      }
+    } while ((unsigned)(w >> 32) != tag);
+  }
+  v = __uint_as_float((unsigned)w);
+  return true;
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -232,6 +267,35 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
     }
     // (b) wait for the left / bottom H halos (and, on interface tiles, for the
     //     reduced update of the previous step), then fetch halos and y together
+    constexpr bool LL = sizeof(T) == 4;
+    // tags: local step + 1 (the LL buffers are zeroed before every launch, so 0 never matches)
+    const unsigned tag_prev = (unsigned)ls, tag_cur = (unsigned)(ls + 1);
+    if (LL && ls > 0) {
+      // fp32: every fetching thread polls its own tagged words (no flags)
+      const int hb_ = (ls - 1) & 1;
+      bool ok = true;
+      for (int jl = tid; jl < TY && ok; jl += nthr) {
+        float v = 0.f;
+        if (left >= 0) ok = ll_ld(P.lhyR + ((int64_t)hb_ * nT + left) * TY + jl, tag_prev, v, P.abort_flag);
+        hL[jl] = (T)v;
+      }
+      for (int il = tid; il < TX && ok; il += nthr) {
+        float v = 0.f;
+        if (bottom >= 0) ok = ll_ld(P.lhxT + ((int64_t)hb_ * nT + bottom) * TX + il, tag_prev, v, P.abort_flag);
+        hB[il] = (T)v;
+      }
+      for (int r = tid; r < rows_hi - rows_lo && ok; r += nthr) {
+        const int64_t yo = rs[r].yo;
+        const int sc = rs[r].src;
+        float v = 0.f;
+        if (yo >= 0) ok = ll_ld(P.ly + (int64_t)hb_ * P.ysz + yo, tag_prev, v, P.abort_flag);
+        yv[r] = (T)v;
+        if (sc >= 0) yv[P.maxrows + r] = (step < P.R.n_wave) ? P.R.wave[step * P.R.n_cols + sc] : (T)0;
+      }
+      if (!ok) s_abort = 1;
+      __syncthreads();
+      if (s_abort) break;
+    } else {
     if (ls > 0) {
       if (tid == 0) {
         bool ok = true;
@@ -265,6 +329,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
         if (sc >= 0) yv[P.maxrows + r] = (step < P.R.n_wave) ? P.R.wave[step * P.R.n_cols + sc] : (T)0;
       }
     }
+    }
     __syncthreads();
     // (c) first column and first row
     for (int q = tid; q < TX + TY - 1; q += nthr) {
@@ -291,9 +356,18 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       T e = sEz[c] - x.c.apply(acc);
       if (x.src >= 0 && step < P.R.n_wave) e -= x.cs * yv[P.maxrows + r];
       sEz[c] = e;
-      if (x.yo >= 0) __stcg(P.G + x.yo, e);
+      if (x.yo >= 0) {
+        if constexpr (LL) ll_st(P.lG + (int64_t)(ls & 1) * P.ysz + x.yo, (float)e, tag_cur);
+        else __stcg(P.G + x.yo, e);
+      }
     }
     __syncthreads();
+    if constexpr (LL) {
+      const int eb_ = ls & 1;
+      for (int jl = tid; jl < TY; jl += nthr) ll_st(P.lezL + ((int64_t)eb_ * nT + t) * TY + jl, (float)sEz[jl * TX], tag_cur);
+      for (int il = tid; il < TX; il += nthr) ll_st(P.lezB + ((int64_t)eb_ * nT + t) * TX + il, (float)sEz[il], tag_cur);
+      if (dslot >= 0) P2_STAMP(dslot, 2);
+    } else {
     {
       const int eb_ = ls & 1;
       for (int jl = tid; jl < TY; jl += nthr) __stcg(P.ezL + ((int64_t)eb_ * nT + t) * TY + jl, sEz[jl * TX]);
@@ -305,6 +379,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       __threadfence();
       st_release_u32(P.fE + t, (unsigned)(ls + 1));
       if (has_if) atomicAdd(P.gready, 1u);
+    }
     }
     // ------------------------------------------------------------- H phase
     auto h_cell = [&](int il, int jl) {
@@ -331,6 +406,24 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       }
     }
     // (b) right / top E halos
+    if constexpr (LL) {
+      const int eb_ = ls & 1;
+      bool ok = true;
+      for (int jl = tid; jl < TY && ok; jl += nthr) {
+        float v = 0.f;
+        if (right >= 0) ok = ll_ld(P.lezL + ((int64_t)eb_ * nT + right) * TY + jl, tag_cur, v, P.abort_flag);
+        eR[jl] = (T)v;
+      }
+      for (int il = tid; il < TX && ok; il += nthr) {
+        float v = 0.f;
+        if (top >= 0) ok = ll_ld(P.lezB + ((int64_t)eb_ * nT + top) * TX + il, tag_cur, v, P.abort_flag);
+        eT[il] = (T)v;
+      }
+      if (!ok) s_abort = 1;
+      __syncthreads();
+      if (s_abort) break;
+      if (dslot >= 0) P2_STAMP(dslot, 3);
+    } else {
     if (tid == 0) {
       bool ok = true;
       if (right >= 0) ok = p2_wait(P.fE + right, (unsigned)(ls + 1), P.abort_flag);
@@ -348,6 +441,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
         eT[il] = (top >= 0) ? __ldcg(P.ezB + ((int64_t)eb_ * nT + top) * TX + il) : (T)0;
     }
     __syncthreads();
+    }
     // (c) last column and last row
     for (int q = tid; q < TX + TY - 1; q += nthr) {
       const int il = q < TX ? q : TX - 1, jl = q < TX ? TY - 1 : q - TX;
@@ -358,8 +452,15 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
     __syncthreads();
     {
       const int hb_ = ls & 1;
-      for (int jl = tid; jl < TY; jl += nthr) __stcg(P.hyR + ((int64_t)hb_ * nT + t) * TY + jl, sHy[jl * TX + TX - 1]);
-      for (int il = tid; il < TX; il += nthr) __stcg(P.hxT + ((int64_t)hb_ * nT + t) * TX + il, sHx[(TY - 1) * TX + il]);
+      if constexpr (LL) {
+        for (int jl = tid; jl < TY; jl += nthr)
+          ll_st(P.lhyR + ((int64_t)hb_ * nT + t) * TY + jl, (float)sHy[jl * TX + TX - 1], tag_cur);
+        for (int il = tid; il < TX; il += nthr)
+          ll_st(P.lhxT + ((int64_t)hb_ * nT + t) * TX + il, (float)sHx[(TY - 1) * TX + il], tag_cur);
+      } else {
+        for (int jl = tid; jl < TY; jl += nthr) __stcg(P.hyR + ((int64_t)hb_ * nT + t) * TY + jl, sHy[jl * TX + TX - 1]);
+        for (int il = tid; il < TX; il += nthr) __stcg(P.hxT + ((int64_t)hb_ * nT + t) * TX + il, sHx[(TY - 1) * TX + il]);
+      }
     }
     // coarse probes owned by this tile (fields after the step)
     for (int q = pr_lo + tid; q < pr_hi; q += nthr) {
@@ -373,7 +474,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
     }
     __syncthreads();
     if (dslot >= 0) P2_STAMP(dslot, 4);
-    if (tid == 0) { __threadfence(); st_release_u32(P.fH + t, (unsigned)(ls + 1)); }
+    if (!LL && tid == 0) { __threadfence(); st_release_u32(P.fH + t, (unsigned)(ls + 1)); }
   }
   __syncthreads();
   if (!s_abort) {
@@ -424,10 +525,15 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
     const int p = (P.p0 + ls) & 1;
     const bool do_check = P.check_every > 0 && (step % P.check_every) == 0;
     if (rc == 0) P2_STAMP(2, 0);
+    constexpr bool LL = sizeof(T) == 4;
+    const unsigned tag_prev = (unsigned)ls, tag_cur = (unsigned)(ls + 1);
     // inputs e~, h~ of this step: every reduced CTA finished the previous one
-    if (tid == 0 && ls > 0 && !p2_wait(P.reddone, (unsigned)(P.n_red_ctas * ls), P.abort_flag)) s_abort = 1;
-    __syncthreads();
-    if (s_abort) break;
+    // (fp32: the tagged copies are polled word by word below)
+    if (!LL) {
+      if (tid == 0 && ls > 0 && !p2_wait(P.reddone, (unsigned)(P.n_red_ctas * ls), P.abort_flag)) s_abort = 1;
+      __syncthreads();
+      if (s_abort) break;
+    }
     int g = r_lo;
     bool waited = false;
     while (g < r_hi) {
@@ -438,6 +544,30 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
       const int qe = FB.qe, ni = FB.n_if, qh = FB.qh, C = FB.C;
       const T* e_in = P.eb[p];
       const T* h_in = P.hb[p];
+      if (LL) {
+        // e~, h~ (tagged copies of the previous step, or the plain state at ls == 0) and G, all polled
+        const int pl = (ls - 1) & 1, pc = ls & 1;
+        bool ok = true;
+        for (int c = tid; c < FB.Cp && ok; c += nthr) {
+          float v = 0.f;
+          if (c < qe) {
+            if (ls > 0) ok = ll_ld(P.leb + (int64_t)pl * P.esz + FB.e_off + c, tag_prev, v, P.abort_flag);
+            else v = (float)__ldcg(e_in + FB.e_off + c);
+          } else if (c < qe + ni) {
+            ok = ll_ld(P.lG + (int64_t)pc * P.ysz + FB.y_off + (c - qe), tag_cur, v, P.abort_flag);
+          } else if (c < C) {
+            if (ls > 0) ok = ll_ld(P.lhb + (int64_t)pl * P.hsz + FB.h_off + (c - qe - ni), tag_prev, v, P.abort_flag);
+            else v = (float)__ldcg(h_in + FB.h_off + (c - qe - ni));
+          }
+          Xs[c] = (T)v;
+        }
+        if (!ok) s_abort = 1;
+        if (!waited && rc == 0) P2_STAMP(2, 1);
+        __syncthreads();
+        if (s_abort) break;
+        if (!waited && rc == 0) P2_STAMP(2, 2);
+        waited = true;
+      } else {
       for (int c = tid; c < FB.Cp; c += nthr) {
         if (c >= qe && c < qe + ni) continue;
         T v = 0;
@@ -455,6 +585,7 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
       }
       for (int c = qe + tid; c < qe + ni; c += nthr) Xs[c] = __ldcg(P.G + FB.y_off + (c - qe));
       __syncthreads();
+      }
       const int warp = tid >> 5, nw = nthr >> 5;
       for (int gg = g + warp; gg < g_end; gg += nw) {
         const int r = gg - P.row0[b];
@@ -466,9 +597,17 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lx == 0) {
-          if (r < qh) __stcg(P.hb[p ^ 1] + FB.h_off + r, acc);
-          else if (r < qh + ni) __stcg(P.y + FB.y_off + (r - qh), acc);
-          else if (r < qh + ni + qe) __stcg(P.eb[p ^ 1] + FB.e_off + (r - qh - ni), acc);
+          const int pc = ls & 1;
+          if (r < qh) {
+            __stcg(P.hb[p ^ 1] + FB.h_off + r, acc);
+            if constexpr (LL) ll_st(P.lhb + (int64_t)pc * P.hsz + FB.h_off + r, (float)acc, tag_cur);
+          } else if (r < qh + ni) {
+            __stcg(P.y + FB.y_off + (r - qh), acc);
+            if constexpr (LL) ll_st(P.ly + (int64_t)pc * P.ysz + FB.y_off + (r - qh), (float)acc, tag_cur);
+          } else if (r < qh + ni + qe) {
+            __stcg(P.eb[p ^ 1] + FB.e_off + (r - qh - ni), acc);
+            if constexpr (LL) ll_st(P.leb + (int64_t)pc * P.esz + FB.e_off + (r - qh - ni), (float)acc, tag_cur);
+          }
           else {
             const int q = r - qh - ni - qe;
             P.ring[(step % P.cap) * (int64_t)P.n_probe + FB.probe_id[q]] = acc;
@@ -481,7 +620,7 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
     }
     if (s_abort) break;
     if (rc == 0) P2_STAMP(2, 3);
-    if (tid == 0) { __threadfence(); atomicAdd(P.reddone, 1u); }
+    if (!LL && tid == 0) { __threadfence(); atomicAdd(P.reddone, 1u); }
   }
   if (first_bad >= 0) atomicMin(P.bad_step, (unsigned long long)first_bad);
 }

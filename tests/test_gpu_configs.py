@@ -302,3 +302,62 @@ def test_tiny4_batch8_leapfrog_skinny_gemm(skinny, monkeypatch):
         ora = run_oracle(prob, 300, member=m)
         es, ep, _ = compare(prob, gpu, ora, member=m)
         assert es <= 1e-4 and ep <= 1e-4, (m, es, ep)
+
+
+@pytest.mark.parametrize("case,prec,tile,grid", [
+    ("config3_small", 32, "2,4", 0), ("config3_small", 32, "2,6", 7), ("config3_small", 32, "4,3", 0),
+    ("config3_small", 64, "2,3", 5), ("config3_small", 64, "1,6", 0),
+    ("tiny5", 32, "2,6", 0), ("tiny5", 32, "2,4", 13), ("tiny5", 64, "2,3", 0), ("tiny5", 32, "4,3", 3),
+    ("tiny4_b16", 32, "4,3", 0), ("tiny4_b16", 32, "4,3", 11), ("tiny4_b16", 64, "2,3", 0),
+])
+def test_tile_stencil_bitwise_equals_tma_stencil(case, prec, tile, grid, monkeypatch):
+    # the tile stencil (stencil3d.cuh: persistent CTAs on balanced ranges of
+    # column-planes, W elements per thread, NS-stage ring across segment
+    # boundaries, mask multipliers, z-wall fix-ups) against the reference TMA
+    # stencils (stencil3d_tma_kernel / stencil3d_tma_vec_kernel), from random
+    # states on the unknowns incl. interface / source rows: bit for bit, 7
+    # steps; small grids make ranges start and end mid-column
+    from paper_1406_7042_b200.fdtd import Sim
+    from sampled_state import random_state
+    if case == "tiny4_b16":
+        scn, prob = _prep("tiny4", precision=prec)
+        w = np.asarray(prob["sources"]["wave"])
+        amp = np.linspace(1.0, -1.3, 16)
+        prob = dict(prob, sources=dict(prob["sources"], wave=w[:, :, :1] * amp[None, None, :]), batch=16)
+    else:
+        scn, prob = _prep(case, precision=prec)
+    prob = dict(prob, init={})
+    if "mat_coef" in prob:
+        arrays, _, _ = random_state(prob, seed=5)
+    else:
+        # uniform problem: random values everywhere (fdtd_set_state stores the
+        # E entries that are not unknowns as 0; H keeps them, both kernels alike)
+        nx, ny, nz = prob["n"]
+        S = (nx + 1) * (ny + 1) * (nz + 1)
+        rng = np.random.default_rng(5)
+        arrays = {c: rng.uniform(-1, 1, (int(prob.get("batch", 1)), S)) for c in range(6)}
+    monkeypatch.setenv("FDTD_KCHUNK", "9")
+
+    def run(old):
+        if old:
+            monkeypatch.setenv("FDTD_STENCIL_OLD", "1")
+            monkeypatch.delenv("FDTD_TILE", raising=False)
+        else:
+            monkeypatch.delenv("FDTD_STENCIL_OLD", raising=False)
+            monkeypatch.setenv("FDTD_TILE", tile)
+            if grid:
+                monkeypatch.setenv("FDTD_TILE_GRID", str(grid))
+        sim = Sim(prob, precision=prec, graph_steps=0)
+        paths = sim.path()
+        for c in range(6):
+            sim.set_state(c, arrays[c])
+        sim.step(7)
+        sim.sync()
+        out = [sim.get_state(c) for c in range(8)]
+        sim.close()
+        return out, paths
+
+    (a, pa), (b, pb) = run(True), run(False)
+    assert "tile3d" in pb and "tile3d" not in pa, (pa, pb)
+    for c in range(8):
+        assert np.array_equal(a[c], b[c]), c
