@@ -437,7 +437,11 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     {
       fdtd::TileCfg c;
       c.BY = 8;
-      if (B == 1) { c.MB = 0; c.W = 2; c.NS = sizeof(T) == 4 ? 6 : 3; }
+      if (B == 1) {
+        c.MB = 0; c.W = 2; c.NS = sizeof(T) == 4 ? 6 : 3;
+        // short z extent: 32-cell tiles give more columns (items) than 64-cell ones
+        if (sizeof(T) == 4 && nz + 1 < 64) c.W = 1;
+      }
       else { c.MB = B; c.W = kW; c.NS = 3; }
       if (const char* e = getenv("FDTD_TILE")) sscanf(e, "%d,%d", &c.W, &c.NS);
       const int64_t span = (int64_t)px * B * (ny + 1) * (nz + 1) + (int64_t)px * B + 64;
@@ -875,25 +879,23 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     const int per_sm = std::max(1, fdtd::tile_blocks_per_sm<T>(tcfg, uniform, tile_smem));
     int G = per_sm * sms;
     if (const char* e = getenv("FDTD_TILE_GRID")) G = std::max(1, atoi(e));
-    // z-chunking: minimise the planes of the busiest CTA slot, counting the
-    // two extra planes (lead H plane, trailing plane) each item loads
+    // z-chunking (one item per CTA, hardware scheduling; measured on B200,
+    // DESIGN.md §5.3): chunks of at most 24 planes (fp32, batch 1) or 8 (fp64,
+    // batched) and at least 4 items per resident CTA slot, but not below 8
+    // planes (each item loads 1-2 extra planes)
     {
       const int nzp = nz + 1;
-      double best = 1e300;
-      int best_kc = nzp;
-      for (int nch = 1; nch <= nzp; ++nch) {
-        const int kc = (nzp + nch - 1) / nch;
-        if (kc < 4 && nch > 1) break;
-        const int nch_eff = (nzp + kc - 1) / kc;
-        const int64_t items = (int64_t)tsplit.ncols * nch_eff;
-        const int64_t rounds = (items + G - 1) / G;
-        const double cost = (double)rounds * (kc + (nch_eff > 1 ? 2 : 1));
-        if (cost < best * 0.999) { best = cost; best_kc = kc; }
-      }
-      if (const char* e = getenv("FDTD_TILE_KC")) best_kc = std::max(1, atoi(e));
-      tsplit.kc = best_kc;
-      tsplit.nitems = tsplit.ncols * ((nzp + best_kc - 1) / best_kc);
+      const int kmax = (sizeof(T) == 4 && B == 1) ? 24 : 8;
+      int nch = std::max((nzp + kmax - 1) / kmax, (int)((4LL * G + tsplit.ncols - 1) / tsplit.ncols));
+      nch = std::max(1, std::min(nch, nzp / 8));
+      int kc = (nzp + nch - 1) / nch;
+      if (const char* e = getenv("FDTD_TILE_KC")) kc = std::max(1, atoi(e));
+      tsplit.kc = kc;
+      tsplit.nitems = tsplit.ncols * ((nzp + kc - 1) / kc);
     }
+    // persistent (round-robin items over resident CTAs) only on request:
+    // measured slower than one CTA per item
+    if (!getenv("FDTD_TILE_GRID")) G = tsplit.nitems;
     tile_grid = std::min(tsplit.nitems, G);
     if (getenv("FDTD_VERBOSE"))
       fprintf(stderr, "fdtd: tile stencil W=%d NS=%d MB=%d smem=%zu per_sm=%d grid=%d items=%d (cols %d x kc %d)\n",

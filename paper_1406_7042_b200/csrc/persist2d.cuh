@@ -271,20 +271,24 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
     // tags: local step + 1 (the LL buffers are zeroed before every launch, so 0 never matches)
     const unsigned tag_prev = (unsigned)ls, tag_cur = (unsigned)(ls + 1);
     if (LL && ls > 0) {
-      // fp32: every fetching thread polls its own tagged words (no flags)
+      // fp32: every fetching thread polls its own tagged words (no flags); the
+      // left halo, the bottom halo and the y values go to disjoint threads so
+      // all polls are in flight at once
       const int hb_ = (ls - 1) & 1;
       bool ok = true;
-      for (int jl = tid; jl < TY && ok; jl += nthr) {
+      for (int q = tid; q < TY + TX && ok; q += nthr) {
         float v = 0.f;
-        if (left >= 0) ok = ll_ld(P.lhyR + ((int64_t)hb_ * nT + left) * TY + jl, tag_prev, v, P.abort_flag);
-        hL[jl] = (T)v;
+        if (q < TY) {
+          if (left >= 0) ok = ll_ld(P.lhyR + ((int64_t)hb_ * nT + left) * TY + q, tag_prev, v, P.abort_flag);
+          hL[q] = (T)v;
+        } else {
+          if (bottom >= 0) ok = ll_ld(P.lhxT + ((int64_t)hb_ * nT + bottom) * TX + (q - TY), tag_prev, v, P.abort_flag);
+          hB[q - TY] = (T)v;
+        }
       }
-      for (int il = tid; il < TX && ok; il += nthr) {
-        float v = 0.f;
-        if (bottom >= 0) ok = ll_ld(P.lhxT + ((int64_t)hb_ * nT + bottom) * TX + il, tag_prev, v, P.abort_flag);
-        hB[il] = (T)v;
-      }
-      for (int r = tid; r < rows_hi - rows_lo && ok; r += nthr) {
+      const int nrw = rows_hi - rows_lo;
+      const int r0 = (nthr - TY - TX) > 0 ? (TY + TX) : 0;   // y polls on the threads after the halo ones
+      for (int r = (tid - r0 + nthr) % nthr; r < nrw && ok; r += nthr) {
         const int64_t yo = rs[r].yo;
         const int sc = rs[r].src;
         float v = 0.f;
@@ -409,15 +413,15 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
     if constexpr (LL) {
       const int eb_ = ls & 1;
       bool ok = true;
-      for (int jl = tid; jl < TY && ok; jl += nthr) {
+      for (int q = tid; q < TY + TX && ok; q += nthr) {
         float v = 0.f;
-        if (right >= 0) ok = ll_ld(P.lezL + ((int64_t)eb_ * nT + right) * TY + jl, tag_cur, v, P.abort_flag);
-        eR[jl] = (T)v;
-      }
-      for (int il = tid; il < TX && ok; il += nthr) {
-        float v = 0.f;
-        if (top >= 0) ok = ll_ld(P.lezB + ((int64_t)eb_ * nT + top) * TX + il, tag_cur, v, P.abort_flag);
-        eT[il] = (T)v;
+        if (q < TY) {
+          if (right >= 0) ok = ll_ld(P.lezL + ((int64_t)eb_ * nT + right) * TY + q, tag_cur, v, P.abort_flag);
+          eR[q] = (T)v;
+        } else {
+          if (top >= 0) ok = ll_ld(P.lezB + ((int64_t)eb_ * nT + top) * TX + (q - TY), tag_cur, v, P.abort_flag);
+          eT[q - TY] = (T)v;
+        }
       }
       if (!ok) s_abort = 1;
       __syncthreads();

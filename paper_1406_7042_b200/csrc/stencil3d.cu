@@ -22,6 +22,7 @@ bool tile_dispatch(const TileCfg& c, F&& f) {
     if (c.MB == 0 && c.W == 2 && c.NS == 4) { f(TileKernels<T, 4, 2, 0, 3>{}); return true; }
     if (c.MB == 0 && c.W == 2 && c.NS == 6) { f(TileKernels<T, 6, 2, 0, 2>{}); return true; }
     if (c.MB == 0 && c.W == 4 && c.NS == 3) { f(TileKernels<T, 3, 4, 0, 2>{}); return true; }
+    if (c.MB == 0 && c.W == 1 && c.NS == 6) { f(TileKernels<T, 6, 1, 0, 3>{}); return true; }
     if (c.MB == 16 && c.W == 4 && c.NS == 3) { f(TileKernels<T, 3, 4, 16, 2>{}); return true; }
   } else {
     if (c.MB == 0 && c.W == 2 && c.NS == 3) { f(TileKernels<T, 3, 2, 0, 2>{}); return true; }
