@@ -1027,7 +1027,7 @@ int Impl<T>::setup_persist() {
       nr = std::min(capacity - nt, std::max(1, (Rtot + 7) / 8));
       if (nr < 1) continue;
       r = (Rtot + nr - 1) / nr;
-      sm = std::max(tile_sm, sizeof(T) * (size_t)(1 + r) * Cmax + 64);
+      sm = std::max(tile_sm, sizeof(T) * ((size_t)(1 + r) * Cmax + (size_t)r * 32) + 64);
       if (sm > 220 * 1024) continue;
       CK(cudaFuncSetAttribute(fdtd::persist2d_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdtd::persist2d_kernel<T>, 512, sm));
@@ -1321,8 +1321,12 @@ int Impl<T>::build_fused(const fdtd_probes* probes) {
     const int Cp = (CM + PADC - 1) / PADC * PADC;
     const int RMp = (RM + ROWS - 1) / ROWS * ROWS;      // zero rows up to a whole tile
     std::vector<T> Mt((size_t)RMp * Cp, (T)0);
+    // device column order [e~ ; h~ ; G] (composition above in [e~ ; G ; h~]):
+    // the G columns last, so a consumer can contract the e~, h~ part before
+    // G arrives (persist2d.cuh) in the same per-lane order as one pass
+    auto dcol = [&](int c) { return c < qe ? c : (c < qe + ni ? qe + qh + (c - qe) : qe + (c - qe - ni)); };
     for (int r = 0; r < RM; ++r)
-      for (int c = 0; c < CM; ++c) Mt[(size_t)r * Cp + c] = (T)M[(size_t)r * CM + c];
+      for (int c = 0; c < CM; ++c) Mt[(size_t)r * Cp + dcol(c)] = (T)M[(size_t)r * CM + c];
     D.M_d = dalloc<T>(Mt.size());
     if (!D.M_d || upload(D.M_d, Mt)) return fail(FDTD_ENOMEM, "fused matrix allocation failed");
     D.R_M = RM; D.C_M = CM;

@@ -771,7 +771,7 @@ stencil3d_tma_vec_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int
 // ---------------------------------------------------------------------------
 // reduced blocks.  Small blocks ("fused", see fdtd_api.cu): one GEMV with the
 // precomposed update matrix M per step,
-//   [h~' ; y' ; e~'' ; probe rows] = M [e~ ; G ; h~],
+//   [h~' ; y' ; e~'' ; probe rows] = M [e~ ; h~ ; G] (G columns last),
 // spread over many CTAs (16 rows each); every CTA stages the input vector in
 // shared memory ([N][C] so that lanes read consecutive columns).
 // ---------------------------------------------------------------------------
@@ -914,10 +914,10 @@ reduced_fused_kernel(const __grid_constant__ FusedParams<T> P) {
     const int2 ct = fused_tile(P, (int)blockIdx.x);
     const FusedBlock<T>& FB = P.fb[ct.x];
     const int C = FB.C, Cp = FB.Cp, N = FB.N, qe = FB.qe, qh = FB.qh, ni = FB.n_if;
-    // stage X = [e~ ; G ; h~ ; 0-padding] as [N][Cp]
+    // stage X = [e~ ; h~ ; G ; 0-padding] as [N][Cp]
     for (int t = threadIdx.x; t < qe * N; t += blockDim.x) X[(t % N) * Cp + t / N] = P.e_in[FB.e_off + t];
-    for (int t = threadIdx.x; t < ni * N; t += blockDim.x) X[(t % N) * Cp + qe + t / N] = P.G[FB.y_off + t];
-    for (int t = threadIdx.x; t < qh * N; t += blockDim.x) X[(t % N) * Cp + qe + ni + t / N] = P.h_in[FB.h_off + t];
+    for (int t = threadIdx.x; t < qh * N; t += blockDim.x) X[(t % N) * Cp + qe + t / N] = P.h_in[FB.h_off + t];
+    for (int t = threadIdx.x; t < ni * N; t += blockDim.x) X[(t % N) * Cp + qe + qh + t / N] = P.G[FB.y_off + t];
     for (int t = threadIdx.x; t < (Cp - C) * N; t += blockDim.x) X[(t % N) * Cp + C + t / N] = (T)0;
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
@@ -965,7 +965,7 @@ reduced_fused_kernel(const __grid_constant__ FusedParams<T> P) {
 
 // ---------------------------------------------------------------------------
 // Batched reduced blocks (N = instances x batch >= 4 columns): the same fused
-// update [h~' ; y' ; e~'' ; probe rows] = M [e~ ; G ; h~] as a register-tiled
+// update [h~' ; y' ; e~'' ; probe rows] = M [e~ ; h~ ; G] as a register-tiled
 // SIMT GEMM.  A cluster of KS CTAs shares one tile of TR rows: CTA `rank`
 // contracts the K-slice [rank*Cp/KS, (rank+1)*Cp/KS) -- its slice of X staged
 // in shared memory as [k][NP] (the natural [q][N] layout of the states: a
@@ -983,7 +983,7 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
   constexpr int TR = 8 * GPW * RPW;            // rows per tile
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Ps = reinterpret_cast<T*>(smem_raw);      // [TR][NP] partial tile
-  T* Xs = Ps + TR * NP;                        // [kc][NP] slice of [e~ ; G ; h~]
+  T* Xs = Ps + TR * NP;                        // [kc][NP] slice of [e~ ; h~ ; G]
   const int64_t step = *P.d_step;
   const bool check = P.check_every > 0 && (step % P.check_every) == 0;
   bool bad = false;
@@ -996,7 +996,7 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
   if (active) {
     ct = fused_tile(P, tile);
     const FusedBlock<T>& FB = P.fb[ct.x];
-    const int N = FB.N, C = FB.C, qe = FB.qe, ni = FB.n_if;
+    const int N = FB.N, C = FB.C, qe = FB.qe, qh = FB.qh;
     const int kc = FB.Cp / KS, k_lo = (int)rank * kc;
     T* Ms = Xs + kc * NP;                      // [TR][kc + VN] slice of M (padded pitch)
     const int mp = kc + VN;
@@ -1011,8 +1011,8 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
         const int kk = t / (NP / VN), n = (t % (NP / VN)) * VN, k = k_lo + kk;
         const T* src = P.e_in;                 // any valid address when zero-filled
         if (k < qe) src = P.e_in + FB.e_off + (int64_t)k * N + n;
-        else if (k < qe + ni) src = P.G + FB.y_off + (int64_t)(k - qe) * N + n;
-        else if (k < C) src = P.h_in + FB.h_off + (int64_t)(k - qe - ni) * N + n;
+        else if (k < qe + qh) src = P.h_in + FB.h_off + (int64_t)(k - qe) * N + n;
+        else if (k < C) src = P.G + FB.y_off + (int64_t)(k - qe - qh) * N + n;
         cp_async16(Xs + kk * NP + n, src, k < C);
       }
     } else {
@@ -1024,8 +1024,8 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
           v[w] = 0;
           if (t < kc * NP && n < N && k < C) {
             if (k < qe) v[w] = P.e_in[FB.e_off + (int64_t)k * N + n];
-            else if (k < qe + ni) v[w] = P.G[FB.y_off + (int64_t)(k - qe) * N + n];
-            else v[w] = P.h_in[FB.h_off + (int64_t)(k - qe - ni) * N + n];
+            else if (k < qe + qh) v[w] = P.h_in[FB.h_off + (int64_t)(k - qe) * N + n];
+            else v[w] = P.G[FB.y_off + (int64_t)(k - qe - qh) * N + n];
           }
         }
 #pragma unroll

@@ -16,7 +16,7 @@
 //            the neighbours' published E halos of step n.
 //   reduced  every CTA keeps a few rows of the fused update matrix M
 //            resident in shared memory and computes them once all interface
-//            tiles published G: [h~' ; y' ; e~'' ; probe rows] = M [e~ ; G ; h~].
+//            tiles published G: [h~' ; y' ; e~'' ; probe rows] = M [e~ ; h~ ; G].
 //
 // Synchronisation is point to point through monotonic per-tile flags (fE, fH:
 // phases completed) and two counters (gready: interface tiles that published
@@ -513,6 +513,7 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
   const int rc = blockIdx.x - P.ntx * P.nty;
   T* Xs = reinterpret_cast<T*>(smem_raw);       // [Cmax]
   T* Ms = Xs + P.Cmax;                          // [rpc][Cmax]
+  T* Ps = Ms + (size_t)P.rpc * P.Cmax;          // [rpc][32] per-lane partial sums
   const int tid = threadIdx.x, nthr = blockDim.x, lx = tid & 31;
   const int r_lo = min(rc * P.rpc, P.Rtot), r_hi = min(r_lo + P.rpc, P.Rtot);
   for (int g = r_lo; g < r_hi; ++g) {
@@ -548,56 +549,72 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
       const int qe = FB.qe, ni = FB.n_if, qh = FB.qh, C = FB.C;
       const T* e_in = P.eb[p];
       const T* h_in = P.hb[p];
-      if (LL) {
-        // e~, h~ (tagged copies of the previous step, or the plain state at ls == 0) and G, all polled
-        const int pl = (ls - 1) & 1, pc = ls & 1;
+      const int nv = FB.Cp / VN;
+      const int nv_eh = (qe + qh) / VN;            // vectors wholly in the e~, h~ columns
+      const int warp = tid >> 5, nw = nthr >> 5;
+      // (1) e~, h~ (+ zero padding): the previous reduced step's outputs (fp32:
+      //     tagged copies, or the plain state at ls == 0); no wait on G
+      {
+        const int pl = (ls - 1) & 1;
         bool ok = true;
         for (int c = tid; c < FB.Cp && ok; c += nthr) {
+          if (c >= qe + qh && c < C) continue;
           float v = 0.f;
+          T tv = 0;
           if (c < qe) {
-            if (ls > 0) ok = ll_ld(P.leb + (int64_t)pl * P.esz + FB.e_off + c, tag_prev, v, P.abort_flag);
-            else v = (float)__ldcg(e_in + FB.e_off + c);
-          } else if (c < qe + ni) {
-            ok = ll_ld(P.lG + (int64_t)pc * P.ysz + FB.y_off + (c - qe), tag_cur, v, P.abort_flag);
-          } else if (c < C) {
-            if (ls > 0) ok = ll_ld(P.lhb + (int64_t)pl * P.hsz + FB.h_off + (c - qe - ni), tag_prev, v, P.abort_flag);
-            else v = (float)__ldcg(h_in + FB.h_off + (c - qe - ni));
+            if (LL && ls > 0) ok = ll_ld(P.leb + (int64_t)pl * P.esz + FB.e_off + c, tag_prev, v, P.abort_flag), tv = (T)v;
+            else tv = __ldcg(e_in + FB.e_off + c);
+          } else if (c < qe + qh) {
+            if (LL && ls > 0) ok = ll_ld(P.lhb + (int64_t)pl * P.hsz + FB.h_off + (c - qe), tag_prev, v, P.abort_flag), tv = (T)v;
+            else tv = __ldcg(h_in + FB.h_off + (c - qe));
           }
+          Xs[c] = tv;
+        }
+        if (!ok) s_abort = 1;
+      }
+      __syncthreads();
+      if (s_abort) break;
+      // (2) the e~, h~ part of every row: per-lane partial sums in the same
+      //     order as one pass over all columns (the G columns are last)
+      for (int gg = g + warp; gg < g_end; gg += nw) {
+        const V* a = reinterpret_cast<const V*>(Ms + (gg - r_lo) * P.Cmax);
+        T acc = 0;
+        for (int cc = lx; cc < nv_eh; cc += 32) acc += vdot<T>(a[cc], reinterpret_cast<const V*>(Xs)[cc]);
+        Ps[(gg - r_lo) * 32 + lx] = acc;
+      }
+      if (!waited && rc == 0) P2_STAMP(2, 1);
+      // (3) G of this step
+      if (LL) {
+        const int pc = ls & 1;
+        bool ok = true;
+        for (int c = qe + qh + tid; c < C && ok; c += nthr) {
+          float v = 0.f;
+          ok = ll_ld(P.lG + (int64_t)pc * P.ysz + FB.y_off + (c - qe - qh), tag_cur, v, P.abort_flag);
           Xs[c] = (T)v;
         }
         if (!ok) s_abort = 1;
-        if (!waited && rc == 0) P2_STAMP(2, 1);
         __syncthreads();
         if (s_abort) break;
-        if (!waited && rc == 0) P2_STAMP(2, 2);
-        waited = true;
       } else {
-      for (int c = tid; c < FB.Cp; c += nthr) {
-        if (c >= qe && c < qe + ni) continue;
-        T v = 0;
-        if (c < qe) v = __ldcg(e_in + FB.e_off + c);
-        else if (c < C) v = __ldcg(h_in + FB.h_off + (c - qe - ni));
-        Xs[c] = v;
-      }
-      if (!waited) {
-        if (rc == 0) P2_STAMP(2, 1);
-        if (tid == 0 && !p2_wait(P.gready, (unsigned)(P.n_if_tiles * (ls + 1)), P.abort_flag)) s_abort = 1;
+        if (!waited) {
+          if (tid == 0 && !p2_wait(P.gready, (unsigned)(P.n_if_tiles * (ls + 1)), P.abort_flag)) s_abort = 1;
+          __syncthreads();
+          if (s_abort) break;
+        }
+        for (int c = qe + qh + tid; c < C; c += nthr) Xs[c] = __ldcg(P.G + FB.y_off + (c - qe - qh));
         __syncthreads();
-        if (s_abort) break;
-        waited = true;
-        if (rc == 0) P2_STAMP(2, 2);
       }
-      for (int c = qe + tid; c < qe + ni; c += nthr) Xs[c] = __ldcg(P.G + FB.y_off + (c - qe));
-      __syncthreads();
-      }
-      const int warp = tid >> 5, nw = nthr >> 5;
+      if (!waited && rc == 0) P2_STAMP(2, 2);
+      waited = true;
+      // (4) the rest of every row, reduction, outputs
       for (int gg = g + warp; gg < g_end; gg += nw) {
         const int r = gg - P.row0[b];
         const V* a = reinterpret_cast<const V*>(Ms + (gg - r_lo) * P.Cmax);
-        T acc = 0;
-        const int nv = FB.Cp / VN;
-#pragma unroll 8
-        for (int cc = lx; cc < nv; cc += 32) acc += vdot<T>(a[cc], reinterpret_cast<const V*>(Xs)[cc]);
+        T acc = Ps[(gg - r_lo) * 32 + lx];
+        int cc0 = lx;
+        while (cc0 < nv_eh) cc0 += 32;
+#pragma unroll 4
+        for (int cc = cc0; cc < nv; cc += 32) acc += vdot<T>(a[cc], reinterpret_cast<const V*>(Xs)[cc]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lx == 0) {

@@ -223,14 +223,19 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
     }
     // element offset of plane kk (E) in the output arrays; H(kk-1) is at oe - sz
     uint32_t oe = (uint32_t)((int64_t)a * sz + colo);
-    uint32_t m_next = 0, m_cur = 0, m_prev = 0;  // material ids (XV: W bytes packed)
+    // material ids (XV: W bytes packed), loaded 3 planes ahead of use
+    uint32_t m_n1 = 0, m_n2 = 0, m_n3 = 0, m_cur = 0, m_prev = 0;
     auto load_mat = [&](int k) -> uint32_t {
       const uint8_t* p = mat_id + (int64_t)k * d.plane + scol;
       if constexpr (XV && W == 4) return *reinterpret_cast<const uint32_t*>(p);
       else if constexpr (XV && W == 2) return *reinterpret_cast<const uint16_t*>(p);
       else return (uint32_t)__ldg(p);
     };
-    if (!UNIFORM) m_next = load_mat(a);
+    if (!UNIFORM) {
+      m_n1 = load_mat(a);
+      if (a + 1 <= kl) m_n2 = load_mat(a + 1);
+      if (a + 2 <= kl) m_n3 = load_mat(a + 2);
+    }
     for (int kk = a; kk <= kl; ++kk) {
       mbar_wait(&bars[st], phase);
       const T* h = Ring + st * STG + hoff;
@@ -249,8 +254,8 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
       }
       const L ex0 = IO::ld(e + 0 * EP), ey0 = IO::ld(e + 1 * EP), ez0 = IO::ld(e + 2 * EP);
       if (!UNIFORM) {
-        m_prev = m_cur; m_cur = m_next;
-        if (kk + 1 <= kl) m_next = load_mat(kk + 1);
+        m_prev = m_cur; m_cur = m_n1; m_n1 = m_n2; m_n2 = m_n3;
+        if (kk + 3 <= kl) m_n3 = load_mat(kk + 3);
       }
       L ex, ey, ez;
       uint8_t ifm_any = 0;
