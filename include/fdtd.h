@@ -195,9 +195,11 @@ int64_t fdtd_launch_count(const fdtd_t* h);
  *   4  cluster-split GEMM kernel for fused reduced blocks (else warp-per-row)
  *   8  leap-frog GEMV path for at least one large reduced block
  *  16  the 3-D tile stencil (W elements per thread, NS-plane TMA ring; with bit 2)
+ *  32  tensor-core (tcgen05, 3xTF32) GEMM for y = S_E h~ of a batched leap-frog block
  * Environment overrides (testing): FDTD_PERSIST=0, FDTD_NO_TMA,
  * FDTD_FUSED=gemv|gemm, FDTD_KCHUNK=<planes>, FDTD_STENCIL_OLD=1 (the
- * reference TMA stencils instead of the tile stencil), FDTD_TILE=<W>,<NS>. */
+ * reference TMA stencils instead of the tile stencil), FDTD_TILE=<W>,<NS>, FDTD_NO_TC=1
+ * (SIMT GEMM instead of the tensor-core one). */
 int32_t fdtd_path(const fdtd_t* h);
 
 /* Per-phase tracing.  fdtd_profile(h, 1) resets the accumulators and makes the

@@ -12,7 +12,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libfdtd.so")
 OBJDIR = os.path.join(HERE, "csrc", "obj")
 SOURCES = ["fdtd_api.cu", "stencil3d.cu"]
-HEADERS = ["kernels.cuh", "persist2d.cuh", "stencil3d.cuh", "stencil3d_launch.h",
+HEADERS = ["kernels.cuh", "persist2d.cuh", "stencil3d.cuh", "stencil3d_launch.h", "tc_gemm.cuh",
            os.path.join("..", "..", "include", "fdtd.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

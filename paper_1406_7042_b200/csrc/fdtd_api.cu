@@ -12,6 +12,7 @@
 #include "kernels.cuh"
 #include "persist2d.cuh"
 #include "stencil3d_launch.h"
+#include "tc_gemm.cuh"
 
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -118,6 +119,8 @@ struct BlockDev {
   T *K_d = nullptr, *KT_d = nullptr, *SE_d = nullptr, *SET_d = nullptr, *ge_d = nullptr, *gh_d = nullptr;
   T *Kp_d = nullptr, *KTp_d = nullptr, *SEp_d = nullptr, *Tv_d = nullptr;
   T* part_d = nullptr;                         // [splits][qh][N] S_E^T G partial sums (fp32 GEMM path)
+  bool tc = false;                             // y = S_E h~ on the tensor cores (tc_gemm.cuh, 3xTF32, N = 16)
+  CUtensorMap se_map;                          // TMA map of SEp_d: [n_if][Kph] fp32, 32 x 128 boxes, 128-byte swizzle
   int splits = 0;                              // > 0: tall-skinny fp32 GEMM kernels for the S_E products
   int Kph = 0, Kpe = 0;                        // padded row pitches (multiples of 32 * VEC)
   // state offsets (elements) in the concatenated buffers
@@ -207,6 +210,7 @@ struct Impl : public fdtd_t {
   bool use_tile = false;        // the tile stencil (stencil3d.cuh) is the 3-D path
   fdtd::TileCfg tcfg;
   fdtd::TileSplit tsplit;
+  int tc_grid = 148;            // CTAs of the tensor-core skinny GEMM (one per SM, persistent over row tiles)
   int tile_grid = 0;
   size_t tile_smem = 0;
   static constexpr int kW = 16 / (int)sizeof(T);
@@ -593,6 +597,20 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
         D.splits = std::max(1, std::min(2 * 148 / ctile, D.n_if / 64));
         D.part_d = dalloc<T>((size_t)D.splits * D.qh * D.N);
         if (!D.part_d) return fail(FDTD_ENOMEM, "block %d: partial-sum workspace allocation failed", b);
+        if (D.N == fdtd::tc::BN && !getenv("FDTD_NO_TC")) {
+          PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+          cudaDriverEntryPointQueryResult qres;
+          if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault,
+                                      &qres) == cudaSuccess && encode && qres == cudaDriverEntryPointSuccess) {
+            const cuuint64_t gdim[2] = {(cuuint64_t)D.Kph, (cuuint64_t)D.n_if};
+            const cuuint64_t gstr[1] = {(cuuint64_t)D.Kph * sizeof(float)};
+            const cuuint32_t box[2] = {(cuuint32_t)fdtd::tc::BK, (cuuint32_t)fdtd::tc::BM};
+            const cuuint32_t es[2] = {1, 1};
+            D.tc = encode(&D.se_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)D.SEp_d, gdim, gstr, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+          }
+        }
       }
     }
   }
@@ -921,6 +939,15 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       if (!D.fused && (size_t)std::max(D.Kph, D.Kpe) * D.N * sizeof(T) > (size_t)big)
         return fail(FDTD_ENOTSUP, "reduced block too large for the staged leap-frog GEMV (q x N)");
     for (auto& D : blocks) {
+      if (!D.tc) continue;
+      CK(cudaFuncSetAttribute(fdtd::tc::tc_skinny_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              fdtd::tc::SMEM_BYTES));
+      int dev = 0, sms = 148;
+      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      tc_grid = sms;
+      if (const char* e = getenv("FDTD_TC_GRID")) tc_grid = std::max(1, atoi(e));
+    }
+    for (auto& D : blocks) {
       if (!D.splits) continue;
       const int NQ = D.N / 4;
       const int sn = gemm_nn_smem(NQ, D.Kph), stn = gemm_tn_smem(NQ);
@@ -953,7 +980,10 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     int e = setup_persist();
     if (e) return e;
   }
-  path_bits = (persist ? 1 : 0) | (use_tma ? 2 : 0) | (fused_gemm ? 4 : 0) | (any_leap ? 8 : 0) | (use_tile ? 16 : 0);
+  bool any_tc = false;
+  for (auto& D : blocks) any_tc |= D.tc;
+  path_bits = (persist ? 1 : 0) | (use_tma ? 2 : 0) | (fused_gemm ? 4 : 0) | (any_leap ? 8 : 0) | (use_tile ? 16 : 0) |
+              (any_tc ? 32 : 0);
   CK(cudaStreamSynchronize(stream));
   return FDTD_OK;
 }
@@ -1227,7 +1257,7 @@ int Impl<T>::launch_persist(int64_t n, int64_t* count) {
       fprintf(stderr, "slot %d (%s):\n", sl, sl == 0 ? "tile 0" : sl == 1 ? "interface tile" : "reduced CTA 0");
       for (int st = 0; st < 8; ++st) {
         fprintf(stderr, "  step %d:", 100 + st);
-        for (int k = 0; k < 5; ++k) {
+        for (int k = 0; k < 7; ++k) {
           const unsigned long long v = h[(sl * 8 + st) * 8 + k];
           fprintf(stderr, " %8.3f", v ? (double)(v - t0) * 1e-3 : -1.0);
         }
@@ -1474,8 +1504,15 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
           fdtd::reduce_axpy_f32_kernel<<<(D.qh * D.N + 255) / 256, 256, 0, st>>>(
               D.qh, D.N, D.splits, (const float*)D.part_d, (const float*)D.Tv_d, (const float*)D.gh_d, (float*)h);
           ++n;
-          n += launch_gemm_nn(D.n_if, D.qh, D.Kph, D.N, (const float*)D.SEp_d, (const float*)h,
-                              (float*)(y_all + D.y_off), nullptr, 1.f, false, ds, check_every, d_bad, st);
+          if (D.tc) {
+            const int tiles = (D.n_if + fdtd::tc::BM - 1) / fdtd::tc::BM;
+            fdtd::tc::tc_skinny_gemm_kernel<<<std::min(tiles, tc_grid), fdtd::tc::NTHREADS, fdtd::tc::SMEM_BYTES, st>>>(
+                D.se_map, D.n_if, D.qh, (const float*)h, (float*)(y_all + D.y_off), ds, check_every, d_bad);
+            ++n;
+          } else {
+            n += launch_gemm_nn(D.n_if, D.qh, D.Kph, D.N, (const float*)D.SEp_d, (const float*)h,
+                                (float*)(y_all + D.y_off), nullptr, 1.f, false, ds, check_every, d_bad, st);
+          }
           continue;
         }
       }

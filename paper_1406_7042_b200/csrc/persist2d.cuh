@@ -265,6 +265,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
         e_cell(il, jl);
       }
     }
+    if (dslot >= 0) P2_STAMP(dslot, 5);
     // (b) wait for the left / bottom H halos (and, on interface tiles, for the
     //     reduced update of the previous step), then fetch halos and y together
     constexpr bool LL = sizeof(T) == 4;
@@ -299,6 +300,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       if (!ok) s_abort = 1;
       __syncthreads();
       if (s_abort) break;
+      if (dslot >= 0) P2_STAMP(dslot, 1);
     } else {
     if (ls > 0) {
       if (tid == 0) {
@@ -366,6 +368,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       }
     }
     __syncthreads();
+    if (dslot >= 0) P2_STAMP(dslot, 6);
     if constexpr (LL) {
       const int eb_ = ls & 1;
       for (int jl = tid; jl < TY; jl += nthr) ll_st(P.lezL + ((int64_t)eb_ * nT + t) * TY + jl, (float)sEz[jl * TX], tag_cur);

@@ -361,3 +361,26 @@ def test_tile_stencil_bitwise_equals_tma_stencil(case, prec, tile, grid, monkeyp
     assert "tile3d" in pb and "tile3d" not in pa, (pa, pb)
     for c in range(8):
         assert np.array_equal(a[c], b[c]), c
+
+
+@pytest.mark.parametrize("tc", ["on", "off"])
+def test_tiny4_batch16_leapfrog_tensor_core_gemm(tc, monkeypatch):
+    # y = S_E h~ on the tensor cores (tcgen05 kind::tf32, 3xTF32; N = 16
+    # members) against the oracle for two members over 300 steps, and "off"
+    # (SIMT GEMM) as the control
+    scn, prob = _prep("tiny4", precision=32)
+    w = np.asarray(prob["sources"]["wave"])
+    amp = np.linspace(1.0, -1.3, 16)
+    prob = dict(prob, sources=dict(prob["sources"], wave=w[:, :, :1] * amp[None, None, :]), batch=16)
+    monkeypatch.setenv("FDTD_FORCE_SKINNY", "1")
+    if tc == "off":
+        monkeypatch.setenv("FDTD_NO_TC", "1")
+    from paper_1406_7042_b200.fdtd import Sim
+    sim = Sim(prob, precision=32, reduced_form="leapfrog")
+    assert ("tc_gemm" in sim.path()) == (tc == "on"), sim.path()
+    sim.close()
+    gpu = run_gpu(prob, 300, precision=32, reduced_form="leapfrog")
+    for m in (0, 13):
+        ora = run_oracle(prob, 300, member=m)
+        es, ep, _ = compare(prob, gpu, ora, member=m)
+        assert es <= 1e-4 and ep <= 1e-4, (m, es, ep)
