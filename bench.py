@@ -267,9 +267,13 @@ def bench_ours(args):
         grid_bytes += w * (2 * qe * qh + 2 * nif * qh + 4 * (qe + qh + nif) * Nb)
     grid_kernel = None
     if grid_ms > 0:
-        grid_kernel = {"kernel": "reduced leap-frog GEMVs (rowblock/colsum, a4+a6)",
-                       "algorithmic_bytes_per_step": grid_bytes, "avg_ms": grid_ms,
-                       "achieved": grid_bytes / (grid_ms * 1e-3) / 1e9}
+        kname = ("reduced leap-frog products (a4+a6): split-K TN GEMMs for K~' h~, K~'^T e~, S_E^T G; "
+                 "y = S_E h~ on tcgen05 (3xTF32)" if "tc_gemm" in sim.path() else
+                 "reduced leap-frog products (a4+a6): GEMV / SIMT GEMM kernels")
+        ach = grid_bytes / (grid_ms * 1e-3) / 1e9
+        grid_kernel = {"kernel": kname, "bound": "hbm", "algorithmic_bytes_per_step": grid_bytes, "avg_ms": grid_ms,
+                       "achieved": ach, "peak": peak, "frac": ach / peak,
+                       "note": "eager per-step launches with CUDA events (includes launch gaps)"}
     traffic = None
     tf = os.path.join(ROOT, "profiles", "stencil_traffic.json")
     if os.path.exists(tf):

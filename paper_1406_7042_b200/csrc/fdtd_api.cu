@@ -118,9 +118,13 @@ struct BlockDev {
   // (leap-frog blocks: 16-byte vector loads)
   T *K_d = nullptr, *KT_d = nullptr, *SE_d = nullptr, *SET_d = nullptr, *ge_d = nullptr, *gh_d = nullptr;
   T *Kp_d = nullptr, *KTp_d = nullptr, *SEp_d = nullptr, *Tv_d = nullptr;
-  T* part_d = nullptr;                         // [splits][qh][N] S_E^T G partial sums (fp32 GEMM path)
+  T* part_d = nullptr;                         // [ks + splits][qh][N] K~'^T e~ and S_E^T G partial sums (fp32 GEMM path)
+  T* parte_d = nullptr;                        // [ks][qe][N] K~' h~ partial sums
+  T* gen_d = nullptr;                          // -g_e (the e~ update as an axpy)
+  int ks = 0;                                  // row splits of the K~' products
   bool tc = false;                             // y = S_E h~ on the tensor cores (tc_gemm.cuh, 3xTF32, N = 16)
   CUtensorMap se_map;                          // TMA map of SEp_d: [n_if][Kph] fp32, 32 x 128 boxes, 128-byte swizzle
+  float* xs_d = nullptr;                       // h~ split for the tensor cores: [ceil(qh/32)][hi 512 | lo 512]
   int splits = 0;                              // > 0: tall-skinny fp32 GEMM kernels for the S_E products
   int Kph = 0, Kpe = 0;                        // padded row pitches (multiples of 32 * VEC)
   // state offsets (elements) in the concatenated buffers
@@ -595,8 +599,19 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
         const int TC = 4 * 256 / (D.N / 4);
         const int ctile = (D.qh + TC - 1) / TC;
         D.splits = std::max(1, std::min(2 * 148 / ctile, D.n_if / 64));
-        D.part_d = dalloc<T>((size_t)D.splits * D.qh * D.N);
-        if (!D.part_d) return fail(FDTD_ENOMEM, "block %d: partial-sum workspace allocation failed", b);
+        // the K~' products as split-K TN GEMMs on the stored transposes: 4 column
+        // tiles x ks row splits fill the GPU (a 1024 x 1024 x 16 product is too
+        // small for one CTA per row block)
+        D.ks = std::max(1, std::min(64, std::min(D.qe, D.qh) / 16));
+        D.part_d = dalloc<T>((size_t)(D.ks + D.splits) * D.qh * D.N);
+        D.parte_d = dalloc<T>((size_t)D.ks * D.qe * D.N);
+        D.gen_d = dalloc<T>((size_t)D.qe);
+        if (!D.part_d || !D.parte_d || !D.gen_d) return fail(FDTD_ENOMEM, "block %d: partial-sum workspace allocation failed", b);
+        {
+          std::vector<T> gen(D.qe);
+          for (int r = 0; r < D.qe; ++r) gen[r] = -ge[r];
+          if (upload(D.gen_d, gen)) return FDTD_ECUDA;
+        }
         if (D.N == fdtd::tc::BN && !getenv("FDTD_NO_TC")) {
           PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
           cudaDriverEntryPointQueryResult qres;
@@ -609,6 +624,13 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
             D.tc = encode(&D.se_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)D.SEp_d, gdim, gstr, box, es,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            if (D.tc) {
+              // zero rows beyond qh stay zero; the prologue / set_state fill the rest (tc_split_x)
+              const size_t nxs = (size_t)((D.qh + 31) / 32) * 1024;
+              D.xs_d = dalloc<float>(nxs);
+              if (!D.xs_d) return fail(FDTD_ENOMEM, "block %d: tensor-core operand buffer allocation failed", b);
+              CK(cudaMemsetAsync(D.xs_d, 0, nxs * sizeof(float), stream));
+            }
           }
         }
       }
@@ -1047,9 +1069,11 @@ int Impl<T>::setup_persist() {
                            ((size_t)TX * ty + 15) / 16 * 16 + (2 * sizeof(T) * (size_t)maxrows + 15) / 16 * 16 +
                            sizeof(fdtd::P2Row<T>) * (size_t)maxrows + 64;
     if (tile_sm > 220 * 1024) continue;
-    CK(cudaFuncSetAttribute(fdtd::persist2d_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sm));
+    const void* kfn = (const void*)fdtd::persist2d_kernel<T>;
+    const int nthr = 512;
+    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sm));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdtd::persist2d_kernel<T>, 512, tile_sm));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, nthr, tile_sm));
     const int capacity = per_sm * nsm;
     int nr = 0, r = 0;
     size_t sm = tile_sm;
@@ -1059,8 +1083,8 @@ int Impl<T>::setup_persist() {
       r = (Rtot + nr - 1) / nr;
       sm = std::max(tile_sm, sizeof(T) * ((size_t)(1 + r) * Cmax + (size_t)r * 32) + 64);
       if (sm > 220 * 1024) continue;
-      CK(cudaFuncSetAttribute(fdtd::persist2d_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdtd::persist2d_kernel<T>, 512, sm));
+      CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, nthr, sm));
       nr = (Rtot + r - 1) / r;
       if (per_sm * nsm < nt + nr) continue;
     }
@@ -1490,24 +1514,28 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
       if (D.fused) continue;
       T* e = eb[0] + D.e_off;
       T* h = hb[0] + D.h_off;
-      // a4: e~ -= G_e K~' h~^{n+1/2}
-      n += launch_rowblock<T>(D.qe, D.qh, D.Kph, D.N, D.Kp_d, h, e, D.ge_d, (T)-1, true, ds, check_every, d_bad, st);
-      // a6: T = K~'^T e~ + S_E^T G ; h~ += G_h T ; y = S_E h~
-      n += launch_rowblock<T>(D.qh, D.qe, D.Kpe, D.N, D.KTp_d, e, D.Tv_d, (const T*)nullptr, (T)1, false, ds, 0,
-                              d_bad, st);
       if constexpr (sizeof(T) == 4) {
         if (D.splits > 0) {
-          // S_E^T G: split-K partials, then h~ += G_h (T + sum of partials) in a fixed order;
-          // y = S_E h~: tall-skinny GEMM
+          // a4: e~ -= G_e K~' h~  (split-K TN on K~'^T, then the axpy with -g_e)
+          n += launch_gemm_tn(D.qh, D.qe, D.Kpe, D.N, D.ks, (const float*)D.KTp_d, (const float*)h,
+                              (float*)D.parte_d, st);
+          fdtd::reduce_axpy_f32_kernel<<<(D.qe * D.N + 255) / 256, 256, 0, st>>>(
+              D.qe, D.N, D.ks, (const float*)D.parte_d, nullptr, (const float*)D.gen_d, (float*)e, nullptr);
+          ++n;
+          // a6: h~ += G_h (K~'^T e~ + S_E^T G): both as split-K partials into one
+          // buffer, summed in a fixed order; y = S_E h~ (tensor cores or SIMT)
+          n += launch_gemm_tn(D.qe, D.qh, D.Kph, D.N, D.ks, (const float*)D.Kp_d, (const float*)e,
+                              (float*)D.part_d, st);
           n += launch_gemm_tn(D.n_if, D.qh, D.Kph, D.N, D.splits, (const float*)D.SEp_d,
-                              (const float*)(g_all + D.y_off), (float*)D.part_d, st);
+                              (const float*)(g_all + D.y_off), (float*)D.part_d + (size_t)D.ks * D.qh * D.N, st);
           fdtd::reduce_axpy_f32_kernel<<<(D.qh * D.N + 255) / 256, 256, 0, st>>>(
-              D.qh, D.N, D.splits, (const float*)D.part_d, (const float*)D.Tv_d, (const float*)D.gh_d, (float*)h);
+              D.qh, D.N, D.ks + D.splits, (const float*)D.part_d, nullptr, (const float*)D.gh_d, (float*)h,
+              D.tc ? D.xs_d : nullptr);
           ++n;
           if (D.tc) {
             const int tiles = (D.n_if + fdtd::tc::BM - 1) / fdtd::tc::BM;
             fdtd::tc::tc_skinny_gemm_kernel<<<std::min(tiles, tc_grid), fdtd::tc::NTHREADS, fdtd::tc::SMEM_BYTES, st>>>(
-                D.se_map, D.n_if, D.qh, (const float*)h, (float*)(y_all + D.y_off), ds, check_every, d_bad);
+                D.se_map, D.n_if, D.qh, D.xs_d, (float*)(y_all + D.y_off), ds, check_every, d_bad);
             ++n;
           } else {
             n += launch_gemm_nn(D.n_if, D.qh, D.Kph, D.N, (const float*)D.SEp_d, (const float*)h,
@@ -1516,6 +1544,11 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
           continue;
         }
       }
+      // a4: e~ -= G_e K~' h~^{n+1/2}
+      n += launch_rowblock<T>(D.qe, D.qh, D.Kph, D.N, D.Kp_d, h, e, D.ge_d, (T)-1, true, ds, check_every, d_bad, st);
+      // a6: T = K~'^T e~ + S_E^T G ; h~ += G_h T ; y = S_E h~
+      n += launch_rowblock<T>(D.qh, D.qe, D.Kpe, D.N, D.KTp_d, e, D.Tv_d, (const T*)nullptr, (T)1, false, ds, 0,
+                              d_bad, st);
       if (D.n_if > 0) n += launch_colsum<T>(D.n_if, D.qh, D.Kph, D.N, D.SEp_d, g_all + D.y_off, D.Tv_d, st);
       fdtd::axpy_diag_kernel<T><<<(D.qh * D.N + 255) / 256, 256, 0, st>>>(D.qh, D.N, D.gh_d, D.Tv_d, h);
       ++n;

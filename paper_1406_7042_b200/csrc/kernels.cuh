@@ -1441,15 +1441,26 @@ gemm_tn_f32_partial_kernel(int rows, int cols, int Kp, const float* __restrict__
   }
 }
 
-// h~[c][n] += g_h[c] (T[c][n] + sum_s part[s][c][n])   (splits in order)
+// h[c][n] += g[c] (T[c][n] + sum_s part[s][c][n])   (splits in order; T optional)
+// xs (optional, N = 16): the new h~ split for the tensor-core GEMM of
+// tc_gemm.cuh -- per 32-row chunk of h~, [hi | lo] tiles of [16 n][32 k] in
+// the 128-byte swizzled K-major layout, so one bulk copy per chunk lands them
 static __global__ void reduce_axpy_f32_kernel(int cols, int N, int splits, const float* __restrict__ part,
                                        const float* __restrict__ Tv, const float* __restrict__ gh,
-                                       float* __restrict__ h) {
+                                       float* __restrict__ h, float* __restrict__ xs) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= cols * N) return;
-  float v = Tv[t];
+  float v = Tv ? Tv[t] : 0.f;
   for (int s2 = 0; s2 < splits; ++s2) v += part[(int64_t)s2 * cols * N + t];
-  h[t] += gh[t / N] * v;
+  const float hn = h[t] + gh[t / N] * v;
+  h[t] = hn;
+  if (xs) {
+    const int k = t / N, n = t % N, ch = k >> 5, kk = k & 31;
+    const int o = n * 32 + ((((kk >> 2) ^ (n & 7)) & 7) << 2) + (kk & 3);   // swizzled element offset
+    const float hi = __uint_as_float(__float_as_uint(hn) & 0xFFFFE000u);
+    xs[(int64_t)ch * 1024 + o] = hi;
+    xs[(int64_t)ch * 1024 + 512 + o] = hn - hi;
+  }
 }
 
 template <typename T>

@@ -205,6 +205,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
   P2Row<T>* rs = reinterpret_cast<P2Row<T>*>(yv + ((2 * P.maxrows * (int)sizeof(T) + 15) / 16) * 16 / (int)sizeof(T));
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int lx = tid & 31, ly = tid >> 5, NLY = nthr >> 5;
+  const bool pair = sizeof(T) == 4 && TX == 64;   // paired interior loops (fp32, 64-wide tiles)
   // the tile covers cells i < nx, j < ny: the last storage column / row (PEC
   // wall Ez = 0, H never updated) is constant and written back by CTA 0
   for (int jl = ly; jl < TY; jl += NLY)
@@ -258,12 +259,41 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       const T dd = (hy - hyim) - (hx - hxm);
       sEz[c] = (i > 0 && j > 0) ? sEz[c] + cc.apply(dd) : (T)0;
     };
+    if (pair) {
+      // 64-wide tiles: lane lx owns the cell pair (2 lx, 2 lx + 1) of a row, so
+      // the x-1 neighbour of the second cell is the first cell's register and
+      // the loads are 8-byte pairs (same expression per cell as e_cell)
+      const int ia = 2 * lx;
+      for (int jl = 1 + ly; jl < TY; jl += NLY) {
+        if (j0 + jl >= ny) break;
+        const int c = jl * TX + ia;
+        const float2 hy2 = *reinterpret_cast<const float2*>(sHy + c);
+        const float2 hx2 = *reinterpret_cast<const float2*>(sHx + c);
+        const float2 hxm2 = *reinterpret_cast<const float2*>(sHx + c - TX);
+        const float2 ez2 = *reinterpret_cast<const float2*>(sEz + c);
+        const uint16_t m2 = *reinterpret_cast<const uint16_t*>(smat + c);
+        const int ma = m2 & 0xff, mb = m2 >> 8;
+        float e0 = ez2.x, e1 = ez2.y;
+        if (ia > 0 && i0 + ia < nx && !(!uniform && (ifm[ma] & 4))) {
+          const Coef<T> cc = uniform ? P.u0 : cE[ma];
+          const T dd = (hy2.x - sHy[c - 1]) - (hx2.x - hxm2.x);
+          e0 = (j0 + jl > 0) ? e0 + cc.apply(dd) : (T)0;
+        }
+        if (i0 + ia + 1 < nx && !(!uniform && (ifm[mb] & 4))) {
+          const Coef<T> cc = uniform ? P.u0 : cE[mb];
+          const T dd = (hy2.y - hy2.x) - (hx2.y - hxm2.y);
+          e1 = (j0 + jl > 0) ? e1 + cc.apply(dd) : (T)0;
+        }
+        *reinterpret_cast<float2*>(sEz + c) = make_float2(e0, e1);
+      }
+    } else {
     for (int jl = 1 + ly; jl < TY; jl += NLY) {
       if (j0 + jl >= ny) break;
       for (int il = 1 + lx; il < TX; il += 32) {
         if (i0 + il >= nx) break;
         e_cell(il, jl);
       }
+    }
     }
     if (dslot >= 0) P2_STAMP(dslot, 5);
     // (b) wait for the left / bottom H halos (and, on interface tiles, for the
@@ -405,12 +435,45 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       if (do_check && !(finite_small(ez) && finite_small(hx1) && finite_small(hy1))) bad = true;
     };
     // (a) interior: no E halo needed
+    if (pair) {
+      const int ia = 2 * lx;
+      for (int jl = ly; jl < TY - 1; jl += NLY) {
+        if (j0 + jl >= ny) break;
+        const int c = jl * TX + ia;
+        const float2 ez2 = *reinterpret_cast<const float2*>(sEz + c);
+        const float2 ezj2 = *reinterpret_cast<const float2*>(sEz + c + TX);
+        const float2 hx2 = *reinterpret_cast<const float2*>(sHx + c);
+        const float2 hy2 = *reinterpret_cast<const float2*>(sHy + c);
+        const uint16_t m2 = *reinterpret_cast<const uint16_t*>(smat + c);
+        float hx0 = hx2.x, hy0 = hy2.x, hx1 = hx2.y, hy1 = hy2.y;
+        const bool jin = j0 + jl > 0;
+        if (i0 + ia < nx) {
+          Coef<T> cx, cy;
+          if (uniform) { cx = P.u1; cy = P.u1; }
+          else { const int m = m2 & 0xff; cx = cHx[m]; cy = cHy[m]; }
+          hx0 = (i0 + ia > 0) ? hx2.x - cx.apply(ezj2.x - ez2.x) : hx2.x;
+          hy0 = jin ? hy2.x + cy.apply(ez2.y - ez2.x) : hy2.x;
+          if (do_check && !(finite_small(ez2.x) && finite_small(hx0) && finite_small(hy0))) bad = true;
+        }
+        if (ia + 1 < TX - 1 && i0 + ia + 1 < nx) {
+          Coef<T> cx, cy;
+          if (uniform) { cx = P.u1; cy = P.u1; }
+          else { const int m = m2 >> 8; cx = cHx[m]; cy = cHy[m]; }
+          hx1 = hx2.y - cx.apply(ezj2.y - ez2.y);
+          hy1 = jin ? hy2.y + cy.apply(sEz[c + 2] - ez2.y) : hy2.y;
+          if (do_check && !(finite_small(ez2.y) && finite_small(hx1) && finite_small(hy1))) bad = true;
+        }
+        *reinterpret_cast<float2*>(sHx + c) = make_float2(hx0, hx1);
+        *reinterpret_cast<float2*>(sHy + c) = make_float2(hy0, hy1);
+      }
+    } else {
     for (int jl = ly; jl < TY - 1; jl += NLY) {
       if (j0 + jl >= ny) break;
       for (int il = lx; il < TX - 1; il += 32) {
         if (i0 + il >= nx) break;
         h_cell(il, jl);
       }
+    }
     }
     // (b) right / top E halos
     if constexpr (LL) {

@@ -13,16 +13,23 @@
 //
 // CTA = 10 warps, persistent over 128-row tiles, K in chunks of 32 (one
 // 128-byte swizzle atom per row):
-//   warp 0     TMA producer: A chunk [128 rows][32] fp32, SWIZZLE_128B, into
-//              an NSTG-stage ring (full / empty mbarriers)
-//   warp 1     TMEM allocation (32 columns: two 16-column accumulators) and
-//              MMA issue (one elected thread): per chunk 4 k-steps x 3
-//              products of M=128, N=16, K=8; tcgen05.commit frees the stage
-//   warps 2-5  split: A chunk in place -> a_hi, a_lo; X rows k0..k0+31 ->
-//              x_hi, x_lo (K-major, the same 128-byte swizzle); then
-//              fence.proxy.async and arrive on the stage's split barrier
-//   warps 6-9  epilogue: tcgen05.ld of the accumulator (warp w reads TMEM lanes
-//              32 (w % 4) ..), fp32 stores of the 16 outputs of each row
+//   warp 0     TMA producer: A chunk [128 rows][32] fp32, SWIZZLE_128B, and
+//              the chunk's x_hi | x_lo (bulk copy) into an NSTG-stage ring
+//              (full / empty mbarriers)
+//   warp 1     TMEM allocation (two tile buffers x KSETS accumulator sets x 64
+//              columns; k-step kk of a chunk accumulates into set kk % KSETS, so
+//              consecutive UMMAs do not chain on one accumulator) and
+//              MMA issue (one elected thread): per chunk 4 k-steps x 2
+//              products of M=128, N=32, K=8 (B = [x_hi ; x_lo] stacked, so
+//              a_hi [x_hi|x_lo] and a_lo [x_hi|x_lo]: the three needed terms in
+//              two instructions); tcgen05.commit frees the stage
+//   warps 2-5  split: A chunk in place -> a_hi, a_lo, then fence.proxy.async
+//              and arrive on the stage's split barrier (x_hi, x_lo arrive
+//              pre-split with the A chunk: one bulk copy from the [K/32][hi|lo]
+//              buffer the h~ update writes, reduce_axpy_f32_kernel)
+//   warps 6-9  epilogue: tcgen05.ld of the accumulators (warp w reads TMEM lanes
+//              32 (w % 4) ..), out = a_hi x_hi + (a_hi x_lo + a_lo x_hi), fp32
+//              stores of the 16 outputs of each row
 // Every mbarrier wait is bounded (trap after 2^26 polls) so a protocol error
 // fails the launch instead of hanging the GPU.
 #pragma once
@@ -37,6 +44,8 @@ constexpr int BM = 128;          // rows per tile (UMMA M)
 constexpr int BN = 16;           // columns (UMMA N, batch members)
 constexpr int BK = 32;           // K per chunk: 32 fp32 = one 128-byte swizzle row
 constexpr int NSTG = 5;          // ring stages
+constexpr int KSETS = 1;         // accumulator sets (independent MMA chains; 4 measured no faster), summed in the epilogue
+constexpr int TMEM_COLS = 2 * KSETS * 4 * BN;   // two tile buffers x KSETS x (32 + 32) columns
 constexpr int A_BYTES = BM * BK * 4;            // 16 KB
 constexpr int B_BYTES = BN * BK * 4;            // 2 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // a_hi (in place) | a_lo | x_hi | x_lo
@@ -69,6 +78,12 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t phase) {
     if (it > (1u << 26)) asm volatile("trap;");
   }
 }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
@@ -87,8 +102,10 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)2u << 61;                           // layout: SWIZZLE_128B
   return d;
 }
-// instruction descriptor: D f32, A/B tf32, both K-major, N = 16, M = 128
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// instruction descriptor: D f32, A/B tf32, both K-major, N = 32 (x_hi and x_lo
+// stacked as the 32 rows of one B tile), M = 128
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)((2 * BN) >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
   asm volatile(
@@ -110,7 +127,7 @@ __device__ __forceinline__ uint32_t sw_off(int row, int k) {
 __device__ __forceinline__ float tf32_hi(float a) { return __uint_as_float(__float_as_uint(a) & 0xFFFFE000u); }
 
 __global__ void __launch_bounds__(NTHREADS, 1)
-tc_skinny_gemm_kernel(const __grid_constant__ CUtensorMap amap, int rows, int K, const float* __restrict__ X,
+tc_skinny_gemm_kernel(const __grid_constant__ CUtensorMap amap, int rows, int K, const float* __restrict__ Xs,
                       float* __restrict__ out, const int64_t* __restrict__ d_step, int check_every,
                       unsigned long long* __restrict__ bad_step) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -130,7 +147,7 @@ tc_skinny_gemm_kernel(const __grid_constant__ CUtensorMap amap, int rows, int K,
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(su32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)), "n"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -146,8 +163,10 @@ tc_skinny_gemm_kernel(const __grid_constant__ CUtensorMap amap, int rows, int K,
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
         for (int c = 0; c < nk; ++c) {
           bar_wait(&empty[s], ph ^ 1u);
-          bar_expect_tx(&full[s], A_BYTES);
+          bar_expect_tx(&full[s], A_BYTES + 2 * B_BYTES);
           tma_2d(smem + s * STAGE_BYTES, &amap, c * BK, t * BM, &full[s]);
+          // x_hi | x_lo of this chunk, pre-split and pre-swizzled (reduce_axpy_f32_kernel)
+          bulk_g2s(smem + s * STAGE_BYTES + 2 * A_BYTES, Xs + (int64_t)c * 1024, 2 * B_BYTES, &full[s]);
           if (++s == NSTG) { s = 0; ph ^= 1u; }
         }
     }
@@ -160,7 +179,7 @@ tc_skinny_gemm_kernel(const __grid_constant__ CUtensorMap amap, int rows, int K,
       const int ab = j & 1;
       bar_wait(&acce[ab], ((j >> 1) & 1) ^ 1u);         // epilogue drained this accumulator
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint32_t d = tmem + (uint32_t)(ab * BN);
+      const uint32_t d = tmem + (uint32_t)(ab * KSETS * 4 * BN);
       for (int c = 0; c < nk; ++c) {
         bar_wait(&split[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -171,10 +190,13 @@ tc_skinny_gemm_kernel(const __grid_constant__ CUtensorMap amap, int rows, int K,
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint32_t o = (uint32_t)kk * 32u;       // 8 tf32 = 32 bytes along the swizzled row
             const uint64_t dah = sw128_desc(ahi + o), dal = sw128_desc(alo + o);
-            const uint64_t dxh = sw128_desc(xhi + o), dxl = sw128_desc(xlo + o);
-            mma_tf32(d, dah, dxh, (c > 0 || kk > 0) ? 1u : 0u);
-            mma_tf32(d, dah, dxl, 1u);
-            mma_tf32(d, dal, dxh, 1u);
+            const uint64_t dx = sw128_desc(xhi + o);     // [x_hi ; x_lo]: 32 rows of B
+            (void)xlo;
+            // D0 = a_hi [x_hi | x_lo], D1 = a_lo [x_hi | x_lo] (its x_lo half unused);
+            // one accumulator set per k-step of the chunk: KSETS independent chains
+            const uint32_t dk = d + (uint32_t)((kk % KSETS) * 4 * BN);
+            mma_tf32(dk, dah, dx, (c > 0 || kk >= KSETS) ? 1u : 0u);
+            mma_tf32(dk + 2 * BN, dal, dx, (c > 0 || kk >= KSETS) ? 1u : 0u);
           }
           mma_commit(&empty[s]);                         // stage free once these MMAs completed
           if (c == nk - 1) mma_commit(&accf[ab]);        // accumulator complete
@@ -202,21 +224,6 @@ tc_skinny_gemm_kernel(const __grid_constant__ CUtensorMap amap, int rows, int K,
           *reinterpret_cast<float4*>(st + ch * 16) = hi;
           *reinterpret_cast<float4*>(st + A_BYTES + ch * 16) = lo;
         }
-        // X rows k0 .. k0+31 (16 columns) -> K-major [16 n][32 k], swizzled
-        {
-          const int k0 = c * BK;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int e = q * 128 + tid;                 // 512 elements
-            const int kk = e >> 4, n = e & 15;
-            const int k = k0 + kk;
-            const float x = (k < K) ? __ldg(X + (int64_t)k * BN + n) : 0.f;
-            const float xh = tf32_hi(x);
-            const uint32_t o = sw_off(n, kk);
-            *reinterpret_cast<float*>(st + 2 * A_BYTES + o) = xh;
-            *reinterpret_cast<float*>(st + 2 * A_BYTES + B_BYTES + o) = x - xh;
-          }
-        }
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         bar_arrive(&split[s]);
@@ -232,14 +239,30 @@ tc_skinny_gemm_kernel(const __grid_constant__ CUtensorMap amap, int rows, int K,
       const int ab = j & 1;
       bar_wait(&accf[ab], (j >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      uint32_t v[16];
-      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(ab * BN);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-          "%15}, [%16];\n"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr));
+      uint32_t v[16], u[16], z[16];
+      float acc[16];
+      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(ab * KSETS * 4 * BN);
+#define FDTD_TMEM_LD16(R, A)                                                                                       \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, " \
+               "%14, %15}, [%16];\n"                                                                               \
+               : "=r"(R[0]), "=r"(R[1]), "=r"(R[2]), "=r"(R[3]), "=r"(R[4]), "=r"(R[5]), "=r"(R[6]), "=r"(R[7]),   \
+                 "=r"(R[8]), "=r"(R[9]), "=r"(R[10]), "=r"(R[11]), "=r"(R[12]), "=r"(R[13]), "=r"(R[14]),         \
+                 "=r"(R[15])                                                                                       \
+               : "r"(A))
+#pragma unroll
+      for (int ks = 0; ks < KSETS; ++ks) {
+        const uint32_t a0 = taddr + (uint32_t)(ks * 4 * BN);
+        FDTD_TMEM_LD16(v, a0);                   // a_hi x_hi
+        FDTD_TMEM_LD16(u, a0 + BN);              // a_hi x_lo
+        FDTD_TMEM_LD16(z, a0 + 2 * BN);          // a_lo x_hi
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float term = __uint_as_float(v[e]) + (__uint_as_float(u[e]) + __uint_as_float(z[e]));
+          acc[e] = ks == 0 ? term : acc[e] + term;
+        }
+      }
+#undef FDTD_TMEM_LD16
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       bar_arrive(&acce[ab]);
@@ -248,8 +271,7 @@ tc_skinny_gemm_kernel(const __grid_constant__ CUtensorMap amap, int rows, int K,
         float4* o = reinterpret_cast<float4*>(out + (int64_t)r * BN);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const float4 w = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                                       __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+          const float4 w = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
           o[q] = w;
           if (check) bad |= !(isfinite(w.x) && isfinite(w.y) && isfinite(w.z) && isfinite(w.w) &&
                               fabsf(w.x) <= 1e30f && fabsf(w.y) <= 1e30f && fabsf(w.z) <= 1e30f &&
@@ -261,7 +283,7 @@ tc_skinny_gemm_kernel(const __grid_constant__ CUtensorMap amap, int rows, int K,
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tmem));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(TMEM_COLS));
 }
 
 }  // namespace tc
