@@ -176,7 +176,7 @@ struct Impl : public fdtd_t {
   int NPsel = 32;
   static constexpr int GEMM_KS = 4;
   // rows per thread of the GEMM kernel: 64-row tiles for NP <= 16, 32 for NP = 32
-  static constexpr int gemm_rpw(int np) { return np == 32 ? 4 : np / 4; }
+  static constexpr int gemm_rpw(int np) { return np == 32 ? 2 : np / 4; }
   int64_t step_offset = 0;            // device step = host step + offset (set_state(8))
   size_t fused_smem = 0;
   // probes
