@@ -132,7 +132,7 @@ def algorithmic_bytes_per_cell(prob, precision):
     return words * w + mat
 
 
-def run_oracle_sample(prob, seconds=15.0, max_steps=400):
+def run_oracle_sample(prob, seconds=15.0, max_steps=800):
     """Time the CPU oracle (oracle.problem_step, single-threaded SciPy SpMV) on a
     bounded number of steps of the same workload."""
     try:

@@ -802,6 +802,59 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     rows.e_comp = d_ec; rows.e_off = d_eo; rows.c = d_c; rows.rowptr = d_rp; rows.h_comp = d_hc;
     rows.h_off = d_ho; rows.w = d_w; rows.y_off = d_yo; rows.src = d_src; rows.cs = d_cs; rows.wave = d_wave;
     rows.g_out = g_all;
+    // local-slot form of the rows (3-D): slot s of component ec is the H term
+    //   Ex: 0 Hz(0)  1 Hz(j-1)  2 Hy(0)  3 Hy(k-1)
+    //   Ey: 0 Hz(0)  1 Hz(i-1)  2 Hx(0)  3 Hx(k-1)
+    //   Ez: 0 Hx(0)  1 Hx(j-1)  2 Hy(0)  3 Hy(i-1)
+    rows.lcode = nullptr; rows.lw = nullptr;
+    if (dim == 3 && nr > 0) {
+      std::vector<uint16_t> code(nr);
+      std::vector<T> lw((size_t)nr * 4, (T)0);
+      bool local = true;
+      auto ijk = [&](int64_t s_, int& i, int& j, int& k) {
+        i = (int)(s_ % (nx + 1)); j = (int)((s_ / (nx + 1)) % (ny + 1)); k = (int)(s_ / ((int64_t)(nx + 1) * (ny + 1)));
+      };
+      for (int64_t r = 0; r < nr && local; ++r) {
+        const HRow& h = hrows[r];
+        if (h.w.size() > 4) { local = false; break; }
+        int i, j, k;
+        ijk(h.s, i, j, k);
+        uint16_t cd = (uint16_t)(h.w.size() << 8);
+        for (size_t q = 0; q < h.w.size(); ++q) {
+          const int hc_ = (int)(h.w[q].first / S);
+          int hi, hj, hk;
+          ijk(h.w[q].first % S, hi, hj, hk);
+          const int di = hi - i, dj = hj - j, dk = hk - k;
+          int sl = -1;
+          if (h.comp == 0) {
+            if (hc_ == 5 && di == 0 && dj == 0 && dk == 0) sl = 0;
+            else if (hc_ == 5 && di == 0 && dj == -1 && dk == 0) sl = 1;
+            else if (hc_ == 4 && di == 0 && dj == 0 && dk == 0) sl = 2;
+            else if (hc_ == 4 && di == 0 && dj == 0 && dk == -1) sl = 3;
+          } else if (h.comp == 1) {
+            if (hc_ == 5 && di == 0 && dj == 0 && dk == 0) sl = 0;
+            else if (hc_ == 5 && di == -1 && dj == 0 && dk == 0) sl = 1;
+            else if (hc_ == 3 && di == 0 && dj == 0 && dk == 0) sl = 2;
+            else if (hc_ == 3 && di == 0 && dj == 0 && dk == -1) sl = 3;
+          } else {
+            if (hc_ == 3 && di == 0 && dj == 0 && dk == 0) sl = 0;
+            else if (hc_ == 3 && di == 0 && dj == -1 && dk == 0) sl = 1;
+            else if (hc_ == 4 && di == 0 && dj == 0 && dk == 0) sl = 2;
+            else if (hc_ == 4 && di == -1 && dj == 0 && dk == 0) sl = 3;
+          }
+          if (sl < 0) { local = false; break; }
+          cd |= (uint16_t)(sl << (2 * q));
+          lw[(size_t)r * 4 + q] = (T)h.w[q].second;
+        }
+        code[r] = cd;
+      }
+      if (local && !getenv("FDTD_NO_LOCAL_ROWS")) {
+        uint16_t* d_code = dalloc<uint16_t>(nr);
+        T* d_lw = dalloc<T>((size_t)nr * 4);
+        if (!d_code || !d_lw || upload(d_code, code) || upload(d_lw, lw)) return FDTD_ECUDA;
+        rows.lcode = d_code; rows.lw = d_lw;
+      }
+    }
     for (int c = 0; c < 3; ++c) rows.row_of[c] = nullptr;
     for (int c = 0; c < 3; ++c) {
       bool any = false;

@@ -77,6 +77,12 @@ struct RowsE {
   const T* wave;               // [n_wave][n_src][B]   (n_src = number of waveform columns)
   int64_t n_wave, n_src;
   T* g_out;                    // interface rows publish E^{n+1} at G[y_off] (reduced-chain input)
+  // 3-D rows whose H terms are all the curl neighbours the stencil already
+  // holds (every interface row of the R4 construction): per row the CSR
+  // order as 2-bit slots + the count (lcode), and the weights [4] (lw); null
+  // when some row is not local (stencil3d_tile_kernel then uses eval_row)
+  const uint16_t* lcode;       // bits 0-7: slots of terms 0..3 (2 bits each), bits 8-10: nterm
+  const T* lw;                 // [n_rows][4]
   // list form (for the standalone rows kernel)
   const int32_t* e_comp;       // [n_rows]
   const int64_t* e_off;        // [n_rows]

@@ -106,6 +106,28 @@ struct SegCursor {               // walks the load sequence of one CTA's items
   }
 };
 
+// an explicit row whose H terms are the four curl neighbours h0..h3 (slot
+// order of RowsE::lcode): the expression of eval_row, term by term in CSR order
+template <typename T>
+__device__ __forceinline__ T local_row(const RowsE<T>& R, int r, int b, int B, T e0, T h0, T h1, T h2, T h3,
+                                       const T* __restrict__ y, int64_t step) {
+  const unsigned cd = R.lcode[r];
+  const int nt = (int)(cd >> 8);
+  T acc = 0;
+  for (int q = 0; q < nt; ++q) {
+    const unsigned sl = (cd >> (2 * q)) & 3u;
+    const T hv = sl == 0 ? h0 : sl == 1 ? h1 : sl == 2 ? h2 : h3;
+    acc += R.lw[4 * r + q] * hv;
+  }
+  const int64_t yo = R.y_off[r];
+  if (yo >= 0) acc += y[yo + b];
+  T e = e0 - R.c[r].apply(acc);
+  const int s = R.src[r];
+  if (s >= 0 && step < R.n_wave) e -= R.cs[r] * R.wave[(step * R.n_src + s) * B + b];
+  if (yo >= 0) R.g_out[yo + b] = e;
+  return e;
+}
+
 template <typename T, bool UNIFORM, int NS, int W, int MB, int MINB>
 __global__ void __launch_bounds__(32 * TILE_BY, MINB)
 stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims d, Fields<T> F0,
@@ -289,9 +311,20 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
           if (!f || (XV && i + w > nx)) continue;
           const int64_t sidx = (int64_t)kk * d.plane + scol + (XV ? w : 0);
           const int bw = XV ? 0 : b + w;
-          if (f & 1) ex.v[w] = eval_row(R, R.row_of[0][sidx], bw, B, ex0.v[w], F0, y, step);
-          if (f & 2) ey.v[w] = eval_row(R, R.row_of[1][sidx], bw, B, ey0.v[w], F0, y, step);
-          if (f & 4) ez.v[w] = eval_row(R, R.row_of[2][sidx], bw, B, ez0.v[w], F0, y, step);
+          if (R.lcode) {
+            // local-slot rows: the H terms are this cell's curl neighbours, in
+            // registers (same values, same CSR order as eval_row)
+            if (f & 1) ex.v[w] = local_row(R, R.row_of[0][sidx], bw, B, ex0.v[w], hz_c.v[w], hz_jm.v[w], hy_c.v[w],
+                                           hyk.v[w], y, step);
+            if (f & 2) ey.v[w] = local_row(R, R.row_of[1][sidx], bw, B, ey0.v[w], hz_c.v[w], hz_im.v[w], hx_c.v[w],
+                                           hxk.v[w], y, step);
+            if (f & 4) ez.v[w] = local_row(R, R.row_of[2][sidx], bw, B, ez0.v[w], hx_c.v[w], hx_jm.v[w], hy_c.v[w],
+                                           hy_im.v[w], y, step);
+          } else {
+            if (f & 1) ex.v[w] = eval_row(R, R.row_of[0][sidx], bw, B, ex0.v[w], F0, y, step);
+            if (f & 2) ey.v[w] = eval_row(R, R.row_of[1][sidx], bw, B, ey0.v[w], F0, y, step);
+            if (f & 4) ez.v[w] = eval_row(R, R.row_of[2][sidx], bw, B, ez0.v[w], F0, y, step);
+          }
         }
       }
       T* en = En + ebuf * (3 * EP) + erow;

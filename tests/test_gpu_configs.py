@@ -384,3 +384,34 @@ def test_tiny4_batch16_leapfrog_tensor_core_gemm(tc, monkeypatch):
         ora = run_oracle(prob, 300, member=m)
         es, ep, _ = compare(prob, gpu, ora, member=m)
         assert es <= 1e-4 and ep <= 1e-4, (m, es, ep)
+
+
+@pytest.mark.parametrize("case,prec", [("tiny5", 32), ("tiny5", 64), ("tiny4", 32)])
+def test_local_slot_rows_bitwise_equal_global_rows(case, prec, monkeypatch):
+    # the tile stencil's explicit rows from the register-held curl neighbours
+    # (RowsE::lcode) against the CSR walk over global H (eval_row): bit for bit
+    from paper_1406_7042_b200.fdtd import Sim
+    from sampled_state import random_state
+    scn, prob = _prep(case, precision=prec)
+    prob = dict(prob, init={})
+    arrays, re_, rh_ = random_state(prob, seed=11)
+
+    def run(local):
+        if local:
+            monkeypatch.delenv("FDTD_NO_LOCAL_ROWS", raising=False)
+        else:
+            monkeypatch.setenv("FDTD_NO_LOCAL_ROWS", "1")
+        sim = Sim(prob, precision=prec, graph_steps=0)
+        for c in range(6):
+            sim.set_state(c, arrays[c])
+        sim.step(9)
+        sim.sync()
+        out = [sim.get_state(c) for c in range(8)]
+        pr = sim.probe()
+        sim.close()
+        return out, pr
+
+    (a, pa), (b, pb) = run(True), run(False)
+    for c in range(8):
+        assert np.array_equal(a[c], b[c]), c
+    assert np.array_equal(pa, pb)
