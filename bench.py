@@ -260,11 +260,15 @@ def bench_ours(args):
     # (K~' and K~'^T once each, S_E twice: y = S_E h~ and S_E^T G) + the states
     w = 4 if prec == 32 else 8
     grid_bytes = 0
+    red_flops = 0.0
     for b in prob.get("blocks") or []:
         qe = int(b.get("qe", b.get("q"))); qh = int(b.get("qh", b.get("q")))
         nif = int(np.asarray(b["S_E"]).size // qh)
         Nb = int(b["n_inst"]) * int(prob.get("batch", 1))
         grid_bytes += w * (2 * qe * qh + 2 * nif * qh + 4 * (qe + qh + nif) * Nb)
+        # 4 (q_e q_h + n_if q_h) flops per column per step (each
+        # of K~', S_E applied twice, multiply + add)
+        red_flops += 4.0 * (qe * qh + nif * qh) * Nb
     grid_kernel = None
     if grid_ms > 0:
         kname = ("reduced leap-frog products (a4+a6): split-K TN GEMMs for K~' h~, K~'^T e~, S_E^T G; "
@@ -273,6 +277,7 @@ def bench_ours(args):
         ach = grid_bytes / (grid_ms * 1e-3) / 1e9
         grid_kernel = {"kernel": kname, "bound": "hbm", "algorithmic_bytes_per_step": grid_bytes, "avg_ms": grid_ms,
                        "achieved": ach, "peak": peak, "frac": ach / peak,
+                       "gflops": red_flops / (grid_ms * 1e-3) / 1e9,
                        "note": "eager per-step launches with CUDA events (includes launch gaps)"}
     traffic = None
     tf = os.path.join(ROOT, "profiles", "stencil_traffic.json")
@@ -318,7 +323,16 @@ def bench_ours(args):
         cpu = {"value": cells_of(prob) * ns / el / 1e6, "unit": "Mcell-updates/s", "cores": 1,
                "kind": "oracle",
                "sample": f"{ns} time steps of the same workload in {el:.1f} s (SciPy CSR SpMV, 1 thread)"}
-    per_step = {"phase_ms_per_step": {p: ph[p] / max(ph["steps"], 1) for p in PHASES}, "reduced_grid": grid_kernel}
+    red_ms = ph["reduced"] / max(ph["steps"], 1)
+    reduced_fused = None
+    if red_ms > 0 and grid_ms == 0 and red_flops > 0:
+        # fused blocks: the whole reduced update of a step (one GEMV / GEMM phase)
+        reduced_fused = {"kernel": "fused reduced update (reduced_fused_kernel / reduced_gemm_kernel)",
+                         "algorithmic_gflop_per_step": red_flops / 1e9, "avg_ms": red_ms,
+                         "gflops": red_flops / (red_ms * 1e-3) / 1e9,
+                         "note": "eager per-step launch with CUDA events; FMA roofline: SIMT fp32"}
+    per_step = {"phase_ms_per_step": {p: ph[p] / max(ph["steps"], 1) for p in PHASES}, "reduced_grid": grid_kernel,
+                "reduced_fused": reduced_fused}
     if persistent:
         # the timed path is ONE persistent launch per bench step (n_steps time
         # steps, state resident in shared memory): algorithmic bytes = what a

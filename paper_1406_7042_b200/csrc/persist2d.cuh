@@ -542,7 +542,10 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       }
       P.ring[(step % P.cap) * (int64_t)P.n_probe + P.PR.pid[q]] = acc;
     }
-    __syncthreads();
+    // fp32 tiles without probes need no barrier here: the next E phase writes
+    // only sEz, which nothing after the previous barrier reads (the probe
+    // loop would; the flag path needs every halo store before thread 0's release)
+    if (!LL || pr_hi > pr_lo) __syncthreads();
     if (dslot >= 0) P2_STAMP(dslot, 4);
     if (!LL && tid == 0) { __threadfence(); st_release_u32(P.fH + t, (unsigned)(ls + 1)); }
   }
