@@ -197,6 +197,8 @@ struct Impl : public fdtd_t {
   int64_t graph_kernels = 0;
   T* staging = nullptr;
   size_t staging_bytes = 0;
+  double* d_in64 = nullptr;          // device copy of a set_state input (fp64)
+  int64_t d_in64_n = 0;
   int kchunk_max = 32;         // z-planes per CTA of the 3-D stencils (upper bound)
   // z-chunk: at most kchunk_max planes, at least ~2 waves of CTAs (148 SMs x 3
   // resident), chunks balanced (config 5: 41 planes -> 3 x 14, not 32 + 9)
@@ -215,6 +217,8 @@ struct Impl : public fdtd_t {
   fdtd::TileCfg tcfg;
   fdtd::TileSplit tsplit;
   int tc_grid = 148;            // CTAs of the tensor-core skinny GEMM (one per SM, persistent over row tiles)
+  bool use_pdl = false;         // the fused reduced kernel as a programmatic dependent launch (FDTD_PDL=1;
+                                // measured: config 5 -2 %, config 3 +0.2 %)
   int tile_grid = 0;
   size_t tile_smem = 0;
   static constexpr int kW = 16 / (int)sizeof(T);
@@ -447,11 +451,13 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       c.BY = 8;
       if (B == 1) {
         c.MB = 0; c.W = 2; c.NS = sizeof(T) == 4 ? 6 : 3;
-        // short z extent: 32-cell tiles give more columns (items) than 64-cell ones
-        if (sizeof(T) == 4 && nz + 1 < 64) c.W = 1;
+        // short z extent (config 5: 41 planes, L2-resident, latency-bound): 16-row
+        // tiles with 512 threads (measured 52.4 vs 45.8 Gcell/s for 8-row
+        // tiles; for long z extents the 8-row tiles win: config 3 0.75 vs 0.72)
+        if (sizeof(T) == 4 && nz + 1 < 64) { c.W = 2; c.NS = 4; c.BY = 16; }
       }
       else { c.MB = B; c.W = kW; c.NS = 3; }
-      if (const char* e = getenv("FDTD_TILE")) sscanf(e, "%d,%d", &c.W, &c.NS);
+      if (const char* e = getenv("FDTD_TILE")) { c.BY = 8; sscanf(e, "%d,%d,%d", &c.W, &c.NS, &c.BY); }
       const int64_t span = (int64_t)px * B * (ny + 1) * (nz + 1) + (int64_t)px * B + 64;
       if (fdtd::tile_supported<T>(c) && span < ((int64_t)1 << 31) && !getenv("FDTD_STENCIL_OLD")) {
         use_tile = true; tcfg = c;
@@ -496,6 +502,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     }
     if (getenv("FDTD_NO_TMA")) use_tma = false;
     if (!use_tma) use_tile = false;
+    if (getenv("FDTD_PDL")) use_pdl = true;
     if (const char* e = getenv("FDTD_KCHUNK")) kchunk_max = std::max(1, atoi(e));
   }
 
@@ -1635,22 +1642,34 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   P.check_every = check_every;
   P.bad_step = d_bad;
   const size_t sm = fused_smem;
+  // optional programmatic dependent launch (the kernels wait with
+  // griddepcontrol.wait before reading anything the preceding kernel writes;
+  // without the attribute the wait is a no-op)
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t lc = {};
+  lc.blockDim = dim3(256);
+  lc.dynamicSmemBytes = sm;
+  lc.stream = st;
+  lc.attrs = use_pdl ? pdl : nullptr;
+  lc.numAttrs = use_pdl ? 1 : 0;
   if (fused_gemm) {
-    const unsigned grid = (unsigned)(std::max(n_ctas, 1) * GEMM_KS);
+    lc.gridDim = dim3((unsigned)(std::max(n_ctas, 1) * GEMM_KS));
     switch (NPsel) {
-      case 4: fdtd::reduced_gemm_kernel<T, 4, gemm_rpw(4), GEMM_KS><<<grid, 256, sm, st>>>(P); break;
-      case 8: fdtd::reduced_gemm_kernel<T, 8, gemm_rpw(8), GEMM_KS><<<grid, 256, sm, st>>>(P); break;
-      case 16: fdtd::reduced_gemm_kernel<T, 16, gemm_rpw(16), GEMM_KS><<<grid, 256, sm, st>>>(P); break;
-      default: fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), GEMM_KS><<<grid, 256, sm, st>>>(P); break;
+      case 4: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_gemm_kernel<T, 4, gemm_rpw(4), GEMM_KS>, P)); break;
+      case 8: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_gemm_kernel<T, 8, gemm_rpw(8), GEMM_KS>, P)); break;
+      case 16: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_gemm_kernel<T, 16, gemm_rpw(16), GEMM_KS>, P)); break;
+      default: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), GEMM_KS>, P)); break;
     }
   } else {
-  const unsigned grid = (unsigned)std::max(n_ctas, 1);
-  switch (NBsel) {
-    case 1: fdtd::reduced_fused_kernel<T, 1><<<grid, 256, sm, st>>>(P); break;
-    case 4: fdtd::reduced_fused_kernel<T, 4><<<grid, 256, sm, st>>>(P); break;
-    case 16: fdtd::reduced_fused_kernel<T, 16><<<grid, 256, sm, st>>>(P); break;
-    default: fdtd::reduced_fused_kernel<T, 32><<<grid, 256, sm, st>>>(P); break;
-  }
+    lc.gridDim = dim3((unsigned)std::max(n_ctas, 1));
+    switch (NBsel) {
+      case 1: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_fused_kernel<T, 1>, P)); break;
+      case 4: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_fused_kernel<T, 4>, P)); break;
+      case 16: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_fused_kernel<T, 16>, P)); break;
+      default: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_fused_kernel<T, 32>, P)); break;
+    }
   }
   ++n;
   mark(1, 1);
@@ -1822,6 +1841,23 @@ int Impl<T>::set_state(int which, const double* in, int64_t n) {
   if (which >= 0 && which <= 5) {
     if (n != S * B) return fail(FDTD_EINVAL, "set_state: n must be batch*S");
     if (!F[p][which]) return fail(FDTD_EINVAL, "set_state: component %d unused in 2-D", which);
+    if (!getenv("FDTD_HOST_SET_STATE")) {
+      // on the device: copy the fp64 array, then one scatter / round / mask kernel
+      if (!d_in64) {                  // S * B is fixed per handle: allocated once (owned until destroy)
+        d_in64 = dalloc<double>(S * B);
+        d_in64_n = d_in64 ? S * B : 0;
+      }
+      if (d_in64) {
+        CK(cudaMemsetAsync(F[p][which], 0, sizeof(T) * elems, stream));
+        CK(cudaMemcpyAsync(d_in64, in, sizeof(double) * S * B, cudaMemcpyHostToDevice, stream));
+        const int64_t tot = S * B;
+        fdtd::state_scatter_kernel<T><<<(unsigned)((tot + 255) / 256), 256, 0, stream>>>(
+            d_in64, S, B, nx, ny, nz, px, dim, which, dim == 3 && which <= 2, F[p][which]);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(stream));
+        return FDTD_OK;
+      }
+    }
     std::fill(staging, staging + elems, (T)0);
     // 3-D E entries that are not unknowns (tangential E on the PEC walls) are
     // stored as 0: the stencil keeps their old value (stencil3d.cuh)

@@ -912,6 +912,8 @@ reduced_fused_kernel(const __grid_constant__ FusedParams<T> P) {
   constexpr int VN = Vec<T>::n;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* X = reinterpret_cast<T*>(smem_raw);
+  // launched as a programmatic dependent of the stencil: wait for its results
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   const int64_t step = *P.d_step;
   const bool check = P.check_every > 0 && (step % P.check_every) == 0;
   bool bad = false;
@@ -1011,6 +1013,9 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
       const int u = t / (kc / VN), v = t % (kc / VN);
       cp_async16(Ms + u * mp + v * VN, FB.M + (int64_t)(ct.y + u) * FB.Cp + k_lo + v * VN, true);
     }
+    // M does not depend on the step; the states and G do: launched as a
+    // programmatic dependent of the stencil, wait for it here
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     if (N == NP && N % VN == 0) {
       // X slice, straight 16-byte copies (every k-row is N contiguous words)
       for (int t = threadIdx.x; t < kc * (NP / VN); t += blockDim.x) {
@@ -1467,6 +1472,28 @@ static __global__ void reduce_axpy_f32_kernel(int cols, int N, int splits, const
     xs[(int64_t)ch * 1024 + o] = hi;
     xs[(int64_t)ch * 1024 + 512 + o] = hn - hi;
   }
+}
+
+// fdtd_set_state for a coarse component: in [B][S] fp64 (storage order) ->
+// the padded device layout ((k (ny+1) + j) px + i) B + b, rounded to T; with
+// mask_e, 3-D E entries that are not unknowns are stored as 0 (fdtd.h)
+template <typename T>
+__global__ void state_scatter_kernel(const double* __restrict__ in, int64_t S, int B, int nx, int ny, int nz, int px,
+                                     int dim, int comp, bool mask_e, T* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= S * B) return;
+  const int b = (int)(t / S);
+  const int64_t s = t % S;
+  const int64_t i = s % (nx + 1);
+  int64_t j, k;
+  if (dim == 3) { j = (s / (nx + 1)) % (ny + 1); k = s / ((int64_t)(nx + 1) * (ny + 1)); }
+  else { j = s / (nx + 1); k = 0; }
+  bool keep = true;
+  if (mask_e) {
+    const bool xi = i > 0 && i < nx, yi = j > 0 && j < ny, zi = k > 0 && k < nz;
+    keep = comp == 0 ? (i < nx && yi && zi) : comp == 1 ? (xi && j < ny && zi) : (xi && yi && k < nz);
+  }
+  out[((k * (ny + 1) + j) * px + i) * B + b] = keep ? (T)in[t] : (T)0;
 }
 
 template <typename T>

@@ -8,15 +8,24 @@ namespace fdtd {
 
 namespace {
 
-template <typename T, int NS, int W, int MB, int MINB>
+template <typename T, int NS, int W, int MB, int MINB, int BY = TILE_BY>
 struct TileKernels {
-  static constexpr auto uni = &stencil3d_tile_kernel<T, true, NS, W, MB, MINB>;
-  static constexpr auto mat = &stencil3d_tile_kernel<T, false, NS, W, MB, MINB>;
+  static constexpr auto uni = &stencil3d_tile_kernel<T, true, NS, W, MB, MINB, BY>;
+  static constexpr auto mat = &stencil3d_tile_kernel<T, false, NS, W, MB, MINB, BY>;
 };
 
 template <typename T, typename F>
 bool tile_dispatch(const TileCfg& c, F&& f) {
   // the instantiated variants: B == 1 tiles of 32*W x cells, batched tiles of W members
+  if (c.BY == 16) {
+    // 16-row tiles (512 threads): 15 of 16 rows owned instead of 7 of 8
+    if constexpr (sizeof(T) == 4) {
+      if (c.MB == 0 && c.W == 2 && c.NS == 4) { f(TileKernels<T, 4, 2, 0, 1, 16>{}); return true; }
+    } else {
+      if (c.MB == 0 && c.W == 1 && c.NS == 4) { f(TileKernels<T, 4, 1, 0, 1, 16>{}); return true; }
+    }
+    return false;
+  }
   if (c.BY != TILE_BY) return false;
   if constexpr (sizeof(T) == 4) {
     if (c.MB == 0 && c.W == 2 && c.NS == 4) { f(TileKernels<T, 4, 2, 0, 3>{}); return true; }

@@ -78,7 +78,7 @@ __host__ __device__ constexpr int tile_ep(int RX, int BY, int esz) {
   return ((RX * BY) * esz + 127) / 128 * 128 / esz;
 }
 
-constexpr int TILE_BY = 8;   // tile rows (one warp per row)
+constexpr int TILE_BY = 8;   // default tile rows (one warp per row)
 
 // Persistent work split: the (x, y) tiles are "columns" of nz+1 planes, cut
 // into z-chunks of S.kc planes; item = chunk * ncols + column (chunk-major, so
@@ -128,8 +128,8 @@ __device__ __forceinline__ T local_row(const RowsE<T>& R, int r, int b, int B, T
   return e;
 }
 
-template <typename T, bool UNIFORM, int NS, int W, int MB, int MINB>
-__global__ void __launch_bounds__(32 * TILE_BY, MINB)
+template <typename T, bool UNIFORM, int NS, int W, int MB, int MINB, int BY = TILE_BY>
+__global__ void __launch_bounds__(32 * BY, MINB)
 stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims d, Fields<T> F0,
                       Fields<T> F1, const uint8_t* __restrict__ mat_id, const Coef<T>* __restrict__ gtab,
                       const uint8_t* __restrict__ gifm, int n_mat, Coef<T> u0, Coef<T> u1, RowsE<T> R,
@@ -140,13 +140,16 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
   using L = LV<T, W>;
   using IO = VecIO<T, W>;
   constexpr int RX = 32 * W;                   // elements per tile row
-  constexpr int BY = TILE_BY;
   constexpr int B = XV ? 1 : MB;
   constexpr int SX = (16 / (int)sizeof(T)) > B ? (16 / (int)sizeof(T)) : B;
   constexpr int HW = RX + SX;                  // H box width (elements): SX halo elements + the tile
   constexpr int HP = tile_hp(HW, BY, (int)sizeof(T)), EP = tile_ep(RX, BY, (int)sizeof(T));
   constexpr int STG = 3 * (HP + EP);           // elements per ring stage
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  // programmatic dependent launch: the step's reduced kernel may be scheduled
+  // once every CTA of this grid has started (it then waits for our completion
+  // with griddepcontrol.wait; no stencil CTA is still pending by then)
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int tx = threadIdx.x, ty = threadIdx.y;
   const unsigned base_u = smem_u32(smem_raw);
   unsigned char* smem_al = smem_raw + ((128u - (base_u & 127u)) & 127u);

@@ -309,6 +309,7 @@ def test_tiny4_batch8_leapfrog_skinny_gemm(skinny, monkeypatch):
     ("config3_small", 64, "2,3", 5), ("config3_small", 64, "1,6", 0),
     ("tiny5", 32, "2,6", 0), ("tiny5", 32, "2,4", 13), ("tiny5", 64, "2,3", 0), ("tiny5", 32, "4,3", 3),
     ("tiny4_b16", 32, "4,3", 0), ("tiny4_b16", 32, "4,3", 11), ("tiny4_b16", 64, "2,3", 0),
+    ("config3_small", 32, "2,4,16", 0), ("config3_small", 64, "1,4,16", 0), ("tiny5", 32, "2,4,16", 0),
 ])
 def test_tile_stencil_bitwise_equals_tma_stencil(case, prec, tile, grid, monkeypatch):
     # the tile stencil (stencil3d.cuh: persistent CTAs on balanced ranges of
@@ -415,3 +416,35 @@ def test_local_slot_rows_bitwise_equal_global_rows(case, prec, monkeypatch):
     for c in range(8):
         assert np.array_equal(a[c], b[c]), c
     assert np.array_equal(pa, pb)
+
+
+@pytest.mark.parametrize("case,prec", [("tiny5", 32), ("config3_small", 64), ("tiny4", 32)])
+def test_device_set_state_equals_host_set_state(case, prec, monkeypatch):
+    # fdtd_set_state's device scatter (fp64 copy + one kernel) against the host
+    # scatter loop: identical device arrays (E off the unknowns stored as 0)
+    from paper_1406_7042_b200.fdtd import Sim
+    scn, prob = _prep(case, precision=prec)
+    prob = dict(prob, init={})
+    nx, ny, nz = prob["n"]
+    S = (nx + 1) * (ny + 1) * (nz + 1)
+    rng = np.random.default_rng(7)
+    arrays = {c: rng.uniform(-1, 1, (int(prob.get("batch", 1)), S)) for c in range(6)}
+
+    def run(host):
+        if host:
+            monkeypatch.setenv("FDTD_HOST_SET_STATE", "1")
+        else:
+            monkeypatch.delenv("FDTD_HOST_SET_STATE", raising=False)
+        sim = Sim(prob, precision=prec, graph_steps=0)
+        for c in range(6):
+            sim.set_state(c, arrays[c])
+        out = [sim.get_state(c) for c in range(6)]
+        sim.step(3)
+        sim.sync()
+        out += [sim.get_state(c) for c in range(6)]
+        sim.close()
+        return out
+
+    a, b = run(True), run(False)
+    for c in range(12):
+        assert np.array_equal(a[c], b[c]), c
