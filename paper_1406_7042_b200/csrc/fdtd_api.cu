@@ -1001,7 +1001,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       fprintf(stderr, "fdtd: tile stencil W=%d NS=%d MB=%d smem=%zu per_sm=%d grid=%d items=%d (cols %d x kc %d)\n",
               tcfg.W, tcfg.NS, tcfg.MB, tile_smem, per_sm, tile_grid, tsplit.nitems, tsplit.ncols, tsplit.kc);
   }
-  {
+  if (!use_tile) {                // the reference batched kernel (its tile shape when it is the path)
     const int smv = (int)(sizeof(T) * (3 * 3 * (size_t)(tHBX * (tBY + 1) + 32) + 6 * 3 * (size_t)(tBX * tBY + 32)) +
                           sizeof(fdtd::MatTable<T>) + 512);
     CK(cudaFuncSetAttribute(fdtd::stencil3d_tma_vec_kernel<T, false, 3, kW>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -21,6 +21,7 @@ bool tile_dispatch(const TileCfg& c, F&& f) {
     // 16-row tiles (512 threads): 15 of 16 rows owned instead of 7 of 8
     if constexpr (sizeof(T) == 4) {
       if (c.MB == 0 && c.W == 2 && c.NS == 4) { f(TileKernels<T, 4, 2, 0, 1, 16>{}); return true; }
+      if (c.MB == 16 && c.W == 4 && c.NS == 3) { f(TileKernels<T, 3, 4, 16, 1, 16>{}); return true; }
     } else {
       if (c.MB == 0 && c.W == 1 && c.NS == 4) { f(TileKernels<T, 4, 1, 0, 1, 16>{}); return true; }
     }

@@ -185,13 +185,13 @@ tc_skinny_gemm_kernel(const __grid_constant__ CUtensorMap amap, int rows, int K,
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (lane == 0) {
           const uint32_t base = su32(smem + s * STAGE_BYTES);
-          const uint32_t ahi = base, alo = base + A_BYTES, xhi = base + 2 * A_BYTES, xlo = xhi + B_BYTES;
+          // stage: a_hi | a_lo | x_hi | x_lo, the two x tiles contiguous = one 32-row B
+          const uint32_t ahi = base, alo = base + A_BYTES, xhi = base + 2 * A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint32_t o = (uint32_t)kk * 32u;       // 8 tf32 = 32 bytes along the swizzled row
             const uint64_t dah = sw128_desc(ahi + o), dal = sw128_desc(alo + o);
             const uint64_t dx = sw128_desc(xhi + o);     // [x_hi ; x_lo]: 32 rows of B
-            (void)xlo;
             // D0 = a_hi [x_hi | x_lo], D1 = a_lo [x_hi | x_lo] (its x_lo half unused);
             // one accumulator set per k-step of the chunk: KSETS independent chains
             const uint32_t dk = d + (uint32_t)((kk % KSETS) * 4 * BN);

@@ -310,6 +310,7 @@ def test_tiny4_batch8_leapfrog_skinny_gemm(skinny, monkeypatch):
     ("tiny5", 32, "2,6", 0), ("tiny5", 32, "2,4", 13), ("tiny5", 64, "2,3", 0), ("tiny5", 32, "4,3", 3),
     ("tiny4_b16", 32, "4,3", 0), ("tiny4_b16", 32, "4,3", 11), ("tiny4_b16", 64, "2,3", 0),
     ("config3_small", 32, "2,4,16", 0), ("config3_small", 64, "1,4,16", 0), ("tiny5", 32, "2,4,16", 0),
+    ("tiny4_b16", 32, "4,3,16", 0),
 ])
 def test_tile_stencil_bitwise_equals_tma_stencil(case, prec, tile, grid, monkeypatch):
     # the tile stencil (stencil3d.cuh: persistent CTAs on balanced ranges of
