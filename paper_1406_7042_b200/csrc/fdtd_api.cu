@@ -175,6 +175,7 @@ struct Impl : public fdtd_t {
   bool fused_gemm = false;
   int NPsel = 32;
   static constexpr int GEMM_KS = 4;
+  int gks = GEMM_KS;            // cluster K-split of the fused GEMM (N = 32: 8 by default, FDTD_GEMM_KS = 2 | 4 | 8)
   // rows per thread of the GEMM kernel: 64-row tiles for NP <= 16, 32 for NP = 32
   static constexpr int gemm_rpw(int np) { return np == 32 ? 2 : np / 4; }
   int64_t step_offset = 0;            // device step = host step + offset (set_state(8))
@@ -1051,6 +1052,8 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 8, gemm_rpw(8), GEMM_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
     CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 16, gemm_rpw(16), GEMM_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
     CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), GEMM_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+    CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+    CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
   }
   if (!fused_gemm && fused_smem > 48 * 1024) {
     CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
@@ -1375,7 +1378,11 @@ int Impl<T>::build_fused(const fdtd_probes* probes) {
   // overrides); the GEMM kernel's shared memory must fit
   {
     const int TRg = 8 * (32 / NPsel) * gemm_rpw(NPsel);
-    const size_t need = (size_t)(TRg * NPsel + maxCp / GEMM_KS * NPsel + TRg * (maxCp / GEMM_KS + 16 / sizeof(T))) * sizeof(T);
+    if (NPsel == 32) {
+      gks = 8;                  // measured: config 5 53.2 (K-split 8) vs 52.2 (4) vs 50.8 (2) Gcell/s
+      if (const char* e = getenv("FDTD_GEMM_KS")) { const int k = atoi(e); if (k == 2 || k == 4 || k == 8) gks = k; }
+    }
+    const size_t need = (size_t)(TRg * NPsel + maxCp / gks * NPsel + TRg * (maxCp / gks + 16 / sizeof(T))) * sizeof(T);
     fused_gemm = maxN >= 4;
     if (const char* e = getenv("FDTD_FUSED")) fused_gemm = std::string(e) == "gemm";
     if (need > 200 * 1024) fused_gemm = false;
@@ -1460,8 +1467,8 @@ int Impl<T>::build_fused(const fdtd_probes* probes) {
   rows_per_cta = ROWS;
   n_ctas = (int)ctas.size();
   NBsel = maxN <= 1 ? 1 : maxN <= 4 ? 4 : maxN <= 16 ? 16 : 32;
-  fused_smem = fused_gemm ? (size_t)(ROWS * NPsel + max_cols / GEMM_KS * NPsel +
-                                     ROWS * (max_cols / GEMM_KS + 16 / sizeof(T))) * sizeof(T)
+  fused_smem = fused_gemm ? (size_t)(ROWS * NPsel + max_cols / gks * NPsel +
+                                     ROWS * (max_cols / gks + 16 / sizeof(T))) * sizeof(T)
                           : (size_t)max_cols * maxN * sizeof(T);
   if (fused_smem > 200 * 1024)
     return fail(FDTD_ENOTSUP, "fused reduced kernel needs %zu bytes of shared memory (> 200 KB)", fused_smem);
@@ -1655,12 +1662,16 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   lc.attrs = use_pdl ? pdl : nullptr;
   lc.numAttrs = use_pdl ? 1 : 0;
   if (fused_gemm) {
-    lc.gridDim = dim3((unsigned)(std::max(n_ctas, 1) * GEMM_KS));
+    lc.gridDim = dim3((unsigned)(std::max(n_ctas, 1) * gks));
     switch (NPsel) {
       case 4: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_gemm_kernel<T, 4, gemm_rpw(4), GEMM_KS>, P)); break;
       case 8: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_gemm_kernel<T, 8, gemm_rpw(8), GEMM_KS>, P)); break;
       case 16: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_gemm_kernel<T, 16, gemm_rpw(16), GEMM_KS>, P)); break;
-      default: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), GEMM_KS>, P)); break;
+      default:
+        if (gks == 2) CK(cudaLaunchKernelEx(&lc, fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), 2>, P));
+        else if (gks == 8) CK(cudaLaunchKernelEx(&lc, fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), 8>, P));
+        else CK(cudaLaunchKernelEx(&lc, fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), GEMM_KS>, P));
+        break;
     }
   } else {
     lc.gridDim = dim3((unsigned)std::max(n_ctas, 1));
