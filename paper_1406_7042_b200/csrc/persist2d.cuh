@@ -228,6 +228,8 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
     }
   }
   const int rows_lo = P.R.tile_ptr[t], rows_hi = P.R.tile_ptr[t + 1];
+  // explicit-row cells exist only in tiles with rows (the others skip the check)
+  const bool tile_rows = !uniform && rows_hi > rows_lo;
   for (int r = rows_lo + tid; r < rows_hi; r += nthr) {
     P2Row<T> x;
     x.c = P.R.c[r]; x.cs = P.R.cs[r]; x.yo = P.R.yo[r]; x.li = P.R.li[r]; x.src = P.R.src[r];
@@ -251,7 +253,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       const int i = i0 + il, j = j0 + jl;
       const int c = jl * TX + il;
       const int m = smat[c];
-      if (!uniform && (ifm[m] & 4)) return;                // explicit row below
+      if (tile_rows && (ifm[m] & 4)) return;               // explicit row below
       const T hy = sHy[c], hx = sHx[c];
       const T hyim = (il > 0) ? sHy[c - 1] : hL[jl];
       const T hxm = (jl > 0) ? sHx[c - TX] : hB[il];
@@ -274,12 +276,12 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
         const uint16_t m2 = *reinterpret_cast<const uint16_t*>(smat + c);
         const int ma = m2 & 0xff, mb = m2 >> 8;
         float e0 = ez2.x, e1 = ez2.y;
-        if (ia > 0 && i0 + ia < nx && !(!uniform && (ifm[ma] & 4))) {
+        if (ia > 0 && i0 + ia < nx && !(tile_rows && (ifm[ma] & 4))) {
           const Coef<T> cc = uniform ? P.u0 : cE[ma];
           const T dd = (hy2.x - sHy[c - 1]) - (hx2.x - hxm2.x);
           e0 = (j0 + jl > 0) ? e0 + cc.apply(dd) : (T)0;
         }
-        if (i0 + ia + 1 < nx && !(!uniform && (ifm[mb] & 4))) {
+        if (i0 + ia + 1 < nx && !(tile_rows && (ifm[mb] & 4))) {
           const Coef<T> cc = uniform ? P.u0 : cE[mb];
           const T dd = (hy2.y - hy2.x) - (hx2.y - hxm2.y);
           e1 = (j0 + jl > 0) ? e1 + cc.apply(dd) : (T)0;
