@@ -132,34 +132,52 @@ def algorithmic_bytes_per_cell(prob, precision):
     return words * w + mat
 
 
-def run_oracle_sample(prob, seconds=15.0, max_steps=800):
-    """Time the CPU oracle (oracle.problem_step, single-threaded SciPy SpMV) on a
-    bounded number of steps of the same workload."""
-    try:
-        from threadpoolctl import threadpool_limits
-        lim = threadpool_limits(limits=1)
-    except Exception:
-        lim = None
-    from oracle import problem_step as ps
-    from oracle.matrix_form import step_leapfrog
-    rec = ps.build(prob)
-    E, H = ps.initial_state(rec, prob, 0)
-    PE, PH = ps.probe_matrices(rec)
-    done, t0 = 0, time.perf_counter()
-    while done < max_steps:
-        su = None
-        if len(rec.src_row) and done < rec.wave.shape[0]:
-            su = np.zeros(len(E))
-            np.add.at(su, rec.src_row, -rec.src_coef * rec.wave[done, rec.src_col, 0])
-        E, H = step_leapfrog(E, H, rec.GE, rec.GH, rec.KE, rec.KH, su_E=su)
-        _ = PE @ E + PH @ H
-        done += 1
-        if time.perf_counter() - t0 > seconds:
-            break
-    el = time.perf_counter() - t0
-    if lim is not None:
-        lim.unregister() if hasattr(lim, "unregister") else None
-    return done, el
+class OracleStepper:
+    """The CPU oracle (oracle.problem_step: SciPy CSR SpMV, single-threaded)
+    stepping batch member 0 of a workload; assembly once, then timed steps."""
+
+    def __init__(self, prob):
+        from oracle import problem_step as ps
+        t0 = time.perf_counter()
+        self.rec = ps.build(prob)
+        self.t_build = time.perf_counter() - t0
+        self.E, self.H = ps.initial_state(self.rec, prob, 0)
+        self.PE, self.PH = ps.probe_matrices(self.rec)
+        self.step_no = 0
+
+    def run(self, max_steps, seconds=1e9):
+        from oracle.matrix_form import step_leapfrog
+        try:
+            from threadpoolctl import threadpool_limits
+            lim = threadpool_limits(limits=1)
+        except Exception:
+            lim = None
+        rec = self.rec
+        done, t0 = 0, time.perf_counter()
+        while done < max_steps:
+            su = None
+            if len(rec.src_row) and self.step_no < rec.wave.shape[0]:
+                su = np.zeros(len(self.E))
+                np.add.at(su, rec.src_row, -rec.src_coef * rec.wave[self.step_no, rec.src_col, 0])
+            self.E, self.H = step_leapfrog(self.E, self.H, rec.GE, rec.GH, rec.KE, rec.KH, su_E=su)
+            _ = self.PE @ self.E + self.PH @ self.H
+            done += 1
+            self.step_no += 1
+            if time.perf_counter() - t0 > seconds:
+                break
+        el = time.perf_counter() - t0
+        if lim is not None and hasattr(lim, "unregister"):
+            lim.unregister()
+        return done, el
+
+
+def run_oracle_sample(prob, seconds=15.0, max_steps=800, member_cells=None):
+    """Time the oracle on a bounded number of steps of the same workload.
+    Returns (steps, seconds, assembly seconds)."""
+    st = OracleStepper(prob)
+    st.run(2)                                   # warm-up (first-touch of the matrices)
+    done, el = st.run(max_steps, seconds)
+    return done, el, st.t_build
 
 
 def bench_reference(args):
@@ -170,21 +188,23 @@ def bench_reference(args):
     scn, prob, info = build_workload(args.config, args.precision)
     cells = cells_of(prob)
     per = max(1, args.ref_steps)
+    st = OracleStepper(prob)
     tot_steps, tot_t = 0, 0.0
     for i in range(args.warmup + args.steps):
-        n, el = run_oracle_sample(prob, seconds=1e9, max_steps=per)
+        n, el = st.run(per)
         if i >= args.warmup:
             tot_steps += n
             tot_t += el
     val = cells * tot_steps / tot_t / 1e6
-    sample = f"{per} oracle time steps per bench step of {WORKLOADS[args.config].split(':')[0]}"
+    sample = (f"{per} oracle time steps (batch member 0) per bench step of {WORKLOADS[args.config].split(':')[0]}; "
+              f"matrix assembly {st.t_build:.0f} s not timed")
     out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "Mcell-updates/s",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": WORKLOADS[args.config], "oracle_steps_per_step": per},
            "cpu_baseline": {"value": val, "unit": "Mcell-updates/s", "cores": 1, "kind": "oracle",
-                            "sample": sample},
+                            "sample": sample, **cpu_info()},
            "e2e": {"value": val, "unit": "Mcell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
@@ -193,23 +213,63 @@ def bench_reference(args):
 METRIC = "Mcell-updates/s (coarse grid + reduced blocks) at 1 B200"
 
 
-def bench_ours(args):
+def _fp32_peak_gflops():
+    """SIMT FP32 FMA peak: SMs x 128 lanes x 2 flop x max SM clock."""
     import torch
-    from paper_1406_7042_b200 import build as B
-    from paper_1406_7042_b200.dist import barrier, finalize, init, reduce_max, reduce_sum
+    pr = torch.cuda.get_device_properties(0)
+    mhz = 1965.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", mhz))
+    except Exception:
+        pass
+    return pr.multi_processor_count * 128 * 2 * mhz * 1e-3
+
+
+def _tf32_peak_gflops():
+    """Dense TF32 tensor peak: the measured bf16 figure x the nominal tf32/bf16
+    ratio 1/2 (B200_PROFILING.md)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]) * 1e3 / 2
+    except Exception:
+        return 2250e3 / 2
+
+
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    pools = None
+    try:
+        from threadpoolctl import threadpool_info
+        pools = [{k: d.get(k) for k in ("internal_api", "num_threads")} for d in threadpool_info()]
+    except Exception:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "threadpools": pools}
+
+
+def measure(config, prec, steps, warmup, args, rank=0, world=1, local=0, headline=False):
+    """One configuration: W warm-up runs, K timed runs of the whole workload
+    (``n_steps`` time steps each, inputs resident in HBM), then the per-kernel
+    profile, the end-to-end run with host buffers and the CPU oracle sample."""
+    import torch
+    from paper_1406_7042_b200.dist import barrier, reduce_max, reduce_sum
     from paper_1406_7042_b200.fdtd import PHASES, Sim
-    B.build()
-    rank, world, local = init()
-    prec = args.precision
-    scn, prob, info = build_workload(args.config, prec, rank)
+    scn, prob, info = build_workload(config, prec, rank)
     n_steps = int(args.time_steps or scn["n_steps"])
     cells = cells_of(prob) * int(prob.get("batch", 1))
     stream = torch.cuda.current_stream()
-    sim = Sim(prob, precision=prec, probe_capacity=(args.warmup + args.steps + 2) * n_steps + 16,
+    sim = Sim(prob, precision=prec, probe_capacity=(warmup + steps + 2) * n_steps + 16,
               graph_steps=args.graph_steps)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    # warm-up (W full runs)
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         sim.step(n_steps)
     sim.sync()
     _ = sim.probe()
@@ -220,7 +280,7 @@ def bench_ours(args):
     clocks.start()
     evs = []
     l0 = sim.launch_count()
-    for _ in range(args.steps):
+    for _ in range(steps):
         flush.zero_()                                  # L2 flush between timed iterations
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -235,11 +295,12 @@ def bench_ours(args):
     launches = sim.launch_count() - l0
     ms = sum(a.elapsed_time(b) for a, b in evs)
     ms_max = reduce_max(ms)
-    units = reduce_sum(float(cells) * n_steps * args.steps)
+    units = reduce_sum(float(cells) * n_steps * steps)
     value = units / (ms_max / 1e3) / 1e6
     sim.sync()
     _ = sim.probe()
-    # per-kernel device times (eager launches with CUDA events on the same stream)
+    # per-kernel device times: eager launches with CUDA events on the launching
+    # stream (the same kernels the graphs replay)
     prof_steps = min(n_steps, args.profile_steps)
     sim.profile(True)
     sim.step(prof_steps)
@@ -247,57 +308,76 @@ def bench_ours(args):
     ph = sim.phase_times()
     sim.profile(False)
     _ = sim.probe()
-    stencil_ms = ph["stencil"] / max(ph["steps"], 1)
-    grid_ms = ph["reduced_grid"] / max(ph["steps"], 1)
-    step_ms_prof = sum(ph[p] for p in PHASES) / max(ph["steps"], 1)
+    nph = max(ph["steps"], 1)
+    stencil_ms = ph["stencil"] / nph
+    grid_ms = ph["reduced_grid"] / nph
+    red_ms = ph["reduced"] / nph
+    step_ms_prof = sum(ph[p] for p in PHASES) / nph
     peak, peak_kind = _peaks()
     bpc = algorithmic_bytes_per_cell(prob, prec)
-    alg_bytes = bpc * cells_of(prob) * int(prob.get("batch", 1))
-    achieved = alg_bytes / (stencil_ms * 1e-3) / 1e9
+    alg_bytes = bpc * cells
     paths = sim.path()
     persistent = "persistent2d" in paths
-    # leap-frog reduced blocks (config 4): the HBM-streamed matrices per step
-    # (K~' and K~'^T once each, S_E twice: y = S_E h~ and S_E^T G) + the states
     w = 4 if prec == 32 else 8
-    grid_bytes = 0
-    red_flops = 0.0
+    # reduced blocks: algorithmic bytes (K~' and S_E each read twice) and flops
+    # (4 (q_e q_h + n_if q_h) per column per step)
+    red_bytes, red_flops = 0, 0.0
     for b in prob.get("blocks") or []:
         qe = int(b.get("qe", b.get("q"))); qh = int(b.get("qh", b.get("q")))
         nif = int(np.asarray(b["S_E"]).size // qh)
         Nb = int(b["n_inst"]) * int(prob.get("batch", 1))
-        grid_bytes += w * (2 * qe * qh + 2 * nif * qh + 4 * (qe + qh + nif) * Nb)
-        # 4 (q_e q_h + n_if q_h) flops per column per step (each
-        # of K~', S_E applied twice, multiply + add)
+        red_bytes += w * (2 * qe * qh + 2 * nif * qh + 4 * (qe + qh + nif) * Nb)
         red_flops += 4.0 * (qe * qh + nif * qh) * Nb
-    grid_kernel = None
-    if grid_ms > 0:
-        kname = ("reduced leap-frog products (a4+a6): split-K TN GEMMs for K~' h~, K~'^T e~, S_E^T G; "
-                 "y = S_E h~ on tcgen05 (3xTF32)" if "tc_gemm" in sim.path() else
-                 "reduced leap-frog products (a4+a6): GEMV / SIMT GEMM kernels")
-        ach = grid_bytes / (grid_ms * 1e-3) / 1e9
-        grid_kernel = {"kernel": kname, "bound": "hbm", "algorithmic_bytes_per_step": grid_bytes, "avg_ms": grid_ms,
-                       "achieved": ach, "peak": peak, "frac": ach / peak,
-                       "gflops": red_flops / (grid_ms * 1e-3) / 1e9,
+    fp32_peak = _fp32_peak_gflops()
+    reduced = None
+    if red_flops > 0:
+        step_ms = ms_max / steps / n_steps
+        if persistent:
+            # the reduced CTAs of the persistent kernel: their rows of M stay in
+            # shared memory for the whole launch; their throughput is the
+            # step's (they run beside the tiles), bounded by the exchange chain
+            gf = red_flops / (step_ms * 1e-3) / 1e9
+            reduced = {"kernel": "persist2d reduced CTAs (fused M rows resident in shared memory)",
+                       "bound": "latency (G -> reduced CTAs -> y chain per step)", "gflops": gf,
+                       "roofline_gflops": fp32_peak, "frac": gf / fp32_peak,
+                       "algorithmic_gflop_per_step": red_flops / 1e9,
+                       "note": "flops per time step / measured ms per time step of the timed launch"}
+        elif grid_ms > 0:
+            # leap-frog blocks streamed from HBM (config 4): AI = 8 flop/B
+            ai = red_flops / red_bytes
+            roof = min(ai * peak, _tf32_peak_gflops() if "tc_gemm" in paths else fp32_peak)
+            gf = red_flops / (grid_ms * 1e-3) / 1e9
+            ach = red_bytes / (grid_ms * 1e-3) / 1e9
+            reduced = {"kernel": ("leap-frog reduced products (a4+a6): split-K TN GEMMs K~' h~, K~'^T e~, "
+                                  "S_E^T G; y = S_E h~ on tcgen05 (3xTF32)" if "tc_gemm" in paths else
+                                  "leap-frog reduced products (a4+a6): GEMV / SIMT GEMM kernels"),
+                       "bound": "hbm", "avg_ms": grid_ms, "algorithmic_bytes_per_step": red_bytes,
+                       "achieved_gbs": ach, "hbm_frac": ach / peak, "gflops": gf,
+                       "roofline_gflops": roof, "frac": gf / roof,
                        "note": "eager per-step launches with CUDA events (includes launch gaps)"}
+        elif red_ms > 0:
+            gf = red_flops / (red_ms * 1e-3) / 1e9
+            reduced = {"kernel": "fused reduced update (reduced_fused_kernel / reduced_gemm_kernel)",
+                       "bound": "latency (L2-resident M, one GEMM phase per step)", "avg_ms": red_ms,
+                       "gflops": gf, "roofline_gflops": fp32_peak, "frac": gf / fp32_peak,
+                       "algorithmic_gflop_per_step": red_flops / 1e9,
+                       "note": "eager per-step launch with CUDA events; SIMT fp32 FMA roofline"}
     traffic = None
     tf = os.path.join(ROOT, "profiles", "stencil_traffic.json")
     if os.path.exists(tf):
         try:
             with open(tf) as f:
                 tj = json.load(f)
-            traffic = tj.get(f"config{args.config}_fp{prec}" + ("_persistent" if persistent else ""))
+            traffic = tj.get(f"config{config}_fp{prec}" + ("_persistent" if persistent else ""))
         except Exception:
             traffic = None
-    # end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
         comps = (0, 1, 2, 3, 4, 5) if prob["dim"] == 3 else (2, 3, 4)
         host_state = {c: np.zeros((sim.B, sim.S)) for c in comps}
-        wsize = 4 if prec == 32 else 8
-        h2d = len(comps) * sim.S * sim.B * wsize
-        e2e_ms = 0.0
-        d2h = 0
-        # one untimed end-to-end warm-up (first-use allocations of the upload path)
+        # fdtd_set_state takes fp64 host arrays (fdtd.h): those are the bytes copied
+        h2d = sum(host_state[c].nbytes for c in comps)
+        e2e_ms, d2h = 0.0, 0
         for c in comps:
             sim.set_state(c, host_state[c])
         sim.step(min(n_steps, 32))
@@ -311,69 +391,98 @@ def bench_ours(args):
             series = sim.probe()
             t1 = time.perf_counter()
             e2e_ms += (t1 - t0) * 1e3
-            d2h = series.size * wsize
+            d2h = series.nbytes
         e2e_ms /= max(1, args.e2e_steps)
         e2e_ms = reduce_max(e2e_ms)
         e2e = {"value": float(cells) * n_steps * world / (e2e_ms / 1e3) / 1e6, "unit": "Mcell-updates/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
+               "note": "fdtd_set_state of every coarse component from fp64 host arrays, fdtd_step, "
+                       "fdtd_probe (fp64 series) per bench step"}
     sim.close()
+    del flush
+    torch.cuda.empty_cache()
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and args.config == 4:
-        cpu = {"value": None, "unit": "Mcell-updates/s", "cores": 1, "kind": "oracle",
-               "sample": "unavailable: the oracle's matrix form of config 4 (8.5 M cells + a 65,024 x 1,024 "
-                         "coupling block) exceeds host memory; parity uses oracle.problem_step."
-                         "sampled_hybrid_step"}
-    elif rank == 0 and world == 1 and not args.no_cpu:
-        ns, el = run_oracle_sample(prob, seconds=args.cpu_seconds)
-        cpu = {"value": cells_of(prob) * ns / el / 1e6, "unit": "Mcell-updates/s", "cores": 1,
-               "kind": "oracle",
-               "sample": f"{ns} time steps of the same workload in {el:.1f} s (SciPy CSR SpMV, 1 thread)"}
-    red_ms = ph["reduced"] / max(ph["steps"], 1)
-    reduced_fused = None
-    if red_ms > 0 and grid_ms == 0 and red_flops > 0:
-        # fused blocks: the whole reduced update of a step (one GEMV / GEMM phase)
-        reduced_fused = {"kernel": "fused reduced update (reduced_fused_kernel / reduced_gemm_kernel)",
-                         "algorithmic_gflop_per_step": red_flops / 1e9, "avg_ms": red_ms,
-                         "gflops": red_flops / (red_ms * 1e-3) / 1e9,
-                         "note": "eager per-step launch with CUDA events; FMA roofline: SIMT fp32"}
-    per_step = {"phase_ms_per_step": {p: ph[p] / max(ph["steps"], 1) for p in PHASES}, "reduced_grid": grid_kernel,
-                "reduced_fused": reduced_fused}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            ns, el, t_build = run_oracle_sample(prob, seconds=args.cpu_seconds, member_cells=cells_of(prob))
+            cpu = {"value": cells_of(prob) * ns / el / 1e6, "unit": "Mcell-updates/s", "cores": 1,
+                   "kind": "oracle",
+                   "sample": (f"{ns} time steps of batch member 0 of the same workload in {el:.1f} s "
+                              f"(oracle.problem_step, SciPy CSR SpMV, 1 thread; matrix assembly {t_build:.0f} s "
+                              "not timed)" + ("; per-member rate (the batch's members are independent)"
+                                              if int(prob.get("batch", 1)) > 1 else "")),
+                   **cpu_info()}
+        except MemoryError as ex:
+            cpu = {"value": None, "unit": "Mcell-updates/s", "cores": 1, "kind": "oracle",
+                   "sample": f"unavailable: {ex}", **cpu_info()}
+    per_step = {"phase_ms_per_step": {p: ph[p] / nph for p in PHASES}}
     if persistent:
-        # the timed path is ONE persistent launch per bench step (n_steps time
-        # steps, state resident in shared memory): algorithmic bytes = what a
-        # streaming step moves (state read + write) x n_steps; DRAM traffic of
-        # the launch (ncu) is ~ the state once in and once out
-        launch_ms = ms_max / args.steps
+        # ONE persistent launch per bench step (n_steps time steps, state
+        # resident in shared memory): algorithmic bytes = what a streaming step
+        # moves (state read + write) x n_steps; the launch's DRAM traffic is
+        # ~ the state once in and once out
+        launch_ms = ms_max / steps
         alg_launch = alg_bytes * n_steps
         ach = alg_launch / (launch_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": traffic, "kernel": "persist2d (tiles resident in shared memory, whole run per launch)",
+                "traffic": traffic, "kernel": "persist2d_kernel (tiles resident in shared memory, whole run "
+                                              "per launch; HBM-equivalent effective bandwidth, SURVEY §8(d))",
                 "algorithmic_bytes_per_launch": alg_launch, "avg_launch_ms": launch_ms, "share_of_step": 1.0,
                 "peak_kind": peak_kind, "paths": paths,
-                "per_step_kernels_eager_profile": dict(per_step, stencil_achieved_gbs=achieved)}
+                "per_step_kernels_eager_profile": dict(per_step, stencil_achieved_gbs=alg_bytes / (stencil_ms * 1e-3) / 1e9)}
     else:
+        achieved = alg_bytes / (stencil_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
-                "kernel": "stencil2d (fused E->H)" if prob["dim"] == 2 else "stencil3d (fused E->H)",
+                "kernel": "stencil2d (fused E->H)" if prob["dim"] == 2 else "stencil3d_tile_kernel (fused E->H)",
                 "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": stencil_ms,
                 "share_of_step": stencil_ms / step_ms_prof if step_ms_prof else None,
                 "peak_kind": peak_kind, "paths": paths, **per_step}
+    out = {"value": value, "ms_per_step": ms_max / steps, "steps": steps, "warmup": warmup,
+           "dtype": "f32" if prec == 32 else "f64",
+           "config": {"workload": WORKLOADS[config], "time_steps_per_step": n_steps, "cells": cells_of(prob),
+                      "batch": int(prob.get("batch", 1)), "q": [b["q"] for b in prob.get("blocks") or []],
+                      "l2": ("flushed (256 MB write) between timed steps; state resident in shared memory for "
+                             "the whole launch" if persistent else
+                             "flushed (256 MB write) between timed steps")},
+           "roofline": roof, "reduced_block": reduced, "cpu_baseline": cpu, "e2e": e2e,
+           "gpu_launches": int(launches), "clocks": clk,
+           "prep": {k: v for k, v in info.items() if k in ("n_if", "alpha", "coarse_sigma", "coarse_limit")}}
+    return out
+
+
+METRIC_CONFIGS = {"config2_fp32": (2, 32), "config3_fp32": (3, 32), "config3_fp64": (3, 64),
+                  "config5_fp32": (5, 32)}
+
+
+def bench_ours(args):
+    from paper_1406_7042_b200 import build as B
+    from paper_1406_7042_b200.dist import finalize, init
+    B.build()
+    rank, world, local = init()
+    head = measure(args.config, args.precision, args.steps, args.warmup, args, rank, world, local, headline=True)
+    per = {}
+    if args.per_config and world == 1:
+        for name, (c, p) in METRIC_CONFIGS.items():
+            if c == args.config and p == args.precision:
+                continue
+            try:
+                per[name] = measure(c, p, args.per_config_steps, max(3, args.per_config_warmup), args,
+                                    rank, world, local)
+            except Exception as ex:       # report, never hide: the headline line still prints
+                per[name] = {"error": f"{type(ex).__name__}: {ex}"}
     if rank == 0:
-        out = {"metric": METRIC, "value": value, "unit": "Mcell-updates/s", "n_gpus": world,
-               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        cfg = dict(head["config"])
+        cfg.update(parallelism=f"replicas x{world}")
+        out = {"metric": METRIC, "value": head["value"], "unit": "Mcell-updates/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-               "dtype": "f32" if prec == 32 else "f64",
-               "data": "synthetic (seeded, SURVEY §8(d) recipe)",
-               "config": {"workload": WORKLOADS[args.config], "time_steps_per_step": n_steps,
-                          "cells": cells_of(prob), "q": [b["q"] for b in prob.get("blocks") or []],
-                          "parallelism": f"replicas x{world}",
-                          "l2": ("flushed (256 MB write) between timed steps; state resident in shared "
-                                 "memory for the whole launch" if persistent else
-                                 "flushed (256 MB write) between timed steps; the state is L2-resident "
-                                 "within a step when it fits (126 MB L2)")},
-               "roofline": roof,
-               "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
-               "prep": {k: v for k, v in info.items() if k in ("n_if", "alpha", "coarse_sigma", "coarse_limit")}}
+               "dtype": head["dtype"], "data": "synthetic (seeded, SURVEY §8(d) recipe)",
+               "config": cfg, "roofline": head["roofline"], "reduced_block": head["reduced_block"],
+               "cpu_baseline": head["cpu_baseline"], "e2e": head["e2e"], "gpu_launches": head["gpu_launches"],
+               "clocks": head["clocks"], "prep": head["prep"]}
+        if per:
+            out["per_config"] = per
         print(json.dumps(out), flush=True)
     finalize()
     return 0
@@ -385,7 +494,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--precision", type=int, default=None)
     ap.add_argument("--graph-steps", type=int, default=32)
     ap.add_argument("--profile-steps", type=int, default=2000)
@@ -395,6 +504,10 @@ def main(argv=None):
     ap.add_argument("--time-steps", type=int, default=0, help="override the workload's time steps per bench step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-per-config", dest="per_config", action="store_false",
+                    help="only the headline configuration (default: also configs 2, 3 fp32/fp64, 5)")
+    ap.add_argument("--per-config-steps", type=int, default=3)
+    ap.add_argument("--per-config-warmup", type=int, default=3)
     args = ap.parse_args(argv)
     if args.precision is None:
         args.precision = 32 if args.config in (2, 3, 4, 5) else 64

@@ -88,14 +88,3 @@ def update_matrix(R, F):
 
 def update_eigenvalues(R, F):
     return np.linalg.eigvals(update_matrix(R, F))
-
-
-def max_abs_eig_sparse(R, F, k=6):
-    """Largest |lambda| of (R+F)^{-1}(R-F) via ARPACK (for systems too big for a
-    dense eig).  Uses a sparse LU of R+F."""
-    lu = spla.splu((R + F).tocsc())
-    M = (R - F).tocsr()
-    op = spla.LinearOperator(R.shape, matvec=lambda v: lu.solve(M @ v), dtype=float)
-    vals = spla.eigs(op, k=k, which="LM", return_eigenvectors=False, tol=1e-12,
-                     maxiter=20000)
-    return float(np.max(np.abs(vals)))

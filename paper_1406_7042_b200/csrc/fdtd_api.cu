@@ -690,6 +690,22 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       gdst.push_back((int64_t)l * D.N + (int64_t)in * B);        // within the block's [n_if][N]
     }
   }
+  // the converse: every E unknown whose material carries an if_mask bit must
+  // be an interface row (the per-step and the persistent kernels skip such
+  // cells in the regular update; without a row the cell would be frozen in
+  // one path and updated in the other)
+  if (!uniform) {
+    bool any_bit = false;
+    for (size_t m = 0; m < ifmask.size(); ++m) any_bit |= (ifmask[m] & 7) != 0;
+    if (any_bit)
+      for (int64_t s = 0; s < S; ++s) {
+        const uint8_t bits = ifmask[ids[s]] & 7;
+        if (!bits) continue;
+        for (int c = 0; c < 3; ++c)
+          if (((bits >> c) & 1) && is_e(c) && !row_of.count((int64_t)c * S + s))
+            return fail(FDTD_EINVAL, "storage index %lld: if_mask bit %d set but no interface row", (long long)s, c);
+      }
+  }
   int64_t n_src = 0, n_wave = 0, n_cols = 0;
   std::vector<T> wave;
   std::vector<int32_t> wcol;
@@ -1144,6 +1160,25 @@ int Impl<T>::setup_persist() {
       nr = std::min(capacity - nt, std::max(1, (Rtot + 7) / 8));
       if (nr < 1) continue;
       r = (Rtot + nr - 1) / nr;
+      // fp32 LL exchange: a reduced CTA whose rows of some block are ALL probe
+      // rows is on no dependency chain (nothing waits for its outputs), so the
+      // block's e~ / h~ owners could overwrite the tagged copies it still has
+      // to read.  Choose the rows per CTA so that every CTA that holds probe
+      // rows of a block also holds an h~ / y / e~ row of that block (whose
+      // output the owners' next step waits for).
+      auto probe_only = [&](int rr) {
+        for (int a = 0; a < Rtot; a += rr) {
+          const int bnd = std::min(Rtot, a + rr);
+          for (int b = 0; b < nfb; ++b) {
+            const int r0 = p_row0[b], r1 = p_row0[b + 1];
+            const int s0 = std::max(a, r0), s1 = std::min(bnd, r1);
+            if (s0 < s1 && s0 >= r0 + fblocks[b].qh + fblocks[b].n_if + fblocks[b].qe) return true;
+          }
+        }
+        return false;
+      };
+      while (r < Rtot && probe_only(r)) ++r;
+      if (probe_only(r)) continue;
       sm = std::max(tile_sm, sizeof(T) * ((size_t)(1 + r) * Cmax + (size_t)r * 32) + 64);
       if (sm > 220 * 1024) continue;
       CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -1733,10 +1768,15 @@ int Impl<T>::step(int64_t n) {
     const int64_t chunk = std::min(n, room);
     int64_t done = 0;
     if (persist && !prof && graph_steps > 0 && chunk > 0) {
-      int e = launch_persist(chunk, &launches);
-      if (e) return e;
-      host_step += chunk;
-      done = chunk;
+      // one launch runs at most 2^30 steps (the kernel's step count and the
+      // LL exchange tags are 32-bit)
+      while (done < chunk) {
+        const int64_t part = std::min<int64_t>(chunk - done, (int64_t)1 << 30);
+        int e = launch_persist(part, &launches);
+        if (e) return e;
+        host_step += part;
+        done += part;
+      }
     }
     while (done < chunk) {
       const int64_t left = chunk - done;

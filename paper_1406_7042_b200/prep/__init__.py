@@ -96,8 +96,12 @@ def coarse_piece_sigma(P: fit.Hybrid, alpha, full=None):
                            random_state=np.random.default_rng(0))[0])
 
 
-def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=None):
-    """scenario (synth) -> (problem description dict, info dict)."""
+def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=None, keep_basis=False):
+    """scenario (synth) -> (problem description dict, info dict).  ``keep_basis``
+    keeps every projection basis in ``info`` (verification of large models;
+    implies no cache)."""
+    if keep_basis:
+        cache = False
     t0 = time.time()
     key = _hash(scn, "v")
     path = os.path.join(CACHE_DIR, f"{scn.get('name', 'scn')}-{key}.pkl")
@@ -281,10 +285,10 @@ def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=N
     info.update(alpha=alpha, t_total=time.time() - t0, n_mat=int(len(uniq)))
     # the bases are kept for verification only when small (they are not part of
     # the problem description: the GPU never needs V beyond probe rows)
-    info["basis_blocks"] = [dict(V1=b["V1"] if b["V1"].size < 4_000_000 else None,
-                                 V2=b["V2"] if b["V2"].size < 4_000_000 else None,
+    info["basis_blocks"] = [dict(V1=b["V1"] if keep_basis or b["V1"].size < 4_000_000 else None,
+                                 V2=b["V2"] if keep_basis or b["V2"].size < 4_000_000 else None,
                                  Kt_pre=b["Kt_pre"],
-                                 S_E_pre=b["S_E_pre"] if b["S_E_pre"].size <= BIG_DENSE else None,
+                                 S_E_pre=b["S_E_pre"] if keep_basis or b["S_E_pre"].size <= BIG_DENSE else None,
                                  if_ids=b["if_ids"])
                             for b in blocks]
     if cache:

@@ -327,11 +327,21 @@ def scenario(which, precision=None, n_steps=None, **kw):
         # config-5 structure on a small domain: 2 stubs per side, r_z = 4, q = 16
         s = microstrip3d("tiny5", 105, 60, 48, 10, 0.25e-3, 2, (6, 54), 5, 3, 3.38, 3, (6, 12),
                          6, (2, 4), 4, 16, 0.6, 300, precision or 64, spacing=12)
+    elif which == "micro4":
+        # config-4 structure small enough for a dense eigen-decomposition of the
+        # whole reduced-hybrid update matrix (brute-force stability, ~2 K unknowns)
+        s = waveguide3d("micro4", 106, 12, 5, 4, 0.5e-3, (5, 7), 4, 2, 1, 8, 1, 2, (10, 2, 2),
+                        0.8, 100, precision or 64)
+    elif which == "micro5":
+        # config-5 structure (PEC strips through z-refined regions, two models)
+        s = microstrip3d("micro5", 107, 14, 12, 4, 0.25e-3, 1, (2, 12), 2, 2, 3.38, 2, (2, 2),
+                         4, (1, 3), 4, 8, 0.6, 100, precision or 64, spacing=4)
     elif which == "config3_small":
         s = cavity3d_random("config3_small", 3, 64, 48, 40, 1e-3, 0.99, 200, precision or 32)
     else:
         raise KeyError(which)
-    if precision is not None and which not in (3, "tiny3d", "config3_small", 4, "tiny4", 5, "tiny5"):
+    if precision is not None and which not in (3, "tiny3d", "config3_small", 4, "tiny4", 5, "tiny5", "micro4",
+                                               "micro5"):
         s["precision"] = precision
     if n_steps is not None and n_steps != s["n_steps"]:
         s["n_steps"] = n_steps

@@ -8,7 +8,21 @@ import numpy as np
 from oracle import problem_step as ps
 
 
-def run_gpu(problem, n_steps, precision=None, member_init=None, chunks=None, **kw):
+def gpu_reduced_order(vec_by_member, problem):
+    """[B][q_total] per-member reduced vectors -> the binding's set_state order
+    [block][inst][B][q]."""
+    out, o = [], 0
+    for b in problem["blocks"]:
+        q = int(b.get("qe", b.get("q")))
+        for i in range(int(b["n_inst"])):
+            out.append(vec_by_member[:, o:o + q].ravel())
+            o += q
+    return np.concatenate(out)
+
+
+def run_gpu(problem, n_steps, precision=None, member_init=None, chunks=None, start=None, **kw):
+    """``start``: optional dict(arrays={comp: [B][S]}, red_e=[B][q], red_h=[B][q],
+    step=int) -- a (random) starting state instead of the problem's init."""
     from paper_1406_7042_b200.fdtd import Sim
     sim = Sim(problem, precision=precision, **kw)
     init = problem.get("init") or {}
@@ -17,6 +31,13 @@ def run_gpu(problem, n_steps, precision=None, member_init=None, chunks=None, **k
         if a.shape[0] != sim.B:
             a = np.broadcast_to(a, (sim.B, sim.S))
         sim.set_state(int(c), a)
+    if start is not None:
+        for c, a in start["arrays"].items():
+            sim.set_state(int(c), a)
+        if problem.get("blocks"):
+            sim.set_state(6, gpu_reduced_order(start["red_e"], problem))
+            sim.set_state(7, gpu_reduced_order(start["red_h"], problem))
+        sim.set_state(8, [float(start.get("step", 0))])
     for n in (chunks or [n_steps]):
         sim.step(n)
     sim.sync()
@@ -51,8 +72,6 @@ def state_vectors(gpu, ora, member=0):
             g[m] = gpu["state"][int(c)][member][pos[m]]
         g_parts.append(g)
         o_parts.append(vec)
-    # reduced: GPU layout [block][inst][B][q]; the oracle's [block][inst][q] (one member)
-    blocks = getattr(rec, "_blocks", None)
     return np.concatenate(g_parts), np.concatenate(o_parts)
 
 
@@ -75,25 +94,88 @@ def block_shapes(problem):
     return sh
 
 
-def rel_l2(a, b):
+class VacuousReference(AssertionError):
+    """A parity subset whose reference is identically zero proves nothing."""
+
+
+def rel_l2(a, b, name="subset", allow_zero=False):
+    """||a - b|| / ||b||; a non-empty subset with ||b|| == 0 fails (a vacuous
+    comparison) unless ``allow_zero``."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
     nb = np.linalg.norm(b)
-    return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+    if nb == 0:
+        if b.size and not allow_zero:
+            raise VacuousReference(f"{name}: the reference is identically zero ({b.size} values)")
+        return float(np.linalg.norm(a))
+    return float(np.linalg.norm(a - b) / nb)
 
 
-def compare(problem, gpu, ora, member=0):
-    """Relative L2 errors: coarse+reduced state, and the worst probe series."""
-    g, o = state_vectors(gpu, ora, member)
+def max_abs(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if not b.size:
+        return 0.0, 0.0
+    return float(np.max(np.abs(a - b))), float(np.max(np.abs(b)))
+
+
+last_report = {}
+
+
+def subset_errors(subsets, allow_zero=()):
+    """{name: (gpu values, reference values)} -> {name: dict(rel_l2, max_abs,
+    ref_max, n)}; empty subsets are skipped, zero references fail."""
+    out = {}
+    for name, (g, o) in subsets.items():
+        o = np.asarray(o, np.float64)
+        if o.size == 0:
+            continue
+        ma, rm = max_abs(g, o)
+        out[name] = dict(rel_l2=rel_l2(g, o, name, allow_zero=name in allow_zero), max_abs=ma, ref_max=rm,
+                         n=int(o.size))
+    return out
+
+
+def compare(problem, gpu, ora, member=0, allow_zero=()):
+    """Per-subset relative L2 errors (coarse regular unknowns, interface rows,
+    e~, h~, each probe series) -- each subset on its own, so an error in the
+    512 reduced unknowns cannot hide behind 3 M coarse ones.  Returns
+    (worst state-subset error, worst probe error, ||reference state||); the
+    full report is in ``parity.last_report``."""
+    rec = ora["rec"]
+    S = rec.S
+    n_if = 0 if problem.get("interface") is None else len(problem["interface"]["unknown"])
+    Ne_c = len(rec.e_ids)
+    n_reg = Ne_c - n_if
+
+    def gather(ids):
+        comp = ids // S
+        pos = ids % S
+        g = np.empty(len(ids))
+        for c in np.unique(comp):
+            m = comp == c
+            g[m] = gpu["state"][int(c)][member][pos[m]]
+        return g
+
     B = int(problem.get("batch", 1))
     sh = block_shapes(problem)
-    ge = reduced_member(gpu["red_e"], sh, B, member, "e")
-    gh = reduced_member(gpu["red_h"], sh, B, member, "h")
-    g_all = np.concatenate([g, ge, gh])
-    o_all = np.concatenate([o, ora["red_e"], ora["red_h"]])
-    err_state = rel_l2(g_all, o_all)
-    err_probe = 0.0
+    subsets = {
+        "coarse": (np.concatenate([gather(rec.e_ids[:n_reg]), gather(rec.h_ids)]),
+                   np.concatenate([ora["E"][:n_reg], ora["H"][:len(rec.h_ids)]])),
+        "interface": (gather(rec.e_ids[n_reg:]), ora["E"][n_reg:Ne_c]),
+        "red_e": (reduced_member(gpu["red_e"], sh, B, member, "e"), ora["red_e"]),
+        "red_h": (reduced_member(gpu["red_h"], sh, B, member, "h"), ora["red_h"]),
+    }
     if gpu["probes"] is not None and len(gpu["probes"]):
         gp = gpu["probes"][:, :, member]
         op = ora["probes"]
         for p in range(op.shape[1]):
-            err_probe = max(err_probe, rel_l2(gp[:, p], op[:, p]))
-    return err_state, err_probe, float(np.linalg.norm(o_all))
+            subsets[f"probe{p}"] = (gp[:, p], op[:, p])
+    rep = subset_errors(subsets, allow_zero)
+    last_report.clear()
+    last_report.update(rep)
+    es = max([v["rel_l2"] for k, v in rep.items() if not k.startswith("probe")] or [0.0])
+    ep = max([v["rel_l2"] for k, v in rep.items() if k.startswith("probe")] or [0.0])
+    norm = float(np.sqrt(sum(np.sum(np.asarray(o) ** 2) for k, (g, o) in subsets.items()
+                             if not k.startswith("probe"))))
+    return es, ep, norm

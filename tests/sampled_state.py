@@ -51,8 +51,14 @@ def random_state(problem, seed, B=None, window=None):
 
 
 def oracle_vectors(rec, arrays, red_e, red_h, member):
-    E = np.concatenate([np.array([arrays[int(u // rec.S)][member][int(u % rec.S)] for u in rec.e_ids]),
-                        red_e[member]])
-    H = np.concatenate([np.array([arrays[int(u // rec.S)][member][int(u % rec.S)] for u in rec.h_ids]),
-                        red_h[member]])
+    """The state in the oracle's vector ordering [E_c ; e~], [H_c ; h~]."""
+    def gather(ids):
+        comp, pos = ids // rec.S, ids % rec.S
+        out = np.empty(len(ids))
+        for c in np.unique(comp):
+            m = comp == c
+            out[m] = np.asarray(arrays[int(c)])[member][pos[m]]
+        return out
+    E = np.concatenate([gather(rec.e_ids), red_e[member]])
+    H = np.concatenate([gather(rec.h_ids), red_h[member]])
     return E, H

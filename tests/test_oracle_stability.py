@@ -174,6 +174,14 @@ def test_expansion_points_eq19():
     assert np.allclose(np.abs(z), 1.1)
     assert np.allclose(z[::-1], np.conj(z))             # z_{-l} = conj(z_l)
     assert np.allclose(rd.expansion_points(1.1, 0, 30e9, dt), [1.1])
+    # the angles of Eq. (19), evaluated by hand: f_max dt = 0.03, so
+    # l = 1: 2 pi (1/2) 0.03 = 0.0942478 rad, 1.1 (cos, sin) = (1.0951182, 0.1035191)
+    # l = 2: 2 pi (2/2) 0.03 = 0.1884956 rad, 1.1 (cos, sin) = (1.0805160, 0.2061194)
+    # (a wrong angle -- a dropped 2 pi, l instead of l/L, f_max instead of
+    # f_max dt -- moves these)
+    want = [1.0805160 - 0.2061194j, 1.0951182 - 0.1035191j, 1.1 + 0j,
+            1.0951182 + 0.1035191j, 1.0805160 + 0.2061194j]
+    assert np.allclose(z, want, rtol=0, atol=2e-7)
 
 
 def test_cube_resonances_P311():

@@ -1,0 +1,238 @@
+"""The oracle verifies the 3-D reduced models the preprocessing library emits
+(configs 4 and 5 in small form: tiny4 -- x-graded slab with a solid PEC iris,
+tiny5 -- z-refined regions crossed by PEC strips, two shared models) and the
+q = 256 model of config 2, by the invariants SURVEY §8(c) O5-O7 lists:
+
+* D-orthonormal bases in the ORACLE's own masses (reading R5(vi));
+* projection (14)-(16): K~ = V1^T K_ff V2 and S_E = K_cf V2
+  with the oracle's own K_ff, K_cf (oracle.hybrid, reading R4);
+* enforcement (§III-A, reading R7) recomputed by the oracle
+  from those matrices, and the post-enforcement max-sigma law;
+* congruent regions really are translated copies in the oracle's assembly;
+* stability of the whole reduced hybrid the GPU steps: the leap-frog of the
+  problem description (oracle.problem_step) satisfies sigma_max(G_E^1/2 K_E
+  G~_H^1/2) < 2, and, on the micro variants, every eigenvalue of its update
+  matrix lies on the unit circle (brute force, Fig. 2)."""
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from oracle import hybrid as hy
+from oracle import problem_step as ps
+from oracle import stability as st
+from synth import scenario
+
+from paper_1406_7042_b200 import prep
+from paper_1406_7042_b200.prep import fit
+
+GAMMA = 0.9999
+
+
+def _pec_predicate(scn):
+    preds = []
+    if scn.get("pec_sheets"):
+        preds.append(hy.sheet_pec(scn["pec_sheets"], scn["boxes"]))
+    if any(b.get("pec_fine") for b in scn["boxes"]):
+        preds.append(hy.block_pec(scn["boxes"]))
+    if not preds:
+        return None
+    return lambda key: any(p(key) for p in preds)
+
+
+def _oracle_hybrid(scn, n=None, offset=(0, 0, 0), eps=None):
+    boxes = [hy.Box(tuple(int(v) for v in np.subtract(b["lo"], offset[:len(b["lo"])])),
+                    tuple(int(v) for v in np.subtract(b["hi"], offset[:len(b["hi"])])), tuple(b["r"]))
+             for b in scn["boxes"]]
+    return hy.assemble(scn["dim"], n or scn["n"], scn["delta"], scn["eps_r"] if eps is None else eps, boxes,
+                       scn["eps0"], scn["mu0"], pec_e_extra=_pec_predicate(scn))
+
+
+def _fine_perm(hs, part, box, dim):
+    """prep's fine interior order (flat ids e_int / h_int) -> oracle rows."""
+    nf = part.fine.n
+    shf = fit.sshape(nf, dim)
+
+    def fl(key):
+        _, b, c, (i, j, k) = key
+        return c * int(np.prod(shf)) + int(np.ravel_multi_index((k if dim == 3 else 0, j, i), shf))
+    oe = {fl(hs.e_keys[r]): r for r in np.nonzero((hs.e_tag == 2) & (hs.e_box == box))[0]}
+    oh = {fl(hs.h_keys[r]): r for r in np.nonzero((hs.h_tag == 2) & (hs.h_box == box))[0]}
+    assert set(oe) == set(part.e_int.tolist()) and set(oh) == set(part.h_int.tolist())
+    return np.array([oe[v] for v in part.e_int]), np.array([oh[v] for v in part.h_int])
+
+
+def _coarse_rows(hs, if_ids, S, shp, dim, offset=(0, 0, 0)):
+    rows = []
+    for u in if_ids:
+        pos = np.unravel_index(int(u % S), shp)
+        i, j, k = int(pos[-1]), int(pos[-2]), (int(pos[0]) if dim == 3 else 0)
+        rows.append(hs.e_index[("c", int(u // S), (i - offset[0], j - offset[1], k - offset[2]))])
+    return np.array(rows)
+
+
+def _first_of_class(scn):
+    seen, firsts, classes = set(), [], {}
+    for bi, b in enumerate(scn["boxes"]):
+        m = int(b.get("model", bi))
+        classes.setdefault(m, []).append(bi)
+        if m not in seen:
+            seen.add(m)
+            firsts.append(bi)
+    return firsts, classes
+
+
+def _check_block(scn, hs, P, part, bi, bb, blk, dt_c, offset=(0, 0, 0)):
+    dim = scn["dim"]
+    pe, ph_ = _fine_perm(hs, part, bi, dim)
+    V1, V2 = bb["V1"], bb["V2"]
+    q = V1.shape[1]
+    # D-orthonormal in the oracle's masses (R5(vi)): D~ = I, G = dt I
+    assert np.allclose(V1.T @ (hs.De[pe][:, None] * V1), np.eye(q), atol=1e-11)
+    assert np.allclose(V2.T @ (hs.Dm[ph_][:, None] * V2), np.eye(q), atol=1e-11)
+    # projection with the oracle's K_ff, K_cf (survey O6)
+    Kff = hs.K[pe][:, ph_]
+    Kt = V1.T @ (Kff @ V2)
+    assert np.allclose(bb["Kt_pre"], Kt, rtol=0, atol=1e-10 * np.abs(Kt).max())
+    rows = _coarse_rows(hs, bb["if_ids"], P.S, fit.sshape(P.n, dim), dim, offset)
+    assert np.all(hs.e_tag[rows] == 1)
+    SE = np.asarray(hs.K[rows][:, ph_] @ V2)
+    assert np.allclose(bb["S_E_pre"], SE, rtol=0, atol=1e-10 * np.abs(SE).max())
+    # no coupling from coarse H to fine E (K_fc = 0) in the oracle's assembly
+    Kfc = hs.K[pe][:, np.nonzero(hs.h_tag < 2)[0]]
+    assert Kfc.nnz == 0 or abs(Kfc).max() == 0.0
+    # enforcement recomputed by the oracle (reading R7), with the lumped masses
+    alpha = st.split_alpha(scn["dt"], dt_c)
+    Kp, SEp, rep = st.enforce_hybrid_block(np.ones(q), Kt, SE, np.ones(q), hs.De[rows], alpha, scn["dt"])
+    assert np.allclose(np.asarray(blk["K"], np.float64), Kp, rtol=0, atol=1e-9 * np.abs(Kp).max())
+    SEb = np.asarray(blk["S_E"], np.float64)
+    tol_se = 1e-9 if SEb.dtype == np.float64 and np.asarray(blk["S_E"]).dtype != np.float32 else 1e-6
+    assert np.allclose(SEb, SEp, rtol=0, atol=tol_se * np.abs(SEp).max())
+    # post-enforcement max-sigma law: sigma'_max = min(sigma_max, gamma 2/dt)
+    sig0 = st.singular_values(np.concatenate([np.ones(q), alpha * hs.De[rows]]), np.vstack([Kt, SE]), np.ones(q))
+    sig1 = st.singular_values(np.concatenate([np.ones(q), alpha * hs.De[rows]]),
+                              np.vstack([np.asarray(blk["K"], np.float64), SEb]), np.ones(q))
+    lim = GAMMA * 2 / scn["dt"]
+    assert np.isclose(sig1[0], min(sig0[0], lim), rtol=1e-9)
+    return pe, ph_, rows, int(np.sum(sig0 > lim))
+
+
+@pytest.fixture(scope="module", params=["tiny4", "tiny5"])
+def built3(request):
+    scn = scenario(request.param)
+    prob, info = prep.build_problem(scn, cache=False)
+    return scn, prob, info
+
+
+def test_3d_models_projection_enforcement(built3):
+    scn, prob, info = built3
+    hs = _oracle_hybrid(scn)
+    P = fit.assemble(3, scn["n"], scn["delta"], scn["eps_r"], scn["boxes"], scn["eps0"], scn["mu0"],
+                     pec_extra=prep._pec_extra(scn))
+    dt_c = scn["delta"] / (scn["c0"] * math.sqrt(3))
+    firsts, classes = _first_of_class(scn)
+    n_clip = 0
+    for k, bi in enumerate(firsts):
+        pe, ph_, rows, nc = _check_block(scn, hs, P, P.boxes[bi], bi, info["basis_blocks"][k],
+                                         prob["blocks"][k], dt_c)
+        n_clip += nc
+        # the other instances of the class: translated copies in the ORACLE's
+        # assembly (same local K_ff, K_cf, masses), so one model serves them
+        for bj in classes[int(scn["boxes"][bi].get("model", bi))][1:]:
+            pe2, ph2 = _fine_perm(hs, P.boxes[bj], bj, 3)
+            rows2 = _coarse_rows(hs, P.boxes[bj].if_ids, P.S, fit.sshape(P.n, 3), 3)
+            assert abs(hs.K[pe2][:, ph2] - hs.K[pe][:, ph_]).max() == 0.0
+            assert abs(hs.K[rows2][:, ph2] - hs.K[rows][:, ph_]).max() == 0.0
+            assert np.array_equal(hs.De[pe2], hs.De[pe]) and np.array_equal(hs.Dm[ph2], hs.Dm[ph_])
+            assert np.allclose(hs.De[rows2], hs.De[rows], rtol=1e-15)
+    if scn["name"] == "tiny4":
+        assert n_clip > 0                 # dt above the fine CFL: enforcement acts
+
+
+def _leapfrog_sigma(prob):
+    """sigma_max of G_E^1/2 K_E G~_H^1/2 for the recursion the GPU steps
+    (oracle.problem_step): E' = E - G_E K_E H, H' = H + G_H K_H E'.  K_H is
+    D K_E^T with a positive diagonal row scaling D (reading R8); the leap-frog
+    is stable iff sigma_max < 2 (its update eigenvalues then lie on the unit
+    circle).  Returns (sigma_max, rec)."""
+    rec = ps.build(prob)
+    KE = rec.KE.tocsr()
+    KH = rec.KH.tocsr()
+    KE.eliminate_zeros(); KH.eliminate_zeros()
+    KET = KE.T.tocsr()
+    KET.sort_indices(); KH.sort_indices()
+    assert np.array_equal(KET.indptr, KH.indptr) and np.array_equal(KET.indices, KH.indices)
+    ratio = KH.data / KET.data
+    D = np.empty(KH.shape[0])
+    for r in range(KH.shape[0]):
+        seg = ratio[KH.indptr[r]:KH.indptr[r + 1]]
+        if len(seg):
+            assert np.all(seg > 0) and np.ptp(seg) <= 1e-12 * seg.max(), r
+            D[r] = seg[0]
+        else:
+            D[r] = 1.0
+    A = sp.diags(np.sqrt(rec.GE)) @ KE @ sp.diags(np.sqrt(rec.GH * D))
+    if min(A.shape) < 3000:
+        smax = float(np.linalg.svd(A.toarray(), compute_uv=False)[0])
+    else:
+        smax = float(spla.svds(A, k=1, return_singular_vectors=False, tol=1e-10)[0])
+    return smax, rec
+
+
+def test_3d_whole_reduced_hybrid_stable(built3):
+    # condition (26) / (8) on the WHOLE reduced hybrid the GPU steps (coarse
+    # stencil + interface rows + every block instance), not the local block
+    scn, prob, info = built3
+    smax, _ = _leapfrog_sigma(prob)
+    assert smax < 2.0 * (1 - 1e-6), smax
+
+
+@pytest.mark.parametrize("name", ["micro4", "micro5"])
+def test_micro_update_eigenvalues_on_unit_circle(name):
+    # brute force: the dense update matrix of the
+    # problem's leap-frog -- every eigenvalue on the unit circle (lossless)
+    scn = scenario(name)
+    prob, info = prep.build_problem(scn, cache=False)
+    if name == "micro4":
+        assert info["blocks"][0]["n_clipped"] > 0
+    smax, rec = _leapfrog_sigma(prob)
+    assert smax < 2.0
+    NE, NH = rec.KE.shape
+    GE, GH = sp.diags(rec.GE), sp.diags(rec.GH)
+    KE, KH = rec.KE, rec.KH
+    # x = [E; H] -> [E - G_E K_E H ; H + G_H K_H (E - G_E K_E H)]
+    top = sp.hstack([sp.eye(NE), -GE @ KE])
+    bot = sp.hstack([GH @ KH, sp.eye(NH) - GH @ KH @ GE @ KE])
+    U = sp.vstack([top, bot]).toarray()
+    lam = np.abs(np.linalg.eigvals(U))
+    assert lam.max() <= 1 + 1e-9, lam.max()
+    assert lam.min() >= 1 - 1e-9, lam.min()
+    # the same model without the perturbation (prep's pre-enforcement matrices)
+    # is unstable when something was clipped (F7: the naive model blows up)
+    if name == "micro4":
+        bb = info["basis_blocks"][0]
+        pre = dict(prob, blocks=[dict(prob["blocks"][0], K=bb["Kt_pre"], S_E=bb["S_E_pre"])])
+        s_pre, _ = _leapfrog_sigma(pre)
+        assert s_pre > 2.0, s_pre
+
+
+@pytest.mark.slow
+def test_config2_q256_model_against_oracle():
+    # config 2's q = 256 model (recipe B, 64 x 64-cell box refined 8x): the
+    # oracle assembles the box with a 3-cell coarse margin (the local matrices
+    # K_ff, K_cf and the lumped interface masses depend only on the cells next
+    # to the box surface) and checks basis, projection and enforcement
+    scn = scenario(2)
+    prob, info = prep.build_problem(scn, keep_basis=True)
+    m = 3
+    b = scn["boxes"][0]
+    lo, hi = np.array(b["lo"][:2]) - m, np.array(b["hi"][:2]) + m
+    eps = np.asarray(scn["eps_r"]).reshape(scn["n"][1], scn["n"][0])[lo[1]:hi[1], lo[0]:hi[0]]
+    sub = dict(scn, n=(int(hi[0] - lo[0]), int(hi[1] - lo[1]), 1))
+    off = (int(lo[0]), int(lo[1]), 0)
+    hs = _oracle_hybrid(sub, n=sub["n"], offset=off, eps=eps)
+    P = fit.assemble(2, scn["n"], scn["delta"], scn["eps_r"], scn["boxes"], scn["eps0"], scn["mu0"])
+    dt_c = scn["delta"] / (scn["c0"] * math.sqrt(2))
+    _check_block(sub, hs, P, P.boxes[0], 0, info["basis_blocks"][0], prob["blocks"][0], dt_c, offset=off)
