@@ -168,13 +168,19 @@ def build(problem) -> HybridRecursion:
         rr = np.repeat(np.arange(n_if), np.diff(rp))
         r_.append(n_reg + rr); c_.append(cols); v_.append(vals)
         GE_if = np.asarray(itf["c"], np.float64)
-        for r in range(n_if):
-            bl, inst, loc = int(itf["block"][r]), int(itf["inst"][r]), int(itf["local"][r])
-            b = blocks[bl]
+        # interface row r couples to every h~ of its block instance with the
+        # weights S_E[local(r)] (rows grouped by (block, instance), same entries
+        # as a loop over r)
+        blk_, ins_, loc_ = (np.asarray(itf[k], np.int64) for k in ("block", "inst", "local"))
+        for bl in np.unique(blk_):
+            b = blocks[int(bl)]
             qe, qh = qe_qh(b)
-            o = Nh_c + red_off[bl][1] + inst * qh
-            r_.append(np.full(qh, n_reg + r)); c_.append(o + np.arange(qh))
-            v_.append(np.asarray(b["S_E"], np.float64)[loc])
+            SEb = np.asarray(b["S_E"])
+            for inst in np.unique(ins_[blk_ == bl]):
+                rows = np.nonzero((blk_ == bl) & (ins_ == inst))[0]
+                o = Nh_c + red_off[int(bl)][1] + int(inst) * qh
+                r_.append(np.repeat(n_reg + rows, qh)); c_.append(np.tile(o + np.arange(qh), len(rows)))
+                v_.append(SEb[loc_[rows]].astype(np.float64).ravel())
     GE_red, GH_red = [], []
     for bl, b in enumerate(blocks):
         qe, qh = qe_qh(b)
@@ -191,23 +197,25 @@ def build(problem) -> HybridRecursion:
 
     # ---- K_H: coarse H rows = K_inc^T over active E (interface E included,
     # with the incidence weights: surface H rows row-scaled, reading R8) -------
-    e_yee_rows = []
-    for fid in e_ids:
-        c, p = int(fid // S), int(fid % S)
-        e_yee_rows.append(int(ys.index[c].ravel()[p]))
-    e_yee_rows = np.array(e_yee_rows, np.int64)
+    e_yee_rows = np.empty(len(e_ids), np.int64)
+    for c in np.unique(e_ids // S):
+        m = (e_ids // S) == c
+        e_yee_rows[m] = ys.index[int(c)].ravel()[e_ids[m] % S]
     if np.any(e_yee_rows < 0):
         raise ValueError("an active E unknown lies on a PEC wall")
     KHc = (Kinc[e_yee_rows][:, cols_yee].T).tocoo()      # Nh_c x Ne_c
     r_, c_, v_ = [KHc.row], [KHc.col], [KHc.data]
     if n_if:
-        for r in range(n_if):
-            bl, inst, loc = int(itf["block"][r]), int(itf["inst"][r]), int(itf["local"][r])
-            b = blocks[bl]
+        # the transpose of the interface-row couplings above (h~ rows, E_if columns)
+        for bl in np.unique(blk_):
+            b = blocks[int(bl)]
             qe, qh = qe_qh(b)
-            o = red_off[bl][1] + inst * qh
-            r_.append(Nh_c + o + np.arange(qh)); c_.append(np.full(qh, n_reg + r))
-            v_.append(np.asarray(b["S_E"], np.float64)[loc])
+            SEb = np.asarray(b["S_E"])
+            for inst in np.unique(ins_[blk_ == bl]):
+                rows = np.nonzero((blk_ == bl) & (ins_ == inst))[0]
+                o = red_off[int(bl)][1] + int(inst) * qh
+                r_.append(np.tile(Nh_c + o + np.arange(qh), len(rows))); c_.append(np.repeat(n_reg + rows, qh))
+                v_.append(SEb[loc_[rows]].astype(np.float64).ravel())
     for bl, b in enumerate(blocks):
         qe, qh = qe_qh(b)
         Kt = np.asarray(b["K"], np.float64).reshape(qe, qh)
@@ -224,9 +232,15 @@ def build(problem) -> HybridRecursion:
 
     # ---- sources ---------------------------------------------------------------
     src = problem.get("sources")
-    epos = {int(v): i for i, v in enumerate(e_ids)}
+    e_sort = np.argsort(e_ids, kind="stable")
+
+    def epos_of(u):                       # position of unknown id u in e_ids
+        k = int(np.searchsorted(e_ids, u, sorter=e_sort))
+        if k >= len(e_ids) or e_ids[e_sort[k]] != u:
+            raise KeyError(u)
+        return int(e_sort[k])
     if src is not None and len(src["unknown"]):
-        src_row = np.array([epos[int(u)] for u in src["unknown"]], np.int64)
+        src_row = np.array([epos_of(int(u)) for u in src["unknown"]], np.int64)
         src_coef = np.asarray(src["coef"], np.float64)
         wave = np.asarray(src["wave"], np.float64)
         col = src.get("column")
@@ -236,7 +250,13 @@ def build(problem) -> HybridRecursion:
         src_col = np.zeros(0, np.int64)
 
     # ---- probes ----------------------------------------------------------------
-    hposd = {int(v): i for i, v in enumerate(h_ids)}
+    h_sort = np.argsort(h_ids, kind="stable")
+
+    def hpos_of(u):
+        k = int(np.searchsorted(h_ids, u, sorter=h_sort))
+        if k >= len(h_ids) or h_ids[h_sort[k]] != u:
+            raise KeyError(u)
+        return int(h_sort[k])
     probe_rows = []
     prb = problem.get("probes") or []
     for p in prb:
@@ -245,9 +265,9 @@ def build(problem) -> HybridRecursion:
             ids = [int(u) for u in p["unknowns"]]
             ws = [float(w) for w in p["weights"]]
             if all((u // S) in ecomps for u in ids):
-                probe_rows.append(("E", {epos[u]: w for u, w in zip(ids, ws)}))
+                probe_rows.append(("E", {epos_of(u): w for u, w in zip(ids, ws)}))
             elif all((u // S) in hcomps for u in ids):
-                probe_rows.append(("H", {hposd[u]: w for u, w in zip(ids, ws)}))
+                probe_rows.append(("H", {hpos_of(u): w for u, w in zip(ids, ws)}))
             else:
                 raise ValueError("a coarse probe mixes E and H unknowns")
         else:

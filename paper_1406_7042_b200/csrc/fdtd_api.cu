@@ -294,6 +294,17 @@ struct Impl : public fdtd_t {
   std::vector<double> hpr_w;
   bool persist = false;
   int p_maxrows = 0;
+  int p_K = 0, p_D = 2;                             // temporal blocking: halo depth K, y / G ring depth D
+  const void* p_kfn = nullptr;                      // the persist2d_kernel instantiation launched
+  static const void* p2_kernel(int TX, int K) {
+    if constexpr (sizeof(T) == 4) {
+      if (TX == 64 && K == 4) return (const void*)fdtd::persist2d_kernel<T, 64, 4>;
+      if (TX == 64 && K == 2) return (const void*)fdtd::persist2d_kernel<T, 64, 2>;
+      if (TX == 32 && K == 4) return (const void*)fdtd::persist2d_kernel<T, 32, 4>;
+      if (TX == 32 && K == 2) return (const void*)fdtd::persist2d_kernel<T, 32, 2>;
+    }
+    return (const void*)fdtd::persist2d_kernel<T>;
+  }
   int pTX = 0, pTY = 0, pntx = 0, pnty = 0, p_nif_tiles = 0, p_nred = 0, p_Rtot = 0, p_rpc = 0, p_Cmax = 0;
   int p_row0[fdtd::kMaxFusedBlocks + 1] = {};
   size_t p_smem = 0;
@@ -1129,10 +1140,28 @@ int Impl<T>::setup_persist() {
   // tiles cover cells i < nx, j < ny (the last storage column / row is constant)
   const int TX = (nx <= 32) ? 32 : 64;
   const int ntx = (nx + TX - 1) / TX;
+  // temporal blocking (persist2d_tb_tile, fp32): K-cell halos, square tiles
+  // (off by default: measured slower than the per-step exchange on config 2,
+  // the interface tiles stay bound to the per-step reduced
+  // chain, so the blocks only add redundant halo work)
+  int K = 0;
+  if (const char* e = getenv("FDTD_P2K")) K = std::max(0, atoi(e));
+  if (sizeof(T) != 4 || (K != 2 && K != 4)) K = 0;       // the instantiated shapes (p2_kernel)
+  p_K = K;
+  p_D = 2;
+  if (K > 0) while (p_D < 2 * (K + 1)) p_D *= 2;      // y / G ring: a halo holder lags <= K steps
+  // the tiles whose (extended) region holds cell (i, j): [lo, hi] per axis
+  auto tile_span = [&](int i, int T_, int nt_, int& lo, int& hi) {
+    if (K == 0) { lo = hi = i / T_; return; }
+    lo = 0;
+    while (lo * T_ + T_ + K <= i) ++lo;
+    hi = std::min(nt_ - 1, (i + K) / T_);
+  };
   int TY = 0, nty = 0, rpc = 0, nT = 0, nR = 0;
   size_t smem = 0;
   for (int cand : {64, 96, 128, 32}) {
-    const int ty = (ny <= 32) ? 32 : cand;
+    const int ty = K > 0 ? TX : ((ny <= 32) ? 32 : cand);
+    if (K > 0 && cand != 64) continue;
     const int nt_y = (ny + ty - 1) / ty;
     const int nt = ntx * nt_y;
     int maxrows = 0;
@@ -1140,15 +1169,24 @@ int Impl<T>::setup_persist() {
       std::vector<int> cnt(ntx * nt_y, 0);
       for (const auto& x : xrows) {
         const int i = (int)(x.s % (nx + 1)), j = (int)(x.s / (nx + 1));
-        if (i < nx && j < ny) maxrows = std::max(maxrows, ++cnt[(j / ty) * ntx + i / TX]);
+        if (i >= nx || j >= ny) continue;
+        int xl, xh, yl, yh;
+        tile_span(i, TX, ntx, xl, xh);
+        tile_span(j, ty, nt_y, yl, yh);
+        for (int b = yl; b <= yh; ++b)
+          for (int a = xl; a <= xh; ++a) maxrows = std::max(maxrows, ++cnt[b * ntx + a]);
       }
     }
-    const size_t tile_sm = sizeof(T) * ((size_t)3 * TX * ty + 2 * TX + 2 * ty) +
+    const size_t EXs = (size_t)TX + 2 * K;
+    const size_t tile_sm = K > 0 ?
+        sizeof(T) * 3 * EXs * EXs + 3 * fdtd::MAX_MAT * sizeof(fdtd::Coef<T>) + fdtd::MAX_MAT +
+            (EXs * EXs + 15) / 16 * 16 + sizeof(fdtd::P2Row<T>) * (size_t)maxrows + 64 :
+        sizeof(T) * ((size_t)3 * TX * ty + 2 * TX + 2 * ty) +
                            3 * fdtd::MAX_MAT * sizeof(fdtd::Coef<T>) + fdtd::MAX_MAT +
                            ((size_t)TX * ty + 15) / 16 * 16 + (2 * sizeof(T) * (size_t)maxrows + 15) / 16 * 16 +
                            sizeof(fdtd::P2Row<T>) * (size_t)maxrows + 64;
     if (tile_sm > 220 * 1024) continue;
-    const void* kfn = (const void*)fdtd::persist2d_kernel<T>;
+    const void* kfn = p2_kernel(TX, K);
     const int nthr = 512;
     CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_sm));
     int per_sm = 0;
@@ -1179,21 +1217,24 @@ int Impl<T>::setup_persist() {
       };
       while (r < Rtot && probe_only(r)) ++r;
       if (probe_only(r)) continue;
-      sm = std::max(tile_sm, sizeof(T) * ((size_t)(1 + r) * Cmax + (size_t)r * 32) + 64);
+      sm = std::max(tile_sm, sizeof(T) * ((size_t)(1 + r) * Cmax + (size_t)r * 32) + 64 +
+                                 (sizeof(T) == 4 ? (size_t)r * 32 * 8 + 32 + (size_t)r * Cmax * 2 : 0));
       if (sm > 220 * 1024) continue;
       CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, nthr, sm));
       nr = (Rtot + r - 1) / r;
       if (per_sm * nsm < nt + nr) continue;
     }
-    TY = ty; nty = nt_y; nT = nt; nR = nr; rpc = r; smem = sm; p_maxrows = maxrows;
+    TY = ty; nty = nt_y; nT = nt; nR = nr; rpc = r; smem = sm; p_maxrows = maxrows; p_kfn = kfn;
     break;
   }
+  if (TY == 0) return why_not(6);
   auto storage_ijk = [&](int64_t s_, int& i, int& j, int& k) {   // 2-D storage index
     i = (int)(s_ % (nx + 1)); j = (int)(s_ / (nx + 1)); k = 0;
   };
   // explicit rows -> tiles, with the H terms as local slots
   std::vector<std::vector<int>> by_tile(nT);
+  std::vector<std::vector<int32_t>> li_tile(nT);     // per tile: the row's local index (extended with K > 0)
   std::vector<int32_t> li(xrows.size());
   std::vector<int8_t> nterm(xrows.size()), slot(4 * xrows.size(), 0);
   std::vector<T> wv(4 * xrows.size(), (T)0);
@@ -1218,7 +1259,20 @@ int Impl<T>::setup_persist() {
     }
     nterm[r] = (int8_t)x.w.size();
     li[r] = (j % TY) * TX + (i % TX);
-    by_tile[(j / TY) * ntx + (i / TX)].push_back((int)r);
+    if (K == 0) {
+      by_tile[(j / TY) * ntx + (i / TX)].push_back((int)r);
+      li_tile[(j / TY) * ntx + (i / TX)].push_back(li[r]);
+    } else {
+      int xl, xh, yl, yh;
+      tile_span(i, TX, ntx, xl, xh);
+      tile_span(j, TY, nty, yl, yh);
+      const int EXi = TX + 2 * K;
+      for (int b = yl; b <= yh; ++b)
+        for (int a = xl; a <= xh; ++a) {
+          by_tile[b * ntx + a].push_back((int)r);
+          li_tile[b * ntx + a].push_back((j - (b * TY - K)) * EXi + (i - (a * TX - K)));
+        }
+    }
   }
   std::vector<int32_t> tptr(1, 0), rli, rsrc;
   std::vector<int8_t> rnt, rsl;
@@ -1227,10 +1281,16 @@ int Impl<T>::setup_persist() {
   std::vector<int64_t> ryo;
   std::vector<uint8_t> tif(nT, 0);
   int nif_tiles = 0;
+  std::vector<int8_t> rown;
   for (int t = 0; t < nT; ++t) {
-    for (int r : by_tile[t]) {
+    for (size_t q = 0; q < by_tile[t].size(); ++q) {
+      const int r = by_tile[t][q];
       const XRow& x = xrows[r];
-      rli.push_back(li[r]); rnt.push_back(nterm[r]);
+      {
+        const int i = (int)(x.s % (nx + 1)), j = (int)(x.s / (nx + 1));
+        rown.push_back((int8_t)((j / TY) * ntx + (i / TX) == t));
+      }
+      rli.push_back(li_tile[t][q]); rnt.push_back(nterm[r]);
       for (int q = 0; q < 4; ++q) { rsl.push_back(slot[4 * r + q]); rw.push_back(wv[4 * r + q]); }
       rc.push_back(make_coef<T>(x.c)); ryo.push_back(x.y); rsrc.push_back(x.src_col); rcs.push_back((T)x.cs);
       if (x.y >= 0) tif[t] = 1;
@@ -1260,7 +1320,7 @@ int Impl<T>::setup_persist() {
       ppid.push_back(q);
       for (int64_t k = hpr_rp[q]; k < hpr_rp[q + 1]; ++k) {
         const int i = (int)(hpr_off[k] % px), j = (int)(hpr_off[k] / px);
-        pli.push_back((j % TY) * TX + (i % TX));
+        pli.push_back(K > 0 ? ((j % TY) + K) * (TX + 2 * K) + (i % TX) + K : (j % TY) * TX + (i % TX));
         pcomp.push_back((int8_t)(hpr_src[k] - 2));
         pw.push_back((T)hpr_w[k]);
       }
@@ -1278,7 +1338,7 @@ int Impl<T>::setup_persist() {
     return FDTD_OK;
   };
   const int32_t *d_tptr, *d_li, *d_src, *d_pptr, *d_ppid, *d_ptp, *d_pli;
-  const int8_t *d_nt, *d_sl, *d_pcomp;
+  const int8_t *d_nt, *d_sl, *d_pcomp, *d_own;
   const T *d_w, *d_cs, *d_pw;
   const fdtd::Coef<T>* d_c;
   const int64_t* d_yo;
@@ -1288,16 +1348,19 @@ int Impl<T>::setup_persist() {
   FDTD_UP(tptr, d_tptr); FDTD_UP(rli, d_li); FDTD_UP(rsrc, d_src); FDTD_UP(pptr, d_pptr); FDTD_UP(ppid, d_ppid);
   FDTD_UP(ptp, d_ptp); FDTD_UP(pli, d_pli); FDTD_UP(rnt, d_nt); FDTD_UP(rsl, d_sl); FDTD_UP(pcomp, d_pcomp);
   FDTD_UP(rw, d_w); FDTD_UP(rcs, d_cs); FDTD_UP(pw, d_pw); FDTD_UP(rc, d_c); FDTD_UP(ryo, d_yo); FDTD_UP(tif, d_tif);
+  FDTD_UP(rown, d_own);
 #undef FDTD_UP
-  p_rows = fdtd::P2Rows<T>{d_tptr, d_li, d_c, d_nt, d_sl, d_w, d_yo, d_src, d_cs, rows.wave, rows.n_wave, rows.n_src};
+  p_rows = fdtd::P2Rows<T>{d_tptr, d_li, d_c, d_nt, d_sl, d_w, d_yo, d_src, d_cs, rows.wave, rows.n_wave, rows.n_src,
+                           d_own};
   p_probes = fdtd::P2Probes<T>{d_pptr, d_ppid, d_ptp, d_pli, d_pcomp, d_pw};
   p_tile_if = const_cast<uint8_t*>(d_tif);
   p_ezL = dalloc<T>((size_t)2 * nT * TY); p_hyR = dalloc<T>((size_t)2 * nT * TY);
   p_ezB = dalloc<T>((size_t)2 * nT * TX); p_hxT = dalloc<T>((size_t)2 * nT * TX);
   p_flags = dalloc<unsigned>((size_t)2 * nT + 3);
   if (sizeof(T) == 4) {
-    p_ll_words = (size_t)2 * nT * (2 * TY + 2 * TX) + 2 * (size_t)(2 * std::max<int64_t>(y_size, 1) +
-                                                                   std::max<int64_t>(e_size, 1) + std::max<int64_t>(h_size, 1));
+    p_ll_words = (size_t)2 * nT * (2 * TY + 2 * TX) + (size_t)2 * p_D * std::max<int64_t>(y_size, 1) +
+                 2 * (size_t)(std::max<int64_t>(e_size, 1) + std::max<int64_t>(h_size, 1)) +
+                 (size_t)2 * nT * 4 * 3 * K * TX;
     p_ll = dalloc<unsigned long long>(p_ll_words);
     if (!p_ll) return fail(FDTD_ENOMEM, "persistent-path allocation failed");
   }
@@ -1309,8 +1372,8 @@ int Impl<T>::setup_persist() {
   persist = true;
   if (getenv("FDTD_VERBOSE")) {
     fprintf(stderr, "fdtd: persistent 2-D path: %d x %d tiles of %d x %d, %d reduced CTAs x %d rows, smem %zu, "
-            "maxrows %d (P2Row %zu B), interface tiles %d\n", ntx, nty, TX, TY, nR, rpc, smem, p_maxrows,
-            sizeof(fdtd::P2Row<T>), nif_tiles);
+            "maxrows %d (P2Row %zu B), interface tiles %d, temporal blocking K %d (ring %d)\n", ntx, nty, TX, TY, nR,
+            rpc, smem, p_maxrows, sizeof(fdtd::P2Row<T>), nif_tiles, p_K, p_D);
     for (int t = 0; t < nT; ++t)
       if (tptr[t + 1] > tptr[t]) fprintf(stderr, "  tile %d: rows %d..%d\n", t, tptr[t], tptr[t + 1]);
   }
@@ -1350,10 +1413,18 @@ int Impl<T>::launch_persist(int64_t n, int64_t* count) {
     P.lezB = q; q += (size_t)2 * nT * pTX;
     P.lhxT = q; q += (size_t)2 * nT * pTX;
     P.ysz = std::max<int64_t>(y_size, 1); P.esz = std::max<int64_t>(e_size, 1); P.hsz = std::max<int64_t>(h_size, 1);
-    P.lG = q; q += 2 * P.ysz;
-    P.ly = q; q += 2 * P.ysz;
+    P.lG = q; q += (size_t)p_D * P.ysz;
+    P.ly = q; q += (size_t)p_D * P.ysz;
     P.leb = q; q += 2 * P.esz;
     P.lhb = q; q += 2 * P.hsz;
+    P.lband = q;
+  }
+  P.K = p_K;
+  P.ymask = p_D - 1;
+  P.sleep_ns = 0;
+  if (p_K > 0) {
+    static const unsigned sl = getenv("FDTD_P2SLEEP") ? (unsigned)atoi(getenv("FDTD_P2SLEEP")) : 0u;
+    P.sleep_ns = sl;
   }
   static unsigned long long* dbg = nullptr;
   if (getenv("FDTD_P2DBG")) {
@@ -1367,7 +1438,7 @@ int Impl<T>::launch_persist(int64_t n, int64_t* count) {
     P.dbg_tile_if = ti;
   }
   void* args[] = {&P};
-  CK(cudaLaunchCooperativeKernel((const void*)fdtd::persist2d_kernel<T>, dim3(nT + p_nred), dim3(512), args, p_smem,
+  CK(cudaLaunchCooperativeKernel(p_kfn, dim3(nT + p_nred), dim3(512), args, p_smem,
                                  stream));
   *count += 1;
   if (P.dbg && n >= 108) {
@@ -1417,7 +1488,7 @@ int Impl<T>::build_fused(const fdtd_probes* probes) {
       gks = 8;                  // measured: config 5 53.2 (K-split 8) vs 52.2 (4) vs 50.8 (2) Gcell/s
       if (const char* e = getenv("FDTD_GEMM_KS")) { const int k = atoi(e); if (k == 2 || k == 4 || k == 8) gks = k; }
     }
-    const size_t need = (size_t)(TRg * NPsel + maxCp / gks * NPsel + TRg * (maxCp / gks + 16 / sizeof(T))) * sizeof(T);
+    const size_t need = (size_t)(TRg * NPsel + maxCp / gks * NPsel + TRg * (maxCp / gks + 2)) * sizeof(double);
     fused_gemm = maxN >= 4;
     if (const char* e = getenv("FDTD_FUSED")) fused_gemm = std::string(e) == "gemm";
     if (need > 200 * 1024) fused_gemm = false;
@@ -1485,9 +1556,36 @@ int Impl<T>::build_fused(const fdtd_probes* probes) {
       for (int c = 0; c < CM; ++c) Mt[(size_t)r * Cp + dcol(c)] = (T)M[(size_t)r * CM + c];
     D.M_d = dalloc<T>(Mt.size());
     if (!D.M_d || upload(D.M_d, Mt)) return fail(FDTD_ENOMEM, "fused matrix allocation failed");
+    // fp32: the composed matrix is stored compensated, M = hi (fp32) + lo
+    // (bf16 of the fp32 remainder), relative error ~2^-33 (reading R14): the
+    // rounding of one fp32 M alone drifts the reduced state coherently
+    // (config 2: 1.2e-4 after 20,000 steps against the fp64 oracle)
+    uint16_t* Ml_d = nullptr;
+    if (sizeof(T) == 4) {
+      std::vector<uint16_t> Ml((size_t)RMp * Cp, 0);
+      for (int r = 0; r < RM; ++r)
+        for (int c = 0; c < CM; ++c) {
+          const double m = M[(size_t)r * CM + c];
+          const float rem = (float)(m - (double)(float)m);
+          uint32_t u;
+          std::memcpy(&u, &rem, 4);
+          u += 0x7fffu + ((u >> 16) & 1u);                 // round to nearest even
+          Ml[(size_t)r * Cp + dcol(c)] = (uint16_t)(u >> 16);
+        }
+      Ml_d = dalloc<uint16_t>(Ml.size());
+      if (!Ml_d || upload(Ml_d, Ml)) return fail(FDTD_ENOMEM, "fused matrix allocation failed");
+    }
+    double* M64_d = nullptr;
+    if (sizeof(T) == 4 && fused_gemm) {
+      std::vector<double> M64((size_t)RMp * Cp, 0.0);
+      for (int r = 0; r < RM; ++r)
+        for (int c = 0; c < CM; ++c) M64[(size_t)r * Cp + dcol(c)] = M[(size_t)r * CM + c];
+      M64_d = dalloc<double>(M64.size());
+      if (!M64_d || upload(M64_d, M64)) return fail(FDTD_ENOMEM, "fused matrix allocation failed");
+    }
     D.R_M = RM; D.C_M = CM;
     fdtd::FusedBlock<T> f{};
-    f.qe = qe; f.qh = qh; f.n_if = ni; f.N = D.N; f.R = RM; f.C = CM; f.Cp = Cp; f.M = D.M_d;
+    f.qe = qe; f.qh = qh; f.n_if = ni; f.N = D.N; f.R = RM; f.C = CM; f.Cp = Cp; f.M = D.M_d; f.Ml = Ml_d; f.M64 = M64_d;
     f.e_off = D.e_off; f.h_off = D.h_off; f.y_off = D.y_off;
     f.n_probe_rows = np;
     int32_t* pp = dalloc<int32_t>(std::max(np, 1));
@@ -1502,8 +1600,7 @@ int Impl<T>::build_fused(const fdtd_probes* probes) {
   rows_per_cta = ROWS;
   n_ctas = (int)ctas.size();
   NBsel = maxN <= 1 ? 1 : maxN <= 4 ? 4 : maxN <= 16 ? 16 : 32;
-  fused_smem = fused_gemm ? (size_t)(ROWS * NPsel + max_cols / gks * NPsel +
-                                     ROWS * (max_cols / gks + 16 / sizeof(T))) * sizeof(T)
+  fused_smem = fused_gemm ? (size_t)(ROWS * NPsel + max_cols / gks * NPsel + ROWS * (max_cols / gks + 2)) * sizeof(double)
                           : (size_t)max_cols * maxN * sizeof(T);
   if (fused_smem > 200 * 1024)
     return fail(FDTD_ENOTSUP, "fused reduced kernel needs %zu bytes of shared memory (> 200 KB)", fused_smem);

@@ -795,6 +795,8 @@ template <typename T>
 struct FusedBlock {
   int qe, qh, n_if, N, R, C, Cp;   // Cp: padded row pitch (multiple of 32 * VEC)
   const T* M;                      // [R][Cp]
+  const uint16_t* Ml;              // fp32 runs: [R][Cp] bf16 low parts, M = M + Ml to ~2^-33 (R14)
+  const double* M64;               // fp32 runs: [R][Cp] fp64 copy (the batched GEMM kernel)
   int64_t e_off, h_off, y_off;
   int n_probe_rows;
   const int32_t* probe_id;
@@ -846,6 +848,29 @@ __device__ __forceinline__ float vdot<float>(const float4& a, const float4& x) {
 template <>
 __device__ __forceinline__ double vdot<double>(const double2& a, const double2& x) {
   return a.x * x.x + a.y * x.y;
+}
+
+// four bf16 (the low parts of a compensated fp32 matrix, R14) -> float4
+__device__ __forceinline__ float4 bf16x4(uint2 u) {
+  return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                     __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+}
+
+// (a + l) . x with a, l, x fp32: exact products summed in fp64, fixed order
+// (the compensated fused update of fp32 runs, reading R14)
+__device__ __forceinline__ double dot_hilo(const float4& a, const float4& l, const float4& x) {
+  double s = (double)a.x * (double)x.x;
+  s = fma((double)l.x, (double)x.x, s);
+  s = fma((double)a.y, (double)x.y, s);
+  s = fma((double)l.y, (double)x.y, s);
+  s = fma((double)a.z, (double)x.z, s);
+  s = fma((double)l.z, (double)x.z, s);
+  s = fma((double)a.w, (double)x.w, s);
+  s = fma((double)l.w, (double)x.w, s);
+  return s;
+}
+__device__ __forceinline__ double dot_hilo_reg(const float4& a, const float4& l, const float* x) {
+  return dot_hilo(a, l, make_float4(x[0], x[1], x[2], x[3]));
 }
 
 template <typename T>
@@ -936,19 +961,43 @@ reduced_fused_kernel(const __grid_constant__ FusedParams<T> P) {
       for (int n = 0; n < NB; ++n) acc[n] = 0;
       const V* a = reinterpret_cast<const V*>(FB.M + (int64_t)r * Cp);
       const int nv = Cp / VN;
+      if constexpr (sizeof(T) == 4) {
+        // compensated matrix, fp64 accumulation of exact fp32 products,
+        // rounded once (reading R14)
+        const uint2* al = reinterpret_cast<const uint2*>(FB.Ml + (int64_t)r * Cp);
+        double acd[NB];
+#pragma unroll
+        for (int n = 0; n < NB; ++n) acd[n] = 0.0;
+#pragma unroll 4
+        for (int c = lane; c < nv; c += 32) {
+          const float4 av = reinterpret_cast<const float4*>(a)[c];
+          const float4 lv = bf16x4(al[c]);
+#pragma unroll
+          for (int n = 0; n < NB; ++n)
+            if (n < N) acd[n] += dot_hilo(av, lv, reinterpret_cast<const float4*>(X + n * Cp)[c]);
+        }
+#pragma unroll
+        for (int n = 0; n < NB; ++n) {
+          double v = acd[n];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          acc[n] = (T)v;
+        }
+      } else {
 #pragma unroll 8
-      for (int c = lane; c < nv; c += 32) {
-        const V av = a[c];
+        for (int c = lane; c < nv; c += 32) {
+          const V av = a[c];
 #pragma unroll
-        for (int n = 0; n < NB; ++n)
-          if (n < N) acc[n] += vdot<T>(av, reinterpret_cast<const V*>(X + n * Cp)[c]);
-      }
+          for (int n = 0; n < NB; ++n)
+            if (n < N) acc[n] += vdot<T>(av, reinterpret_cast<const V*>(X + n * Cp)[c]);
+        }
 #pragma unroll
-      for (int n = 0; n < NB; ++n) {
-        T v = acc[n];
+        for (int n = 0; n < NB; ++n) {
+          T v = acc[n];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        acc[n] = v;
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          acc[n] = v;
+        }
       }
       if (lane < N) {
         T v = 0;
@@ -985,13 +1034,14 @@ reduced_fused_kernel(const __grid_constant__ FusedParams<T> P) {
 template <typename T, int NP, int RPW, int KS>
 __global__ void __cluster_dims__(KS, 1, 1) __launch_bounds__(256)
 reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
-  using V = typename Vec<T>::type;
-  constexpr int VN = Vec<T>::n;
+  // fp64 arithmetic for both precisions: fp32 runs read an fp64 copy of M
+  // (M64, composed in fp64 and never rounded to fp32) and stage their fp32
+  // states as fp64, so the update is rounded once (reading R14)
   constexpr int GPW = 32 / NP;                 // row groups per warp
   constexpr int TR = 8 * GPW * RPW;            // rows per tile
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* Ps = reinterpret_cast<T*>(smem_raw);      // [TR][NP] partial tile
-  T* Xs = Ps + TR * NP;                        // [kc][NP] slice of [e~ ; h~ ; G]
+  double* Ps = reinterpret_cast<double*>(smem_raw);   // [TR][NP] partial tile
+  double* Xs = Ps + TR * NP;                          // [kc][NP] slice of [e~ ; h~ ; G]
   const int64_t step = *P.d_step;
   const bool check = P.check_every > 0 && (step % P.check_every) == 0;
   bool bad = false;
@@ -1006,63 +1056,51 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
     const FusedBlock<T>& FB = P.fb[ct.x];
     const int N = FB.N, C = FB.C, qe = FB.qe, qh = FB.qh;
     const int kc = FB.Cp / KS, k_lo = (int)rank * kc;
-    T* Ms = Xs + kc * NP;                      // [TR][kc + VN] slice of M (padded pitch)
-    const int mp = kc + VN;
-    // M slice: 16-byte cp.async, all in flight at once
-    for (int t = threadIdx.x; t < TR * (kc / VN); t += blockDim.x) {
-      const int u = t / (kc / VN), v = t % (kc / VN);
-      cp_async16(Ms + u * mp + v * VN, FB.M + (int64_t)(ct.y + u) * FB.Cp + k_lo + v * VN, true);
+    double* Ms = Xs + kc * NP;                 // [TR][kc + 2] slice of M (padded pitch)
+    const int mp = kc + 2;
+    const double* Msrc = (sizeof(T) == 4) ? FB.M64 : reinterpret_cast<const double*>(FB.M);
+    // M slice: 16-byte cp.async (two doubles), all in flight at once
+    for (int t = threadIdx.x; t < TR * (kc / 2); t += blockDim.x) {
+      const int u = t / (kc / 2), v = t % (kc / 2);
+      cp_async16(Ms + u * mp + v * 2, Msrc + (int64_t)(ct.y + u) * FB.Cp + k_lo + v * 2, true);
     }
+    cp_async_commit();
     // M does not depend on the step; the states and G do: launched as a
     // programmatic dependent of the stencil, wait for it here
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    if (N == NP && N % VN == 0) {
-      // X slice, straight 16-byte copies (every k-row is N contiguous words)
-      for (int t = threadIdx.x; t < kc * (NP / VN); t += blockDim.x) {
-        const int kk = t / (NP / VN), n = (t % (NP / VN)) * VN, k = k_lo + kk;
-        const T* src = P.e_in;                 // any valid address when zero-filled
-        if (k < qe) src = P.e_in + FB.e_off + (int64_t)k * N + n;
-        else if (k < qe + qh) src = P.h_in + FB.h_off + (int64_t)(k - qe) * N + n;
-        else if (k < C) src = P.G + FB.y_off + (int64_t)(k - qe - qh) * N + n;
-        cp_async16(Xs + kk * NP + n, src, k < C);
-      }
-    } else {
-      for (int t0 = threadIdx.x; t0 < kc * NP; t0 += 8 * 256) {
-        T v[8];
+    for (int t0 = threadIdx.x; t0 < kc * NP; t0 += 8 * 256) {
+      double v[8];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          const int t = t0 + w * 256, kk = t / NP, n = t % NP, k = k_lo + kk;
-          v[w] = 0;
-          if (t < kc * NP && n < N && k < C) {
-            if (k < qe) v[w] = P.e_in[FB.e_off + (int64_t)k * N + n];
-            else if (k < qe + qh) v[w] = P.h_in[FB.h_off + (int64_t)(k - qe) * N + n];
-            else v[w] = P.G[FB.y_off + (int64_t)(k - qe - qh) * N + n];
-          }
+      for (int w = 0; w < 8; ++w) {
+        const int t = t0 + w * 256, kk = t / NP, n = t % NP, k = k_lo + kk;
+        v[w] = 0.0;
+        if (t < kc * NP && n < N && k < C) {
+          if (k < qe) v[w] = (double)P.e_in[FB.e_off + (int64_t)k * N + n];
+          else if (k < qe + qh) v[w] = (double)P.h_in[FB.h_off + (int64_t)(k - qe) * N + n];
+          else v[w] = (double)P.G[FB.y_off + (int64_t)(k - qe - qh) * N + n];
         }
-#pragma unroll
-        for (int w = 0; w < 8; ++w)
-          if (t0 + w * 256 < kc * NP) Xs[t0 + w * 256] = v[w];
       }
+#pragma unroll
+      for (int w = 0; w < 8; ++w)
+        if (t0 + w * 256 < kc * NP) Xs[t0 + w * 256] = v[w];
     }
-    cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int n = lane % NP, g = lane / NP;
     const int rl0 = (warp * GPW + g) * RPW;
-    T acc[RPW];
+    double acc[RPW];
 #pragma unroll
-    for (int u = 0; u < RPW; ++u) acc[u] = 0;
-    const int nv = kc / VN;
+    for (int u = 0; u < RPW; ++u) acc[u] = 0.0;
+    const int nv = kc / 2;
 #pragma unroll 4
     for (int kv = 0; kv < nv; ++kv) {
-      T x[VN];
-#pragma unroll
-      for (int j = 0; j < VN; ++j) x[j] = Xs[(kv * VN + j) * NP + n];
+      const double x0 = Xs[(2 * kv) * NP + n], x1 = Xs[(2 * kv + 1) * NP + n];
 #pragma unroll
       for (int u = 0; u < RPW; ++u) {
-        const V m = *reinterpret_cast<const V*>(Ms + (rl0 + u) * mp + kv * VN);
-        acc[u] += vdot_reg<T>(m, x);
+        const double2 m = *reinterpret_cast<const double2*>(Ms + (rl0 + u) * mp + 2 * kv);
+        acc[u] = fma(m.x, x0, acc[u]);
+        acc[u] = fma(m.y, x1, acc[u]);
       }
     }
 #pragma unroll
@@ -1078,9 +1116,10 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
     for (int t = threadIdx.x; t < RPR * NP; t += blockDim.x) {
       const int rl = (int)rank * RPR + t / NP, n = t % NP;
       const int r = ct.y + rl;
-      T v = 0;
+      double vs = 0;
 #pragma unroll
-      for (int q = 0; q < KS; ++q) v += dsmem_load<T>(ps_local + (unsigned)((rl * NP + n) * sizeof(T)), (unsigned)q);
+      for (int q = 0; q < KS; ++q) vs += dsmem_load<double>(ps_local + (unsigned)((rl * NP + n) * sizeof(double)), (unsigned)q);
+      const T v = (T)vs;
       if (r >= FB.R || n >= N) continue;
       if (r < qh) P.h_out[FB.h_off + (int64_t)r * N + n] = v;
       else if (r < qh + ni) P.y[FB.y_off + (int64_t)(r - qh) * N + n] = v;

@@ -46,6 +46,7 @@ struct P2Rows {                 // explicit rows grouped by tile (CSR over tiles
   const T* cs;
   const T* wave;                // [n_wave][n_cols]
   int64_t n_wave, n_cols;
+  const int8_t* own;            // temporal blocking: 1 if the row's cell is in the tile's owned region
 };
 
 template <typename T>
@@ -55,7 +56,7 @@ struct P2Row {                  // one explicit row, cached in shared memory
   T cs;
   int64_t yo;
   int32_t li, src;
-  int8_t nterm, slot[4];
+  int8_t nterm, slot[4], own;
 };
 
 template <typename T>
@@ -104,7 +105,14 @@ struct Persist2D {
   unsigned long long *lG, *ly;                     // [2][y_size]
   unsigned long long *leb, *lhb;                   // [2][e_size] / [2][h_size]
   int64_t ysz, esz, hsz;
+  int ymask;                    // G / y ring depth - 1 (1: double buffer; temporal blocking: >= K)
+  // temporal blocking (persist2d_tb_tile): K-cell halos, exchanged every K steps
+  int K;                        // 0: per-step exchange (persist2d_tile)
+  unsigned long long* lband;    // [2][nT][4 sides][3 fields][K][T] tagged words
+  unsigned sleep_ns;            // poll back-off of the temporal-blocking kernel
 };
+
+template <bool B> struct BoolC { static constexpr bool value = B; };
 
 // LL words: a 64-bit relaxed store/load is single-copy atomic, so a reader that
 // sees the expected tag also sees the value stored with it; no fence, no flag
@@ -118,12 +126,16 @@ __device__ __forceinline__ unsigned long long ll_raw(const unsigned long long* p
   return w;
 }
 // spin until the word carries `tag`; false on abort / timeout (~1 s of SM clock)
-__device__ __forceinline__ bool ll_ld(const unsigned long long* p, unsigned tag, float& v, int* abort_flag) {
+// (sleep_ns > 0: back off after 8 failed polls, leaving the issue slots to
+// the co-resident CTA -- the temporal-blocking kernel)
+__device__ __forceinline__ bool ll_ld(const unsigned long long* p, unsigned tag, float& v, int* abort_flag,
+                                      unsigned sleep_ns = 0) {
   unsigned long long w = ll_raw(p);
   if ((unsigned)(w >> 32) != tag) {
     const long long t0 = clock64();
     unsigned it = 0;
     do {
+      if (sleep_ns && it >= 8) __nanosleep(sleep_ns);
       w = ll_raw(p);
       if ((++it & 63u) == 0) {
         if (*reinterpret_cast<volatile int*>(abort_flag)) return false;
@@ -325,7 +337,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
         const int64_t yo = rs[r].yo;
         const int sc = rs[r].src;
         float v = 0.f;
-        if (yo >= 0) ok = ll_ld(P.ly + (int64_t)hb_ * P.ysz + yo, tag_prev, v, P.abort_flag);
+        if (yo >= 0) ok = ll_ld(P.ly + (int64_t)((ls - 1) & P.ymask) * P.ysz + yo, tag_prev, v, P.abort_flag);
         yv[r] = (T)v;
         if (sc >= 0) yv[P.maxrows + r] = (step < P.R.n_wave) ? P.R.wave[step * P.R.n_cols + sc] : (T)0;
       }
@@ -395,7 +407,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       if (x.src >= 0 && step < P.R.n_wave) e -= x.cs * yv[P.maxrows + r];
       sEz[c] = e;
       if (x.yo >= 0) {
-        if constexpr (LL) ll_st(P.lG + (int64_t)(ls & 1) * P.ysz + x.yo, (float)e, tag_cur);
+        if constexpr (LL) ll_st(P.lG + (int64_t)(ls & P.ymask) * P.ysz + x.yo, (float)e, tag_cur);
         else __stcg(P.G + x.yo, e);
       }
     }
@@ -584,7 +596,11 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
   const int rc = blockIdx.x - P.ntx * P.nty;
   T* Xs = reinterpret_cast<T*>(smem_raw);       // [Cmax]
   T* Ms = Xs + P.Cmax;                          // [rpc][Cmax]
-  T* Ps = Ms + (size_t)P.rpc * P.Cmax;          // [rpc][32] per-lane partial sums
+  T* Ps = Ms + (size_t)P.rpc * P.Cmax;          // [rpc][32] per-lane partial sums (fp64 runs)
+  double* Pd = reinterpret_cast<double*>(Ps + (size_t)P.rpc * 32 + 2);  // fp32 runs: [rpc][32] fp64 partials
+  Pd = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(Pd) + 15) & ~(uintptr_t)15);
+  uint16_t* Mls = reinterpret_cast<uint16_t*>(Pd + (size_t)P.rpc * 32);   // fp32: [rpc][Cmax] bf16 (R14)
+  constexpr bool LO = sizeof(T) == 4;
   const int tid = threadIdx.x, nthr = blockDim.x, lx = tid & 31;
   const int r_lo = min(rc * P.rpc, P.Rtot), r_hi = min(r_lo + P.rpc, P.Rtot);
   for (int g = r_lo; g < r_hi; ++g) {
@@ -593,6 +609,10 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
     const FusedBlock<T>& FB = P.fb[b];
     const T* src = FB.M + (int64_t)(g - P.row0[b]) * FB.Cp;
     for (int c = tid; c < P.Cmax; c += nthr) Ms[(g - r_lo) * P.Cmax + c] = (c < FB.Cp) ? src[c] : (T)0;
+    if constexpr (LO) {
+      const uint16_t* sl = FB.Ml + (int64_t)(g - P.row0[b]) * FB.Cp;
+      for (int c = tid; c < P.Cmax; c += nthr) Mls[(g - r_lo) * P.Cmax + c] = (c < FB.Cp) ? sl[c] : (uint16_t)0;
+    }
   }
   __syncthreads();
   long long first_bad = -1;
@@ -633,10 +653,10 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
           float v = 0.f;
           T tv = 0;
           if (c < qe) {
-            if (LL && ls > 0) ok = ll_ld(P.leb + (int64_t)pl * P.esz + FB.e_off + c, tag_prev, v, P.abort_flag), tv = (T)v;
+            if (LL && ls > 0) ok = ll_ld(P.leb + (int64_t)pl * P.esz + FB.e_off + c, tag_prev, v, P.abort_flag, P.sleep_ns), tv = (T)v;
             else tv = __ldcg(e_in + FB.e_off + c);
           } else if (c < qe + qh) {
-            if (LL && ls > 0) ok = ll_ld(P.lhb + (int64_t)pl * P.hsz + FB.h_off + (c - qe), tag_prev, v, P.abort_flag), tv = (T)v;
+            if (LL && ls > 0) ok = ll_ld(P.lhb + (int64_t)pl * P.hsz + FB.h_off + (c - qe), tag_prev, v, P.abort_flag, P.sleep_ns), tv = (T)v;
             else tv = __ldcg(h_in + FB.h_off + (c - qe));
           }
           Xs[c] = tv;
@@ -649,18 +669,25 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
       //     order as one pass over all columns (the G columns are last)
       for (int gg = g + warp; gg < g_end; gg += nw) {
         const V* a = reinterpret_cast<const V*>(Ms + (gg - r_lo) * P.Cmax);
-        T acc = 0;
-        for (int cc = lx; cc < nv_eh; cc += 32) acc += vdot<T>(a[cc], reinterpret_cast<const V*>(Xs)[cc]);
-        Ps[(gg - r_lo) * 32 + lx] = acc;
+        if constexpr (LO) {
+          const uint2* al = reinterpret_cast<const uint2*>(Mls + (gg - r_lo) * P.Cmax);
+          double acd = 0.0;
+          for (int cc = lx; cc < nv_eh; cc += 32)
+            acd += dot_hilo(reinterpret_cast<const float4*>(a)[cc], bf16x4(al[cc]), reinterpret_cast<const float4*>(Xs)[cc]);
+          Pd[(gg - r_lo) * 32 + lx] = acd;
+        } else {
+          T acc = 0;
+          for (int cc = lx; cc < nv_eh; cc += 32) acc += vdot<T>(a[cc], reinterpret_cast<const V*>(Xs)[cc]);
+          Ps[(gg - r_lo) * 32 + lx] = acc;
+        }
       }
       if (!waited && rc == 0) P2_STAMP(2, 1);
       // (3) G of this step
       if (LL) {
-        const int pc = ls & 1;
         bool ok = true;
         for (int c = qe + qh + tid; c < C && ok; c += nthr) {
           float v = 0.f;
-          ok = ll_ld(P.lG + (int64_t)pc * P.ysz + FB.y_off + (c - qe - qh), tag_cur, v, P.abort_flag);
+          ok = ll_ld(P.lG + (int64_t)(ls & P.ymask) * P.ysz + FB.y_off + (c - qe - qh), tag_cur, v, P.abort_flag, P.sleep_ns);
           Xs[c] = (T)v;
         }
         if (!ok) s_abort = 1;
@@ -681,13 +708,27 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
       for (int gg = g + warp; gg < g_end; gg += nw) {
         const int r = gg - P.row0[b];
         const V* a = reinterpret_cast<const V*>(Ms + (gg - r_lo) * P.Cmax);
-        T acc = Ps[(gg - r_lo) * 32 + lx];
         int cc0 = lx;
         while (cc0 < nv_eh) cc0 += 32;
+        T acc;
+        if constexpr (LO) {
+          // compensated matrix, fp64 accumulation of exact fp32 products,
+          // rounded once (reading R14)
+          const uint2* al = reinterpret_cast<const uint2*>(Mls + (gg - r_lo) * P.Cmax);
+          double acd = Pd[(gg - r_lo) * 32 + lx];
 #pragma unroll 4
-        for (int cc = cc0; cc < nv; cc += 32) acc += vdot<T>(a[cc], reinterpret_cast<const V*>(Xs)[cc]);
+          for (int cc = cc0; cc < nv; cc += 32)
+            acd += dot_hilo(reinterpret_cast<const float4*>(a)[cc], bf16x4(al[cc]), reinterpret_cast<const float4*>(Xs)[cc]);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          for (int o = 16; o > 0; o >>= 1) acd += __shfl_xor_sync(0xffffffffu, acd, o);
+          acc = (T)acd;
+        } else {
+          acc = Ps[(gg - r_lo) * 32 + lx];
+#pragma unroll 4
+          for (int cc = cc0; cc < nv; cc += 32) acc += vdot<T>(a[cc], reinterpret_cast<const V*>(Xs)[cc]);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        }
         if (lx == 0) {
           const int pc = ls & 1;
           if (r < qh) {
@@ -695,7 +736,7 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
             if constexpr (LL) ll_st(P.lhb + (int64_t)pc * P.hsz + FB.h_off + r, (float)acc, tag_cur);
           } else if (r < qh + ni) {
             __stcg(P.y + FB.y_off + (r - qh), acc);
-            if constexpr (LL) ll_st(P.ly + (int64_t)pc * P.ysz + FB.y_off + (r - qh), (float)acc, tag_cur);
+            if constexpr (LL) ll_st(P.ly + (int64_t)(ls & P.ymask) * P.ysz + FB.y_off + (r - qh), (float)acc, tag_cur);
           } else if (r < qh + ni + qe) {
             __stcg(P.eb[p ^ 1] + FB.e_off + (r - qh - ni), acc);
             if constexpr (LL) ll_st(P.leb + (int64_t)pc * P.esz + FB.e_off + (r - qh - ni), (float)acc, tag_cur);
@@ -717,15 +758,378 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
   if (first_bad >= 0) atomicMin(P.bad_step, (unsigned long long)first_bad);
 }
 
-template <typename T>
+
+// ---------------------------------------------------------------------------
+// Temporal blocking.  Each tile keeps its TT x TT owned
+// cells plus a K-cell halo on every side in shared memory (EX = TT + 2K per
+// axis) and advances K steps between two halo exchanges.  Every sub-step
+// updates E on extended rows / columns 1..EX-1 and H on 0..EX-2 (all cells
+// whose stencil lies inside the extended tile); the values that are exact
+// shrink by one cell per half-step from the outside, so after K sub-steps the
+// owned region is exact -- every value produced bit for bit as the per-step
+// kernels do (same expression, same inputs) -- and the rest of the halo holds
+// finite junk until the next exchange overwrites it.  Then every tile
+// publishes four K-wide bands of its owned region (tagged LL words, double
+// buffered by block parity) and reads its neighbours' bands (edges, corners)
+// into its halo.  The interface rows still couple to the reduced CTAs every
+// step (G out, y in): a tile evaluates every explicit row of its extended
+// region (halo rows redundantly) but only the owner publishes G.  y and G live
+// in rings of depth ymask + 1 >= 2 (K + 1): a halo holder may lag the owner by
+// up to K steps (one block), the bound that keeps every y slot alive until it
+// is read.  fp32 only (the LL words carry 32-bit values); cells in pairs
+// (8-byte shared loads), compile-time tile shape.
+// ---------------------------------------------------------------------------
+
+// poll n tagged words at once: issue every load, then spin only on the words
+// that do not yet carry `tag` (the exchange costs one L2 round trip, not n)
+template <int NMAX>
+__device__ __forceinline__ bool ll_ld_batch(const unsigned long long* const* p, int n, unsigned tag, float* v,
+                                            int* abort_flag, unsigned sleep_ns) {
+  unsigned long long w[NMAX];
+#pragma unroll
+  for (int k = 0; k < NMAX; ++k)
+    if (k < n) w[k] = ll_raw(p[k]);
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < NMAX; ++k) {
+    if (k >= n) continue;
+    if ((unsigned)(w[k] >> 32) != tag) {
+      float x = 0.f;
+      ok = ok && ll_ld(p[k], tag, x, abort_flag, sleep_ns);
+      v[k] = x;
+    } else {
+      v[k] = __uint_as_float((unsigned)w[k]);
+    }
+  }
+  return ok;
+}
+
+template <typename T, int TT, int K>
+__device__ void persist2d_tb_tile(const Persist2D<T>& P, unsigned char* smem_raw, int& s_abort) {
+  static_assert(sizeof(T) == 4, "temporal blocking uses the fp32 LL exchange");
+  constexpr int EX = TT + 2 * K, EE = EX * EX;
+  constexpr int NPR = EX / 2;                       // cell pairs per extended row
+  constexpr int NTHR = 512;
+  constexpr int BAND = 3 * K * TT;                  // words per published side
+  static_assert(EX % 2 == 0, "pairs");
+  const int nT = P.ntx * P.nty;
+  const int t = blockIdx.x;
+  const int tx_ = t % P.ntx, ty_ = t / P.ntx;
+  const int gx0 = tx_ * TT - K, gy0 = ty_ * TT - K;   // global cell of extended (0, 0)
+  const int nx = P.nx, ny = P.ny, px = P.px;
+  const bool uniform = (P.mat_id == nullptr);
+  // every extended cell strictly inside the domain (no wall, no outside cell):
+  // the loops need no per-cell domain masks
+  const bool inner = gx0 >= 1 && gy0 >= 1 && gx0 + EX <= nx && gy0 + EX <= ny;
+  T* sEz = reinterpret_cast<T*>(smem_raw);
+  T* sHx = sEz + EE;
+  T* sHy = sHx + EE;
+  Coef<T>* cE = reinterpret_cast<Coef<T>*>(sHy + EE);
+  Coef<T>* cHx = cE + MAX_MAT;
+  Coef<T>* cHy = cHx + MAX_MAT;
+  uint8_t* ifm = reinterpret_cast<uint8_t*>(cHy + MAX_MAT);
+  uint8_t* smat = ifm + MAX_MAT;     // [EE]
+  P2Row<T>* rs = reinterpret_cast<P2Row<T>*>(smat + ((EE + 15) / 16) * 16);
+  const int tid = threadIdx.x;
+  for (int c = tid; c < EE; c += NTHR) {
+    const int x = c % EX, y = c / EX;
+    const int gi = gx0 + x, gj = gy0 + y;
+    T ez = 0, hx = 0, hy = 0;
+    uint8_t m = 0;
+    if (gi >= 0 && gj >= 0 && gi < nx && gj < ny) {
+      const int64_t o = (int64_t)gj * px + gi;
+      ez = P.Fin[0][o]; hx = P.Fin[1][o]; hy = P.Fin[2][o];
+      if (!uniform) m = P.mat_id[o];
+    }
+    sEz[c] = ez; sHx[c] = hx; sHy[c] = hy; smat[c] = m;
+  }
+  if (!uniform) {
+    for (int q = tid; q < P.n_mat; q += NTHR) {
+      cE[q] = P.gtab[q * 6 + 2]; cHx[q] = P.gtab[q * 6 + 3]; cHy[q] = P.gtab[q * 6 + 4];
+      ifm[q] = P.gifm[q];
+    }
+  }
+  // one material on the whole extended tile (most tiles): coefficients from
+  // registers, no per-cell table lookups
+  __shared__ int s_mmin, s_mmax;
+  if (tid == 0) { s_mmin = 255; s_mmax = 0; }
+  __syncthreads();
+  if (!uniform) {
+    int lo_ = 255, hi_ = 0;
+    for (int c = tid; c < EE; c += NTHR) { const int m = smat[c]; lo_ = min(lo_, m); hi_ = max(hi_, m); }
+    atomicMin(&s_mmin, lo_);
+    atomicMax(&s_mmax, hi_);
+  }
+  const int rows_lo = P.R.tile_ptr[t], rows_hi = P.R.tile_ptr[t + 1];
+  const int nrw = rows_hi - rows_lo;
+  const bool tile_rows = !uniform && nrw > 0;
+  for (int r = rows_lo + tid; r < rows_hi; r += NTHR) {
+    P2Row<T> x;
+    x.c = P.R.c[r]; x.cs = P.R.cs[r]; x.yo = P.R.yo[r]; x.li = P.R.li[r]; x.src = P.R.src[r];
+    x.nterm = P.R.nterm[r]; x.own = P.R.own[r];
+    for (int k = 0; k < 4; ++k) { x.w[k] = P.R.w[4 * r + k]; x.slot[k] = P.R.slot[4 * r + k]; }
+    rs[r - rows_lo] = x;
+  }
+  __syncthreads();
+  const int pr_lo = P.PR.tile_ptr[t], pr_hi = P.PR.tile_ptr[t + 1];
+  const bool hl = tx_ > 0, hr = tx_ + 1 < P.ntx, hb = ty_ > 0, ht = ty_ + 1 < P.nty;
+  long long first_bad = -1;
+  int ls = 0, blk = 0;
+  bool aborted = false;
+  const int dslot = (t == 0) ? 0 : (t == P.dbg_tile_if ? 1 : -1);
+  // mono: one material (uniform problems included); its coefficients in registers
+  const bool mono = uniform || (s_mmin == s_mmax && !tile_rows);
+  const int m0 = uniform ? 0 : s_mmin;
+  const Coef<T> ce0 = uniform ? P.u0 : cE[m0], cx0 = uniform ? P.u1 : cHx[m0], cy0 = uniform ? P.u1 : cHy[m0];
+  constexpr int DY = NTHR / NPR, DP = NTHR % NPR;     // pair-index stride as (rows, pairs)
+  while (ls < P.nsteps && !aborted) {
+    const int nb = min(K, P.nsteps - ls);
+    if (dslot >= 0) P2_STAMP(dslot, 5);
+    if (blk > 0) {
+      // ---- halo in: the neighbours' owned bands at the end of block blk-1
+      //      (edges K x TT, corners K x K, three fields)
+      const unsigned tag = (unsigned)blk;
+      const unsigned long long* src = P.lband + (size_t)((blk - 1) & 1) * nT * 4 * BAND;
+      constexpr int N_EDGE = 4 * BAND, N_ALL = N_EDGE + 4 * 3 * K * K;
+      constexpr int PER = (N_ALL + NTHR - 1) / NTHR;
+      const unsigned long long* ptr[PER];
+      T* dst[PER];
+      int n = 0;
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int q = tid + k * NTHR;
+        if (q >= N_ALL) continue;
+        int nbr = -1, side = 0, f, kk, u, x, y;
+        if (q < N_EDGE) {
+          const int e = q / BAND, rem = q % BAND;
+          f = rem / (K * TT); kk = (rem / TT) % K; u = rem % TT;
+          if (e == 0) { if (hl) nbr = t - 1; side = 1; x = kk; y = K + u; }
+          else if (e == 1) { if (hr) nbr = t + 1; side = 0; x = K + TT + kk; y = K + u; }
+          else if (e == 2) { if (hb) nbr = t - P.ntx; side = 3; x = K + u; y = kk; }
+          else { if (ht) nbr = t + P.ntx; side = 2; x = K + u; y = K + TT + kk; }
+        } else {
+          const int qq = q - N_EDGE;
+          const int e = qq / (3 * K * K), rem = qq % (3 * K * K);
+          f = rem / (K * K); kk = (rem / K) % K; const int v2 = rem % K;
+          // a corner K x K block sits in the diagonal neighbour's left / right band
+          if (e == 0) { if (hl && hb) nbr = t - P.ntx - 1; side = 1; x = kk; y = v2; u = TT - K + v2; }
+          else if (e == 1) { if (hr && hb) nbr = t - P.ntx + 1; side = 0; x = K + TT + kk; y = v2; u = TT - K + v2; }
+          else if (e == 2) { if (hl && ht) nbr = t + P.ntx - 1; side = 1; x = kk; y = K + TT + v2; u = v2; }
+          else { if (hr && ht) nbr = t + P.ntx + 1; side = 0; x = K + TT + kk; y = K + TT + v2; u = v2; }
+        }
+        if (nbr < 0) continue;
+        ptr[n] = src + ((size_t)nbr * 4 + side) * BAND + ((size_t)f * K + kk) * TT + u;
+        dst[n] = (f == 0 ? sEz : (f == 1 ? sHx : sHy)) + y * EX + x;
+        ++n;
+      }
+      float v[PER];
+      const bool ok = ll_ld_batch<PER>(ptr, n, tag, v, P.abort_flag, P.sleep_ns);
+#pragma unroll
+      for (int k = 0; k < PER; ++k)
+        if (k < n) *dst[k] = (T)v[k];
+      if (!ok) s_abort = 1;
+      __syncthreads();
+      if (s_abort) { aborted = true; break; }
+    }
+    for (int s = 1; s <= nb; ++s, ++ls) {
+      const int64_t step = P.step0 + ls;
+      const bool do_check = P.check_every > 0 && (step % P.check_every) == 0;
+      const unsigned tag_prev = (unsigned)ls, tag_cur = (unsigned)(ls + 1);
+      if (dslot >= 0) P2_STAMP(dslot, 0);
+      // ---- E on extended rows 1..EX-1, cell pairs (x, x+1); explicit-row
+      //      cells (and x = 0) keep their value here
+      auto e_pass = [&](auto MONO) {
+        constexpr bool MN = decltype(MONO)::value;
+        int y = 1 + tid / NPR, pp = tid % NPR;
+        for (; y < EX; y += DY) {
+          const int x = 2 * pp;
+          const int c = y * EX + x;
+          const float2 hy2 = *reinterpret_cast<const float2*>(sHy + c);
+          const float2 hx2 = *reinterpret_cast<const float2*>(sHx + c);
+          const float2 hxm2 = *reinterpret_cast<const float2*>(sHx + c - EX);
+          const float2 ez2 = *reinterpret_cast<const float2*>(sEz + c);
+          float e0 = ez2.x, e1 = ez2.y;
+          int ma = 0, mb = 0;
+          if (!MN) { const uint16_t m2 = *reinterpret_cast<const uint16_t*>(smat + c); ma = m2 & 0xff; mb = m2 >> 8; }
+          bool ua = x > 0, ub = true;                 // update cell a / b
+          bool za = false, zb = false;                // wall: E = 0
+          if (!inner) {
+            const int gi = gx0 + x, gj = gy0 + y;
+            const bool rowin = gj >= 0 && gj < ny;
+            ua = ua && rowin && gi >= 0 && gi < nx;
+            ub = rowin && gi + 1 >= 0 && gi + 1 < nx;
+            za = gi <= 0 || gj <= 0;
+            zb = gi + 1 <= 0 || gj <= 0;
+          }
+          if (!MN && tile_rows) { ua = ua && !(ifm[ma] & 4); ub = ub && !(ifm[mb] & 4); }
+          if (ua) {
+            const Coef<T> cc = MN ? ce0 : cE[ma];
+            const T dd = (hy2.x - sHy[c - 1]) - (hx2.x - hxm2.x);
+            e0 = za ? (T)0 : e0 + cc.apply(dd);
+          }
+          if (ub) {
+            const Coef<T> cc = MN ? ce0 : cE[mb];
+            const T dd = (hy2.y - hy2.x) - (hx2.y - hxm2.y);
+            e1 = zb ? (T)0 : e1 + cc.apply(dd);
+          }
+          *reinterpret_cast<float2*>(sEz + c) = make_float2(e0, e1);
+          pp += DP;
+          if (pp >= NPR) { pp -= NPR; ++y; }
+        }
+      };
+      if (mono) e_pass(BoolC<true>{}); else e_pass(BoolC<false>{});
+      if (dslot >= 0) P2_STAMP(dslot, 1);
+      // ---- explicit rows (eval_row order: terms, y, source); only the owner
+      //      publishes E_if into G
+      bool ok = true;
+      for (int r = tid; r < nrw && ok; r += NTHR) {
+        const P2Row<T>& xr = rs[r];
+        const int c = xr.li;
+        if (c % EX == 0 || c < EX) continue;        // stencil outside the extended tile
+        T yvv = 0;
+        if (xr.yo >= 0) {
+          if (ls == 0) yvv = __ldcg(P.y + xr.yo);
+          else {
+            float v = 0.f;
+            ok = ll_ld(P.ly + (int64_t)((ls - 1) & P.ymask) * P.ysz + xr.yo, tag_prev, v, P.abort_flag, P.sleep_ns);
+            yvv = (T)v;
+          }
+        }
+        T acc = 0;
+        for (int k = 0; k < xr.nterm; ++k) {
+          const int sl = xr.slot[k];
+          const T hv = sl == 0 ? sHy[c] : (sl == 1 ? sHy[c - 1] : (sl == 2 ? sHx[c] : sHx[c - EX]));
+          acc += xr.w[k] * hv;
+        }
+        if (xr.yo >= 0) acc += yvv;
+        T e = sEz[c] - xr.c.apply(acc);
+        if (xr.src >= 0 && step < P.R.n_wave) e -= xr.cs * P.R.wave[step * P.R.n_cols + xr.src];
+        sEz[c] = e;
+        if (xr.own && xr.yo >= 0) ll_st(P.lG + (int64_t)(ls & P.ymask) * P.ysz + xr.yo, (float)e, tag_cur);
+      }
+      if (dslot >= 0) P2_STAMP(dslot, 2);
+      if (!ok) s_abort = 1;
+      __syncthreads();
+      if (s_abort) { aborted = true; break; }
+      if (dslot >= 0) P2_STAMP(dslot, 3);
+      // ---- H on extended rows 0..EX-2 (the pair's second cell needs x+2 < EX)
+      bool bad = false;
+      auto h_pass = [&](auto MONO) {
+        constexpr bool MN = decltype(MONO)::value;
+        int y = tid / NPR, pp = tid % NPR;
+        for (; y < EX - 1; y += DY) {
+          const int x = 2 * pp;
+          const int c = y * EX + x;
+          const float2 ez2 = *reinterpret_cast<const float2*>(sEz + c);
+          const float2 ezj2 = *reinterpret_cast<const float2*>(sEz + c + EX);
+          const float2 hx2 = *reinterpret_cast<const float2*>(sHx + c);
+          const float2 hy2 = *reinterpret_cast<const float2*>(sHy + c);
+          float hx0 = hx2.x, hy0 = hy2.x, hx1 = hx2.y, hy1 = hy2.y;
+          int ma = 0, mb = 0;
+          if (!MN) { const uint16_t m2 = *reinterpret_cast<const uint16_t*>(smat + c); ma = m2 & 0xff; mb = m2 >> 8; }
+          const bool lastp = x + 2 >= EX;
+          bool ua = true, ub = !lastp, xa = true, xb = true, ya = true, yb = true;
+          if (!inner) {
+            const int gi = gx0 + x, gj = gy0 + y;
+            const bool rowin = gj >= 0 && gj < ny;
+            ua = rowin && gi >= 0 && gi < nx;
+            ub = ub && rowin && gi + 1 >= 0 && gi + 1 < nx;
+            xa = gi > 0; xb = gi + 1 > 0;
+            ya = gj > 0; yb = ya;
+          }
+          if (ua) {
+            const Coef<T> cx = MN ? cx0 : cHx[ma], cy = MN ? cy0 : cHy[ma];
+            hx0 = xa ? hx2.x - cx.apply(ezj2.x - ez2.x) : hx2.x;
+            hy0 = ya ? hy2.x + cy.apply(ez2.y - ez2.x) : hy2.x;
+          }
+          if (ub) {
+            const Coef<T> cx = MN ? cx0 : cHx[mb], cy = MN ? cy0 : cHy[mb];
+            hx1 = xb ? hx2.y - cx.apply(ezj2.y - ez2.y) : hx2.y;
+            hy1 = yb ? hy2.y + cy.apply(sEz[c + 2] - ez2.y) : hy2.y;
+          }
+          *reinterpret_cast<float2*>(sHx + c) = make_float2(hx0, hx1);
+          *reinterpret_cast<float2*>(sHy + c) = make_float2(hy0, hy1);
+          if (do_check && y >= K && y < K + TT && x >= K && x < K + TT) {
+            if (ua && !(finite_small(ez2.x) && finite_small(hx0) && finite_small(hy0))) bad = true;
+            if (ub && !(finite_small(ez2.y) && finite_small(hx1) && finite_small(hy1))) bad = true;
+          }
+          pp += DP;
+          if (pp >= NPR) { pp -= NPR; ++y; }
+        }
+      };
+      if (mono) h_pass(BoolC<true>{}); else h_pass(BoolC<false>{});
+      if (bad && first_bad < 0) first_bad = step;
+      __syncthreads();
+      if (dslot >= 0) P2_STAMP(dslot, 4);
+      if (pr_hi > pr_lo) {
+        for (int q = pr_lo + tid; q < pr_hi; q += NTHR) {
+          T acc = 0;
+          for (int k = P.PR.term_ptr[q]; k < P.PR.term_ptr[q + 1]; ++k) {
+            const int c = P.PR.term_li[k], cp = P.PR.term_comp[k];
+            const T v = cp == 0 ? sEz[c] : (cp == 1 ? sHx[c] : sHy[c]);
+            acc += P.PR.term_w[k] * v;
+          }
+          P.ring[(step % P.cap) * (int64_t)P.n_probe + P.PR.pid[q]] = acc;
+        }
+        __syncthreads();
+      }
+    }
+    if (aborted) break;
+    // ---- halo out: the owned bands at the end of this block (none after the last)
+    if (ls < P.nsteps) {
+      const unsigned tag = (unsigned)(blk + 1);
+      unsigned long long* dst = P.lband + (size_t)(blk & 1) * nT * 4 * BAND + (size_t)t * 4 * BAND;
+      for (int q = tid; q < 4 * BAND; q += NTHR) {
+        const int side = q / BAND, rem = q % BAND;
+        const int f = rem / (K * TT), kk = (rem / TT) % K, u = rem % TT;
+        int x, y;
+        if (side == 0) { x = K + kk; y = K + u; }                 // owned columns 0..K-1
+        else if (side == 1) { x = TT + kk; y = K + u; }           // owned columns TT-K..TT-1
+        else if (side == 2) { x = K + u; y = K + kk; }            // owned rows 0..K-1
+        else { x = K + u; y = TT + kk; }                          // owned rows TT-K..TT-1
+        const T* srcf = f == 0 ? sEz : (f == 1 ? sHx : sHy);
+        ll_st(dst + q, (float)srcf[y * EX + x], tag);
+      }
+    }
+    ++blk;
+  }
+  __syncthreads();
+  if (!s_abort) {
+    for (int c = tid; c < TT * TT; c += NTHR) {
+      const int x = c % TT, y = c / TT;
+      const int i = tx_ * TT + x, j = ty_ * TT + y;
+      if (i >= nx || j >= ny) continue;
+      const int64_t o = (int64_t)j * px + i;
+      const int e = (y + K) * EX + x + K;
+      P.Fout[0][o] = sEz[e]; P.Fout[1][o] = sHx[e]; P.Fout[2][o] = sHy[e];
+    }
+    if (t == 0) {
+      for (int q = tid; q < (ny + 1) + nx; q += NTHR) {
+        const int i = q <= ny ? nx : q - (ny + 1), j = q <= ny ? q : ny;
+        const int64_t o = (int64_t)j * px + i;
+        P.Fout[0][o] = P.nsteps > 0 ? (T)0 : P.Fin[0][o];
+        P.Fout[1][o] = P.Fin[1][o]; P.Fout[2][o] = P.Fin[2][o];
+      }
+      if (tid == 0) *P.d_step_out = P.step0 + P.nsteps;
+    }
+  }
+  if (first_bad >= 0) atomicMin(P.bad_step, (unsigned long long)first_bad);
+}
+
+// TBK > 0: temporal blocking with TBT x TBT tiles and K = TBK (fp32)
+template <typename T, int TBT = 0, int TBK = 0>
 __global__ void __launch_bounds__(512, 2)
 persist2d_kernel(const __grid_constant__ Persist2D<T> P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int s_abort;
   if (threadIdx.x == 0) s_abort = 0;
   __syncthreads();
-  if ((int)blockIdx.x < P.ntx * P.nty) persist2d_tile<T>(P, smem_raw, s_abort);
-  else persist2d_reduced<T>(P, smem_raw, s_abort);
+  if ((int)blockIdx.x < P.ntx * P.nty) {
+    if constexpr (TBK > 0) persist2d_tb_tile<T, TBT, TBK>(P, smem_raw, s_abort);
+    else persist2d_tile<T>(P, smem_raw, s_abort);
+  } else {
+    persist2d_reduced<T>(P, smem_raw, s_abort);
+  }
 }
 
 }  // namespace fdtd

@@ -51,7 +51,19 @@ def run_gpu(problem, n_steps, precision=None, member_init=None, chunks=None, sta
     return dict(state=st, red_e=red_e, red_h=red_h, probes=probes, launches=launches)
 
 
-def run_oracle(problem, n_steps, member=0):
+def run_oracle(problem, n_steps, member=0, start=None):
+    """``start``: the run_gpu start dict (random state + source step)."""
+    if start is not None:
+        from sampled_state import oracle_vectors
+        rec = ps.build(problem)
+        B = int(problem.get("batch", 1))
+        re_ = start.get("red_e", np.zeros((B, 0)))
+        rh_ = start.get("red_h", np.zeros((B, 0)))
+        state = oracle_vectors(rec, start["arrays"], re_, rh_, member)
+        E, H, probes, rec = ps.run(problem, n_steps, member=member, state=state,
+                                   start_step=int(start.get("step", 0)), rec=rec)
+        st, re, rh = ps.to_storage(rec, E, H)
+        return dict(state=st, red_e=re, red_h=rh, probes=probes, rec=rec, E=E, H=H)
     E, H, probes, rec = ps.run(problem, n_steps, member=member)
     st, re, rh = ps.to_storage(rec, E, H)
     return dict(state=st, red_e=re, red_h=rh, probes=probes, rec=rec, E=E, H=H)

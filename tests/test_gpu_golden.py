@@ -17,7 +17,6 @@ check here is vacuous: after the full run every subset carries the wave.
 Tolerances: the north star's (fp64: 1e-12 relative L2; fp32: 1e-4 relative
 L2 for fields and probe series).  Elementwise: |gpu - oracle| <= TOL_MAX *
 max|oracle| per subset (DESIGN.md §3 derives TOL_MAX from the fp32 drift)."""
-import glob
 import json
 import os
 
@@ -58,10 +57,12 @@ def _fingerprint(prob):
     return fingerprint(prob)
 
 
-@pytest.mark.parametrize("config,prec,members", CASES, ids=[f"config{c}-fp{p}" for c, p, _ in CASES])
-def test_full_run_against_oracle_golden(config, prec, members):
+def golden_report(config, prec, members, golden_prec=None, **sim_kw):
+    """Run the CUDA path for the golden's full length; return ({subset: (rel
+    L2, max-abs / max|ref|)}, paths).  ``golden_prec``: the golden to compare
+    with (default: the run's precision)."""
     from paper_1406_7042_b200.fdtd import Sim
-    golds = {m: _golden(config, prec, m) for m in members}
+    golds = {m: _golden(config, golden_prec or prec, m) for m in members}
     scn, prob = _problem(config, prec)
     fp = _fingerprint(prob)
     for m, g in golds.items():
@@ -69,7 +70,7 @@ def test_full_run_against_oracle_golden(config, prec, members):
         # to rounding (the host LAPACK may differ from the golden's machine)
         assert np.allclose(fp, g["fingerprint"], rtol=1e-11, atol=0), (fp, g["fingerprint"])
     n_steps = int(json.loads(str(golds[members[0]]["meta"]))["n_steps"])
-    sim = Sim(prob, precision=prec, graph_steps=32)
+    sim = Sim(prob, precision=prec, graph_steps=sim_kw.pop("graph_steps", 32), **sim_kw)
     for c, a in (prob.get("init") or {}).items():
         sim.set_state(int(c), a)
     sim.step(n_steps)
@@ -96,7 +97,6 @@ def test_full_run_against_oracle_golden(config, prec, members):
     paths = sim.path()
     sim.close()
     sh = block_shapes(prob)
-    tol, tmax = TOL[prec], TOL_MAX[prec]
     report = {}
     for m, g in golds.items():
         subsets = {"coarse": (got[m]["sample"], g["sample_val"]),
@@ -116,17 +116,27 @@ def test_full_run_against_oracle_golden(config, prec, members):
             d = float(np.max(np.abs(a - b)))
             bm = float(np.max(np.abs(b)))
             report[f"m{m}.{name}"] = (e, d / bm)
-            assert e <= tol, (m, name, e, paths)
-            assert d <= tmax * bm, (m, name, d, bm, paths)
         norm_g = np.sqrt(got[m]["sq"])
         norm_o = float(g["norms"][5])
-        report[f"m{m}.norm"] = abs(norm_g - norm_o) / norm_o
-        assert abs(norm_g - norm_o) <= tol * norm_o, (m, norm_g, norm_o)
+        report[f"m{m}.norm"] = (abs(norm_g - norm_o) / norm_o, 0.0)
+    return report, paths, n_steps
+
+
+@pytest.mark.parametrize("config,prec,members", CASES, ids=[f"config{c}-fp{p}" for c, p, _ in CASES])
+def test_full_run_against_oracle_golden(config, prec, members):
+    report, paths, n_steps = golden_report(config, prec, members)
     print(f"config {config} fp{prec} ({n_steps} steps, paths {paths}):",
-          json.dumps({k: v for k, v in report.items()}, default=float))
+          json.dumps({k: [float(f"{v[0]:.3e}"), float(f"{v[1]:.3e}")] for k, v in report.items()}))
+    tol, tmax = TOL[prec], TOL_MAX[prec]
+    bad = {k: v for k, v in report.items() if v[0] > tol or v[1] > tmax}
+    assert not bad, (bad, paths)
 
 
-def test_goldens_present():
-    have = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLD, "config*.npz")))
-    want = sorted(f"config{c}_fp{p}_m{m}.npz" for c, p, ms in CASES for m in ms)
-    assert set(want) <= set(have), sorted(set(want) - set(have))
+def test_config2_fp64_run_against_golden():
+    # the same problem description stepped in fp64 on the GPU (the golden is
+    # the oracle's fp64 run of it): isolates the problem identity and the
+    # recursion from fp32 rounding -- the north star's fp64 bar
+    report, paths, _ = golden_report(2, 64, (0,), golden_prec=32)
+    print("config 2 fp64:", json.dumps({k: float(f"{v[0]:.3e}") for k, v in report.items()}))
+    bad = {k: v for k, v in report.items() if v[0] > TOL[64]}
+    assert not bad, (bad, paths)

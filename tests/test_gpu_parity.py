@@ -15,6 +15,7 @@ from oracle import stability as st
 from synth import scenario
 
 from oracle_problem import problem_from_oracle, uniform_problem
+import parity
 from parity import compare, run_gpu, run_oracle
 
 pytestmark = pytest.mark.gpu
