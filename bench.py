@@ -401,20 +401,7 @@ def measure(config, prec, steps, warmup, args, rank=0, world=1, local=0, headlin
     sim.close()
     del flush
     torch.cuda.empty_cache()
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        try:
-            ns, el, t_build = run_oracle_sample(prob, seconds=args.cpu_seconds, member_cells=cells_of(prob))
-            cpu = {"value": cells_of(prob) * ns / el / 1e6, "unit": "Mcell-updates/s", "cores": 1,
-                   "kind": "oracle",
-                   "sample": (f"{ns} time steps of batch member 0 of the same workload in {el:.1f} s "
-                              f"(oracle.problem_step, SciPy CSR SpMV, 1 thread; matrix assembly {t_build:.0f} s "
-                              "not timed)" + ("; per-member rate (the batch's members are independent)"
-                                              if int(prob.get("batch", 1)) > 1 else "")),
-                   **cpu_info()}
-        except MemoryError as ex:
-            cpu = {"value": None, "unit": "Mcell-updates/s", "cores": 1, "kind": "oracle",
-                   "sample": f"unavailable: {ex}", **cpu_info()}
+    cpu = None          # filled in by bench_ours from the oracle worker processes
     per_step = {"phase_ms_per_step": {p: ph[p] / nph for p in PHASES}}
     if persistent:
         # ONE persistent launch per bench step (n_steps time steps, state
@@ -455,11 +442,48 @@ METRIC_CONFIGS = {"config2_fp32": (2, 32), "config3_fp32": (3, 32), "config3_fp6
                   "config5_fp32": (5, 32)}
 
 
+def oracle_sample_worker(config, prec, seconds):
+    """CPU-oracle timing of one workload in its own process (single-threaded
+    SciPy), run beside the GPU measurements so the bench stays within minutes.
+    Returns the cpu_baseline dict."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=1)
+    except Exception:
+        pass
+    try:
+        _, prob, _ = build_workload(config, prec)
+        ns, el, t_build = run_oracle_sample(prob, seconds=seconds)
+        return {"value": cells_of(prob) * ns / el / 1e6, "unit": "Mcell-updates/s", "cores": 1, "kind": "oracle",
+                "sample": (f"{ns} time steps of batch member 0 of the same workload in {el:.1f} s "
+                           f"(oracle.problem_step, SciPy CSR SpMV, 1 thread, in a worker process beside the GPU "
+                           f"run; matrix assembly {t_build:.0f} s not timed)" +
+                           ("; per-member rate (the batch's members are independent)"
+                            if int(prob.get("batch", 1)) > 1 else "")),
+                **cpu_info()}
+    except MemoryError as ex:
+        return {"value": None, "unit": "Mcell-updates/s", "cores": 1, "kind": "oracle",
+                "sample": f"unavailable: {ex}", **cpu_info()}
+
+
 def bench_ours(args):
     from paper_1406_7042_b200 import build as B
     from paper_1406_7042_b200.dist import finalize, init
     B.build()
     rank, world, local = init()
+    futs, pool = {}, None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # the oracle samples in worker processes (spawned before CUDA work),
+        # one per distinct oracle problem (config 3's fp32 and fp64 lines share
+        # the fp64 oracle run of the same problem)
+        import concurrent.futures as cf
+        import multiprocessing as mp
+        jobs = {args.config: (args.config, args.precision)}
+        if args.per_config:
+            for name, (c, p) in METRIC_CONFIGS.items():
+                jobs.setdefault(c, (c, p))
+        pool = cf.ProcessPoolExecutor(max_workers=len(jobs), mp_context=mp.get_context("spawn"))
+        futs = {c: pool.submit(oracle_sample_worker, c, p, args.cpu_seconds) for c, (c_, p) in jobs.items()}
     head = measure(args.config, args.precision, args.steps, args.warmup, args, rank, world, local, headline=True)
     per = {}
     if args.per_config and world == 1:
@@ -471,6 +495,18 @@ def bench_ours(args):
                                     rank, world, local)
             except Exception as ex:       # report, never hide: the headline line still prints
                 per[name] = {"error": f"{type(ex).__name__}: {ex}"}
+    if futs:
+        for c, f in futs.items():
+            try:
+                res = f.result(timeout=1800)
+            except Exception as ex:
+                res = {"value": None, "kind": "oracle", "cores": 1, "sample": f"failed: {type(ex).__name__}: {ex}"}
+            if c == args.config:
+                head["cpu_baseline"] = res
+            for name, v in per.items():
+                if isinstance(v, dict) and METRIC_CONFIGS[name][0] == c:
+                    v["cpu_baseline"] = res
+        pool.shutdown()
     if rank == 0:
         cfg = dict(head["config"])
         cfg.update(parallelism=f"replicas x{world}")
@@ -499,7 +535,7 @@ def main(argv=None):
     ap.add_argument("--graph-steps", type=int, default=32)
     ap.add_argument("--profile-steps", type=int, default=2000)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-steps", type=int, default=20)
     ap.add_argument("--time-steps", type=int, default=0, help="override the workload's time steps per bench step")
     ap.add_argument("--no-e2e", action="store_true")

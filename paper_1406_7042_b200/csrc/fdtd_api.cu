@@ -117,9 +117,10 @@ struct BlockDev {
   // unpadded matrices (fused blocks: prologue GEMVs) and padded-row copies
   // (leap-frog blocks: 16-byte vector loads)
   T *K_d = nullptr, *KT_d = nullptr, *SE_d = nullptr, *SET_d = nullptr, *ge_d = nullptr, *gh_d = nullptr;
-  T *Kp_d = nullptr, *KTp_d = nullptr, *SEp_d = nullptr, *Tv_d = nullptr;
-  T* part_d = nullptr;                         // [ks + splits][qh][N] K~'^T e~ and S_E^T G partial sums (fp32 GEMM path)
-  T* parte_d = nullptr;                        // [ks][qe][N] K~' h~ partial sums
+  T *Kp_d = nullptr, *KTp_d = nullptr, *SEp_d = nullptr;
+  double* Tv_d = nullptr;                      // K~'^T e~ + S_E^T G, unrounded (R14)
+  double* part_d = nullptr;                    // [ks + splits][qh][N] K~'^T e~ and S_E^T G partial sums (fp32 GEMM path, fp64)
+  double* parte_d = nullptr;                   // [ks][qe][N] K~' h~ partial sums
   T* gen_d = nullptr;                          // -g_e (the e~ update as an axpy)
   int ks = 0;                                  // row splits of the K~' products
   bool tc = false;                             // y = S_E h~ on the tensor cores (tc_gemm.cuh, 3xTF32, N = 16)
@@ -228,6 +229,15 @@ struct Impl : public fdtd_t {
   static constexpr int NPHASE = 3;       // stencil (+ explicit rows), reduced (+ probes), leapfrog GEMVs
   bool prof = false;
   cudaEvent_t ev[2 * NPHASE] = {};
+  // split step: the stencil items of the columns that hold
+  // interface rows run first, the reduced update runs on a second stream
+  // beside the rest of the stencil
+  bool split = false;
+  int n_ifc = 0;                       // interface columns (first in colperm)
+  int* colperm_d = nullptr;
+  std::vector<std::pair<int, int>> split_rows;     // (i, j) of the explicit rows that read y
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t evA = nullptr, evR = nullptr;
   double phase_ms[NPHASE] = {0};
   int64_t phase_n[NPHASE] = {0};
 
@@ -346,14 +356,14 @@ static int launch_gemv(int rows, int cols, int N, const T* A, const T* X, T* out
   return 1;
 }
 
-template <typename T>
-static int launch_rowblock(int rows, int K, int Kp, int N, const T* A, const T* X, T* out, const T* g, T alpha,
+template <typename T, typename OT>
+static int launch_rowblock(int rows, int K, int Kp, int N, const T* A, const T* X, OT* out, const T* g, T alpha,
                            bool acc, const int64_t* d_step, int check_every, unsigned long long* bad,
                            cudaStream_t st) {
   if (rows <= 0) return 0;
   const size_t sm = (size_t)Kp * N * sizeof(T);
   const int blocks = std::min((rows + 7) / 8, 148 * 2);
-#define FDTD_RB(NB) fdtd::rowblock_gemv_kernel<T, NB><<<blocks, 256, sm, st>>>(rows, K, Kp, N, A, X, out, g, alpha, acc, d_step, check_every, bad)
+#define FDTD_RB(NB) fdtd::rowblock_gemv_kernel<T, NB, OT><<<blocks, 256, sm, st>>>(rows, K, Kp, N, A, X, out, g, alpha, acc, d_step, check_every, bad)
   if (N <= 1) FDTD_RB(1);
   else if (N <= 4) FDTD_RB(4);
   else if (N <= 16) FDTD_RB(16);
@@ -363,7 +373,7 @@ static int launch_rowblock(int rows, int K, int Kp, int N, const T* A, const T* 
 }
 
 template <typename T>
-static int launch_colsum(int rows, int cols, int Kp, int N, const T* A, const T* X, T* out, cudaStream_t st) {
+static int launch_colsum(int rows, int cols, int Kp, int N, const T* A, const T* X, double* out, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return 0;
   const int cpt = std::min((cols + 255) / 256, 4);
   const int ytiles = (cols + 256 * cpt - 1) / (256 * cpt);
@@ -382,7 +392,7 @@ static int gemm_nn_smem(int NQ, int Kp) {
 }
 static int gemm_tn_smem(int NQ) {
   const int TC = 4 * 256 / NQ;
-  return (int)(sizeof(float) * 3 * 16 * ((size_t)TC + 4 * NQ));
+  return (int)(sizeof(float) * 3 * 16 * ((size_t)TC + 4 * NQ) + sizeof(double) * 16 * ((size_t)TC + 4 * NQ));
 }
 // y = S_E h~ (rows = n_if) and S_E^T G partials for the fp32 GEMM path
 static int launch_gemm_nn(int rows, int K, int Kp, int N, const float* A, const float* X, float* out, const float* g,
@@ -396,7 +406,7 @@ static int launch_gemm_nn(int rows, int K, int Kp, int N, const float* A, const 
 #undef FDTD_GNN
   return 1;
 }
-static int launch_gemm_tn(int rows, int cols, int Kp, int N, int splits, const float* A, const float* G, float* part,
+static int launch_gemm_tn(int rows, int cols, int Kp, int N, int splits, const float* A, const float* G, double* part,
                           cudaStream_t st) {
   const int NQ = N / 4, TC = 4 * 256 / NQ;
   const dim3 grid((cols + TC - 1) / TC, splits);
@@ -610,7 +620,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       for (int r = 0; r < D.n_if; ++r)
         for (int c = 0; c < D.qh; ++c) SEp[(size_t)r * D.Kph + c] = SE[(size_t)r * D.qh + c];
       D.Kp_d = dalloc<T>(Kp.size()); D.KTp_d = dalloc<T>(KTp.size());
-      D.SEp_d = dalloc<T>(std::max<size_t>(SEp.size(), 1)); D.Tv_d = dalloc<T>((size_t)D.qh * D.N);
+      D.SEp_d = dalloc<T>(std::max<size_t>(SEp.size(), 1)); D.Tv_d = dalloc<double>((size_t)D.qh * D.N);
       if (!D.Kp_d || !D.KTp_d || !D.SEp_d || !D.Tv_d) return fail(FDTD_ENOMEM, "block %d allocation failed", b);
       if (upload(D.Kp_d, Kp) || upload(D.KTp_d, KTp) || upload(D.SEp_d, SEp)) return FDTD_ECUDA;
       if (sizeof(T) == 4 && (D.N == 8 || D.N == 16 || D.N == 32) &&
@@ -622,8 +632,8 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
         // tiles x ks row splits fill the GPU (a 1024 x 1024 x 16 product is too
         // small for one CTA per row block)
         D.ks = std::max(1, std::min(64, std::min(D.qe, D.qh) / 16));
-        D.part_d = dalloc<T>((size_t)(D.ks + D.splits) * D.qh * D.N);
-        D.parte_d = dalloc<T>((size_t)D.ks * D.qe * D.N);
+        D.part_d = dalloc<double>((size_t)(D.ks + D.splits) * D.qh * D.N);
+        D.parte_d = dalloc<double>((size_t)D.ks * D.qe * D.N);
         D.gen_d = dalloc<T>((size_t)D.qe);
         if (!D.part_d || !D.parte_d || !D.gen_d) return fail(FDTD_ENOMEM, "block %d: partial-sum workspace allocation failed", b);
         {
@@ -697,6 +707,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       h.y = D.y_off + (int64_t)l * D.N + (int64_t)in * B;
       row_of[u] = (int)hrows.size();
       hrows.push_back(h);
+      split_rows.push_back({(int)(s % (nx + 1)), (int)((s / (nx + 1)) % (ny + 1))});
       gcomp.push_back(c); goff.push_back(dev_off(s)); gblk.push_back(b);
       gdst.push_back((int64_t)l * D.N + (int64_t)in * B);        // within the block's [n_if][N]
     }
@@ -1029,6 +1040,39 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       fprintf(stderr, "fdtd: tile stencil W=%d NS=%d MB=%d smem=%zu per_sm=%d grid=%d items=%d (cols %d x kc %d)\n",
               tcfg.W, tcfg.NS, tcfg.MB, tile_smem, per_sm, tile_grid, tsplit.nitems, tsplit.ncols, tsplit.kc);
   }
+  // (opt-in, FDTD_SPLIT=1: measured no gain on config 4 and a loss on config
+  // 5, DESIGN.md §12 -- the second grid waits for SM slots the stencil holds)
+  if (dim == 3 && use_tile && n_blocks > 0 && tile_grid == tsplit.nitems && getenv("FDTD_SPLIT") &&
+      std::string(getenv("FDTD_SPLIT")) == "1") {
+    // columns whose tile footprint (with a one-cell margin) holds an explicit
+    // row that reads y: they evaluate the interface rows, so they run before
+    // the reduced update; every other column runs beside it
+    const int cells_x = (tcfg.MB > 0) ? tBX / B : tBX;           // cells per tile row
+    std::vector<char> isif(tsplit.ncols, 0);
+    const int nty_ = tsplit.ncols / tsplit.ntx;
+    for (const auto& h : split_rows) {
+      const int i = h.first, j = h.second;
+      for (int ty_ = std::max(0, (j - 1 - tBY) / tsplit.outy); ty_ < nty_ && ty_ * tsplit.outy <= j + 1; ++ty_)
+        for (int tx_ = std::max(0, (i - 1 - cells_x) / tsplit.outx); tx_ < tsplit.ntx && tx_ * tsplit.outx <= i + 1; ++tx_) {
+          const int x0 = tx_ * tsplit.outx, y0 = ty_ * tsplit.outy;
+          if (i >= x0 - 1 && i <= x0 + cells_x && j >= y0 - 1 && j <= y0 + tBY) isif[ty_ * tsplit.ntx + tx_] = 1;
+        }
+    }
+    std::vector<int> perm;
+    for (int c = 0; c < tsplit.ncols; ++c) if (isif[c]) perm.push_back(c);
+    n_ifc = (int)perm.size();
+    for (int c = 0; c < tsplit.ncols; ++c) if (!isif[c]) perm.push_back(c);
+    if (n_ifc > 0 && n_ifc < tsplit.ncols) {
+      colperm_d = dalloc<int>(perm.size());
+      if (!colperm_d || upload(colperm_d, perm)) return fail(FDTD_ENOMEM, "split-step allocation failed");
+      CK(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&evA, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&evR, cudaEventDisableTiming));
+      split = true;
+    }
+    if (getenv("FDTD_VERBOSE"))
+      fprintf(stderr, "fdtd: split step %s: %d interface columns of %d\n", split ? "on" : "off", n_ifc, tsplit.ncols);
+  }
   if (!use_tile) {                // the reference batched kernel (its tile shape when it is the path)
     const int smv = (int)(sizeof(T) * (3 * 3 * (size_t)(tHBX * (tBY + 1) + 32) + 6 * 3 * (size_t)(tBX * tBY + 32)) +
                           sizeof(fdtd::MatTable<T>) + 512);
@@ -1045,6 +1089,10 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     CK(cudaFuncSetAttribute(fdtd::rowblock_gemv_kernel<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(fdtd::rowblock_gemv_kernel<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CK(cudaFuncSetAttribute(fdtd::rowblock_gemv_kernel<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(fdtd::rowblock_gemv_kernel<T, 1, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(fdtd::rowblock_gemv_kernel<T, 4, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(fdtd::rowblock_gemv_kernel<T, 16, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CK(cudaFuncSetAttribute(fdtd::rowblock_gemv_kernel<T, 32, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     for (auto& D : blocks)
       if (!D.fused && (size_t)std::max(D.Kph, D.Kpe) * D.N * sizeof(T) > (size_t)big)
         return fail(FDTD_ENOTSUP, "reduced block too large for the staged leap-frog GEMV (q x N)");
@@ -1650,7 +1698,23 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   mark(0, 0);
   const size_t tabsz = uniform ? 0 : sizeof(fdtd::MatTable<T>);
   const fdtd::Dims dm{nx, ny, nz, px, B, plane};
-  if (dim == 3 && use_tile) {
+  // split step (§5.6): interface columns (A) now, the reduced update on st2,
+  // the other columns (B) beside it, then the probe / counter tail
+  const bool sp = split && !profile;
+  fdtd::TileSplit SA = tsplit, SB = tsplit;
+  if (sp) {
+    const int nch = tsplit.nitems / tsplit.ncols;
+    SA.colperm = SB.colperm = colperm_d;
+    SA.col0 = 0; SA.ncols = n_ifc; SA.nitems = n_ifc * nch;
+    SB.col0 = n_ifc; SB.ncols = tsplit.ncols - n_ifc; SB.nitems = SB.ncols * nch;
+  }
+  const cudaStream_t rs = sp ? st2 : st;    // the reduced update's stream
+  if (dim == 3 && use_tile && sp) {
+    CK(fdtd::tile_launch<T>(tcfg, uniform, SA.nitems, tile_smem, st, tma[p], SA, dm, F0, F1, mat_id, tab,
+                            ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad));
+    CK(cudaEventRecord(evA, st));
+    CK(cudaStreamWaitEvent(st2, evA, 0));
+  } else if (dim == 3 && use_tile) {
     CK(fdtd::tile_launch<T>(tcfg, uniform, tile_grid, tile_smem, st, tma[p], tsplit, dm, F0, F1, mat_id, tab,
                             ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad));
   } else if (dim == 3 && use_tma) {
@@ -1717,43 +1781,43 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
         if (D.splits > 0) {
           // a4: e~ -= G_e K~' h~  (split-K TN on K~'^T, then the axpy with -g_e)
           n += launch_gemm_tn(D.qh, D.qe, D.Kpe, D.N, D.ks, (const float*)D.KTp_d, (const float*)h,
-                              (float*)D.parte_d, st);
-          fdtd::reduce_axpy_f32_kernel<<<(D.qe * D.N + 255) / 256, 256, 0, st>>>(
-              D.qe, D.N, D.ks, (const float*)D.parte_d, nullptr, (const float*)D.gen_d, (float*)e, nullptr);
+                              D.parte_d, rs);
+          fdtd::reduce_axpy_f32_kernel<<<(D.qe * D.N + 255) / 256, 256, 0, rs>>>(
+              D.qe, D.N, D.ks, D.parte_d, nullptr, (const float*)D.gen_d, (float*)e, nullptr);
           ++n;
           // a6: h~ += G_h (K~'^T e~ + S_E^T G): both as split-K partials into one
           // buffer, summed in a fixed order; y = S_E h~ (tensor cores or SIMT)
           n += launch_gemm_tn(D.qe, D.qh, D.Kph, D.N, D.ks, (const float*)D.Kp_d, (const float*)e,
-                              (float*)D.part_d, st);
+                              D.part_d, rs);
           n += launch_gemm_tn(D.n_if, D.qh, D.Kph, D.N, D.splits, (const float*)D.SEp_d,
-                              (const float*)(g_all + D.y_off), (float*)D.part_d + (size_t)D.ks * D.qh * D.N, st);
-          fdtd::reduce_axpy_f32_kernel<<<(D.qh * D.N + 255) / 256, 256, 0, st>>>(
-              D.qh, D.N, D.ks + D.splits, (const float*)D.part_d, nullptr, (const float*)D.gh_d, (float*)h,
+                              (const float*)(g_all + D.y_off), D.part_d + (size_t)D.ks * D.qh * D.N, rs);
+          fdtd::reduce_axpy_f32_kernel<<<(D.qh * D.N + 255) / 256, 256, 0, rs>>>(
+              D.qh, D.N, D.ks + D.splits, D.part_d, nullptr, (const float*)D.gh_d, (float*)h,
               D.tc ? D.xs_d : nullptr);
           ++n;
           if (D.tc) {
             const int tiles = (D.n_if + fdtd::tc::BM - 1) / fdtd::tc::BM;
-            fdtd::tc::tc_skinny_gemm_kernel<<<std::min(tiles, tc_grid), fdtd::tc::NTHREADS, fdtd::tc::SMEM_BYTES, st>>>(
+            fdtd::tc::tc_skinny_gemm_kernel<<<std::min(tiles, tc_grid), fdtd::tc::NTHREADS, fdtd::tc::SMEM_BYTES, rs>>>(
                 D.se_map, D.n_if, D.qh, D.xs_d, (float*)(y_all + D.y_off), ds, check_every, d_bad);
             ++n;
           } else {
             n += launch_gemm_nn(D.n_if, D.qh, D.Kph, D.N, (const float*)D.SEp_d, (const float*)h,
-                                (float*)(y_all + D.y_off), nullptr, 1.f, false, ds, check_every, d_bad, st);
+                                (float*)(y_all + D.y_off), nullptr, 1.f, false, ds, check_every, d_bad, rs);
           }
           continue;
         }
       }
       // a4: e~ -= G_e K~' h~^{n+1/2}
-      n += launch_rowblock<T>(D.qe, D.qh, D.Kph, D.N, D.Kp_d, h, e, D.ge_d, (T)-1, true, ds, check_every, d_bad, st);
+      n += launch_rowblock<T>(D.qe, D.qh, D.Kph, D.N, D.Kp_d, h, e, D.ge_d, (T)-1, true, ds, check_every, d_bad, rs);
       // a6: T = K~'^T e~ + S_E^T G ; h~ += G_h T ; y = S_E h~
       n += launch_rowblock<T>(D.qh, D.qe, D.Kpe, D.N, D.KTp_d, e, D.Tv_d, (const T*)nullptr, (T)1, false, ds, 0,
-                              d_bad, st);
-      if (D.n_if > 0) n += launch_colsum<T>(D.n_if, D.qh, D.Kph, D.N, D.SEp_d, g_all + D.y_off, D.Tv_d, st);
-      fdtd::axpy_diag_kernel<T><<<(D.qh * D.N + 255) / 256, 256, 0, st>>>(D.qh, D.N, D.gh_d, D.Tv_d, h);
+                              d_bad, rs);
+      if (D.n_if > 0) n += launch_colsum<T>(D.n_if, D.qh, D.Kph, D.N, D.SEp_d, g_all + D.y_off, D.Tv_d, rs);
+      fdtd::axpy_diag_kernel<T><<<(D.qh * D.N + 255) / 256, 256, 0, rs>>>(D.qh, D.N, D.gh_d, D.Tv_d, h);
       ++n;
       if (D.n_if > 0)
         n += launch_rowblock<T>(D.n_if, D.qh, D.Kph, D.N, D.SEp_d, h, y_all + D.y_off, (const T*)nullptr, (T)1, false,
-                                ds, check_every, d_bad, st);
+                                ds, check_every, d_bad, rs);
     }
     mark(2, 1);
   }
@@ -1781,6 +1845,7 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   P.check_every = check_every;
   P.bad_step = d_bad;
   const size_t sm = fused_smem;
+  P.tail_mode = sp ? 1 : 0;
   // optional programmatic dependent launch (the kernels wait with
   // griddepcontrol.wait before reading anything the preceding kernel writes;
   // without the attribute the wait is a no-op)
@@ -1790,10 +1855,12 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   cudaLaunchConfig_t lc = {};
   lc.blockDim = dim3(256);
   lc.dynamicSmemBytes = sm;
-  lc.stream = st;
-  lc.attrs = use_pdl ? pdl : nullptr;
-  lc.numAttrs = use_pdl ? 1 : 0;
-  if (fused_gemm) {
+  lc.stream = rs;
+  lc.attrs = (use_pdl && !sp) ? pdl : nullptr;
+  lc.numAttrs = (use_pdl && !sp) ? 1 : 0;
+  if (sp && n_ctas == 0) {
+    // leap-frog blocks only: nothing fused to run on st2
+  } else if (fused_gemm) {
     lc.gridDim = dim3((unsigned)(std::max(n_ctas, 1) * gks));
     switch (NPsel) {
       case 4: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_gemm_kernel<T, 4, gemm_rpw(4), GEMM_KS>, P)); break;
@@ -1814,7 +1881,19 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
       default: CK(cudaLaunchKernelEx(&lc, fdtd::reduced_fused_kernel<T, 32>, P)); break;
     }
   }
-  ++n;
+  if (!(sp && n_ctas == 0)) ++n;
+  if (sp) {
+    CK(cudaEventRecord(evR, st2));
+    CK(fdtd::tile_launch<T>(tcfg, uniform, SB.nitems, tile_smem, st, tma[p], SB, dm, F0, F1, mat_id, tab,
+                            ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad));
+    CK(cudaStreamWaitEvent(st, evR, 0));
+    // probes (coarse fields after the whole stencil) and the step counter
+    fdtd::FusedParams<T> Q = P;
+    Q.n_ctas = 0;
+    Q.tail_mode = 0;
+    fdtd::reduced_fused_kernel<T, 1><<<1, 256, 0, st>>>(Q);
+    n += 2;
+  }
   mark(1, 1);
   CK(cudaGetLastError());
   if (profile) {

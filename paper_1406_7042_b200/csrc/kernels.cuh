@@ -812,6 +812,7 @@ struct FusedParams {
   int tile0[kMaxFusedBlocks + 1];   // first tile (CTA / cluster) of each block
   int nfb;
   int n_ctas, B, rows_per_cta;
+  int tail_mode;                // 0: probes + step counter here; 1: divergence flag only (split step, §5.6)
   const T* e_in; T* e_out;      // e~^{n+1} in, e~^{n+2} out
   const T* h_in; T* h_out;      // h~^{n+1/2} in, h~^{n+3/2} out
   T* y;
@@ -909,6 +910,10 @@ __device__ __forceinline__ double dsmem_load<double>(unsigned local_addr, unsign
 template <typename T>
 __device__ __forceinline__ void fused_tail(const FusedParams<T>& P, int64_t step, bool bad) {
   const int B = P.B;
+  if (P.tail_mode == 1) {               // probes and counter run in the tail launch after the stencil
+    if (bad) atomicMin(P.bad_step, (unsigned long long)step);
+    return;
+  }
   // coarse probes and leapfrog-path reduced probes
   if (blockIdx.x == 0) {
     for (int t = threadIdx.x; t < P.pr.n_probe * B; t += blockDim.x) {
@@ -1207,10 +1212,13 @@ __global__ void gemv_rows_kernel(int rows, int cols, int N, const T* __restrict_
 //    per CTA (A row-major is read once, coalesced); partial sums in registers,
 //    then one atomicAdd per (c, n) per CTA.
 // ---------------------------------------------------------------------------
-template <typename T, int NB>
+// (products and sums in fp64 for both precisions, one rounding of the output:
+// the leap-frog increments are small differences of large sums, reading R14;
+// OT = double keeps an intermediate sum unrounded)
+template <typename T, int NB, typename OT = T>
 __global__ void __launch_bounds__(256)
 rowblock_gemv_kernel(int rows, int K, int Kp, int N, const T* __restrict__ A, const T* __restrict__ X,
-                     T* __restrict__ out, const T* __restrict__ g, T alpha, bool accumulate,
+                     OT* __restrict__ out, const T* __restrict__ g, T alpha, bool accumulate,
                      const int64_t* __restrict__ d_step, int check_every, unsigned long long* bad_step) {
   using V = typename Vec<T>::type;
   constexpr int VN = Vec<T>::n;
@@ -1228,32 +1236,38 @@ rowblock_gemv_kernel(int rows, int K, int Kp, int N, const T* __restrict__ A, co
   bool bad = false;
   const int nv = Kp / VN;
   for (int r = w0; r < rows; r += nw) {
-    T acc[NB];
+    double acc[NB];
 #pragma unroll
     for (int n = 0; n < NB; ++n) acc[n] = 0;
     const V* a = reinterpret_cast<const V*>(A + (int64_t)r * Kp);
 #pragma unroll 4
     for (int c = lane; c < nv; c += 32) {
       const V av = a[c];
+      const T* ap = reinterpret_cast<const T*>(&av);
 #pragma unroll
       for (int n = 0; n < NB; ++n)
-        if (n < N) acc[n] += vdot<T>(av, reinterpret_cast<const V*>(Xs + n * Kp)[c]);
+        if (n < N) {
+          const V xv = reinterpret_cast<const V*>(Xs + n * Kp)[c];
+          const T* xp = reinterpret_cast<const T*>(&xv);
+#pragma unroll
+          for (int j = 0; j < VN; ++j) acc[n] = fma((double)ap[j], (double)xp[j], acc[n]);
+        }
     }
 #pragma unroll
     for (int n = 0; n < NB; ++n) {
-      T v = acc[n];
+      double v = acc[n];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       acc[n] = v;
     }
     if (lane < N) {
-      T v = 0;
+      double v = 0;
 #pragma unroll
       for (int n = 0; n < NB; ++n)
         if (n == lane) v = acc[n];
-      const T gr = g ? g[r] : (T)1;
-      T* o = out + (int64_t)r * N + lane;
-      const T res = (accumulate ? *o : (T)0) + alpha * gr * v;
+      const double gr = g ? (double)g[r] : 1.0;
+      OT* o = out + (int64_t)r * N + lane;
+      const OT res = (OT)((accumulate ? (double)*o : 0.0) + (double)alpha * gr * v);
       *o = res;
       if (check && !finite_small((double)res)) bad = true;
     }
@@ -1264,28 +1278,28 @@ rowblock_gemv_kernel(int rows, int K, int Kp, int N, const T* __restrict__ A, co
 template <typename T, int NB, int CPT>
 __global__ void __launch_bounds__(256)
 colsum_gemv_kernel(int rows, int cols, int Kp, int N, const T* __restrict__ A, const T* __restrict__ X,
-                   T* __restrict__ out) {
+                   double* __restrict__ out) {
   // thread t owns columns c = c0 + t + 256 * u (u < CPT), c0 = 256 * CPT * blockIdx.y;
-  // rows [r0, r1) of this CTA
+  // rows [r0, r1) of this CTA; fp64 products and sums (reading R14)
   const int c0 = 256 * CPT * blockIdx.y;
   const int chunk = (rows + gridDim.x - 1) / gridDim.x;
   const int r0 = blockIdx.x * chunk, r1 = min(rows, r0 + chunk);
-  T acc[CPT][NB];
+  double acc[CPT][NB];
 #pragma unroll
   for (int u = 0; u < CPT; ++u)
 #pragma unroll
     for (int n = 0; n < NB; ++n) acc[u][n] = 0;
   for (int r = r0; r < r1; ++r) {
-    T xv[NB];
+    double xv[NB];
 #pragma unroll
-    for (int n = 0; n < NB; ++n) xv[n] = (n < N) ? X[(int64_t)r * N + n] : (T)0;
+    for (int n = 0; n < NB; ++n) xv[n] = (n < N) ? (double)X[(int64_t)r * N + n] : 0.0;
     const T* a = A + (int64_t)r * Kp;
 #pragma unroll
     for (int u = 0; u < CPT; ++u) {
       const int c = c0 + threadIdx.x + 256 * u;
-      const T av = (c < cols) ? a[c] : (T)0;
+      const double av = (c < cols) ? (double)a[c] : 0.0;
 #pragma unroll
-      for (int n = 0; n < NB; ++n) acc[u][n] += av * xv[n];
+      for (int n = 0; n < NB; ++n) acc[u][n] = fma(av, xv[n], acc[u][n]);
     }
   }
 #pragma unroll
@@ -1300,11 +1314,11 @@ colsum_gemv_kernel(int rows, int cols, int Kp, int N, const T* __restrict__ A, c
 
 // h~ += G_h * T   (T = K~'^T e~ + S_E^T G accumulated by the two kernels above)
 template <typename T>
-__global__ void axpy_diag_kernel(int rows, int N, const T* __restrict__ g, const T* __restrict__ Tv,
+__global__ void axpy_diag_kernel(int rows, int N, const T* __restrict__ g, const double* __restrict__ Tv,
                                  T* __restrict__ h) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= rows * N) return;
-  h[t] += g[t / N] * Tv[t];
+  h[t] = (T)fma((double)g[t / N], Tv[t], (double)h[t]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1421,7 +1435,7 @@ gemm_nn_f32_kernel(int rows, int K, int Kp, const float* __restrict__ A, const f
 template <int NQ>
 __global__ void __launch_bounds__(256, 2)
 gemm_tn_f32_partial_kernel(int rows, int cols, int Kp, const float* __restrict__ A, const float* __restrict__ G,
-                           float* __restrict__ part) {
+                           double* __restrict__ part) {
   constexpr int N = 4 * NQ;
   constexpr int CQ = 256 / NQ;                 // column quads per tile
   constexpr int TC = 4 * CQ;
@@ -1429,6 +1443,8 @@ gemm_tn_f32_partial_kernel(int rows, int cols, int Kp, const float* __restrict__
   extern __shared__ __align__(16) float smf[];
   float* As = smf;                             // [NS][RC][TC]
   float* Gs = As + NS * RC * TC;               // [NS][RC][N]
+  double* Ad = reinterpret_cast<double*>(Gs + NS * RC * N);   // the current chunk in fp64: [RC][TC]
+  double* Gd = Ad + RC * TC;                                   // [RC][N]
   const int tid = threadIdx.x;
   const int nq = tid % NQ, cq = tid / NQ;
   const int c0 = blockIdx.x * TC;
@@ -1457,37 +1473,55 @@ gemm_tn_f32_partial_kernel(int rows, int cols, int Kp, const float* __restrict__
   };
   issue(0);
   issue(1);
-  float acc[4][4];
+  // fp64 accumulation of the exact fp32 products (reading R14): the leap-frog
+  // sums K~'^T e~ + S_E^T G cancel to a small h~ increment, so fp32 partial
+  // sums alone lose ~1e-4 of it (measured, R14)
+  double acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
+    for (int c = 0; c < 4; ++c) acc[i][c] = 0.0;
   for (int ch = 0; ch < nch; ++ch) {
     issue(ch + 2);
     cp_async_wait<2>();
     __syncthreads();
-    const float* a = As + (size_t)(ch % NS) * RC * TC + cq * 4;
-    const float* gg = Gs + (size_t)(ch % NS) * RC * N + nq * 4;
-#pragma unroll
-    for (int rr = 0; rr < RC; ++rr) {
-      const float4 a4 = *reinterpret_cast<const float4*>(a + rr * TC);
-      const float4 g4 = *reinterpret_cast<const float4*>(gg + rr * N);
-      const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        acc[i][0] += av[i] * g4.x; acc[i][1] += av[i] * g4.y;
-        acc[i][2] += av[i] * g4.z; acc[i][3] += av[i] * g4.w;
+    {
+      // convert the chunk to fp64 once (each element once, not once per
+      // thread that reads it)
+      const float* a = As + (size_t)(ch % NS) * RC * TC;
+      const float* gg = Gs + (size_t)(ch % NS) * RC * N;
+      for (int q = tid; q < RC * TC / 4; q += 256) {
+        const float4 v = reinterpret_cast<const float4*>(a)[q];
+        reinterpret_cast<double2*>(Ad)[2 * q] = make_double2(v.x, v.y);
+        reinterpret_cast<double2*>(Ad)[2 * q + 1] = make_double2(v.z, v.w);
       }
+      for (int q = tid; q < RC * N; q += 256) Gd[q] = (double)gg[q];
     }
     __syncthreads();
+    const double* a = Ad + cq * 4;
+    const double* gg = Gd + nq * 4;
+#pragma unroll 4
+    for (int rr = 0; rr < RC; ++rr) {
+      const double2 a01 = *reinterpret_cast<const double2*>(a + rr * TC);
+      const double2 a23 = *reinterpret_cast<const double2*>(a + rr * TC + 2);
+      const double2 g01 = *reinterpret_cast<const double2*>(gg + rr * N);
+      const double2 g23 = *reinterpret_cast<const double2*>(gg + rr * N + 2);
+      const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i][0] = fma(av[i], g01.x, acc[i][0]); acc[i][1] = fma(av[i], g01.y, acc[i][1]);
+        acc[i][2] = fma(av[i], g23.x, acc[i][2]); acc[i][3] = fma(av[i], g23.y, acc[i][3]);
+      }
+    }
   }
   cp_async_wait<0>();
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int c = c0 + cq * 4 + i;
     if (c >= cols) continue;
-    *reinterpret_cast<float4*>(part + ((int64_t)blockIdx.y * cols + c) * N + nq * 4) =
-        make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    double2* o = reinterpret_cast<double2*>(part + ((int64_t)blockIdx.y * cols + c) * N + nq * 4);
+    o[0] = make_double2(acc[i][0], acc[i][1]);
+    o[1] = make_double2(acc[i][2], acc[i][3]);
   }
 }
 
@@ -1495,14 +1529,15 @@ gemm_tn_f32_partial_kernel(int rows, int cols, int Kp, const float* __restrict__
 // xs (optional, N = 16): the new h~ split for the tensor-core GEMM of
 // tc_gemm.cuh -- per 32-row chunk of h~, [hi | lo] tiles of [16 n][32 k] in
 // the 128-byte swizzled K-major layout, so one bulk copy per chunk lands them
-static __global__ void reduce_axpy_f32_kernel(int cols, int N, int splits, const float* __restrict__ part,
+static __global__ void reduce_axpy_f32_kernel(int cols, int N, int splits, const double* __restrict__ part,
                                        const float* __restrict__ Tv, const float* __restrict__ gh,
                                        float* __restrict__ h, float* __restrict__ xs) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= cols * N) return;
-  float v = Tv ? Tv[t] : 0.f;
+  double v = Tv ? (double)Tv[t] : 0.0;
   for (int s2 = 0; s2 < splits; ++s2) v += part[(int64_t)s2 * cols * N + t];
-  const float hn = h[t] + gh[t / N] * v;
+  // fp64 partials, one rounding of the new state (R14)
+  const float hn = (float)fma((double)gh[t / N], v, (double)h[t]);
   h[t] = hn;
   if (xs) {
     const int k = t / N, n = t % N, ch = k >> 5, kk = k & 31;

@@ -95,7 +95,7 @@ struct SegCursor {               // walks the load sequence of one CTA's items
     item = it;
     done = it >= S.nitems;
     if (done) return;
-    col = it % S.ncols;
+    col = S.column(it % S.ncols);
     a = (it / S.ncols) * S.kc;
     b = min(a + S.kc, S.nzp);
     kl = min(b, nz);
@@ -206,7 +206,7 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
   unsigned ebuf = 0;                           // En buffer of the current plane
   for (int item = blockIdx.x; item < S.nitems; item += gridDim.x) {
     // ---- item start: this thread's cell in the column's tile
-    const int col = item % S.ncols;
+    const int col = S.column(item % S.ncols);
     const int a = (item / S.ncols) * S.kc, bseg = min(a + S.kc, S.nzp), kl = min(bseg, nz);
     const int i0 = (col % S.ntx) * S.outx, j0 = (col / S.ntx) * S.outy;
     const int i = i0 + ci, j = j0 + ty;

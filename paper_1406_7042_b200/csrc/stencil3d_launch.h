@@ -20,6 +20,11 @@ cudaError_t tile_prepare(const TileCfg& c, size_t smem);
 struct TileSplit {
   int ntx, outx, outy, nzp;      // tiles in x, tile pitch in cells (x, y), nz + 1
   int ncols, kc, nitems;         // tiles, planes per z-chunk, items = tiles * chunks
+  // optional column subset: the launch covers columns colperm[col0 .. col0 +
+  // ncols) (the interface columns or the rest); null: all
+  const int* colperm = nullptr;
+  int col0 = 0;
+  __host__ __device__ __forceinline__ int column(int c) const { return colperm ? colperm[col0 + c] : c; }
 };
 
 template <typename T>
