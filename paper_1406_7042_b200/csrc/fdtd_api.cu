@@ -306,6 +306,7 @@ struct Impl : public fdtd_t {
   int p_maxrows = 0;
   int p_K = 0, p_D = 2;                             // temporal blocking: halo depth K, y / G ring depth D
   const void* p_kfn = nullptr;                      // the persist2d_kernel instantiation launched
+  T* p_yin = nullptr;                               // y before the launch (persist2d.cuh, fp32)
   static const void* p2_kernel(int TX, int K) {
     if constexpr (sizeof(T) == 4) {
       if (TX == 64 && K == 4) return (const void*)fdtd::persist2d_kernel<T, 64, 4>;
@@ -631,7 +632,8 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
         // the K~' products as split-K TN GEMMs on the stored transposes: 4 column
         // tiles x ks row splits fill the GPU (a 1024 x 1024 x 16 product is too
         // small for one CTA per row block)
-        D.ks = std::max(1, std::min(64, std::min(D.qe, D.qh) / 16));
+        D.ks = std::max(1, std::min(32, std::min(D.qe, D.qh) / 16));
+        if (const char* e = getenv("FDTD_KS")) D.ks = std::max(1, atoi(e));
         D.part_d = dalloc<double>((size_t)(D.ks + D.splits) * D.qh * D.N);
         D.parte_d = dalloc<double>((size_t)D.ks * D.qe * D.N);
         D.gen_d = dalloc<T>((size_t)D.qe);
@@ -1009,6 +1011,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     const int outy = tBY - 1;
     tsplit.ntx = (nx + 1 + tOUTX - 1) / tOUTX;
     tsplit.outx = tOUTX; tsplit.outy = outy; tsplit.nzp = nz + 1;
+    tsplit.jitter = getenv("FDTD_JITTER") ? std::max(0, atoi(getenv("FDTD_JITTER"))) : 0;
     tsplit.ncols = tsplit.ntx * ((ny + 1 + outy - 1) / outy);
     int sms = 148;
     {
@@ -1447,6 +1450,13 @@ int Impl<T>::launch_persist(int64_t n, int64_t* count) {
   for (size_t b = 0; b <= fblocks.size(); ++b) P.row0[b] = p_row0[b];
   P.nfb = (int)fblocks.size(); P.Rtot = p_Rtot; P.rpc = p_rpc; P.Cmax = p_Cmax;
   P.eb[0] = eb[0]; P.eb[1] = eb[1]; P.hb[0] = hb[0]; P.hb[1] = hb[1]; P.y = y_all; P.G = g_all;
+  P.y_in = y_all;
+  if (p_ll && y_size > 0) {
+    if (!p_yin) p_yin = dalloc<T>(y_size);
+    if (!p_yin) return fail(FDTD_ENOMEM, "persistent-path allocation failed");
+    CK(cudaMemcpyAsync(p_yin, y_all, sizeof(T) * y_size, cudaMemcpyDeviceToDevice, stream));
+    P.y_in = p_yin;
+  }
   P.ring = ring; P.cap = cap; P.n_probe = n_probe;
   P.step0 = host_step + step_offset; P.p0 = p0; P.nsteps = (int)n;
   P.d_step_out = d_step + p1;
@@ -1469,6 +1479,7 @@ int Impl<T>::launch_persist(int64_t n, int64_t* count) {
   }
   P.K = p_K;
   P.ymask = p_D - 1;
+  P.jitter = getenv("FDTD_JITTER") ? (unsigned)std::max(0, atoi(getenv("FDTD_JITTER"))) : 0u;
   P.sleep_ns = 0;
   if (p_K > 0) {
     static const unsigned sl = getenv("FDTD_P2SLEEP") ? (unsigned)atoi(getenv("FDTD_P2SLEEP")) : 0u;
@@ -1536,7 +1547,8 @@ int Impl<T>::build_fused(const fdtd_probes* probes) {
       gks = 8;                  // measured: config 5 53.2 (K-split 8) vs 52.2 (4) vs 50.8 (2) Gcell/s
       if (const char* e = getenv("FDTD_GEMM_KS")) { const int k = atoi(e); if (k == 2 || k == 4 || k == 8) gks = k; }
     }
-    const size_t need = (size_t)(TRg * NPsel + maxCp / gks * NPsel + TRg * (maxCp / gks + 2)) * sizeof(double);
+    const size_t need = (size_t)(TRg * NPsel + TRg * (maxCp / gks + 2)) * sizeof(double) +
+                        (size_t)maxCp / gks * NPsel * sizeof(T);
     fused_gemm = maxN >= 4;
     if (const char* e = getenv("FDTD_FUSED")) fused_gemm = std::string(e) == "gemm";
     if (need > 200 * 1024) fused_gemm = false;
@@ -1648,7 +1660,8 @@ int Impl<T>::build_fused(const fdtd_probes* probes) {
   rows_per_cta = ROWS;
   n_ctas = (int)ctas.size();
   NBsel = maxN <= 1 ? 1 : maxN <= 4 ? 4 : maxN <= 16 ? 16 : 32;
-  fused_smem = fused_gemm ? (size_t)(ROWS * NPsel + max_cols / gks * NPsel + ROWS * (max_cols / gks + 2)) * sizeof(double)
+  fused_smem = fused_gemm ? (size_t)(ROWS * NPsel + ROWS * (max_cols / gks + 2)) * sizeof(double) +
+                                (size_t)max_cols / gks * NPsel * sizeof(T)
                           : (size_t)max_cols * maxN * sizeof(T);
   if (fused_smem > 200 * 1024)
     return fail(FDTD_ENOTSUP, "fused reduced kernel needs %zu bytes of shared memory (> 200 KB)", fused_smem);
@@ -1782,7 +1795,7 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
           // a4: e~ -= G_e K~' h~  (split-K TN on K~'^T, then the axpy with -g_e)
           n += launch_gemm_tn(D.qh, D.qe, D.Kpe, D.N, D.ks, (const float*)D.KTp_d, (const float*)h,
                               D.parte_d, rs);
-          fdtd::reduce_axpy_f32_kernel<<<(D.qe * D.N + 255) / 256, 256, 0, rs>>>(
+          fdtd::reduce_axpy_f32_kernel<<<(D.qe * D.N + 31) / 32, 256, 0, rs>>>(
               D.qe, D.N, D.ks, D.parte_d, nullptr, (const float*)D.gen_d, (float*)e, nullptr);
           ++n;
           // a6: h~ += G_h (K~'^T e~ + S_E^T G): both as split-K partials into one
@@ -1791,7 +1804,7 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
                               D.part_d, rs);
           n += launch_gemm_tn(D.n_if, D.qh, D.Kph, D.N, D.splits, (const float*)D.SEp_d,
                               (const float*)(g_all + D.y_off), D.part_d + (size_t)D.ks * D.qh * D.N, rs);
-          fdtd::reduce_axpy_f32_kernel<<<(D.qh * D.N + 255) / 256, 256, 0, rs>>>(
+          fdtd::reduce_axpy_f32_kernel<<<(D.qh * D.N + 31) / 32, 256, 0, rs>>>(
               D.qh, D.N, D.ks + D.splits, D.part_d, nullptr, (const float*)D.gh_d, (float*)h,
               D.tc ? D.xs_d : nullptr);
           ++n;

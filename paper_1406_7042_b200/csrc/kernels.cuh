@@ -1046,7 +1046,7 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
   constexpr int TR = 8 * GPW * RPW;            // rows per tile
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Ps = reinterpret_cast<double*>(smem_raw);   // [TR][NP] partial tile
-  double* Xs = Ps + TR * NP;                          // [kc][NP] slice of [e~ ; h~ ; G]
+  T* Xs = reinterpret_cast<T*>(Ps + TR * NP);         // [kc][NP] slice of [e~ ; h~ ; G] (run precision)
   const int64_t step = *P.d_step;
   const bool check = P.check_every > 0 && (step % P.check_every) == 0;
   bool bad = false;
@@ -1061,7 +1061,7 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
     const FusedBlock<T>& FB = P.fb[ct.x];
     const int N = FB.N, C = FB.C, qe = FB.qe, qh = FB.qh;
     const int kc = FB.Cp / KS, k_lo = (int)rank * kc;
-    double* Ms = Xs + kc * NP;                 // [TR][kc + 2] slice of M (padded pitch)
+    double* Ms = reinterpret_cast<double*>(Xs + kc * NP);   // [TR][kc + 2] slice of M (padded pitch)
     const int mp = kc + 2;
     const double* Msrc = (sizeof(T) == 4) ? FB.M64 : reinterpret_cast<const double*>(FB.M);
     // M slice: 16-byte cp.async (two doubles), all in flight at once
@@ -1073,22 +1073,36 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
     // M does not depend on the step; the states and G do: launched as a
     // programmatic dependent of the stencil, wait for it here
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    for (int t0 = threadIdx.x; t0 < kc * NP; t0 += 8 * 256) {
-      double v[8];
-#pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        const int t = t0 + w * 256, kk = t / NP, n = t % NP, k = k_lo + kk;
-        v[w] = 0.0;
-        if (t < kc * NP && n < N && k < C) {
-          if (k < qe) v[w] = (double)P.e_in[FB.e_off + (int64_t)k * N + n];
-          else if (k < qe + qh) v[w] = (double)P.h_in[FB.h_off + (int64_t)(k - qe) * N + n];
-          else v[w] = (double)P.G[FB.y_off + (int64_t)(k - qe - qh) * N + n];
-        }
+    constexpr int VN = Vec<T>::n;
+    if (N == NP && N % VN == 0) {
+      // X slice, straight 16-byte copies (every k-row is N contiguous words)
+      for (int t = threadIdx.x; t < kc * (NP / VN); t += blockDim.x) {
+        const int kk = t / (NP / VN), n = (t % (NP / VN)) * VN, k = k_lo + kk;
+        const T* src = P.e_in;                 // any valid address when zero-filled
+        if (k < qe) src = P.e_in + FB.e_off + (int64_t)k * N + n;
+        else if (k < qe + qh) src = P.h_in + FB.h_off + (int64_t)(k - qe) * N + n;
+        else if (k < C) src = P.G + FB.y_off + (int64_t)(k - qe - qh) * N + n;
+        cp_async16(Xs + kk * NP + n, src, k < C);
       }
+    } else {
+      for (int t0 = threadIdx.x; t0 < kc * NP; t0 += 8 * 256) {
+        T v[8];
 #pragma unroll
-      for (int w = 0; w < 8; ++w)
-        if (t0 + w * 256 < kc * NP) Xs[t0 + w * 256] = v[w];
+        for (int w = 0; w < 8; ++w) {
+          const int t = t0 + w * 256, kk = t / NP, n = t % NP, k = k_lo + kk;
+          v[w] = 0;
+          if (t < kc * NP && n < N && k < C) {
+            if (k < qe) v[w] = P.e_in[FB.e_off + (int64_t)k * N + n];
+            else if (k < qe + qh) v[w] = P.h_in[FB.h_off + (int64_t)(k - qe) * N + n];
+            else v[w] = P.G[FB.y_off + (int64_t)(k - qe - qh) * N + n];
+          }
+        }
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+          if (t0 + w * 256 < kc * NP) Xs[t0 + w * 256] = v[w];
+      }
     }
+    cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1100,7 +1114,7 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
     const int nv = kc / 2;
 #pragma unroll 4
     for (int kv = 0; kv < nv; ++kv) {
-      const double x0 = Xs[(2 * kv) * NP + n], x1 = Xs[(2 * kv + 1) * NP + n];
+      const double x0 = (double)Xs[(2 * kv) * NP + n], x1 = (double)Xs[(2 * kv + 1) * NP + n];
 #pragma unroll
       for (int u = 0; u < RPW; ++u) {
         const double2 m = *reinterpret_cast<const double2*>(Ms + (rl0 + u) * mp + 2 * kv);
@@ -1529,13 +1543,28 @@ gemm_tn_f32_partial_kernel(int rows, int cols, int Kp, const float* __restrict__
 // xs (optional, N = 16): the new h~ split for the tensor-core GEMM of
 // tc_gemm.cuh -- per 32-row chunk of h~, [hi | lo] tiles of [16 n][32 k] in
 // the 128-byte swizzled K-major layout, so one bulk copy per chunk lands them
-static __global__ void reduce_axpy_f32_kernel(int cols, int N, int splits, const double* __restrict__ part,
+// 256 threads = 32 outputs x 8 split groups: each thread sums a contiguous
+// range of the splits, then the 8 group sums of an output are added in group
+// order (fixed order, deterministic; 8x the memory-level parallelism of one
+// thread per output walking all splits)
+static __global__ void __launch_bounds__(256) reduce_axpy_f32_kernel(int cols, int N, int splits, const double* __restrict__ part,
                                        const float* __restrict__ Tv, const float* __restrict__ gh,
                                        float* __restrict__ h, float* __restrict__ xs) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= cols * N) return;
+  __shared__ double gs[8][32];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + lane;
+  const int s_lo = (int)((int64_t)splits * grp / 8), s_hi = (int)((int64_t)splits * (grp + 1) / 8);
+  double acc = 0.0;
+  if (t < cols * N) {
+#pragma unroll 4
+    for (int s2 = s_lo; s2 < s_hi; ++s2) acc += part[(int64_t)s2 * cols * N + t];
+  }
+  gs[grp][lane] = acc;
+  __syncthreads();
+  if (grp != 0 || t >= cols * N) return;
   double v = Tv ? (double)Tv[t] : 0.0;
-  for (int s2 = 0; s2 < splits; ++s2) v += part[(int64_t)s2 * cols * N + t];
+#pragma unroll
+  for (int g2 = 0; g2 < 8; ++g2) v += gs[g2][lane];
   // fp64 partials, one rounding of the new state (R14)
   const float hn = (float)fma((double)gh[t / N], v, (double)h[t]);
   h[t] = hn;

@@ -91,6 +91,9 @@ struct Persist2D {
   int row0[kMaxFusedBlocks + 1];          // first global row of each block
   int nfb, Rtot, rpc, Cmax;           // rpc: rows per reduced CTA (CTAs nT .. nT+n_red_ctas-1)
   T* eb[2]; T* hb[2]; T* y; T* G;
+  const T* y_in;                // fp32: a copy of y taken before the launch, read at local step 0 (the
+                                // reduced CTAs overwrite y during the launch; a temporal-blocking halo
+                                // tile is on no chain that orders its step-0 read before that write)
   T* ring; int64_t cap; int n_probe;
   int64_t step0; int p0; int nsteps;
   int64_t* d_step_out;
@@ -110,7 +113,18 @@ struct Persist2D {
   int K;                        // 0: per-step exchange (persist2d_tile)
   unsigned long long* lband;    // [2][nT][4 sides][3 fields][K][T] tagged words
   unsigned sleep_ns;            // poll back-off of the temporal-blocking kernel
+  unsigned jitter;              // race testing (FDTD_JITTER=ns): pseudo-random per-warp delays
 };
+
+// race testing: warp-level pseudo-random delay of 0..P.jitter ns at a phase point
+#define P2_JITTER(P, salt)                                                                        \
+  do {                                                                                            \
+    if ((P).jitter) {                                                                             \
+      const unsigned hsh_ = (blockIdx.x * 2654435761u) ^ ((unsigned)(salt) * 40503u) ^ ((threadIdx.x >> 5) * 97u); \
+      if ((threadIdx.x & 31) == 0) __nanosleep((hsh_ * 2246822519u >> 7) % (P).jitter);           \
+      __syncwarp();                                                                               \
+    }                                                                                             \
+  } while (0)
 
 template <bool B> struct BoolC { static constexpr bool value = B; };
 
@@ -259,6 +273,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
     const int64_t step = P.step0 + ls;
     const bool do_check = P.check_every > 0 && (step % P.check_every) == 0;
     if (dslot >= 0) P2_STAMP(dslot, 0);
+    P2_JITTER(P, 3 * ls);
     // ------------------------------------------------------------- E phase
     // (a) interior cells need no halo: computed before waiting for neighbours
     auto e_cell = [&](int il, int jl) {
@@ -375,7 +390,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       for (int r = tid; r < rows_hi - rows_lo; r += nthr) {
         const int64_t yo = rs[r].yo;
         const int sc = rs[r].src;
-        yv[r] = (yo >= 0) ? __ldcg(P.y + yo) : (T)0;
+        yv[r] = (yo >= 0) ? __ldcg((LL ? P.y_in : P.y) + yo) : (T)0;
         if (sc >= 0) yv[P.maxrows + r] = (step < P.R.n_wave) ? P.R.wave[step * P.R.n_cols + sc] : (T)0;
       }
     }
@@ -432,6 +447,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       if (has_if) atomicAdd(P.gready, 1u);
     }
     }
+    P2_JITTER(P, 3 * ls + 1);
     // ------------------------------------------------------------- H phase
     auto h_cell = [&](int il, int jl) {
       const int i = i0 + il;
@@ -621,6 +637,7 @@ __device__ void persist2d_reduced(const Persist2D<T>& P, unsigned char* smem_raw
     const int p = (P.p0 + ls) & 1;
     const bool do_check = P.check_every > 0 && (step % P.check_every) == 0;
     if (rc == 0) P2_STAMP(2, 0);
+    P2_JITTER(P, 3 * ls + 2);
     constexpr bool LL = sizeof(T) == 4;
     const unsigned tag_prev = (unsigned)ls, tag_cur = (unsigned)(ls + 1);
     // inputs e~, h~ of this step: every reduced CTA finished the previous one
@@ -936,6 +953,7 @@ __device__ void persist2d_tb_tile(const Persist2D<T>& P, unsigned char* smem_raw
       const bool do_check = P.check_every > 0 && (step % P.check_every) == 0;
       const unsigned tag_prev = (unsigned)ls, tag_cur = (unsigned)(ls + 1);
       if (dslot >= 0) P2_STAMP(dslot, 0);
+      P2_JITTER(P, 3 * ls);
       // ---- E on extended rows 1..EX-1, cell pairs (x, x+1); explicit-row
       //      cells (and x = 0) keep their value here
       auto e_pass = [&](auto MONO) {
@@ -988,7 +1006,7 @@ __device__ void persist2d_tb_tile(const Persist2D<T>& P, unsigned char* smem_raw
         if (c % EX == 0 || c < EX) continue;        // stencil outside the extended tile
         T yvv = 0;
         if (xr.yo >= 0) {
-          if (ls == 0) yvv = __ldcg(P.y + xr.yo);
+          if (ls == 0) yvv = __ldcg(P.y_in + xr.yo);
           else {
             float v = 0.f;
             ok = ll_ld(P.ly + (int64_t)((ls - 1) & P.ymask) * P.ysz + xr.yo, tag_prev, v, P.abort_flag, P.sleep_ns);

@@ -262,6 +262,11 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
       if (a + 2 <= kl) m_n3 = load_mat(a + 2);
     }
     for (int kk = a; kk <= kl; ++kk) {
+      if (S.jitter) {
+        const unsigned hsh = (unsigned)(blockIdx.x * 2654435761u) ^ (unsigned)(kk * 40503u) ^ (threadIdx.y * 97u);
+        if ((threadIdx.x & 31) == 0) __nanosleep((hsh * 2246822519u >> 7) % (unsigned)S.jitter);
+        __syncwarp();
+      }
       mbar_wait(&bars[st], phase);
       const T* h = Ring + st * STG + hoff;
       const T* e = Ring + st * STG + 3 * HP + erow;

@@ -24,6 +24,10 @@ struct TileSplit {
   // ncols) (the interface columns or the rest); null: all
   const int* colperm = nullptr;
   int col0 = 0;
+  // race testing (FDTD_JITTER=ns): every warp sleeps a pseudo-random 0..jitter
+  // ns before each plane, shaking the warp / TMA interleaving; results must
+  // stay bitwise identical (tests/test_gpu_races.py)
+  int jitter = 0;
   __host__ __device__ __forceinline__ int column(int c) const { return colperm ? colperm[col0 + c] : c; }
 };
 
