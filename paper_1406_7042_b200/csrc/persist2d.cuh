@@ -996,6 +996,10 @@ __device__ void persist2d_tb_tile(const Persist2D<T>& P, unsigned char* smem_raw
         }
       };
       if (mono) e_pass(BoolC<true>{}); else e_pass(BoolC<false>{});
+      // the pair stores above write an explicit-row cell's OLD value back: the
+      // rows below must start after every warp's pass (found by the jitter
+      // test, tests/test_gpu_races.py)
+      if (nrw > 0) __syncthreads();
       if (dslot >= 0) P2_STAMP(dslot, 1);
       // ---- explicit rows (eval_row order: terms, y, source); only the owner
       //      publishes E_if into G
