@@ -474,10 +474,11 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       c.BY = 8;
       if (B == 1) {
         c.MB = 0; c.W = 2; c.NS = sizeof(T) == 4 ? 6 : 3;
-        // short z extent (config 5: 41 planes, L2-resident, latency-bound): 16-row
-        // tiles with 512 threads (measured 52.4 vs 45.8 Gcell/s for 8-row
-        // tiles; for long z extents the 8-row tiles win: config 3 0.75 vs 0.72)
-        if (sizeof(T) == 4 && nz + 1 < 64) { c.W = 2; c.NS = 4; c.BY = 16; }
+        // short z extent (config 5: 41 planes): the kernel is bound by issue
+        // latency, not bandwidth (time follows the executed-instruction count),
+        // so the variant with three resident CTAs per SM (8-row tiles, 4-plane
+        // ring, <= 85 registers) wins: measured 55 vs 64 us per step
+        if (sizeof(T) == 4 && nz + 1 < 64) { c.W = 2; c.NS = 4; c.BY = 8; }
       }
       else { c.MB = B; c.W = kW; c.NS = 3; }
       if (const char* e = getenv("FDTD_TILE")) { c.BY = 8; sscanf(e, "%d,%d,%d", &c.W, &c.NS, &c.BY); }
@@ -850,59 +851,6 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     rows.e_comp = d_ec; rows.e_off = d_eo; rows.c = d_c; rows.rowptr = d_rp; rows.h_comp = d_hc;
     rows.h_off = d_ho; rows.w = d_w; rows.y_off = d_yo; rows.src = d_src; rows.cs = d_cs; rows.wave = d_wave;
     rows.g_out = g_all;
-    // local-slot form of the rows (3-D): slot s of component ec is the H term
-    //   Ex: 0 Hz(0)  1 Hz(j-1)  2 Hy(0)  3 Hy(k-1)
-    //   Ey: 0 Hz(0)  1 Hz(i-1)  2 Hx(0)  3 Hx(k-1)
-    //   Ez: 0 Hx(0)  1 Hx(j-1)  2 Hy(0)  3 Hy(i-1)
-    rows.lcode = nullptr; rows.lw = nullptr;
-    if (dim == 3 && nr > 0) {
-      std::vector<uint16_t> code(nr);
-      std::vector<T> lw((size_t)nr * 4, (T)0);
-      bool local = true;
-      auto ijk = [&](int64_t s_, int& i, int& j, int& k) {
-        i = (int)(s_ % (nx + 1)); j = (int)((s_ / (nx + 1)) % (ny + 1)); k = (int)(s_ / ((int64_t)(nx + 1) * (ny + 1)));
-      };
-      for (int64_t r = 0; r < nr && local; ++r) {
-        const HRow& h = hrows[r];
-        if (h.w.size() > 4) { local = false; break; }
-        int i, j, k;
-        ijk(h.s, i, j, k);
-        uint16_t cd = (uint16_t)(h.w.size() << 8);
-        for (size_t q = 0; q < h.w.size(); ++q) {
-          const int hc_ = (int)(h.w[q].first / S);
-          int hi, hj, hk;
-          ijk(h.w[q].first % S, hi, hj, hk);
-          const int di = hi - i, dj = hj - j, dk = hk - k;
-          int sl = -1;
-          if (h.comp == 0) {
-            if (hc_ == 5 && di == 0 && dj == 0 && dk == 0) sl = 0;
-            else if (hc_ == 5 && di == 0 && dj == -1 && dk == 0) sl = 1;
-            else if (hc_ == 4 && di == 0 && dj == 0 && dk == 0) sl = 2;
-            else if (hc_ == 4 && di == 0 && dj == 0 && dk == -1) sl = 3;
-          } else if (h.comp == 1) {
-            if (hc_ == 5 && di == 0 && dj == 0 && dk == 0) sl = 0;
-            else if (hc_ == 5 && di == -1 && dj == 0 && dk == 0) sl = 1;
-            else if (hc_ == 3 && di == 0 && dj == 0 && dk == 0) sl = 2;
-            else if (hc_ == 3 && di == 0 && dj == 0 && dk == -1) sl = 3;
-          } else {
-            if (hc_ == 3 && di == 0 && dj == 0 && dk == 0) sl = 0;
-            else if (hc_ == 3 && di == 0 && dj == -1 && dk == 0) sl = 1;
-            else if (hc_ == 4 && di == 0 && dj == 0 && dk == 0) sl = 2;
-            else if (hc_ == 4 && di == -1 && dj == 0 && dk == 0) sl = 3;
-          }
-          if (sl < 0) { local = false; break; }
-          cd |= (uint16_t)(sl << (2 * q));
-          lw[(size_t)r * 4 + q] = (T)h.w[q].second;
-        }
-        code[r] = cd;
-      }
-      if (local && !getenv("FDTD_NO_LOCAL_ROWS")) {
-        uint16_t* d_code = dalloc<uint16_t>(nr);
-        T* d_lw = dalloc<T>((size_t)nr * 4);
-        if (!d_code || !d_lw || upload(d_code, code) || upload(d_lw, lw)) return FDTD_ECUDA;
-        rows.lcode = d_code; rows.lw = d_lw;
-      }
-    }
     for (int c = 0; c < 3; ++c) rows.row_of[c] = nullptr;
     for (int c = 0; c < 3; ++c) {
       bool any = false;
@@ -1030,6 +978,8 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       const int kmax = (sizeof(T) == 4 && B == 1) ? 24 : 8;
       int nch = std::max((nzp + kmax - 1) / kmax, (int)((4LL * G + tsplit.ncols - 1) / tsplit.ncols));
       nch = std::max(1, std::min(nch, nzp / 8));
+      // short z extents: one wave of co-resident CTAs (items <= resident slots)
+      if (sizeof(T) == 4 && B == 1 && nzp < 64) nch = std::max(1, std::min(nch, G / std::max(1, tsplit.ncols)));
       int kc = (nzp + nch - 1) / nch;
       if (const char* e = getenv("FDTD_TILE_KC")) kc = std::max(1, atoi(e));
       tsplit.kc = kc;
@@ -1722,6 +1672,12 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
     SB.col0 = n_ifc; SB.ncols = tsplit.ncols - n_ifc; SB.nitems = SB.ncols * nch;
   }
   const cudaStream_t rs = sp ? st2 : st;    // the reduced update's stream
+  if (dim == 3 && use_tile && rows.n_rows > 0) {
+    // explicit rows first: the tile stencil reads their E^{n+1} back from the new parity
+    const int64_t nt = rows.n_rows * B;
+    fdtd::rows_prepass_kernel<T><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, B, F0, F1, y_all, ds);
+    ++n;
+  }
   if (dim == 3 && use_tile && sp) {
     CK(fdtd::tile_launch<T>(tcfg, uniform, SA.nitems, tile_smem, st, tma[p], SA, dm, F0, F1, mat_id, tab,
                             ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad));

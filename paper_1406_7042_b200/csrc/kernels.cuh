@@ -27,10 +27,18 @@ template <typename T> struct Coef;       // per-material coefficient, hi/lo for 
 template <> struct Coef<float> {
   float hi, lo;
   __device__ __forceinline__ float apply(float d) const { return fmaf(hi, d, lo * d); }
+  // e +- c d with the rounding sequence every stencil kernel uses (bitwise-equality tests)
+  __device__ __forceinline__ float add(float e, float d) const { return e + fmaf(hi, d, lo * d); }
+  __device__ __forceinline__ float sub(float e, float d) const { return e - fmaf(hi, d, lo * d); }
 };
 template <> struct Coef<double> {
   double hi, lo;
   __device__ __forceinline__ double apply(double d) const { return hi * d; }
+  // fp64: one fused multiply-add (what the compiler's contraction makes of
+  // e + hi * d in the reference kernels), spelled out so that restructured code
+  // cannot round differently
+  __device__ __forceinline__ double add(double e, double d) const { return __fma_rn(hi, d, e); }
+  __device__ __forceinline__ double sub(double e, double d) const { return __fma_rn(-hi, d, e); }
 };
 
 constexpr int MAX_MAT = 256;
@@ -77,13 +85,7 @@ struct RowsE {
   const T* wave;               // [n_wave][n_src][B]   (n_src = number of waveform columns)
   int64_t n_wave, n_src;
   T* g_out;                    // interface rows publish E^{n+1} at G[y_off] (reduced-chain input)
-  // 3-D rows whose H terms are all the curl neighbours the stencil already
-  // holds (every interface row of the R4 construction): per row the CSR
-  // order as 2-bit slots + the count (lcode), and the weights [4] (lw); null
-  // when some row is not local (stencil3d_tile_kernel then uses eval_row)
-  const uint16_t* lcode;       // bits 0-7: slots of terms 0..3 (2 bits each), bits 8-10: nterm
-  const T* lw;                 // [n_rows][4]
-  // list form (for the standalone rows kernel)
+  // list form (rows_prepass_kernel)
   const int32_t* e_comp;       // [n_rows]
   const int64_t* e_off;        // [n_rows]
 };
@@ -96,11 +98,30 @@ __device__ __forceinline__ T eval_row(const RowsE<T>& R, int r, int b, int B, T 
     acc += R.w[k] * H0.f[R.h_comp[k]][R.h_off[k] * B + b];
   const int64_t yo = R.y_off[r];
   if (yo >= 0) acc += y[yo + b];
-  T e = e0 - R.c[r].apply(acc);
+  T e = R.c[r].sub(e0, acc);
   const int s = R.src[r];
   if (s >= 0 && step < R.n_wave) e -= R.cs[r] * R.wave[(step * R.n_src + s) * B + b];
   if (yo >= 0) R.g_out[yo + b] = e;        // identical value from every thread computing it
   return e;
+}
+
+// Explicit rows ahead of the 3-D tile stencil: one thread per
+// (row, batch member) evaluates the row from the old parity (the same CSR walk
+// as in the reference stencils, so the value is theirs bit for bit), publishes
+// it into G and stores E^{n+1} of the row's unknown into the NEW parity; the
+// stencil thread that owns the unknown then reads that value back instead of
+// walking the row itself (a chain of dependent global loads per row that made
+// the tiles with interface rows the stragglers of the step).
+template <typename T>
+__global__ void __launch_bounds__(256)
+rows_prepass_kernel(RowsE<T> R, int B, Fields<T> F0, Fields<T> F1, const T* __restrict__ y,
+                    const int64_t* __restrict__ d_step) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= R.n_rows * B) return;
+  const int r = (int)(t / B), b = (int)(t % B);
+  const int64_t o = R.e_off[r] * B + b;
+  const int c = R.e_comp[r];
+  F1.f[c][o] = eval_row(R, r, b, B, F0.f[c][o], F0, y, *d_step);
 }
 
 // ---------------------------------------------------------------------------
@@ -166,7 +187,7 @@ stencil2d_rows_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
     const T hxm = (r == 0) ? hx_jm : hx[r - 1];
     const Coef<T> c = UNIFORM ? u0 : tab->c[m[r]][2];
     const T dd = (hy[r] - hyim[r]) - (hx[r] - hxm);
-    ez[r] = (ci && j > 0 && j < ny) ? ez0[r] + c.apply(dd) : (T)0;
+    ez[r] = (ci && j > 0 && j < ny) ? c.add(ez0[r], dd) : (T)0;
     if (!UNIFORM && (tab->ifm[m[r]] & 4) && i <= nx && j <= ny)
       ez[r] = eval_row(R, R.row_of[2][min(j, ny) * d.px + ii], b, B, ez0[r], F0, y, step);
     sE[(ty * CY + r) * BX + tx] = ez[r];
@@ -184,8 +205,8 @@ stencil2d_rows_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
     Coef<T> cx, cy;
     if (UNIFORM) { cx = u1; cy = u1; }
     else { cx = tab->c[m[r]][3]; cy = tab->c[m[r]][4]; }
-    const T hx1 = (ci && j < ny) ? hx[r] - cx.apply(ez_jp - ez[r]) : hx[r];
-    const T hy1 = (i < nx && j > 0 && j < ny) ? hy[r] + cy.apply(ez_ip - ez[r]) : hy[r];
+    const T hx1 = (ci && j < ny) ? cx.sub(hx[r], ez_jp - ez[r]) : hx[r];
+    const T hy1 = (i < nx && j > 0 && j < ny) ? cy.add(hy[r], ez_ip - ez[r]) : hy[r];
     const int o = o0 + r * rs;
     F1.f[2][o] = ez[r]; F1.f[3][o] = hx1; F1.f[4][o] = hy1;
     if (do_check) bad |= !(finite_small(ez[r]) && finite_small(hx1) && finite_small(hy1));
@@ -324,9 +345,9 @@ stencil3d_pipe_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
     if (UNIFORM) { cx = u0; cy = u0; cz = u0; }
     else { cx = tab->c[m][0]; cy = tab->c[m][1]; cz = tab->c[m][2]; ifmk = tab->ifm[m]; }
     const bool kin = (kk > 0) && (kk < nz);
-    T ex = (ax_ij && kin) ? ex0 + cx.apply((hz_c - hz_jm) - (hy_c - hy_p)) : (T)0;
-    T ey = (ay_ij && kin) ? ey0 + cy.apply((hx_c - hx_p) - (hz_c - hz_im)) : (T)0;
-    T ez = (az_ij && kk < nz) ? ez0 + cz.apply((hy_c - hy_im) - (hx_c - hx_jm)) : (T)0;
+    T ex = (ax_ij && kin) ? cx.add(ex0, (hz_c - hz_jm) - (hy_c - hy_p)) : (T)0;
+    T ey = (ay_ij && kin) ? cy.add(ey0, (hx_c - hx_p) - (hz_c - hz_im)) : (T)0;
+    T ez = (az_ij && kk < nz) ? cz.add(ez0, (hy_c - hy_im) - (hx_c - hx_jm)) : (T)0;
     if (!UNIFORM && ifmk && inside) {
       const int64_t s = (int64_t)kk * d.plane + scol;
       if (ifmk & 1) ex = eval_row(R, R.row_of[0][s], b, B, ex0, F0, y, step);
@@ -350,9 +371,9 @@ stencil3d_pipe_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
       Coef<T> hx_, hy_, hz_;
       if (UNIFORM) { hx_ = u1; hy_ = u1; hz_ = u1; }
       else { hx_ = tab->c[m_prev][3]; hy_ = tab->c[m_prev][4]; hz_ = tab->c[m_prev][5]; }   // plane kk-1
-      const T hx1 = (hx_ij && km < nz) ? hxk - hx_.apply((ez_jp - ezk) - (ey - eyk)) : hxk;
-      const T hy1 = (hy_ij && km < nz) ? hyk - hy_.apply((ex - exk) - (ez_ip - ezk)) : hyk;
-      const T hz1 = (hz_ij && km > 0 && km < nz) ? hzk - hz_.apply((ey_ip - eyk) - (ex_jp - exk)) : hzk;
+      const T hx1 = (hx_ij && km < nz) ? hx_.sub(hxk, (ez_jp - ezk) - (ey - eyk)) : hxk;
+      const T hy1 = (hy_ij && km < nz) ? hy_.sub(hyk, (ex - exk) - (ez_ip - ezk)) : hyk;
+      const T hz1 = (hz_ij && km > 0 && km < nz) ? hz_.sub(hzk, (ey_ip - eyk) - (ex_jp - exk)) : hzk;
       const int64_t o = (int64_t)km * sz + col;
       F1.f[3][o] = hx1; F1.f[4][o] = hy1; F1.f[5][o] = hz1;
       if (do_check) bad |= !(finite_small(hx1) && finite_small(hy1) && finite_small(hz1));
@@ -522,9 +543,9 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int out
     if (UNIFORM) { cx = u0; cy = u0; cz = u0; }
     else { cx = tab->c[m][0]; cy = tab->c[m][1]; cz = tab->c[m][2]; ifmk = tab->ifm[m]; }
     const bool kin = (kk > 0) && (kk < nz);
-    T ex = (ax_ij && kin) ? ex0 + cx.apply((hz_c - hz_jm) - (hy_c - hy_p)) : (T)0;
-    T ey = (ay_ij && kin) ? ey0 + cy.apply((hx_c - hx_p) - (hz_c - hz_im)) : (T)0;
-    T ez = (az_ij && kk < nz) ? ez0 + cz.apply((hy_c - hy_im) - (hx_c - hx_jm)) : (T)0;
+    T ex = (ax_ij && kin) ? cx.add(ex0, (hz_c - hz_jm) - (hy_c - hy_p)) : (T)0;
+    T ey = (ay_ij && kin) ? cy.add(ey0, (hx_c - hx_p) - (hz_c - hz_im)) : (T)0;
+    T ez = (az_ij && kk < nz) ? cz.add(ez0, (hy_c - hy_im) - (hx_c - hx_jm)) : (T)0;
     if (!UNIFORM && ifmk && inside) {
       const int64_t s = (int64_t)kk * d.plane + scol;
       if (ifmk & 1) ex = eval_row(R, R.row_of[0][s], b, B, ex0, F0, y, step);
@@ -548,9 +569,9 @@ stencil3d_tma_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int out
       Coef<T> hx_, hy_, hz_;
       if (UNIFORM) { hx_ = u1; hy_ = u1; hz_ = u1; }
       else { hx_ = tab->c[m_prev][3]; hy_ = tab->c[m_prev][4]; hz_ = tab->c[m_prev][5]; }   // plane kk-1
-      const T hx1 = (hx_ij && km < nz) ? hxk - hx_.apply((ez_jp - ezk) - (ey - eyk)) : hxk;
-      const T hy1 = (hy_ij && km < nz) ? hyk - hy_.apply((ex - exk) - (ez_ip - ezk)) : hyk;
-      const T hz1 = (hz_ij && km > 0 && km < nz) ? hzk - hz_.apply((ey_ip - eyk) - (ex_jp - exk)) : hzk;
+      const T hx1 = (hx_ij && km < nz) ? hx_.sub(hxk, (ez_jp - ezk) - (ey - eyk)) : hxk;
+      const T hy1 = (hy_ij && km < nz) ? hy_.sub(hyk, (ex - exk) - (ez_ip - ezk)) : hyk;
+      const T hz1 = (hz_ij && km > 0 && km < nz) ? hz_.sub(hzk, (ey_ip - eyk) - (ex_jp - exk)) : hzk;
       const int64_t o = (int64_t)km * sz + col;
       F1.f[3][o] = hx1; F1.f[4][o] = hy1; F1.f[5][o] = hz1;
       if (do_check) bad |= !(finite_small(hx1) && finite_small(hy1) && finite_small(hz1));
@@ -714,9 +735,9 @@ stencil3d_tma_vec_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int
     L ex, ey, ez;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      ex.v[w] = (ax_ij && kin) ? ex0.v[w] + cx.apply((hz_c.v[w] - hz_jm.v[w]) - (hy_c.v[w] - hy_p.v[w])) : (T)0;
-      ey.v[w] = (ay_ij && kin) ? ey0.v[w] + cy.apply((hx_c.v[w] - hx_p.v[w]) - (hz_c.v[w] - hz_im.v[w])) : (T)0;
-      ez.v[w] = (az_ij && kk < nz) ? ez0.v[w] + cz.apply((hy_c.v[w] - hy_im.v[w]) - (hx_c.v[w] - hx_jm.v[w])) : (T)0;
+      ex.v[w] = (ax_ij && kin) ? cx.add(ex0.v[w], (hz_c.v[w] - hz_jm.v[w]) - (hy_c.v[w] - hy_p.v[w])) : (T)0;
+      ey.v[w] = (ay_ij && kin) ? cy.add(ey0.v[w], (hx_c.v[w] - hx_p.v[w]) - (hz_c.v[w] - hz_im.v[w])) : (T)0;
+      ez.v[w] = (az_ij && kk < nz) ? cz.add(ez0.v[w], (hy_c.v[w] - hy_im.v[w]) - (hx_c.v[w] - hx_jm.v[w])) : (T)0;
     }
     if (!UNIFORM && ifmk && inside) {
       const int64_t s = (int64_t)kk * d.plane + scol;
@@ -750,9 +771,9 @@ stencil3d_tma_vec_kernel(const __grid_constant__ TmaSet tm, int HBX, int SX, int
       L hx1, hy1, hz1;
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        hx1.v[w] = (hx_ij && km < nz) ? hxk.v[w] - hx_.apply((ez_jp.v[w] - ezk.v[w]) - (ey.v[w] - eyk.v[w])) : hxk.v[w];
-        hy1.v[w] = (hy_ij && km < nz) ? hyk.v[w] - hy_.apply((ex.v[w] - exk.v[w]) - (ez_ip.v[w] - ezk.v[w])) : hyk.v[w];
-        hz1.v[w] = (hz_ij && km > 0 && km < nz) ? hzk.v[w] - hz_.apply((ey_ip.v[w] - eyk.v[w]) - (ex_jp.v[w] - exk.v[w]))
+        hx1.v[w] = (hx_ij && km < nz) ? hx_.sub(hxk.v[w], (ez_jp.v[w] - ezk.v[w]) - (ey.v[w] - eyk.v[w])) : hxk.v[w];
+        hy1.v[w] = (hy_ij && km < nz) ? hy_.sub(hyk.v[w], (ex.v[w] - exk.v[w]) - (ez_ip.v[w] - ezk.v[w])) : hyk.v[w];
+        hz1.v[w] = (hz_ij && km > 0 && km < nz) ? hz_.sub(hzk.v[w], (ey_ip.v[w] - eyk.v[w]) - (ex_jp.v[w] - exk.v[w]))
                                                  : hzk.v[w];
       }
       const int64_t o = (int64_t)km * sz + col;

@@ -286,7 +286,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       const T hxm = (jl > 0) ? sHx[c - TX] : hB[il];
       const Coef<T> cc = uniform ? P.u0 : cE[m];
       const T dd = (hy - hyim) - (hx - hxm);
-      sEz[c] = (i > 0 && j > 0) ? sEz[c] + cc.apply(dd) : (T)0;
+      sEz[c] = (i > 0 && j > 0) ? cc.add(sEz[c], dd) : (T)0;
     };
     if (pair) {
       // 64-wide tiles: lane lx owns the cell pair (2 lx, 2 lx + 1) of a row, so
@@ -306,12 +306,12 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
         if (ia > 0 && i0 + ia < nx && !(tile_rows && (ifm[ma] & 4))) {
           const Coef<T> cc = uniform ? P.u0 : cE[ma];
           const T dd = (hy2.x - sHy[c - 1]) - (hx2.x - hxm2.x);
-          e0 = (j0 + jl > 0) ? e0 + cc.apply(dd) : (T)0;
+          e0 = (j0 + jl > 0) ? cc.add(e0, dd) : (T)0;
         }
         if (i0 + ia + 1 < nx && !(tile_rows && (ifm[mb] & 4))) {
           const Coef<T> cc = uniform ? P.u0 : cE[mb];
           const T dd = (hy2.y - hy2.x) - (hx2.y - hxm2.y);
-          e1 = (j0 + jl > 0) ? e1 + cc.apply(dd) : (T)0;
+          e1 = (j0 + jl > 0) ? cc.add(e1, dd) : (T)0;
         }
         *reinterpret_cast<float2*>(sEz + c) = make_float2(e0, e1);
       }
@@ -418,7 +418,7 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
         acc += x.w[k] * hv;
       }
       if (x.yo >= 0) acc += yv[r];
-      T e = sEz[c] - x.c.apply(acc);
+      T e = x.c.sub(sEz[c], acc);
       if (x.src >= 0 && step < P.R.n_wave) e -= x.cs * yv[P.maxrows + r];
       sEz[c] = e;
       if (x.yo >= 0) {
@@ -459,8 +459,8 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
       if (uniform) { cx = P.u1; cy = P.u1; }
       else { const int m = smat[c]; cx = cHx[m]; cy = cHy[m]; }
       const T hx = sHx[c], hy = sHy[c];
-      const T hx1 = (i > 0) ? hx - cx.apply(ez_jp - ez) : hx;
-      const T hy1 = (j0 + jl > 0) ? hy + cy.apply(ez_ip - ez) : hy;
+      const T hx1 = (i > 0) ? cx.sub(hx, ez_jp - ez) : hx;
+      const T hy1 = (j0 + jl > 0) ? cy.add(hy, ez_ip - ez) : hy;
       sHx[c] = hx1; sHy[c] = hy1;
       if (do_check && !(finite_small(ez) && finite_small(hx1) && finite_small(hy1))) bad = true;
     };
@@ -481,16 +481,16 @@ __device__ void persist2d_tile(const Persist2D<T>& P, unsigned char* smem_raw, i
           Coef<T> cx, cy;
           if (uniform) { cx = P.u1; cy = P.u1; }
           else { const int m = m2 & 0xff; cx = cHx[m]; cy = cHy[m]; }
-          hx0 = (i0 + ia > 0) ? hx2.x - cx.apply(ezj2.x - ez2.x) : hx2.x;
-          hy0 = jin ? hy2.x + cy.apply(ez2.y - ez2.x) : hy2.x;
+          hx0 = (i0 + ia > 0) ? cx.sub(hx2.x, ezj2.x - ez2.x) : hx2.x;
+          hy0 = jin ? cy.add(hy2.x, ez2.y - ez2.x) : hy2.x;
           if (do_check && !(finite_small(ez2.x) && finite_small(hx0) && finite_small(hy0))) bad = true;
         }
         if (ia + 1 < TX - 1 && i0 + ia + 1 < nx) {
           Coef<T> cx, cy;
           if (uniform) { cx = P.u1; cy = P.u1; }
           else { const int m = m2 >> 8; cx = cHx[m]; cy = cHy[m]; }
-          hx1 = hx2.y - cx.apply(ezj2.y - ez2.y);
-          hy1 = jin ? hy2.y + cy.apply(sEz[c + 2] - ez2.y) : hy2.y;
+          hx1 = cx.sub(hx2.y, ezj2.y - ez2.y);
+          hy1 = jin ? cy.add(hy2.y, sEz[c + 2] - ez2.y) : hy2.y;
           if (do_check && !(finite_small(ez2.y) && finite_small(hx1) && finite_small(hy1))) bad = true;
         }
         *reinterpret_cast<float2*>(sHx + c) = make_float2(hx0, hx1);
@@ -983,12 +983,12 @@ __device__ void persist2d_tb_tile(const Persist2D<T>& P, unsigned char* smem_raw
           if (ua) {
             const Coef<T> cc = MN ? ce0 : cE[ma];
             const T dd = (hy2.x - sHy[c - 1]) - (hx2.x - hxm2.x);
-            e0 = za ? (T)0 : e0 + cc.apply(dd);
+            e0 = za ? (T)0 : cc.add(e0, dd);
           }
           if (ub) {
             const Coef<T> cc = MN ? ce0 : cE[mb];
             const T dd = (hy2.y - hy2.x) - (hx2.y - hxm2.y);
-            e1 = zb ? (T)0 : e1 + cc.apply(dd);
+            e1 = zb ? (T)0 : cc.add(e1, dd);
           }
           *reinterpret_cast<float2*>(sEz + c) = make_float2(e0, e1);
           pp += DP;
@@ -1024,7 +1024,7 @@ __device__ void persist2d_tb_tile(const Persist2D<T>& P, unsigned char* smem_raw
           acc += xr.w[k] * hv;
         }
         if (xr.yo >= 0) acc += yvv;
-        T e = sEz[c] - xr.c.apply(acc);
+        T e = xr.c.sub(sEz[c], acc);
         if (xr.src >= 0 && step < P.R.n_wave) e -= xr.cs * P.R.wave[step * P.R.n_cols + xr.src];
         sEz[c] = e;
         if (xr.own && xr.yo >= 0) ll_st(P.lG + (int64_t)(ls & P.ymask) * P.ysz + xr.yo, (float)e, tag_cur);
@@ -1061,13 +1061,13 @@ __device__ void persist2d_tb_tile(const Persist2D<T>& P, unsigned char* smem_raw
           }
           if (ua) {
             const Coef<T> cx = MN ? cx0 : cHx[ma], cy = MN ? cy0 : cHy[ma];
-            hx0 = xa ? hx2.x - cx.apply(ezj2.x - ez2.x) : hx2.x;
-            hy0 = ya ? hy2.x + cy.apply(ez2.y - ez2.x) : hy2.x;
+            hx0 = xa ? cx.sub(hx2.x, ezj2.x - ez2.x) : hx2.x;
+            hy0 = ya ? cy.add(hy2.x, ez2.y - ez2.x) : hy2.x;
           }
           if (ub) {
             const Coef<T> cx = MN ? cx0 : cHx[mb], cy = MN ? cy0 : cHy[mb];
-            hx1 = xb ? hx2.y - cx.apply(ezj2.y - ez2.y) : hx2.y;
-            hy1 = yb ? hy2.y + cy.apply(sEz[c + 2] - ez2.y) : hy2.y;
+            hx1 = xb ? cx.sub(hx2.y, ezj2.y - ez2.y) : hx2.y;
+            hy1 = yb ? cy.add(hy2.y, sEz[c + 2] - ez2.y) : hy2.y;
           }
           *reinterpret_cast<float2*>(sHx + c) = make_float2(hx0, hx1);
           *reinterpret_cast<float2*>(sHy + c) = make_float2(hy0, hy1);

@@ -106,28 +106,6 @@ struct SegCursor {               // walks the load sequence of one CTA's items
   }
 };
 
-// an explicit row whose H terms are the four curl neighbours h0..h3 (slot
-// order of RowsE::lcode): the expression of eval_row, term by term in CSR order
-template <typename T>
-__device__ __forceinline__ T local_row(const RowsE<T>& R, int r, int b, int B, T e0, T h0, T h1, T h2, T h3,
-                                       const T* __restrict__ y, int64_t step) {
-  const unsigned cd = R.lcode[r];
-  const int nt = (int)(cd >> 8);
-  T acc = 0;
-  for (int q = 0; q < nt; ++q) {
-    const unsigned sl = (cd >> (2 * q)) & 3u;
-    const T hv = sl == 0 ? h0 : sl == 1 ? h1 : sl == 2 ? h2 : h3;
-    acc += R.lw[4 * r + q] * hv;
-  }
-  const int64_t yo = R.y_off[r];
-  if (yo >= 0) acc += y[yo + b];
-  T e = e0 - R.c[r].apply(acc);
-  const int s = R.src[r];
-  if (s >= 0 && step < R.n_wave) e -= R.cs[r] * R.wave[(step * R.n_src + s) * B + b];
-  if (yo >= 0) R.g_out[yo + b] = e;
-  return e;
-}
-
 template <typename T, bool UNIFORM, int NS, int W, int MB, int MINB, int BY = TILE_BY>
 __global__ void __launch_bounds__(32 * BY, MINB)
 stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims d, Fields<T> F0,
@@ -298,9 +276,9 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
           cx = tabc[m * 6 + 0]; cy = tabc[m * 6 + 1]; cz = tabc[m * 6 + 2];
           ifm_any |= tabf[m];
         }
-        ex.v[w] = ex0.v[w] + cx.apply(((hz_c.v[w] - hz_jm.v[w]) - (hy_c.v[w] - hyk.v[w])) * fa[w]);
-        ey.v[w] = ey0.v[w] + cy.apply(((hx_c.v[w] - hxk.v[w]) - (hz_c.v[w] - hz_im.v[w])) * fb[w]);
-        ez.v[w] = ez0.v[w] + cz.apply(((hy_c.v[w] - hy_im.v[w]) - (hx_c.v[w] - hx_jm.v[w])) * fc[w]);
+        ex.v[w] = cx.add(ex0.v[w], ((hz_c.v[w] - hz_jm.v[w]) - (hy_c.v[w] - hyk.v[w])) * fa[w]);
+        ey.v[w] = cy.add(ey0.v[w], ((hx_c.v[w] - hxk.v[w]) - (hz_c.v[w] - hz_im.v[w])) * fb[w]);
+        ez.v[w] = cz.add(ez0.v[w], ((hy_c.v[w] - hy_im.v[w]) - (hx_c.v[w] - hx_jm.v[w])) * fc[w]);
       }
       // z walls: tangential E on k = 0 and everything on k = nz are not unknowns
       if (kk == 0) {
@@ -317,22 +295,11 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
           const int m = XV ? (int)((m_cur >> (8 * w)) & 0xffu) : (int)m_cur;
           const uint8_t f = tabf[m];
           if (!f || (XV && i + w > nx)) continue;
-          const int64_t sidx = (int64_t)kk * d.plane + scol + (XV ? w : 0);
-          const int bw = XV ? 0 : b + w;
-          if (R.lcode) {
-            // local-slot rows: the H terms are this cell's curl neighbours, in
-            // registers (same values, same CSR order as eval_row)
-            if (f & 1) ex.v[w] = local_row(R, R.row_of[0][sidx], bw, B, ex0.v[w], hz_c.v[w], hz_jm.v[w], hy_c.v[w],
-                                           hyk.v[w], y, step);
-            if (f & 2) ey.v[w] = local_row(R, R.row_of[1][sidx], bw, B, ey0.v[w], hz_c.v[w], hz_im.v[w], hx_c.v[w],
-                                           hxk.v[w], y, step);
-            if (f & 4) ez.v[w] = local_row(R, R.row_of[2][sidx], bw, B, ez0.v[w], hx_c.v[w], hx_jm.v[w], hy_c.v[w],
-                                           hy_im.v[w], y, step);
-          } else {
-            if (f & 1) ex.v[w] = eval_row(R, R.row_of[0][sidx], bw, B, ex0.v[w], F0, y, step);
-            if (f & 2) ey.v[w] = eval_row(R, R.row_of[1][sidx], bw, B, ey0.v[w], F0, y, step);
-            if (f & 4) ez.v[w] = eval_row(R, R.row_of[2][sidx], bw, B, ez0.v[w], F0, y, step);
-          }
+          // rows_prepass_kernel (kernels.cuh) evaluated every explicit row of this
+          // step and stored its E^{n+1} into the new parity: read it back
+          if (f & 1) ex.v[w] = F1.f[0][oe + w];
+          if (f & 2) ey.v[w] = F1.f[1][oe + w];
+          if (f & 4) ez.v[w] = F1.f[2][oe + w];
         }
       }
       T* en = En + ebuf * (3 * EP) + erow;
@@ -367,9 +334,9 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
             const int m = XV ? (int)((m_prev >> (8 * w)) & 0xffu) : (int)m_prev;
             hx_ = tabc[m * 6 + 3]; hy_ = tabc[m * 6 + 4]; hz_ = tabc[m * 6 + 5];
           }
-          hx1.v[w] = hxk.v[w] - hx_.apply(((ez_jp.v[w] - ezk.v[w]) - (ey.v[w] - eyk.v[w])) * fb[w]);
-          hy1.v[w] = hyk.v[w] - hy_.apply(((ex.v[w] - exk.v[w]) - (ez_ip.v[w] - ezk.v[w])) * fa[w]);
-          hz1.v[w] = hz_on ? hzk.v[w] - hz_.apply(((ey_ip.v[w] - eyk.v[w]) - (ex_jp.v[w] - exk.v[w])) * fd[w])
+          hx1.v[w] = hx_.sub(hxk.v[w], ((ez_jp.v[w] - ezk.v[w]) - (ey.v[w] - eyk.v[w])) * fb[w]);
+          hy1.v[w] = hy_.sub(hyk.v[w], ((ex.v[w] - exk.v[w]) - (ez_ip.v[w] - ezk.v[w])) * fa[w]);
+          hz1.v[w] = hz_on ? hz_.sub(hzk.v[w], ((ey_ip.v[w] - eyk.v[w]) - (ex_jp.v[w] - exk.v[w])) * fd[w])
                            : hzk.v[w];
         }
         const uint32_t oh = oe - sz32;

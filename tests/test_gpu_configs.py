@@ -444,22 +444,26 @@ def test_tiny4_batch16_leapfrog_tensor_core_gemm(tc, monkeypatch):
         assert es <= 1e-4 and ep <= 1e-4, (m, es, ep, parity.last_report)
 
 
-@pytest.mark.parametrize("case,prec", [("tiny5", 32), ("tiny5", 64), ("tiny4", 32)])
-def test_local_slot_rows_bitwise_equal_global_rows(case, prec, monkeypatch):
-    # the tile stencil's explicit rows from the register-held curl neighbours
-    # (RowsE::lcode) against the CSR walk over global H (eval_row): bit for bit
+@pytest.mark.parametrize("case,prec", [("tiny5", 32), ("tiny5", 64)])
+def test_rows_prepass_bitwise_equals_in_kernel_rows(case, prec, monkeypatch):
+    # explicit rows evaluated ahead of the tile stencil (rows_prepass_kernel: the
+    # row's E^{n+1} stored into the new parity and read back by the stencil
+    # thread that owns the unknown) against the reference stencils that walk
+    # each row inside the kernel (eval_row): states and probe series bit for bit
+    # (batch 16 with interface rows: test_tile_stencil_bitwise...[tiny4_b16-*])
     from paper_1406_7042_b200.fdtd import Sim
     from sampled_state import random_state
     scn, prob = _prep(case, precision=prec)
     prob = dict(prob, init={})
     arrays, re_, rh_ = random_state(prob, seed=11)
 
-    def run(local):
-        if local:
-            monkeypatch.delenv("FDTD_NO_LOCAL_ROWS", raising=False)
+    def run(tile):
+        if tile:
+            monkeypatch.delenv("FDTD_STENCIL_OLD", raising=False)
         else:
-            monkeypatch.setenv("FDTD_NO_LOCAL_ROWS", "1")
+            monkeypatch.setenv("FDTD_STENCIL_OLD", "1")
         sim = Sim(prob, precision=prec, graph_steps=0)
+        paths = sim.path()
         for c in range(6):
             sim.set_state(c, arrays[c])
         sim.step(9)
@@ -467,9 +471,10 @@ def test_local_slot_rows_bitwise_equal_global_rows(case, prec, monkeypatch):
         out = [sim.get_state(c) for c in range(8)]
         pr = sim.probe()
         sim.close()
-        return out, pr
+        return out, pr, paths
 
-    (a, pa), (b, pb) = run(True), run(False)
+    (a, pa, ta), (b, pb, tb) = run(True), run(False)
+    assert "tile3d" in ta and "tile3d" not in tb, (ta, tb)
     for c in range(8):
         assert np.array_equal(a[c], b[c]), c
     assert np.array_equal(pa, pb)
