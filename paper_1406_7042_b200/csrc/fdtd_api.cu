@@ -43,6 +43,13 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
+}  // namespace
+namespace fdtd {
+// the thread-local message of fdtd_last_error(), for the other translation units (rom.cu)
+int set_error(int code, const char* msg) { return fail(code, "%s", msg); }
+}  // namespace fdtd
+namespace {
+
 #define CK(call)                                                                   \
   do {                                                                             \
     cudaError_t e_ = (call);                                                       \

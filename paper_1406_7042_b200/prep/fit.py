@@ -210,7 +210,7 @@ def _interp_targets(dim, comp, pos_num, r, lo):
     return terms
 
 
-def assemble(dim, n, delta, eps_r, boxes, eps0, mu0, pec_extra=None):
+def assemble(dim, n, delta, eps_r, boxes, eps0, mu0, pec_extra=None, need_K=None):
     """Hybrid of reading R4.  eps_r: relative permittivity per coarse cell;
     boxes: list of dict(lo, hi, r).  pec_extra(grid, comp, shape) -> bool mask
     adds interior PEC unknowns (grid = -1 coarse, b for box b)."""
@@ -236,7 +236,7 @@ def assemble(dim, n, delta, eps_r, boxes, eps0, mu0, pec_extra=None):
         for c in pec:
             pec[c] = pec[c] | pec_extra(-1, c, shp)
     hz = delta if dim == 3 else 1.0
-    coarse = build_fit(dim, n, (delta, delta, hz), dom, eps, mu, pec, need_K=bool(boxes))
+    coarse = build_fit(dim, n, (delta, delta, hz), dom, eps, mu, pec, need_K=bool(boxes) if need_K is None else need_K)
     ecomps, hcomps = comps_of(dim)
     De_c = {c: coarse.D[c] / scale for c in ecomps}
     Dm_c = {c: coarse.D[c] / scale for c in hcomps}

@@ -289,6 +289,43 @@ def microstrip3d(name, config_id, nx, ny, nz, delta, n_stub_side, line_x, line_w
 # registry
 # ---------------------------------------------------------------------------
 
+# ---------------------------------------------------------------------------
+# whole-domain reduced model of a 2-D PEC cavity, batched over excitation
+# waveforms (stands in for the cavity of P:399-440, Table I)
+# ---------------------------------------------------------------------------
+
+def rom_cavity2d(name, config_id, nx, ny, delta, s_factor, q, batch, n_probes=4, fmax=0.5e9,
+                 n_steps=None, seed=None):
+    """Vacuum PEC cavity of nx x ny cells, one Ez point source, ``n_probes`` Ez
+    probes (seeded nodes).  dt = s_factor x the Eq. (1) limit (the CFL
+    extension factor s of P:312-315); the step count covers the physical time
+    of the paper's 10,000 steps at s = 0.99 (reading A-15).  The batch members
+    differ in their time signature: member 0 is the paper's Gaussian pulse
+    (-20 dB at fmax), the others are modulated Gaussians with seeded centre
+    frequencies in (0.1, 0.8) fmax, bandwidths and amplitudes."""
+    rng = np.random.default_rng(SEED0 + config_id if seed is None else seed)
+    src = _pick_nodes(rng, nx, ny, [], 1, margin=0)
+    prb = _pick_nodes(rng, nx, ny, [], n_probes, margin=0, exclude=src)
+    dt = s_factor * cfl_coarse(2, delta)
+    if n_steps is None:
+        n_steps = int(math.ceil(10000 * 0.99 / s_factor))
+    t = _times(dt, n_steps)
+    wave = np.zeros((n_steps, batch))
+    wave[:, 0] = _gauss(t, gaussian_tau(fmax))
+    for b in range(1, batch):
+        fc = float(rng.uniform(0.1, 0.8)) * fmax
+        tau = gaussian_tau(float(rng.uniform(0.15, 0.4)) * fmax)
+        wave[:, b] = _mod_gauss(t, fc, tau)
+    amp = rng.uniform(0.5, 1.5, size=(1, batch))
+    amp[0, 0] = 1.0
+    return dict(name=name, config_id=config_id, dim=2, n=(nx, ny, 1), delta=delta, eps0=EPS0, mu0=MU0, c0=C0,
+                eps_r=np.ones((ny, nx)), boxes=[], pec_sheets=[], dt=dt, dt_factor=s_factor, s_factor=s_factor,
+                n_steps=n_steps, precision=64, batch=batch, q=q,
+                sources=dict(comp=np.array([2]), idx=np.array([[src[0][0], src[0][1], 0]])),
+                amp=amp, wave=wave, probes=[dict(terms=[(2, (i, j, 0), 1.0)]) for (i, j) in prb], init=None,
+                basis=dict(recipe="A", L=2, M=1.1, fmax=fmax))
+
+
 def scenario(which, precision=None, n_steps=None, **kw):
     """Return the scenario dict for a BASELINE config id (1-5) or a named test
     variant.  ``precision`` / ``n_steps`` override the config's defaults."""
@@ -336,6 +373,14 @@ def scenario(which, precision=None, n_steps=None, **kw):
         # config-5 structure (PEC strips through z-refined regions, two models)
         s = microstrip3d("micro5", 107, 14, 12, 4, 0.25e-3, 1, (2, 12), 2, 2, 3.38, 2, (2, 2),
                          4, (1, 3), 4, 8, 0.6, 100, precision or 64, spacing=4)
+    elif which == "rom2d":
+        # the paper's 2-D cavity (Table I: 101 cells of 1 cm, order 80, 5 points,
+        # M = 1.1, f_max = 0.5 GHz) at s = 4.95, 64 excitation waveforms
+        s = rom_cavity2d("rom2d", 201, 101, 101, 0.01, kw.pop("s_factor", 4.95), kw.pop("q", 80),
+                         kw.pop("batch", 64))
+    elif which == "rom2d_small":
+        s = rom_cavity2d("rom2d_small", 202, 24, 18, 0.01, kw.pop("s_factor", 2.5), kw.pop("q", 20),
+                         kw.pop("batch", 11), n_probes=3, fmax=4e9, n_steps=400)
     elif which == "config3_small":
         s = cavity3d_random("config3_small", 3, 64, 48, 40, 1e-3, 0.99, 200, precision or 32)
     else:
@@ -345,11 +390,12 @@ def scenario(which, precision=None, n_steps=None, **kw):
         s["precision"] = precision
     if n_steps is not None and n_steps != s["n_steps"]:
         s["n_steps"] = n_steps
-        w = s["sources"]["wave"]
+        holder = s["sources"] if "wave" in s["sources"] else s     # reduced-model scenarios keep wave at top level
+        w = holder["wave"]
         if w.shape[0] >= n_steps:
-            s["sources"]["wave"] = w[:n_steps]
+            holder["wave"] = w[:n_steps]
         else:       # beyond the generated record the source is zero (ABI semantics)
             pad = np.zeros((n_steps - w.shape[0],) + w.shape[1:])
-            s["sources"]["wave"] = np.concatenate([w, pad], axis=0)
+            holder["wave"] = np.concatenate([w, pad], axis=0)
     s.update(kw)
     return s

@@ -64,3 +64,34 @@ def test_null_handle_calls():
     assert lib.fdtd_step(None, 1) == 1
     assert lib.fdtd_sync(None) == 1
     assert lib.fdtd_launch_count(None) == 0
+
+
+def test_rom_header_symbols_exported_and_arguments_checked():
+    # include/fdtd_rom.h: every declared symbol is exported; rom_create validates
+    # its arguments before touching the device; no CPU fallback
+    fdtd, lib = _lib()
+    from paper_1406_7042_b200 import rom
+    rom._lib()
+    hdr = open(os.path.join(ROOT, "include", "fdtd_rom.h")).read()
+    declared = set(re.findall(r"\b(rom_[a-z_]+)\s*\(", hdr))
+    assert declared == set(rom.ROM_SYMBOLS)
+    for name in declared:
+        assert hasattr(lib, name)
+    K = np.eye(4)
+    g = np.ones(4)
+    f64 = C.POINTER(C.c_double)
+    p = lambda a: a.ctypes.data_as(f64)
+    h = C.c_void_p()
+    x = rom.RomExcitation(1, None, 0, None)
+    for q_e, batch, code in ((0, 1, 1), (300, 1, 1), (4, 0, 1)):
+        m = rom.RomModel(q_e, 4, 0, 0, 0, p(K), p(g), p(g), None, None, None)
+        x.batch = batch
+        assert lib.rom_create(C.byref(m), C.byref(x), None, 0, C.byref(h)) == code
+        assert lib.fdtd_last_error().decode() and not h.value
+    m = rom.RomModel(4, 4, 0, 0, 0, p(K), p(g), p(g), None, None, None)
+    x.batch = 1
+    assert lib.rom_create(C.byref(m), C.byref(x), None, 7, C.byref(h)) == 1     # cols_per_cluster
+    assert lib.rom_step(None, 1) == 1 and lib.rom_sync(None) == 1
+    import torch
+    if not torch.cuda.is_available():
+        assert lib.rom_create(C.byref(m), C.byref(x), None, 0, C.byref(h)) in (4, 5)
