@@ -442,6 +442,75 @@ METRIC_CONFIGS = {"config2_fp32": (2, 32), "config3_fp32": (3, 32), "config3_fp6
                   "config5_fp32": (5, 32)}
 
 
+def measure_rom(args, batch, steps=5, warmup=3, cpu=True, dmma_peak=None):
+    """the paper's 2-D cavity reduced to order 80 (Table I),
+    stepped for the physical time of its 10,000 steps at s = 4.95, batched over
+    ``batch`` excitation waveforms (rom_* calls, csrc/rom.cu).  Reported beside the
+    hybrid configurations: column-steps/s, GFLOP/s of the two dense products
+    against the measured fp64 tensor-core peak, the oracle timed on the host."""
+    import torch
+    from paper_1406_7042_b200 import rom as R
+    from paper_1406_7042_b200.prep import rom as prom
+    from synth import scenario
+    scn = scenario("rom2d", batch=batch)
+    t0 = time.time()
+    model, info = prom.build_rom(scn)
+    t_prep = time.time() - t0
+    n = int(scn["n_steps"])
+    q = int(model["q_e"])
+    sim = R.Rom(model, model["amp"], model["wave"])
+    geo = sim.info()
+    for _ in range(max(3, warmup)):
+        sim.step(n); sim.probe()
+    ms = []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); sim.step(n); e1.record(); torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        sim.probe()
+    t = sum(ms) / len(ms)
+    colsteps = batch * n / (t * 1e-3)
+    gflops = 4.0 * q * q * batch * n / (t * 1e-3) / 1e9
+    peak = dmma_peak if dmma_peak is not None else R.dmma_peak_tflops()
+    # end to end: create (uploads K~', B~, the waveforms), all steps, the probe series back on the host
+    te = []
+    for _ in range(2):
+        torch.cuda.synchronize(); w0 = time.perf_counter()
+        s2 = R.Rom(model, model["amp"], model["wave"]); s2.step(n); pr = s2.probe(); s2.close()
+        te.append(time.perf_counter() - w0)
+    e2e_t = min(te)
+    out = {"value": colsteps, "unit": "reduced-model column-steps/s", "ms_per_step": t, "steps": steps, "dtype": "f64",
+           "config": {"workload": (f"rom2d: whole-domain reduced model of the 2-D PEC cavity of Table I (101 x 101 cells of "
+                                   f"1 cm, N = {info['Ne'] + info['Nh']}), order q = {q}, 5 expansion points, s = "
+                                   f"{scn['s_factor']} ({info['clipped']} singular values clipped), {batch} excitation "
+                                   f"waveforms, {n} time steps per bench step"),
+                      "time_steps_per_step": n, "batch": batch, "q": [q], "launch": geo, "prep_s": round(t_prep, 1),
+                      "l2": "state and K~' resident on chip for the whole launch (no HBM traffic in steady state)"},
+           "roofline": {"bound": "tensor", "achieved": gflops / 1e3, "peak": peak, "unit": "TFLOP/s",
+                        "frac": gflops / 1e3 / peak if peak and peak > 0 else None, "traffic": None,
+                        "kernel": "rom_persist_kernel (mma.sync m8n8k4 f64, K~' in registers)",
+                        "algorithmic_flops_per_launch": 4.0 * q * q * batch * n,
+                        "peak_kind": "measured here: register-only mma.sync m8n8k4 f64 loop on every SM "
+                                     "(rom_dmma_peak_tflops; fp64 is not in MEASURED_PEAKS.json)"},
+           "us_per_time_step": t * 1e3 / n,
+           "e2e": {"value": batch * n / e2e_t, "unit": "reduced-model column-steps/s",
+                   "h2d_bytes_per_step": int(8 * (model["wave"].size + model["amp"].size + 3 * q * q)),
+                   "d2h_bytes_per_step": int(pr.size * 8), "ms_per_step": e2e_t * 1e3,
+                   "note": "rom_create (uploads), rom_step, rom_probe (fp64 series to the host) per bench step"},
+           "gpu_launches": steps}
+    sim.close()
+    if cpu:
+        from oracle import rom as orom
+        nb = min(batch, 64)
+        w0 = time.perf_counter()
+        orom.run(model, model["amp"][:, :nb], model["wave"][:, :nb], n)
+        el = time.perf_counter() - w0
+        out["cpu_baseline"] = {"value": nb * n / el, "unit": "reduced-model column-steps/s", "cores": 1, "kind": "oracle",
+                               "sample": f"oracle.rom.run: {n} steps x {nb} columns of the same model in {el:.1f} s "
+                                         f"(NumPy/LAPACK Cholesky solves and matmuls)", **cpu_info()}
+    return out
+
+
 def oracle_sample_worker(config, prec, seconds):
     """CPU-oracle timing of one workload in its own process (single-threaded
     SciPy), run beside the GPU measurements so the bench stays within minutes.
@@ -495,6 +564,14 @@ def bench_ours(args):
                                     rank, world, local)
             except Exception as ex:       # report, never hide: the headline line still prints
                 per[name] = {"error": f"{type(ex).__name__}: {ex}"}
+    if args.per_config and world == 1 and rank == 0:
+        try:
+            from paper_1406_7042_b200 import rom as R
+            pk = R.dmma_peak_tflops()
+            per["rom2d_fp64_b64"] = measure_rom(args, 64, cpu=not args.no_cpu, dmma_peak=pk)
+            per["rom2d_fp64_b9472"] = measure_rom(args, 9472, cpu=False, dmma_peak=pk)
+        except Exception as ex:
+            per["rom2d_fp64_b64"] = {"error": f"{type(ex).__name__}: {ex}"}
     if futs:
         for c, f in futs.items():
             try:
@@ -504,7 +581,7 @@ def bench_ours(args):
             if c == args.config:
                 head["cpu_baseline"] = res
             for name, v in per.items():
-                if isinstance(v, dict) and METRIC_CONFIGS[name][0] == c:
+                if isinstance(v, dict) and name in METRIC_CONFIGS and METRIC_CONFIGS[name][0] == c:
                     v["cpu_baseline"] = res
         pool.shutdown()
     if rank == 0:
@@ -544,11 +621,18 @@ def main(argv=None):
                     help="only the headline configuration (default: also configs 2, 3 fp32/fp64, 5)")
     ap.add_argument("--per-config-steps", type=int, default=3)
     ap.add_argument("--per-config-warmup", type=int, default=3)
+    ap.add_argument("--rom-only", action="store_true", help="only the NEXT-3 reduced-model lines (development)")
     args = ap.parse_args(argv)
     if args.precision is None:
         args.precision = 32 if args.config in (2, 3, 4, 5) else 64
     if args.impl == "reference":
         return bench_reference(args)
+    if args.rom_only:
+        from paper_1406_7042_b200 import build as B
+        B.build()
+        for b in (64, 1184, 9472):
+            print(json.dumps({f"rom2d_fp64_b{b}": measure_rom(args, b, cpu=(b == 64))}), flush=True)
+        return 0
     return bench_ours(args)
 
 
