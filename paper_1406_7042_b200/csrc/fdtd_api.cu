@@ -242,6 +242,8 @@ struct Impl : public fdtd_t {
   bool split = false;
   int n_ifc = 0;                       // interface columns (first in colperm)
   int* colperm_d = nullptr;
+  fdtd::RowPackI* rowpack_i = nullptr;      // packed explicit rows (rows_prepass_packed_kernel), null: generic
+  void* rowpack_r = nullptr;
   std::vector<std::pair<int, int>> split_rows;     // (i, j) of the explicit rows that read y
   cudaStream_t st2 = nullptr;
   cudaEvent_t evA = nullptr, evR = nullptr;
@@ -858,6 +860,37 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     rows.e_comp = d_ec; rows.e_off = d_eo; rows.c = d_c; rows.rowptr = d_rp; rows.h_comp = d_hc;
     rows.h_off = d_ho; rows.w = d_w; rows.y_off = d_yo; rows.src = d_src; rows.cs = d_cs; rows.wave = d_wave;
     rows.g_out = g_all;
+    // packed records for the pre-pass of the 3-D tile stencil (<= 4 terms per row,
+    // 32-bit offsets)
+    if (dim == 3 && nr > 0 && !getenv("FDTD_NO_ROWPACK")) {
+      bool ok = true;
+      std::vector<fdtd::RowPackI> pi((size_t)nr);
+      std::vector<fdtd::RowPackR<T>> pr((size_t)nr);
+      for (int64_t r = 0; r < nr && ok; ++r) {
+        const HRow& h = hrows[r];
+        fdtd::RowPackI& a = pi[r];
+        fdtd::RowPackR<T>& q = pr[r];
+        memset(&a, 0, sizeof(a));
+        memset(&q, 0, sizeof(q));
+        if (h.w.size() > 4 || yo[r] >= ((int64_t)1 << 31) || eo[r] >= ((int64_t)1 << 31)) { ok = false; break; }
+        a.e_comp = ec[r]; a.e_off = (int32_t)eo[r]; a.nterm = (int32_t)h.w.size(); a.src = srcv[r];
+        a.y_off = (int32_t)yo[r];
+        for (size_t k = 0; k < h.w.size(); ++k) {
+          const int64_t off = ho[rp[r] + k];
+          if (off >= ((int64_t)1 << 31)) { ok = false; break; }
+          a.h_off[k] = (int32_t)off;
+          a.h_comp |= (hc[rp[r] + k] & 0xff) << (8 * k);
+          q.w[k] = w[rp[r] + k];
+        }
+        q.c = cc[r]; q.cs = cs[r];
+      }
+      if (ok) {
+        rowpack_i = dalloc<fdtd::RowPackI>(nr);
+        fdtd::RowPackR<T>* prd = dalloc<fdtd::RowPackR<T>>(nr);
+        if (!rowpack_i || !prd || upload(rowpack_i, pi) || upload(prd, pr)) return FDTD_ECUDA;
+        rowpack_r = prd;
+      }
+    }
     for (int c = 0; c < 3; ++c) rows.row_of[c] = nullptr;
     for (int c = 0; c < 3; ++c) {
       bool any = false;
@@ -1682,7 +1715,12 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   if (dim == 3 && use_tile && rows.n_rows > 0) {
     // explicit rows first: the tile stencil reads their E^{n+1} back from the new parity
     const int64_t nt = rows.n_rows * B;
-    fdtd::rows_prepass_kernel<T><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, B, F0, F1, y_all, ds);
+    if (rowpack_i)
+      fdtd::rows_prepass_packed_kernel<T><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(
+          rows.n_rows, rowpack_i, (const fdtd::RowPackR<T>*)rowpack_r, B, F0, F1, y_all, rows.g_out, rows.wave,
+          rows.n_wave, rows.n_src, ds);
+    else
+      fdtd::rows_prepass_kernel<T><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, B, F0, F1, y_all, ds);
     ++n;
   }
   if (dim == 3 && use_tile && sp) {

@@ -124,6 +124,64 @@ rows_prepass_kernel(RowsE<T> R, int B, Fields<T> F0, Fields<T> F1, const T* __re
   F1.f[c][o] = eval_row(R, r, b, B, F0.f[c][o], F0, y, *d_step);
 }
 
+// The same pre-pass on packed row records (every row has at most 4 H terms --
+// all interface rows of the R4 construction and all source rows): one level of
+// row-indexed loads (3 x 16 bytes of integers, the reals), then the field / y /
+// waveform loads, instead of eval_row's chain of dependent CSR loads.  The
+// arithmetic is eval_row's, term by term in CSR order.
+struct RowPackI {          // 48 bytes
+  int32_t e_comp, e_off, nterm, src;
+  int32_t h_off[4];
+  int32_t h_comp;          // 4 x 8 bits
+  int32_t y_off;           // -1: none
+  int32_t pad[2];
+};
+template <typename T>
+struct RowPackR {          // 32 (fp32) / 64 (fp64) bytes
+  T w[4];
+  Coef<T> c;
+  T cs;
+  T pad;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+rows_prepass_packed_kernel(int64_t n_rows, const RowPackI* __restrict__ RI, const RowPackR<T>* __restrict__ RR,
+                           int B, Fields<T> F0, Fields<T> F1, const T* __restrict__ y, T* __restrict__ g_out,
+                           const T* __restrict__ wave, int64_t n_wave, int64_t n_src,
+                           const int64_t* __restrict__ d_step) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_rows * B) return;
+  const int r = (int)(t / B), b = (int)(t % B);
+  const int4* pi = reinterpret_cast<const int4*>(RI + r);
+  const int4 i0 = pi[0], i1 = pi[1], i2 = pi[2];
+  const RowPackR<T> rr = RR[r];
+  auto field = [&](int c) -> const T* {
+    return c == 0 ? F0.f[0] : c == 1 ? F0.f[1] : c == 2 ? F0.f[2] : c == 3 ? F0.f[3] : c == 4 ? F0.f[4] : F0.f[5];
+  };
+  const int ec = i0.x, nt = i0.z, src = i0.w, yo = i2.y;
+  const int64_t eo = (int64_t)i0.y * B + b;
+  const int ho[4] = {i1.x, i1.y, i1.z, i1.w};
+  const T e0 = field(ec)[eo];
+  T h[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) h[k] = k < nt ? field((i2.x >> (8 * k)) & 0xff)[(int64_t)ho[k] * B + b] : (T)0;
+  const T yv = yo >= 0 ? y[yo + b] : (T)0;
+  const int64_t step = *d_step;
+  const bool has_src = src >= 0 && step < n_wave;
+  const T wv = has_src ? wave[(step * n_src + src) * B + b] : (T)0;
+  T acc = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (k < nt) acc += rr.w[k] * h[k];
+  if (yo >= 0) acc += yv;
+  T e = rr.c.sub(e0, acc);
+  if (has_src) e -= rr.cs * wv;
+  if (yo >= 0) g_out[yo + b] = e;
+  T* o = ec == 0 ? F1.f[0] : ec == 1 ? F1.f[1] : F1.f[2];
+  o[eo] = e;
+}
+
 // ---------------------------------------------------------------------------
 // 2-D (Ez, Hx, Hy) fused E->H stencil.  Block (BX, BY) threads; each thread owns
 // CY consecutive rows of one column (all its loads are issued before any
