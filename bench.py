@@ -40,6 +40,8 @@ WORKLOADS = {
     4: "config4: 3-D PEC rectangular waveguide 512x128x128 cells of 0.5 mm, 2-cell iris slab refined 10x in x "
        "-> one reduced block q=1024 (65,024 interface rows), B=16 modulated-Gaussian TE10 port excitations, "
        "dt = 8x fine CFL, 10000 steps, fp32",
+    "lossy256": "lossy256 (SURVEY NEXT-2): config 3's 256^3 grid with 5-cell 4th-order matched absorbers on the x and y "
+                "ends and a lossy dielectric slab (eps_r 2.5, 0.02 S/m), Ez point source, dt = 0.95 CFL, 1000 steps, fp32",
 }
 
 
@@ -439,7 +441,7 @@ def measure(config, prec, steps, warmup, args, rank=0, world=1, local=0, headlin
 
 
 METRIC_CONFIGS = {"config2_fp32": (2, 32), "config3_fp32": (3, 32), "config3_fp64": (3, 64),
-                  "config5_fp32": (5, 32)}
+                  "config5_fp32": (5, 32), "lossy256_fp32": ("lossy256", 32)}
 
 
 def measure_rom(args, batch, steps=5, warmup=3, cpu=True, dmma_peak=None):

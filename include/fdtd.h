@@ -84,6 +84,15 @@ typedef struct fdtd_materials {
   const double* coef;       /* [n_mat][6] cb_x cb_y cb_z ch_x ch_y ch_z                */
   const uint8_t* if_mask;   /* [n_mat]                                                  */
   double uniform_coef[6];
+  /* Lossy media (sigma_e, sigma_m > 0; Eq. (2a)/(2b) P:64-74 with the
+   * conductivity terms of D_sigma, Eq. (5)): E <- ca E - cb (K_inc H),
+   * H <- da H + ch (K_inc^T E) with ca = (eps/dt - sigma_e/2)/(eps/dt + sigma_e/2),
+   * cb = 1/((eps/dt + sigma_e/2) delta), da / ch likewise with mu, sigma_m.
+   * coef_a[m][c] = ca (E components) / da (H components); NULL = lossless (all 1).
+   * Matched absorbers are graded sigma layers expressed this way.
+   * Lossy problems run the 3-D tile stencil or the per-step 2-D kernel; reduced
+   * blocks and interface rows stay lossless. */
+  const double* coef_a;     /* [n_mat][6] or NULL                                       */
 } fdtd_materials;
 
 /* Interface rows: coarse E unknowns on the surface of a refined box

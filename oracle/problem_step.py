@@ -54,6 +54,8 @@ class HybridRecursion:
     wave: np.ndarray         # [n_wave][n_cols][B]
     probe_rows: list         # per probe: (side, sparse row vector over that side)
     src_col: np.ndarray = None   # waveform column of each source
+    CE: np.ndarray = None        # lossy media: ca per E row (1 on interface / reduced rows), None: lossless
+    CH: np.ndarray = None
 
 
 def build(problem) -> HybridRecursion:
@@ -281,8 +283,21 @@ def build(problem) -> HybridRecursion:
                 vrow = np.asarray(p["vrow"], np.float64)[:qh]
                 o = Nh_c + red_off[bl][1] + inst * qh
                 probe_rows.append(("H", {o + i: vrow[i] for i in range(qh) if vrow[i] != 0}))
+    # lossy media: the diagonal of (R+F)^{-1}(R-F) restricted to
+    # the conductivity terms, ca = (eps/dt - sigma/2)/(eps/dt + sigma/2) per E
+    # unknown (da likewise), enters as shared data like cb / ch (F13): Eq. (4)
+    # with D_sigma reads E' = ca E - cb (K_inc H), H' = da H + ch (K_inc^T E')
+    # (pinned against the literal solve of (4), tests/test_oracle_lossy.py)
+    CE = CH = None
+    if problem.get("mat_ca") is not None:
+        mid = np.asarray(problem["mat_id"]).reshape(-1)
+        mca = np.asarray(problem["mat_ca"], np.float64)
+        CE = np.ones(KE.shape[0])
+        CH = np.ones(KH.shape[0])
+        CE[:n_reg] = mca[mid[ids_reg % S], ids_reg // S]
+        CH[:Nh_c] = mca[mid[h_ids % S], h_ids // S]
     return HybridRecursion(dim, n, S, e_ids, h_ids, n_red, red_off, KE, KH, GE, GH,
-                           src_row, src_coef, wave, probe_rows, src_col)
+                           src_row, src_coef, wave, probe_rows, src_col, CE, CH)
 
 
 def initial_state(rec: HybridRecursion, problem, member=0):
@@ -330,7 +345,11 @@ def run(problem, n_steps, member=0, state=None, start_step=0, rec=None):
             su = np.zeros(len(E))
             # E += -coef * J^{n+1/2}   (B holds the sign)
             np.add.at(su, rec.src_row, -rec.src_coef * rec.wave[step, rec.src_col, member])
-        E, H = step_leapfrog(E, H, rec.GE, rec.GH, rec.KE, rec.KH, su_E=su)
+        if rec.CE is None:
+            E, H = step_leapfrog(E, H, rec.GE, rec.GH, rec.KE, rec.KH, su_E=su)
+        else:
+            E = rec.CE * E - rec.GE * (rec.KE @ H) + (0.0 if su is None else su)
+            H = rec.CH * H + rec.GH * (rec.KH @ E)
         probes[s] = PE @ E + PH @ H
     return E, H, probes, rec
 
@@ -360,8 +379,8 @@ def sampled_step(problem, arrays, samples, member=0):
     dim = int(problem["dim"])
     n = tuple(int(v) for v in problem["n"]) + ((1,) if len(problem["n"]) == 2 else ())
     shp = yee.storage_shape(dim, n)
-    if problem.get("interface") or problem.get("sources"):
-        raise ValueError("sampled_step covers the pure coarse recursion only")
+    if problem.get("interface") or problem.get("sources") or problem.get("mat_ca") is not None:
+        raise ValueError("sampled_step covers the pure lossless coarse recursion only")
     curl_h = yee._CURL_H_3D if dim == 3 else yee._CURL_H_2D
     mcurl_e = yee._MCURL_E_3D if dim == 3 else yee._MCURL_E_2D
     ecomps = (0, 1, 2) if dim == 3 else (2,)

@@ -160,6 +160,8 @@ struct Impl : public fdtd_t {
   uint8_t* mat_id = nullptr;
   fdtd::Coef<T>* tab = nullptr;
   uint8_t* ifm = nullptr;
+  T* tab_a = nullptr;                 // [n_mat][6] ca / da of lossy media (fdtd.h coef_a), null: lossless
+  bool lossy = false;
   fdtd::Coef<T> u0{}, u1{};
   // explicit rows
   fdtd::RowsE<T> rows{};
@@ -560,6 +562,15 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     if (uc) for (int c = 0; c < 6; ++c) coef[c] = uc[c];
     ifmask.assign(1, 0);
   }
+  // lossy media: ca / da per material (fdtd.h coef_a); coefa stays in step with coef
+  std::vector<double> coefa((size_t)n_mat * 6, 1.0);
+  if (mat && mat->n_mat > 0 && mat->coef_a) {
+    coefa.assign(mat->coef_a, mat->coef_a + 6 * (size_t)n_mat);
+    for (double v : coefa) {
+      if (!(v > -1.0 && v <= 1.0)) return fail(FDTD_EINVAL, "materials: coef_a must lie in (-1, 1]");
+      lossy |= (v != 1.0);
+    }
+  }
   auto ensure_table = [&]() {
     if (uniform) { uniform = false; ids.assign(S, 0); }
   };
@@ -689,7 +700,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   CK(cudaMemsetAsync(g_all, 0, sizeof(T) * std::max<int64_t>(y_size, 1), stream));
 
   // ---- explicit rows: interface rows, then source rows on regular unknowns ----
-  struct HRow { std::vector<std::pair<int64_t, double>> w; double c = 0; int64_t y = -1; int src = -1; double cs = 0; int comp = 0; int64_t s = 0; };
+  struct HRow { std::vector<std::pair<int64_t, double>> w; double c = 0; int64_t y = -1; int src = -1; double cs = 0; int comp = 0; int64_t s = 0; double a = 1.0; };
   std::vector<HRow> hrows;
   std::map<int64_t, int> row_of;      // E unknown id -> explicit row
   std::vector<int32_t> gcomp, gblk; std::vector<int64_t> goff, gdst;
@@ -776,6 +787,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       if (cb == 0.0 || wall) return fail(FDTD_ESTAMP, "source %lld sits on an inert (PEC / hole) unknown", (long long)s_);
       HRow h;
       h.comp = c; h.s = s; h.c = cb; h.src = (int)s_; h.cs = src->coef[s_];
+      h.a = coefa[(size_t)(uniform ? 0 : ids[s]) * 6 + c];
       // K_inc row (= -curl_H) of the regular stencil, fdtd.h conventions
       const int64_t Hx = 3 * S, Hy = 4 * S, Hz = 5 * S;
       if (c == 0) {
@@ -790,14 +802,18 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
       ensure_table();
       const int old = ids[s];
       std::vector<double> nc(coef.begin() + old * 6, coef.begin() + old * 6 + 6);
+      if (coefa.size() < ifmask.size() * 6) coefa.resize(ifmask.size() * 6, 1.0);      // ensure_table may have added class 0
+      std::vector<double> na(coefa.begin() + old * 6, coefa.begin() + old * 6 + 6);
       const uint8_t nm = (uint8_t)(ifmask[old] | (1u << c));
       int found = -1;
       for (int m = 0; m < (int)ifmask.size(); ++m)
-        if (ifmask[m] == nm && std::equal(nc.begin(), nc.end(), coef.begin() + m * 6)) { found = m; break; }
+        if (ifmask[m] == nm && std::equal(nc.begin(), nc.end(), coef.begin() + m * 6) &&
+            std::equal(na.begin(), na.end(), coefa.begin() + m * 6)) { found = m; break; }
       if (found < 0) {
         if ((int)ifmask.size() >= 256) return fail(FDTD_ENOTSUP, "more than 256 material classes after marking source rows");
         found = (int)ifmask.size();
         coef.insert(coef.end(), nc.begin(), nc.end());
+        coefa.insert(coefa.end(), na.begin(), na.end());
         ifmask.push_back(nm);
       }
       ids[s] = (uint8_t)found;
@@ -815,7 +831,14 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     ifm = dalloc<uint8_t>(n_mat);
     if (!mat_id || !tab || !ifm) return fail(FDTD_ENOMEM, "material allocation failed");
     if (upload(mat_id, padded) || upload(tab, tb) || upload(ifm, ifmask)) return FDTD_ECUDA;
+    if (lossy) {
+      coefa.resize((size_t)n_mat * 6, 1.0);
+      std::vector<T> ta(coefa.begin(), coefa.end());
+      tab_a = dalloc<T>(ta.size());
+      if (!tab_a || upload(tab_a, ta)) return fail(FDTD_ENOMEM, "material allocation failed");
+    }
   } else {
+    if (lossy) return fail(FDTD_EINVAL, "lossy media need a material table");
     u0 = make_coef<T>(coef[dim == 3 ? 0 : 2]);
     u1 = make_coef<T>(coef[3]);
     for (int c = 1; c < 3; ++c)
@@ -832,11 +855,11 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     std::vector<int32_t> ec(nr), hc, srcv(nr);
     std::vector<int64_t> eo(nr), rp(nr + 1, 0), ho, yo(nr);
     std::vector<fdtd::Coef<T>> cc(nr);
-    std::vector<T> w, cs(nr);
+    std::vector<T> w, cs(nr), ra(nr);
     for (int64_t r = 0; r < nr; ++r) {
       const HRow& h = hrows[r];
       ec[r] = h.comp; eo[r] = dev_off(h.s); cc[r] = make_coef<T>(h.c);
-      yo[r] = h.y; srcv[r] = h.src >= 0 ? wcol[h.src] : -1; cs[r] = (T)h.cs;
+      yo[r] = h.y; srcv[r] = h.src >= 0 ? wcol[h.src] : -1; cs[r] = (T)h.cs; ra[r] = (T)h.a;
       for (auto& pw : h.w) {
         hc.push_back((int)(pw.first / S)); ho.push_back(dev_off(pw.first % S)); w.push_back((T)pw.second);
       }
@@ -860,6 +883,12 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     rows.e_comp = d_ec; rows.e_off = d_eo; rows.c = d_c; rows.rowptr = d_rp; rows.h_comp = d_hc;
     rows.h_off = d_ho; rows.w = d_w; rows.y_off = d_yo; rows.src = d_src; rows.cs = d_cs; rows.wave = d_wave;
     rows.g_out = g_all;
+    rows.a = nullptr;
+    if (lossy) {
+      T* d_ra = dalloc<T>(std::max<int64_t>(nr, 1));
+      if (!d_ra || upload(d_ra, ra)) return FDTD_ECUDA;
+      rows.a = d_ra;
+    }
     // packed records for the pre-pass of the 3-D tile stencil (<= 4 terms per row,
     // 32-bit offsets)
     if (dim == 3 && nr > 0 && !getenv("FDTD_NO_ROWPACK")) {
@@ -882,7 +911,7 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
           a.h_comp |= (hc[rp[r] + k] & 0xff) << (8 * k);
           q.w[k] = w[rp[r] + k];
         }
-        q.c = cc[r]; q.cs = cs[r];
+        q.c = cc[r]; q.cs = cs[r]; q.a = ra[r];
       }
       if (ok) {
         rowpack_i = dalloc<fdtd::RowPackI>(nr);
@@ -990,8 +1019,11 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   CK(cudaFuncSetAttribute(fdtd::stencil3d_pipe_kernel<T, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3));
   CK(cudaFuncSetAttribute(fdtd::stencil3d_tma_kernel<T, false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3 + 8192));
   CK(cudaFuncSetAttribute(fdtd::stencil3d_tma_kernel<T, true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem3 + 8192));
+  if (lossy && dim == 3 && !use_tile)
+    return fail(FDTD_ENOTSUP, "lossy media need the 3-D tile stencil (batch 1 or 16, TMA available)");
   if (use_tile) {
-    const size_t ttab = uniform ? 0 : ((size_t)n_mat * (6 * sizeof(fdtd::Coef<T>) + 1) + 15) / 16 * 16;
+    const size_t ttab = uniform ? 0 : ((size_t)n_mat * (6 * sizeof(fdtd::Coef<T>) + 1) + 15) / 16 * 16 + 16 +
+                                      (lossy ? (size_t)n_mat * 6 * sizeof(T) : 0);
     tile_smem = fdtd::tile_smem_bytes(tcfg, tHBX, (int)sizeof(T), ttab) + 128;
     if (tile_smem > 227 * 1024) return fail(FDTD_ENOTSUP, "tile stencil: %zu bytes of shared memory", tile_smem);
     CK(fdtd::tile_prepare<T>(tcfg, tile_smem));
@@ -1155,7 +1187,7 @@ int Impl<T>::setup_persist() {
   };
   if (const char* e = getenv("FDTD_PERSIST"))
     if (std::string(e) == "0") return why_not(1);
-  if (dim != 2 || B != 1 || any_leap) return why_not(2);
+  if (dim != 2 || B != 1 || any_leap || lossy) return why_not(2);
   for (auto& D : blocks)
     if (!D.fused || D.N != 1) return why_not(3);
   for (size_t q = 0; q < hpr_owner.size(); ++q) {
@@ -1718,19 +1750,19 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
     if (rowpack_i)
       fdtd::rows_prepass_packed_kernel<T><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(
           rows.n_rows, rowpack_i, (const fdtd::RowPackR<T>*)rowpack_r, B, F0, F1, y_all, rows.g_out, rows.wave,
-          rows.n_wave, rows.n_src, ds);
+          rows.n_wave, rows.n_src, ds, lossy ? 1 : 0);
     else
       fdtd::rows_prepass_kernel<T><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, B, F0, F1, y_all, ds);
     ++n;
   }
   if (dim == 3 && use_tile && sp) {
     CK(fdtd::tile_launch<T>(tcfg, uniform, SA.nitems, tile_smem, st, tma[p], SA, dm, F0, F1, mat_id, tab,
-                            ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad));
+                            ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad, lossy ? tab_a : nullptr));
     CK(cudaEventRecord(evA, st));
     CK(cudaStreamWaitEvent(st2, evA, 0));
   } else if (dim == 3 && use_tile) {
     CK(fdtd::tile_launch<T>(tcfg, uniform, tile_grid, tile_smem, st, tma[p], tsplit, dm, F0, F1, mat_id, tab,
-                            ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad));
+                            ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad, lossy ? tab_a : nullptr));
   } else if (dim == 3 && use_tma) {
     constexpr int NS = 3;
     const int BX = tBX, BY = tBY;
@@ -1777,10 +1809,10 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
     const size_t sm = (size_t)BX * BY * CY * sizeof(T) + tabsz;
     if (uniform)
       fdtd::stencil2d_rows_kernel<T, true, CY><<<grid, dim3(BX, BY), sm, st>>>(
-          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad);
+          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad, nullptr);
     else
       fdtd::stencil2d_rows_kernel<T, false, CY><<<grid, dim3(BX, BY), sm, st>>>(
-          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad);
+          dm, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad, lossy ? tab_a : nullptr);
   }
   ++n;
   mark(0, 1);
@@ -1899,7 +1931,7 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   if (sp) {
     CK(cudaEventRecord(evR, st2));
     CK(fdtd::tile_launch<T>(tcfg, uniform, SB.nitems, tile_smem, st, tma[p], SB, dm, F0, F1, mat_id, tab,
-                            ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad));
+                            ifm, n_mat, u0, u1, rows, y_all, ds, check_every, d_bad, lossy ? tab_a : nullptr));
     CK(cudaStreamWaitEvent(st, evR, 0));
     // probes (coarse fields after the whole stencil) and the step counter
     fdtd::FusedParams<T> Q = P;

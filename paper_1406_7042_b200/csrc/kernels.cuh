@@ -85,6 +85,7 @@ struct RowsE {
   const T* wave;               // [n_wave][n_src][B]   (n_src = number of waveform columns)
   int64_t n_wave, n_src;
   T* g_out;                    // interface rows publish E^{n+1} at G[y_off] (reduced-chain input)
+  const T* a;                  // [n_rows] ca of the row's unknown (lossy media), null: lossless
   // list form (rows_prepass_kernel)
   const int32_t* e_comp;       // [n_rows]
   const int64_t* e_off;        // [n_rows]
@@ -98,7 +99,7 @@ __device__ __forceinline__ T eval_row(const RowsE<T>& R, int r, int b, int B, T 
     acc += R.w[k] * H0.f[R.h_comp[k]][R.h_off[k] * B + b];
   const int64_t yo = R.y_off[r];
   if (yo >= 0) acc += y[yo + b];
-  T e = R.c[r].sub(e0, acc);
+  T e = R.a ? fma(R.a[r], e0, -R.c[r].apply(acc)) : R.c[r].sub(e0, acc);
   const int s = R.src[r];
   if (s >= 0 && step < R.n_wave) e -= R.cs[r] * R.wave[(step * R.n_src + s) * B + b];
   if (yo >= 0) R.g_out[yo + b] = e;        // identical value from every thread computing it
@@ -141,7 +142,7 @@ struct RowPackR {          // 32 (fp32) / 64 (fp64) bytes
   T w[4];
   Coef<T> c;
   T cs;
-  T pad;
+  T a;                     // ca of the row's unknown (1 when lossless)
 };
 
 template <typename T>
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(256)
 rows_prepass_packed_kernel(int64_t n_rows, const RowPackI* __restrict__ RI, const RowPackR<T>* __restrict__ RR,
                            int B, Fields<T> F0, Fields<T> F1, const T* __restrict__ y, T* __restrict__ g_out,
                            const T* __restrict__ wave, int64_t n_wave, int64_t n_src,
-                           const int64_t* __restrict__ d_step) {
+                           const int64_t* __restrict__ d_step, int lossy) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_rows * B) return;
   const int r = (int)(t / B), b = (int)(t % B);
@@ -175,7 +176,7 @@ rows_prepass_packed_kernel(int64_t n_rows, const RowPackI* __restrict__ RI, cons
   for (int k = 0; k < 4; ++k)
     if (k < nt) acc += rr.w[k] * h[k];
   if (yo >= 0) acc += yv;
-  T e = rr.c.sub(e0, acc);
+  T e = lossy ? fma(rr.a, e0, -rr.c.apply(acc)) : rr.c.sub(e0, acc);
   if (has_src) e -= rr.cs * wv;
   if (yo >= 0) g_out[yo + b] = e;
   T* o = ec == 0 ? F1.f[0] : ec == 1 ? F1.f[1] : F1.f[2];
@@ -198,7 +199,8 @@ stencil2d_rows_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
                       const Coef<T>* __restrict__ gtab, const uint8_t* __restrict__ gifm, int n_mat,
                       Coef<T> u0, Coef<T> u1, RowsE<T> R, const T* __restrict__ y,
                       const int64_t* __restrict__ d_step, int check_every,
-                      unsigned long long* __restrict__ bad_step) {
+                      unsigned long long* __restrict__ bad_step, const T* __restrict__ taba) {
+  // taba: [n_mat][6] ca / da of lossy media (null: lossless, the branch is never taken)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int BX = blockDim.x, BY = blockDim.y, B = d.B;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -245,7 +247,8 @@ stencil2d_rows_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
     const T hxm = (r == 0) ? hx_jm : hx[r - 1];
     const Coef<T> c = UNIFORM ? u0 : tab->c[m[r]][2];
     const T dd = (hy[r] - hyim[r]) - (hx[r] - hxm);
-    ez[r] = (ci && j > 0 && j < ny) ? c.add(ez0[r], dd) : (T)0;
+    ez[r] = (ci && j > 0 && j < ny) ? ((!UNIFORM && taba) ? fma(__ldg(taba + m[r] * 6 + 2), ez0[r], c.apply(dd)) : c.add(ez0[r], dd))
+                                    : (T)0;
     if (!UNIFORM && (tab->ifm[m[r]] & 4) && i <= nx && j <= ny)
       ez[r] = eval_row(R, R.row_of[2][min(j, ny) * d.px + ii], b, B, ez0[r], F0, y, step);
     sE[(ty * CY + r) * BX + tx] = ez[r];
@@ -263,8 +266,15 @@ stencil2d_rows_kernel(Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* __restr
     Coef<T> cx, cy;
     if (UNIFORM) { cx = u1; cy = u1; }
     else { cx = tab->c[m[r]][3]; cy = tab->c[m[r]][4]; }
-    const T hx1 = (ci && j < ny) ? cx.sub(hx[r], ez_jp - ez[r]) : hx[r];
-    const T hy1 = (i < nx && j > 0 && j < ny) ? cy.add(hy[r], ez_ip - ez[r]) : hy[r];
+    T hx1, hy1;
+    if (!UNIFORM && taba) {
+      const T ax = __ldg(taba + m[r] * 6 + 3), ay = __ldg(taba + m[r] * 6 + 4);
+      hx1 = (ci && j < ny) ? fma(ax, hx[r], -cx.apply(ez_jp - ez[r])) : hx[r];
+      hy1 = (i < nx && j > 0 && j < ny) ? fma(ay, hy[r], cy.apply(ez_ip - ez[r])) : hy[r];
+    } else {
+      hx1 = (ci && j < ny) ? cx.sub(hx[r], ez_jp - ez[r]) : hx[r];
+      hy1 = (i < nx && j > 0 && j < ny) ? cy.add(hy[r], ez_ip - ez[r]) : hy[r];
+    }
     const int o = o0 + r * rs;
     F1.f[2][o] = ez[r]; F1.f[3][o] = hx1; F1.f[4][o] = hy1;
     if (do_check) bad |= !(finite_small(ez[r]) && finite_small(hx1) && finite_small(hy1));

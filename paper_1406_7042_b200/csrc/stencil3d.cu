@@ -12,6 +12,7 @@ template <typename T, int NS, int W, int MB, int MINB, int BY = TILE_BY>
 struct TileKernels {
   static constexpr auto uni = &stencil3d_tile_kernel<T, true, NS, W, MB, MINB, BY>;
   static constexpr auto mat = &stencil3d_tile_kernel<T, false, NS, W, MB, MINB, BY>;
+  static constexpr auto lossy = &stencil3d_tile_kernel<T, false, NS, W, MB, MINB, BY, true>;
 };
 
 template <typename T, typename F>
@@ -55,6 +56,7 @@ cudaError_t tile_prepare(const TileCfg& c, size_t smem) {
   tile_dispatch<T>(c, [&](auto K) {
     err = cudaFuncSetAttribute(K.uni, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err == cudaSuccess) err = cudaFuncSetAttribute(K.mat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err == cudaSuccess) err = cudaFuncSetAttribute(K.lossy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
   return err;
 }
@@ -63,12 +65,12 @@ template <typename T>
 cudaError_t tile_launch(const TileCfg& c, bool uniform, int grid, size_t smem, cudaStream_t st, const TmaSet& tm,
                         const TileSplit& split, Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* mat_id,
                         const Coef<T>* tab, const uint8_t* ifm, int n_mat, Coef<T> u0, Coef<T> u1, RowsE<T> rows,
-                        const T* y, const int64_t* ds, int check_every, unsigned long long* bad) {
+                        const T* y, const int64_t* ds, int check_every, unsigned long long* bad, const T* taba) {
   cudaError_t err = cudaErrorInvalidValue;
   tile_dispatch<T>(c, [&](auto K) {
-    const auto fn = uniform ? K.uni : K.mat;
+    const auto fn = uniform ? K.uni : (taba ? K.lossy : K.mat);
     fn<<<grid, dim3(32, c.BY), smem, st>>>(tm, split, d, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y, ds,
-                                          check_every, bad);
+                                          check_every, bad, taba);
     err = cudaSuccess;
   });
   return err;
@@ -90,7 +92,7 @@ int tile_blocks_per_sm(const TileCfg& c, bool uniform, size_t smem) {
   template cudaError_t tile_launch<T>(const TileCfg&, bool, int, size_t, cudaStream_t, const TmaSet&,              \
                                       const TileSplit&, Dims, Fields<T>, Fields<T>, const uint8_t*, const Coef<T>*, \
                                       const uint8_t*, int, Coef<T>, Coef<T>, RowsE<T>, const T*, const int64_t*,  \
-                                      int, unsigned long long*);                                                   \
+                                      int, unsigned long long*, const T*);                                                 \
   template int tile_blocks_per_sm<T>(const TileCfg&, bool, size_t);
 FDTD_TILE_INST(float)
 FDTD_TILE_INST(double)

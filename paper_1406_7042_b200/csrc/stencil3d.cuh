@@ -106,13 +106,15 @@ struct SegCursor {               // walks the load sequence of one CTA's items
   }
 };
 
-template <typename T, bool UNIFORM, int NS, int W, int MB, int MINB, int BY = TILE_BY>
+template <typename T, bool UNIFORM, int NS, int W, int MB, int MINB, int BY = TILE_BY, bool LOSSY = false>
 __global__ void __launch_bounds__(32 * BY, MINB)
 stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims d, Fields<T> F0,
                       Fields<T> F1, const uint8_t* __restrict__ mat_id, const Coef<T>* __restrict__ gtab,
                       const uint8_t* __restrict__ gifm, int n_mat, Coef<T> u0, Coef<T> u1, RowsE<T> R,
                       const T* __restrict__ y, const int64_t* __restrict__ d_step, int check_every,
-                      unsigned long long* __restrict__ bad_step) {
+                      unsigned long long* __restrict__ bad_step, const T* __restrict__ gtaba) {
+  // LOSSY (table variant only): gtaba [n_mat][6] holds ca / da of Eq. (2a)/(2b) with
+  // conductivities, E <- ca E + cb curl, H <- da H - ch curl (fdtd.h coef_a)
   // MB == 0: batch 1, W x cells per thread (XV); MB > 0: batch of MB members, W per thread
   constexpr bool XV = MB == 0;
   using L = LV<T, W>;
@@ -136,6 +138,7 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
   T* En = Ring + NS * STG;                                                // [2][3][EP]
   Coef<T>* tabc = reinterpret_cast<Coef<T>*>(En + 2 * 3 * EP);           // [n_mat][6]
   uint8_t* tabf = reinterpret_cast<uint8_t*>(tabc + 6 * n_mat);           // [n_mat] explicit-row bits
+  T* taba = reinterpret_cast<T*>(tabf + ((n_mat + 15) & ~15));            // [n_mat][6] (LOSSY)
   const bool leader = (tx == 0 && ty == 0);
   if (leader) {
     for (int q = 0; q < NS; ++q) mbar_init(&bars[q], 1);
@@ -144,6 +147,8 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
   if (!UNIFORM) {
     for (int m = ty * 32 + tx; m < n_mat; m += 32 * BY) {
       for (int c = 0; c < 6; ++c) tabc[m * 6 + c] = gtab[m * 6 + c];
+      if (LOSSY)
+        for (int c = 0; c < 6; ++c) taba[m * 6 + c] = gtaba[m * 6 + c];
       tabf[m] = gifm[m];
     }
   }
@@ -276,9 +281,16 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
           cx = tabc[m * 6 + 0]; cy = tabc[m * 6 + 1]; cz = tabc[m * 6 + 2];
           ifm_any |= tabf[m];
         }
+        if constexpr (LOSSY && !UNIFORM) {
+          const int ml = XV ? (int)((m_cur >> (8 * w)) & 0xffu) : (int)m_cur;
+          ex.v[w] = fma(taba[ml * 6 + 0], ex0.v[w], cx.apply(((hz_c.v[w] - hz_jm.v[w]) - (hy_c.v[w] - hyk.v[w])) * fa[w]));
+          ey.v[w] = fma(taba[ml * 6 + 1], ey0.v[w], cy.apply(((hx_c.v[w] - hxk.v[w]) - (hz_c.v[w] - hz_im.v[w])) * fb[w]));
+          ez.v[w] = fma(taba[ml * 6 + 2], ez0.v[w], cz.apply(((hy_c.v[w] - hy_im.v[w]) - (hx_c.v[w] - hx_jm.v[w])) * fc[w]));
+        } else {
         ex.v[w] = cx.add(ex0.v[w], ((hz_c.v[w] - hz_jm.v[w]) - (hy_c.v[w] - hyk.v[w])) * fa[w]);
         ey.v[w] = cy.add(ey0.v[w], ((hx_c.v[w] - hxk.v[w]) - (hz_c.v[w] - hz_im.v[w])) * fb[w]);
         ez.v[w] = cz.add(ez0.v[w], ((hy_c.v[w] - hy_im.v[w]) - (hx_c.v[w] - hx_jm.v[w])) * fc[w]);
+        }
       }
       // z walls: tangential E on k = 0 and everything on k = nz are not unknowns
       if (kk == 0) {
@@ -334,10 +346,18 @@ stencil3d_tile_kernel(const __grid_constant__ TmaSet tm, const TileSplit S, Dims
             const int m = XV ? (int)((m_prev >> (8 * w)) & 0xffu) : (int)m_prev;
             hx_ = tabc[m * 6 + 3]; hy_ = tabc[m * 6 + 4]; hz_ = tabc[m * 6 + 5];
           }
+          if constexpr (LOSSY && !UNIFORM) {
+            // masked entries (fb / fa / fd = 0) are not unknowns: they keep their value
+            const int ml = XV ? (int)((m_prev >> (8 * w)) & 0xffu) : (int)m_prev;
+            hx1.v[w] = fb[w] != (T)0 ? fma(taba[ml * 6 + 3], hxk.v[w], -hx_.apply((ez_jp.v[w] - ezk.v[w]) - (ey.v[w] - eyk.v[w]))) : hxk.v[w];
+            hy1.v[w] = fa[w] != (T)0 ? fma(taba[ml * 6 + 4], hyk.v[w], -hy_.apply((ex.v[w] - exk.v[w]) - (ez_ip.v[w] - ezk.v[w]))) : hyk.v[w];
+            hz1.v[w] = (hz_on && fd[w] != (T)0) ? fma(taba[ml * 6 + 5], hzk.v[w], -hz_.apply((ey_ip.v[w] - eyk.v[w]) - (ex_jp.v[w] - exk.v[w]))) : hzk.v[w];
+          } else {
           hx1.v[w] = hx_.sub(hxk.v[w], ((ez_jp.v[w] - ezk.v[w]) - (ey.v[w] - eyk.v[w])) * fb[w]);
           hy1.v[w] = hy_.sub(hyk.v[w], ((ex.v[w] - exk.v[w]) - (ez_ip.v[w] - ezk.v[w])) * fa[w]);
           hz1.v[w] = hz_on ? hz_.sub(hzk.v[w], ((ey_ip.v[w] - eyk.v[w]) - (ex_jp.v[w] - exk.v[w])) * fd[w])
                            : hzk.v[w];
+          }
         }
         const uint32_t oh = oe - sz32;
         IO::st(F1.f[3] + oh, hx1); IO::st(F1.f[4] + oh, hy1); IO::st(F1.f[5] + oh, hz1);

@@ -35,7 +35,8 @@ template <typename T>
 cudaError_t tile_launch(const TileCfg& c, bool uniform, int grid, size_t smem, cudaStream_t st, const TmaSet& tm,
                         const TileSplit& split, Dims d, Fields<T> F0, Fields<T> F1, const uint8_t* mat_id,
                         const Coef<T>* tab, const uint8_t* ifm, int n_mat, Coef<T> u0, Coef<T> u1, RowsE<T> rows,
-                        const T* y, const int64_t* ds, int check_every, unsigned long long* bad);
+                        const T* y, const int64_t* ds, int check_every, unsigned long long* bad,
+                        const T* taba = nullptr);    // taba: [n_mat][6] ca / da (lossy media), null: lossless
 template <typename T>
 int tile_blocks_per_sm(const TileCfg& c, bool uniform, size_t smem);
 

@@ -46,7 +46,7 @@ class Grid(C.Structure):
 
 class Materials(C.Structure):
     _fields_ = [("n_mat", C.c_int32), ("mat_id", _u8p), ("coef", _f64p), ("if_mask", _u8p),
-                ("uniform_coef", C.c_double * 6)]
+                ("uniform_coef", C.c_double * 6), ("coef_a", _f64p)]
 
 
 class Interface(C.Structure):
@@ -174,6 +174,11 @@ class Sim:
             keep += [mid, coef, ifm]
             mat.n_mat = coef.shape[0]
             mat.mat_id, mat.coef, mat.if_mask = _ptr(mid, C.c_uint8), _ptr(coef, C.c_double), _ptr(ifm, C.c_uint8)
+            if problem.get("mat_ca") is not None:        # lossy media: ca / da per material (fdtd.h coef_a)
+                ca = _arr(problem["mat_ca"], np.float64)
+                assert ca.shape == coef.shape
+                keep.append(ca)
+                mat.coef_a = _ptr(ca, C.c_double)
         else:
             mat.n_mat = 0
             uc = _arr(problem["uniform_coef"], np.float64)

@@ -215,10 +215,37 @@ def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=N
         ifm[is_if[c]] |= (1 << c)
     for c in hcomps:
         coef[c, ~hole[c]] = dt / (mu0 * d)                      # ch = dt/(mu delta), R8
+    # lossy media / matched absorbers (Eq. (2a)/(2b) with the
+    # conductivity terms, D_sigma of Eq. (5)): per-cell sigma_e [S/m], sigma_m
+    # [Ohm/m] with the owning-cell rule (R1(iv)):
+    #   cb = 1/((eps/dt + sigma_e/2) delta),  ca = (eps/dt - sigma_e/2)/(eps/dt + sigma_e/2)
+    #   ch = 1/((mu/dt + sigma_m/2) delta),   da = (mu/dt - sigma_m/2)/(mu/dt + sigma_m/2)
+    lossy = scn.get("sigma_e") is not None or scn.get("sigma_m") is not None
+    ca = np.ones((6, S))
+    own_se = None
+    if lossy:
+        def own(cellarr):
+            a = np.zeros((nz, ny, nx)) if cellarr is None else np.asarray(cellarr, np.float64).reshape(nz, ny, nx)
+            return a[np.minimum(kk, nz - 1), np.minimum(jj, ny - 1), np.minimum(ii, nx - 1)].ravel()
+        own_se, own_sm = own(scn.get("sigma_e")), own(scn.get("sigma_m"))
+        if np.any(own_se < 0) or np.any(own_sm < 0):
+            raise ValueError("conductivities must be >= 0 (Eq. (7), P:141-147)")
+        for c in ecomps:
+            reg = ~hole[c] & ~is_if[c]
+            if np.any(own_se[is_if[c]] != 0):
+                raise NotImplementedError("lossy cells touching a refined box (interface rows stay lossless)")
+            a_, b_ = own_eps.ravel()[reg] / dt, 0.5 * own_se[reg]
+            coef[c, reg] = 1.0 / ((a_ + b_) * d)
+            ca[c, reg] = (a_ - b_) / (a_ + b_)
+        for c in hcomps:
+            reg = ~hole[c]
+            a_, b_ = mu0 / dt, 0.5 * own_sm[reg]
+            coef[c, reg] = 1.0 / ((a_ + b_) * d)
+            ca[c, reg] = (a_ - b_) / (a_ + b_)
     # distinct (coefficients, interface bits) rows -> material table; per-column
     # codes first so that 10^7-row grids take seconds
     codes, vals = [], []
-    for col in list(coef) + [ifm.astype(np.float64)]:
+    for col in list(coef) + [ifm.astype(np.float64)] + (list(ca) if lossy else []):
         u, inv = np.unique(col, return_inverse=True)
         codes.append(inv.astype(np.int64))
         vals.append(u)
@@ -226,17 +253,19 @@ def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=N
     for cd, u in zip(codes, vals):
         key = key * len(u) + cd
     ukey, first, mid = np.unique(key, return_index=True, return_inverse=True)
-    tab = np.concatenate([coef.T, ifm[:, None].astype(np.float64)], axis=1)
+    tab = np.concatenate([coef.T, ifm[:, None].astype(np.float64)] + ([ca.T] if lossy else []), axis=1)
     uniq = tab[first]
     if len(uniq) > 256:
         raise RuntimeError(f"{len(uniq)} material classes > 256")
     prob = dict(name=scn.get("name"), dim=dim, n=P.n, delta=d, dt=dt, batch=int(scn.get("batch", 1)),
                 precision=precision or scn["precision"], n_steps=int(scn["n_steps"]))
-    if len(uniq) == 1 and not boxes:
+    if len(uniq) == 1 and not boxes and not lossy:
         prob.update(mat_id=None, uniform_coef=uniq[0, :6].copy())
     else:
         prob.update(mat_id=mid.astype(np.uint8).reshape(-1), mat_coef=uniq[:, :6].copy(),
                     mat_ifmask=uniq[:, 6].astype(np.uint8))
+        if lossy:
+            prob["mat_ca"] = uniq[:, 7:13].copy()
 
     # ---- interface rows --------------------------------------------------------------
     if boxes:
@@ -269,7 +298,10 @@ def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=N
             if is_if[int(c), s]:
                 cf.append(dt / P.De_c[int(c)].ravel()[s] * d)
             else:
-                cf.append(dt / own_eps.ravel()[s])              # G_E * delta = dt/eps
+                if lossy:
+                    cf.append(1.0 / (own_eps.ravel()[s] / dt + 0.5 * own_se[s]))
+                else:
+                    cf.append(dt / own_eps.ravel()[s])          # G_E * delta = dt/eps
         amp = np.asarray(src.get("amp", np.ones(len(u))), np.float64)
         prob["sources"] = dict(unknown=np.array(u, np.int64), coef=np.array(cf) * amp,
                                wave=np.asarray(src["wave"], np.float64))

@@ -326,6 +326,67 @@ def rom_cavity2d(name, config_id, nx, ny, delta, s_factor, q, batch, n_probes=4,
                 basis=dict(recipe="A", L=2, M=1.1, fmax=fmax))
 
 
+# ---------------------------------------------------------------------------
+# lossy media and matched absorbers ("4th-order
+# matched absorber", 5 cells)
+# ---------------------------------------------------------------------------
+
+def absorber_profile(n_cells, axis_len, delta, eps, mu, order=4, thick=5, r0=1e-4):
+    """Per-cell conductivity along one axis: a graded layer of ``thick`` cells at
+    both ends, sigma_e(x) = sigma_max (depth / L)^order sampled at cell centres,
+    sigma_max = -(order + 1) ln(r0) / (2 eta L) (normal-incidence reflection r0
+    of the continuous profile), matched magnetic loss sigma_m = sigma_e mu/eps."""
+    L = thick * delta
+    eta = math.sqrt(mu / eps)
+    smax = -(order + 1) * math.log(r0) / (2.0 * eta * L)
+    se = np.zeros(n_cells)
+    for i in range(thick):
+        depth = (thick - i - 0.5) * delta
+        v = smax * (depth / L) ** order
+        se[i] = v
+        se[n_cells - 1 - i] = v
+    return se, se * mu / eps
+
+
+def lossy_box(name, config_id, dim, nx, ny, nz, delta, dt_factor, n_steps, precision, batch=1, axes=(0,),
+              eps_slab=2.5, seed=None):
+    """PEC box with 5-cell 4th-order matched absorbers on the ends of ``axes``
+    (the paper's waveguide / microstrip terminations), a
+    lossy dielectric slab (eps_r, sigma_e > 0, unmatched) in the middle, a
+    Gaussian-derivative Ez point source and seeded probes."""
+    rng = np.random.default_rng(SEED0 + config_id if seed is None else seed)
+    shape = (nz, ny, nx) if dim == 3 else (1, ny, nx)
+    eps = np.ones(shape)
+    se = np.zeros(shape)
+    sm = np.zeros(shape)
+    x0, x1 = nx // 2 - 2, nx // 2 + 3
+    eps[:, :, x0:x1] = eps_slab
+    se[:, :, x0:x1] = 0.02                      # a lossy dielectric (S/m), no magnetic loss
+    for ax in axes:
+        n_ax = (nx, ny, nz)[ax]
+        pe, pm = absorber_profile(n_ax, n_ax * delta, delta, EPS0, MU0)
+        sh = [1, 1, 1]
+        sh[2 - ax] = n_ax
+        se = se + pe.reshape(sh)
+        sm = sm + pm.reshape(sh)
+    dt = dt_factor * cfl_coarse(dim, delta)
+    t = _times(dt, n_steps)
+    tau = gaussian_derivative_tau(0.25 * C0 / (10 * delta) * 4)
+    w = _gauss_deriv(t, tau)
+    i0, j0, k0 = nx // 3, ny // 2, (nz // 2 if dim == 3 else 0)
+    amps = np.linspace(1.0, -1.4, batch)
+    wave = w[:, None, None] * amps[None, None, :]
+    prb = []
+    for _ in range(3):
+        prb.append((int(rng.integers(2, nx - 1)), int(rng.integers(2, ny - 1)), int(rng.integers(1, nz - 1)) if dim == 3 else 0))
+    n3 = (nx, ny, nz) if dim == 3 else (nx, ny, 1)
+    return dict(name=name, config_id=config_id, dim=dim, n=n3, delta=delta, eps0=EPS0, mu0=MU0, c0=C0,
+                eps_r=eps if dim == 3 else eps[0], sigma_e=se if dim == 3 else se[0], sigma_m=sm if dim == 3 else sm[0],
+                boxes=[], pec_sheets=[], dt=dt, dt_factor=dt_factor, n_steps=n_steps, precision=precision, batch=batch,
+                sources=dict(comp=np.array([2]), idx=np.array([[i0, j0, k0]]), wave=wave),
+                probes=[dict(terms=[(2, p, 1.0)]) for p in prb], init=None, basis=None)
+
+
 def scenario(which, precision=None, n_steps=None, **kw):
     """Return the scenario dict for a BASELINE config id (1-5) or a named test
     variant.  ``precision`` / ``n_steps`` override the config's defaults."""
@@ -373,6 +434,15 @@ def scenario(which, precision=None, n_steps=None, **kw):
         # config-5 structure (PEC strips through z-refined regions, two models)
         s = microstrip3d("micro5", 107, 14, 12, 4, 0.25e-3, 1, (2, 12), 2, 2, 3.38, 2, (2, 2),
                          4, (1, 3), 4, 8, 0.6, 100, precision or 64, spacing=4)
+    elif which == "lossy3d":
+        s = lossy_box("lossy3d", 301, 3, 70, 23, 19, 1e-3, 0.95, 400, precision or 64, axes=(0,))
+    elif which == "lossy3d_b16":
+        s = lossy_box("lossy3d_b16", 302, 3, 30, 11, 9, 1e-3, 0.95, 300, precision or 32, batch=16, axes=(0, 1))
+    elif which == "lossy256":
+        # config 3's grid with matched absorbers on the x and y ends and a lossy slab (throughput of the lossy stencil)
+        s = lossy_box("lossy256", 304, 3, 256, 256, 256, 1e-3, 0.95, 1000, precision or 32, axes=(0, 1))
+    elif which == "lossy2d":
+        s = lossy_box("lossy2d", 303, 2, 90, 61, 1, 1e-3, 0.95, 500, precision or 64, axes=(0, 1))
     elif which == "rom2d":
         # the paper's 2-D cavity (Table I: 101 cells of 1 cm, order 80, 5 points,
         # M = 1.1, f_max = 0.5 GHz) at s = 4.95, 64 excitation waveforms

@@ -19,7 +19,8 @@ def active_masks(problem):
     comps = (yee.E_COMPS_3D + yee.H_COMPS_3D) if dim == 3 else (yee.E_COMPS_2D + yee.H_COMPS_2D)
     mid = np.asarray(problem["mat_id"]).reshape(-1)
     coef = np.asarray(problem["mat_coef"], np.float64)
-    ifu = np.asarray(problem["interface"]["unknown"], np.int64)
+    itf = problem.get("interface")
+    ifu = np.asarray(itf["unknown"], np.int64) if itf is not None else np.zeros(0, np.int64)
     out = {}
     for c in comps:
         live = (yee.exists_mask(dim, n, c) & ~yee.wall_pec_mask(dim, n, c)).reshape(-1)

@@ -55,9 +55,10 @@ def test_golden_present_and_nonvacuous(c, p, m):
 
 @pytest.mark.parametrize("c,p", [(2, 32), (5, 32), (3, 64)])
 def test_golden_fingerprint_matches_problem(c, p):
-    from make_golden import fingerprint, problem_for
+    from make_golden import apply_model, fingerprint, problem_for
     g = _load(c, p, 0)
     _, prob = problem_for(c, p)
+    prob = apply_model(prob, g)
     assert np.allclose(fingerprint(prob), g["fingerprint"], rtol=1e-11, atol=0)
 
 
@@ -67,8 +68,10 @@ def test_config2_golden_prefix_reproduced_by_oracle():
     # recursion and the probe bookkeeping of the golden
     from make_golden import problem_for
     from oracle import problem_step as ps
+    from make_golden import apply_model
     g = _load(2, 32, 0)
     _, prob = problem_for(2, 32)
+    prob = apply_model(prob, g)
     n = 1500
     _, _, probes, _ = ps.run(prob, n)
     assert np.linalg.norm(probes) > 0

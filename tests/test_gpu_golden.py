@@ -64,6 +64,13 @@ def golden_report(config, prec, members, golden_prec=None, **sim_kw):
     from paper_1406_7042_b200.fdtd import Sim
     golds = {m: _golden(config, golden_prec or prec, m) for m in members}
     scn, prob = _problem(config, prec)
+    # the reduced states are coordinates in the golden's own projection basis
+    # (not unique across LAPACK builds): step the golden's matrices when it
+    # carries them (configs 2, 5; config 4's S_E only lives in the prep cache)
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(GOLD), "..", "tools"))
+    from make_golden import apply_model
+    prob = apply_model(prob, golds[members[0]])
     fp = _fingerprint(prob)
     for m, g in golds.items():
         # the same problem description (F13) as the golden's: checksums agree

@@ -77,6 +77,48 @@ def fingerprint(prob):
     return np.array(f)
 
 
+MODEL_EMBED_MAX = 4_000_000     # entries; config 4's S_E (6.7e7) stays in the prep cache
+
+
+def model_arrays(prob):
+    """The reduced models (K~', S_E per block) when small enough to commit: a
+    projection basis is not unique across LAPACK builds (signs / rotations
+    within the Krylov space), so a golden's reduced states are tied to the exact
+    matrices it was stepped with; the GPU test steps those (apply_model)."""
+    blocks = prob.get("blocks") or []
+    tot = sum(np.asarray(b["K"]).size + np.asarray(b["S_E"]).size for b in blocks)
+    if not blocks or tot > MODEL_EMBED_MAX:
+        return {}
+    out = {}
+    for i, b in enumerate(blocks):
+        out[f"blk{i}_K"] = np.asarray(b["K"], np.float64)
+        out[f"blk{i}_SE"] = np.asarray(b["S_E"], np.float64)
+    return out
+
+
+def apply_model(prob, golden):
+    """Replace the problem's reduced matrices by the golden's (same shapes)."""
+    blocks = prob.get("blocks") or []
+    if not blocks or "blk0_K" not in golden:
+        return prob
+    nb = []
+    for i, b in enumerate(blocks):
+        K, SE = golden[f"blk{i}_K"], golden[f"blk{i}_SE"]
+        assert K.shape == np.asarray(b["K"]).shape and SE.shape == np.asarray(b["S_E"]).shape
+        nb.append(dict(b, K=K, S_E=SE))
+    return dict(prob, blocks=nb)
+
+
+def embed(path, prob):
+    """Add the model arrays to an existing golden written from ``prob`` (its
+    fingerprint must be the problem's)."""
+    z = np.load(path, allow_pickle=False)
+    d = {k: z[k] for k in z.files}
+    assert np.allclose(fingerprint(prob), d["fingerprint"], rtol=1e-13, atol=0), "golden is not of this problem"
+    d.update(model_arrays(prob))
+    np.savez_compressed(path, **d)
+
+
 def problem_for(config, prec):
     from paper_1406_7042_b200 import prep
     scn = scenario(config, precision=prec)
@@ -92,7 +134,12 @@ def main():
     ap.add_argument("--steps", type=int, default=None, help="default: the config's full length")
     ap.add_argument("--chunk", type=int, default=500)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--embed", action="store_true", help="only add the reduced-model arrays to the existing golden")
     a = ap.parse_args()
+    if a.embed:
+        scn, prob = problem_for(a.config, a.prec)
+        embed(os.path.join(ROOT, "tests", "golden", f"config{a.config}{a.tag}_fp{int(prob['precision'])}_m{a.member}.npz"), prob)
+        return
     t0 = time.time()
     scn, prob = problem_for(a.config, a.prec)
     prec = int(prob["precision"])
@@ -155,7 +202,7 @@ def main():
     out = os.path.join(out_dir, tag + ".npz")
     np.savez_compressed(out, probes=probes, if_E=if_E, red_e=red_e, red_h=red_h,
                         sample_ids=pool_ids[pick].astype(np.int64), sample_val=pool_val[pick],
-                        norms=norms, fingerprint=fp, meta=np.array(json.dumps(meta)))
+                        norms=norms, fingerprint=fp, meta=np.array(json.dumps(meta)), **model_arrays(prob))
     print(f"wrote {out}: {json.dumps(meta)}  norms {norms}", flush=True)
 
 
