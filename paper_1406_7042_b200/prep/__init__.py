@@ -365,9 +365,27 @@ def _pec_extra(scn):
     sheets = scn.get("pec_sheets") or []
     boxes = scn.get("boxes") or []
     blocks_f = {bi: b.get("pec_fine") or [] for bi, b in enumerate(boxes)}
-    if not sheets and not any(blocks_f.values()):
+    blocks_c = scn.get("pec_blocks") or []      # solid PEC blocks of the coarse grid (closed node boxes; irises)
+    if not sheets and not any(blocks_f.values()) and not blocks_c:
         return None
     dim = scn["dim"]
+
+    def solid_coarse(comp, shape):
+        m = np.zeros(shape, bool)
+        k, j, i = np.indices(shape)
+        ijk = (i, j, k)
+        ax_of = 2 if dim == 2 else comp             # 2-D: Ez edges run along z (one node in the plane)
+        for blk in blocks_c:
+            lo = tuple(blk["lo"]) + (0,) * (3 - len(blk["lo"]))
+            hi = tuple(blk["hi"]) + (0,) * (3 - len(blk["hi"]))
+            inside = np.ones(shape, bool)
+            for a in range(dim):
+                if a == ax_of:
+                    inside &= (ijk[a] >= lo[a]) & (ijk[a] + 1 <= hi[a])
+                else:
+                    inside &= (ijk[a] >= lo[a]) & (ijk[a] <= hi[a])
+            m |= inside
+        return m
 
     def solid(grid, comp, shape):
         """solid PEC blocks given in a box's fine node indices (closed): every
@@ -390,7 +408,11 @@ def _pec_extra(scn):
 
     def f(grid, comp, shape):
         m = np.zeros(shape, bool)
-        if comp > 2 or dim != 3:
+        if comp > 2:
+            return m
+        if grid < 0 and blocks_c:
+            m |= solid_coarse(comp, shape)
+        if dim != 3:
             return m
         m |= solid(grid, comp, shape)
         if comp not in (0, 1) or not sheets:

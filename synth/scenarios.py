@@ -387,6 +387,42 @@ def lossy_box(name, config_id, dim, nx, ny, nz, delta, dt_factor, n_steps, preci
                 probes=[dict(terms=[(2, p, 1.0)]) for p in prb], init=None, basis=None)
 
 
+def iris_guide2d(name, config_id, precision, irises=True, n_steps=20000, dt_factor=0.99):
+    """The 2-D iris waveguide of P:515-517 from its description: 5 cm x 50 cm,
+    40 x 400 cells of 1.25 mm (x along the guide), eps_r = 2.5, PEC side walls,
+    five PEC irises 50 cells apart (2 nodes thick with a 16-cell centred aperture:
+    the printed "length 1.25 cm, aperture 1 cm" is opaque below 9 GHz when read
+    as a 10-cell-long 8-cell-wide channel, so the stand-in uses thin inductive
+    irises that form a band-pass filter inside the 3 GHz band),
+    5-cell 4th-order matched absorbers at both ends, a Gaussian current line
+    source (-20 dB at 3 GHz) near one end and a line probe (sum of Ez across the
+    guide) near the other.  ``irises=False``: the empty guide (S21 reference)."""
+    nx, ny, delta = 400, 40, 1.25e-3
+    eps_r = 2.5
+    pe, pm = absorber_profile(nx, nx * delta, delta, eps_r * EPS0, MU0)
+    se = np.tile(pe, (ny, 1))
+    sm = np.tile(pm, (ny, 1))
+    dt = dt_factor * cfl_coarse(2, delta) * math.sqrt(eps_r)       # Eq. (1) with the guide's wave speed
+    t = _times(dt, n_steps)
+    w = _gauss(t, gaussian_tau(3e9))
+    js = np.arange(1, ny)
+    xs, xp = 20, 380
+    sources = dict(comp=np.full(len(js), 2), idx=np.array([[xs, j, 0] for j in js]),
+                   column=np.zeros(len(js), np.int32), wave=w.reshape(n_steps, 1, 1))
+    probes = [dict(terms=[(2, (xp, int(j), 0), delta) for j in js]),
+              dict(terms=[(2, (xs + 20, int(j), 0), delta) for j in js])]
+    blocks = []
+    if irises:
+        for q in range(5):
+            x0 = 95 + 50 * q
+            blocks.append(dict(lo=(x0, 0), hi=(x0 + 1, 12)))
+            blocks.append(dict(lo=(x0, 28), hi=(x0 + 1, ny)))
+    return dict(name=name, config_id=config_id, dim=2, n=(nx, ny, 1), delta=delta, eps0=EPS0, mu0=MU0, c0=C0,
+                eps_r=np.full((ny, nx), eps_r), sigma_e=se, sigma_m=sm, boxes=[], pec_sheets=[], pec_blocks=blocks,
+                dt=dt, dt_factor=dt_factor, n_steps=n_steps, precision=precision, batch=1, sources=sources,
+                probes=probes, init=None, basis=None)
+
+
 def scenario(which, precision=None, n_steps=None, **kw):
     """Return the scenario dict for a BASELINE config id (1-5) or a named test
     variant.  ``precision`` / ``n_steps`` override the config's defaults."""
@@ -441,6 +477,10 @@ def scenario(which, precision=None, n_steps=None, **kw):
     elif which == "lossy256":
         # config 3's grid with matched absorbers on the x and y ends and a lossy slab (throughput of the lossy stencil)
         s = lossy_box("lossy256", 304, 3, 256, 256, 256, 1e-3, 0.95, 1000, precision or 32, axes=(0, 1))
+    elif which == "iris_guide":
+        s = iris_guide2d("iris_guide", 305, precision or 32, irises=True)
+    elif which == "iris_guide_empty":
+        s = iris_guide2d("iris_guide_empty", 305, precision or 32, irises=False)
     elif which == "lossy2d":
         s = lossy_box("lossy2d", 303, 2, 90, 61, 1, 1e-3, 0.95, 500, precision or 64, axes=(0, 1))
     elif which == "rom2d":

@@ -87,3 +87,36 @@ def test_lossy_unsupported_paths_fail_loudly(monkeypatch):
     monkeypatch.setenv("FDTD_STENCIL_OLD", "1")       # the reference stencils carry no ca term
     with pytest.raises(FdtdError):
         Sim(prob, precision=32)
+
+
+def test_iris_waveguide_s21_within_one_db_of_oracle():
+    # the S-parameter workload of NEXT-2 (stands in for P:515-527, SPEC acceptance
+    # S:557 "waveguide S21 <= 1 dB"): the absorber-terminated 2-D iris guide and
+    # its empty twin, 20,000 steps in fp32 on the GPU; S21 = spectrum of the line
+    # probe behind the irises over the empty guide's (host post-processing)
+    from paper_1406_7042_b200 import prep
+
+    def series(which, gpu):
+        scn = scenario(which, precision=32)
+        prob, _ = prep.build_problem(scn, precision=32)
+        n = scn["n_steps"]
+        if gpu:
+            return run_gpu(prob, n, precision=32)["probes"][:, :, 0], scn
+        from oracle import problem_step as ps
+        return ps.run(prob, n)[2], scn
+
+    out = {}
+    for which in ("iris_guide", "iris_guide_empty"):
+        g, scn = series(which, True)
+        o, _ = series(which, False)
+        for p in range(o.shape[1]):
+            assert parity.rel_l2(g[:, p], o[:, p], f"{which} probe{p}") <= 1e-4
+        out[which] = (g[:, 0], o[:, 0])
+    f = np.fft.rfftfreq(scn["n_steps"], scn["dt"])
+    s21 = [np.fft.rfft(out["iris_guide"][k]) / np.fft.rfft(out["iris_guide_empty"][k]) for k in (0, 1)]
+    band = (f >= 2.0e9) & (f <= 3.0e9)
+    db_g, db_o = (20 * np.log10(np.abs(s[band])) for s in s21)
+    seen = db_o > -40.0
+    assert seen.sum() >= 10 and db_o.max() > -10.0 and db_o.min() < -40.0     # a pass band and stop bands
+    assert np.max(np.abs(db_g[seen] - db_o[seen])) <= 1.0
+    assert db_g.max() <= 0.1                                                   # passive
