@@ -221,6 +221,16 @@ int32_t fdtd_path(const fdtd_t* h);
 int fdtd_profile(fdtd_t* h, int32_t enable);
 int fdtd_phase_times(fdtd_t* h, double* ms, int32_t n);
 
+/* Halo exchange of a slab decomposition along z: copy
+ * z-plane k (0..nz) of coarse component `which` (0..5) between the state and a
+ * caller-owned DEVICE buffer of (ny+1)(nx+1)*batch values of the run precision,
+ * layout [ny+1][nx+1][batch], on the handle's stream (asynchronous; ordered
+ * after the steps enqueued so far).  dir 0: state -> buffer, 1: buffer ->
+ * state.  3-D only.  paper_1406_7042_b200/dist.py (SlabSim) drives it: each
+ * rank owns a slab with one ghost cell layer per internal side and receives
+ * the tangential H of that layer after every step. */
+int fdtd_plane_device(fdtd_t* h, int32_t which, int32_t k, void* dev_buf, int32_t dir);
+
 void fdtd_destroy(fdtd_t* h);
 const char* fdtd_last_error(void);
 int fdtd_version(void);

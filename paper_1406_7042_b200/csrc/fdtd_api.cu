@@ -87,6 +87,7 @@ struct fdtd_t {
   virtual int sync() = 0;
   virtual int set_profile(int on) = 0;
   virtual int phase_times(double* ms, int n) = 0;
+  virtual int plane_io(int which, int k, void* buf, int dir) = 0;
   int64_t launches = 0;
   int32_t path_bits = 0;
 };
@@ -263,6 +264,18 @@ struct Impl : public fdtd_t {
       for (auto& e : ev) CK(cudaEventCreate(&e));
     prof = on != 0;
     for (int i = 0; i < NPHASE; ++i) { phase_ms[i] = 0; phase_n[i] = 0; }
+    return FDTD_OK;
+  }
+  // one z-plane of a coarse component <-> a contiguous device buffer [ny+1][nx+1][B]
+  // (halo exchange of the slab decomposition, fdtd.h fdtd_plane_device)
+  int plane_io(int which, int k, void* buf, int dir) override {
+    if (dim != 3) return fail(FDTD_ENOTSUP, "fdtd_plane_device: 3-D problems only");
+    if (which < 0 || which > 5 || k < 0 || k > nz || !buf || (dir != 0 && dir != 1))
+      return fail(FDTD_EINVAL, "fdtd_plane_device: bad component / plane / buffer / direction");
+    T* f = F[(int)(host_step & 1)][which] + (int64_t)k * plane * B;
+    const size_t w = (size_t)(nx + 1) * B * sizeof(T), pitch = (size_t)px * B * sizeof(T);
+    if (dir == 0) CK(cudaMemcpy2DAsync(buf, w, f, pitch, w, (size_t)(ny + 1), cudaMemcpyDeviceToDevice, stream));
+    else CK(cudaMemcpy2DAsync(f, pitch, buf, w, w, (size_t)(ny + 1), cudaMemcpyDeviceToDevice, stream));
     return FDTD_OK;
   }
   int phase_times(double* ms, int n) override {
@@ -2239,6 +2252,9 @@ int32_t fdtd_path(const fdtd_t* h) { return h ? h->path_bits : 0; }
 int fdtd_profile(fdtd_t* h, int32_t enable) { return h ? h->set_profile(enable) : fail(FDTD_EINVAL, "null handle"); }
 int fdtd_phase_times(fdtd_t* h, double* ms, int32_t n) {
   return h ? h->phase_times(ms, n) : fail(FDTD_EINVAL, "null handle");
+}
+int fdtd_plane_device(fdtd_t* h, int32_t which, int32_t k, void* dev_buf, int32_t dir) {
+  return h ? h->plane_io(which, k, dev_buf, dir) : fail(FDTD_EINVAL, "null handle");
 }
 void fdtd_destroy(fdtd_t* h) {
   if (h) {

@@ -109,6 +109,8 @@ def load_library(path: str = LIB_PATH):
     lib.fdtd_profile.restype = C.c_int
     lib.fdtd_phase_times.argtypes = [C.c_void_p, _f64p, C.c_int32]
     lib.fdtd_phase_times.restype = C.c_int
+    lib.fdtd_plane_device.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32]
+    lib.fdtd_plane_device.restype = C.c_int
     lib.fdtd_destroy.argtypes = [C.c_void_p]
     lib.fdtd_destroy.restype = None
     lib.fdtd_last_error.argtypes = []
@@ -120,7 +122,8 @@ def load_library(path: str = LIB_PATH):
 
 
 EXPORTED_SYMBOLS = ("fdtd_create", "fdtd_step", "fdtd_probe", "fdtd_get_state", "fdtd_set_state",
-                    "fdtd_sync", "fdtd_launch_count", "fdtd_path", "fdtd_profile", "fdtd_phase_times", "fdtd_destroy",
+                    "fdtd_sync", "fdtd_launch_count", "fdtd_path", "fdtd_profile", "fdtd_phase_times", "fdtd_plane_device",
+                    "fdtd_destroy",
                     "fdtd_last_error", "fdtd_version")
 PHASES = ("stencil", "reduced", "reduced_grid")
 
@@ -330,6 +333,10 @@ class Sim:
         d = dict(zip(PHASES, out[:len(PHASES)].tolist()))
         d["steps"] = int(out[-1])
         return d
+
+    def plane_device(self, which, k, dev_ptr, to_state):
+        """z-plane k of coarse component ``which`` <-> a device buffer (asynchronous)."""
+        _check(self.lib.fdtd_plane_device(self.h, int(which), int(k), C.c_void_p(int(dev_ptr)), 1 if to_state else 0))
 
     def launch_count(self):
         return int(self.lib.fdtd_launch_count(self.h))
