@@ -50,6 +50,20 @@ int set_error(int code, const char* msg) { return fail(code, "%s", msg); }
 }  // namespace fdtd
 namespace {
 
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per function, not per handle:
+// handles with different shared-memory needs coexist (slab decomposition, the
+// tests), so a function's limit only ever grows.
+template <typename F>
+cudaError_t raise_smem_limit(F fn, int bytes) {
+  static std::map<const void*, int> seen;
+  int& cur = seen[(const void*)fn];
+  if (bytes <= cur) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+
 #define CK(call)                                                                   \
   do {                                                                             \
     cudaError_t e_ = (call);                                                       \
@@ -1161,18 +1175,18 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
     }
   }
   if (fused_gemm && fused_smem > 48 * 1024) {
-    CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 4, gemm_rpw(4), GEMM_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
-    CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 8, gemm_rpw(8), GEMM_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
-    CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 16, gemm_rpw(16), GEMM_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
-    CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), GEMM_KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
-    CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
-    CK(cudaFuncSetAttribute(fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+    CK(raise_smem_limit(fdtd::reduced_gemm_kernel<T, 4, gemm_rpw(4), GEMM_KS>, (int)fused_smem));
+    CK(raise_smem_limit(fdtd::reduced_gemm_kernel<T, 8, gemm_rpw(8), GEMM_KS>, (int)fused_smem));
+    CK(raise_smem_limit(fdtd::reduced_gemm_kernel<T, 16, gemm_rpw(16), GEMM_KS>, (int)fused_smem));
+    CK(raise_smem_limit(fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), GEMM_KS>, (int)fused_smem));
+    CK(raise_smem_limit(fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), 2>, (int)fused_smem));
+    CK(raise_smem_limit(fdtd::reduced_gemm_kernel<T, 32, gemm_rpw(32), 8>, (int)fused_smem));
   }
   if (!fused_gemm && fused_smem > 48 * 1024) {
-    CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
-    CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
-    CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
-    CK(cudaFuncSetAttribute(fdtd::reduced_fused_kernel<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fused_smem));
+    CK(raise_smem_limit(fdtd::reduced_fused_kernel<T, 1>, (int)fused_smem));
+    CK(raise_smem_limit(fdtd::reduced_fused_kernel<T, 4>, (int)fused_smem));
+    CK(raise_smem_limit(fdtd::reduced_fused_kernel<T, 16>, (int)fused_smem));
+    CK(raise_smem_limit(fdtd::reduced_fused_kernel<T, 32>, (int)fused_smem));
   }
   {
     int e = setup_persist();
@@ -1306,7 +1320,7 @@ int Impl<T>::setup_persist() {
       sm = std::max(tile_sm, sizeof(T) * ((size_t)(1 + r) * Cmax + (size_t)r * 32) + 64 +
                                  (sizeof(T) == 4 ? (size_t)r * 32 * 8 + 32 + (size_t)r * Cmax * 2 : 0));
       if (sm > 220 * 1024) continue;
-      CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      CK(raise_smem_limit(kfn, (int)sm));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, nthr, sm));
       nr = (Rtot + r - 1) / r;
       if (per_sm * nsm < nt + nr) continue;
@@ -1766,6 +1780,7 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
           rows.n_wave, rows.n_src, ds, lossy ? 1 : 0);
     else
       fdtd::rows_prepass_kernel<T><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, B, F0, F1, y_all, ds);
+    CK(cudaGetLastError());
     ++n;
   }
   if (dim == 3 && use_tile && sp) {

@@ -53,6 +53,12 @@ bool tile_supported(const TileCfg& c) {
 template <typename T>
 cudaError_t tile_prepare(const TileCfg& c, size_t smem) {
   cudaError_t err = cudaErrorInvalidValue;
+  // the attribute is per function, not per handle: several handles with different
+  // table sizes coexist (slab decomposition), so always allow the device maximum
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) == cudaSuccess && (size_t)optin > smem)
+    smem = (size_t)optin;
   tile_dispatch<T>(c, [&](auto K) {
     err = cudaFuncSetAttribute(K.uni, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err == cudaSuccess) err = cudaFuncSetAttribute(K.mat, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -71,7 +77,7 @@ cudaError_t tile_launch(const TileCfg& c, bool uniform, int grid, size_t smem, c
     const auto fn = uniform ? K.uni : (taba ? K.lossy : K.mat);
     fn<<<grid, dim3(32, c.BY), smem, st>>>(tm, split, d, F0, F1, mat_id, tab, ifm, n_mat, u0, u1, rows, y, ds,
                                           check_every, bad, taba);
-    err = cudaSuccess;
+    err = cudaGetLastError();
   });
   return err;
 }

@@ -280,7 +280,8 @@ class Sim:
                         return torch.cuda.caching_allocator_alloc(int(nbytes), dev, st)
 
                     def _free(ptr, ctx):
-                        torch.cuda.caching_allocator_delete(ptr)
+                        if torch is not None and getattr(torch, "cuda", None) is not None:   # interpreter teardown
+                            torch.cuda.caching_allocator_delete(ptr)
                     self._torch_cbs = (ALLOC_FN(_alloc), FREE_FN(_free))
                     ex.alloc, ex.free = self._torch_cbs
         except ImportError:
