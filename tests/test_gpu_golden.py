@@ -72,10 +72,23 @@ def golden_report(config, prec, members, golden_prec=None, **sim_kw):
     from make_golden import apply_model
     prob = apply_model(prob, golds[members[0]])
     fp = _fingerprint(prob)
+    same_model = True
     for m, g in golds.items():
-        # the same problem description (F13) as the golden's: checksums agree
-        # to rounding (the host LAPACK may differ from the golden's machine)
-        assert np.allclose(fp, g["fingerprint"], rtol=1e-11, atol=0), (fp, g["fingerprint"])
+        # the same problem description (F13) as the golden's: checksums agree to
+        # rounding.  Entries 2, 3 are the reduced matrices: when the golden does
+        # not carry them (config 4: S_E is 266 MB, it lives in the prep cache)
+        # and the prep was re-run on another LAPACK build, the projection basis
+        # may differ by signs / rotations within the Krylov space -- the same
+        # model in other coordinates.  Then the reduced states (coordinates in
+        # that basis) are not comparable; every physical subset (coarse sample,
+        # interface rows, probe series, norm) still is, and is still checked.
+        gf = g["fingerprint"]
+        rest = [0, 1, 4, 5, 6, 7]
+        assert np.allclose(fp[rest], gf[rest], rtol=1e-11, atol=0), (fp, gf)
+        same_model &= bool(np.allclose(fp[2:4], gf[2:4], rtol=1e-11, atol=0))
+    if not same_model:
+        assert "blk0_K" not in golds[members[0]], "embedded model differs from the fingerprint"
+        print(f"config {config}: reduced model rebuilt in another basis; reduced-state subsets skipped")
     n_steps = int(json.loads(str(golds[members[0]]["meta"]))["n_steps"])
     sim = Sim(prob, precision=prec, graph_steps=sim_kw.pop("graph_steps", 32), **sim_kw)
     for c, a in (prob.get("init") or {}).items():
@@ -111,8 +124,9 @@ def golden_report(config, prec, members, golden_prec=None, **sim_kw):
         if len(sh):
             ge = reduced_member(red_e, sh, B, m, "e")
             gh = reduced_member(red_h, sh, B, m, "h")
-            subsets["red_e"] = (ge, g["red_e"])
-            subsets["red_h"] = (gh, g["red_h"])
+            if same_model:
+                subsets["red_e"] = (ge, g["red_e"])
+                subsets["red_h"] = (gh, g["red_h"])
             got[m]["sq"] += float(np.sum(ge ** 2) + np.sum(gh ** 2))
         for p in range(g["probes"].shape[1]):
             subsets[f"probe{p}"] = (probes[:, p, m], g["probes"][:, p])
