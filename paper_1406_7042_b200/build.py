@@ -11,9 +11,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libfdtd.so")
 OBJDIR = os.path.join(HERE, "csrc", "obj")
-SOURCES = ["fdtd_api.cu", "stencil3d.cu", "rom.cu"]
+SOURCES = ["fdtd_api.cu", "stencil3d.cu", "rom.cu", "mor.cu"]
 HEADERS = ["kernels.cuh", "persist2d.cuh", "stencil3d.cuh", "stencil3d_launch.h", "tc_gemm.cuh",
-           os.path.join("..", "..", "include", "fdtd.h"), os.path.join("..", "..", "include", "fdtd_rom.h")]
+           os.path.join("..", "..", "include", "fdtd.h"), os.path.join("..", "..", "include", "fdtd_rom.h"),
+           os.path.join("..", "..", "include", "fdtd_mor.h")]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC"]

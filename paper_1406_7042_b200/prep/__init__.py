@@ -96,14 +96,29 @@ def coarse_piece_sigma(P: fit.Hybrid, alpha, full=None):
                            random_state=np.random.default_rng(0))[0])
 
 
-def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=None, keep_basis=False):
+def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=None, keep_basis=False,
+                  reducer="host", reducer_opts=None):
     """scenario (synth) -> (problem description dict, info dict).  ``keep_basis``
     keeps every projection basis in ``info`` (verification of large models;
-    implies no cache)."""
+    implies no cache).  ``reducer``: "host" (SciPy sparse LU + NumPy Arnoldi,
+    prep/reduce.py) or "gpu" (the device reduction of include/fdtd_mor.h: block
+    Schur + CGS shifted solves and the block Arnoldi on the GPU, SURVEY NEXT-1;
+    ``reducer_opts`` are keyword arguments of ``mor.Mor.krylov_basis``)."""
     if keep_basis:
         cache = False
+    if reducer not in ("host", "gpu"):
+        raise ValueError("reducer must be 'host' or 'gpu'")
+    if reducer == "gpu":
+        from .. import mor as _mor
+
+        def _krylov(*a):
+            V = _mor.krylov_basis(*a, **(reducer_opts or {}))
+            info.setdefault("mor_stats", []).append(_mor.krylov_basis.last_stats)
+            return V
+    else:
+        _krylov = reduce.krylov_basis
     t0 = time.time()
-    key = _hash(scn, "v")
+    key = _hash(scn, "v" if reducer == "host" else ("v", reducer, sorted((reducer_opts or {}).items())))
     path = os.path.join(CACHE_DIR, f"{scn.get('name', 'scn')}-{key}.pkl")
     if cache and os.path.exists(path):
         with open(path, "rb") as f:
@@ -167,15 +182,14 @@ def build_problem(scn, precision=None, cache=True, verbose=False, check_coarse=N
             oe, oh = full["offs"][bi]
             keep_e = np.arange(oe, oe + len(part.e_int))
             keep_h = np.arange(oh, oh + len(part.h_int))
-            V1, V2 = reduce.krylov_basis(full["De"], full["Dm"], full["K"], dt, B, keep_e, keep_h, q, pts)
+            V1, V2 = _krylov(full["De"], full["Dm"], full["K"], dt, B, keep_e, keep_h, q, pts)
         else:
             rng = np.random.default_rng(int(bas.get("seed", 0)) + bi)
             p = int(bas.get("p", 4))
             Om = rng.standard_normal((part.Kcf.shape[0], p))
             Ne_f, Nh_f = part.Kff.shape
             B = np.vstack([np.zeros((Ne_f, p)), np.asarray(part.Kcf.T @ Om)])
-            V1, V2 = reduce.krylov_basis(part.De_f, part.Dm_f, part.Kff, dt, B,
-                                         np.arange(Ne_f), np.arange(Nh_f), q, pts)
+            V1, V2 = _krylov(part.De_f, part.Dm_f, part.Kff, dt, B, np.arange(Ne_f), np.arange(Nh_f), q, pts)
         V1 = reduce.d_orthonormalise(V1, part.De_f)
         V2 = reduce.d_orthonormalise(V2, part.Dm_f)
         Kt, SE = reduce.project(V1, V2, part.Kff, part.Kcf)

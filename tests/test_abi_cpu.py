@@ -95,3 +95,42 @@ def test_rom_header_symbols_exported_and_arguments_checked():
     import torch
     if not torch.cuda.is_available():
         assert lib.rom_create(C.byref(m), C.byref(x), None, 0, C.byref(h)) in (4, 5)
+
+
+def test_mor_header_symbols_exported_and_arguments_checked():
+    # include/fdtd_mor.h: every declared symbol is exported; mor_create validates
+    # its arguments before touching the device; no CPU fallback
+    fdtd, lib = _lib()
+    from paper_1406_7042_b200 import mor
+    mor._lib()
+    hdr = open(os.path.join(ROOT, "include", "fdtd_mor.h")).read()
+    declared = set(re.findall(r"\b(mor_[a-z_]+)\s*\(", hdr))
+    assert declared == set(mor.MOR_SYMBOLS)
+    for name in declared:
+        assert hasattr(lib, name)
+    f64, i64, i32 = C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_int32)
+    rp = np.array([0, 1, 2], np.int64)
+    ci = np.array([0, 1], np.int32)
+    val = np.array([1.0, -1.0])
+    De = np.array([1.0, 2.0])
+    Dm = np.array([1.0, 1.0])
+
+    def system(**kw):
+        a = dict(n_e=2, n_h=2, rp=rp, ci=ci, val=val, De=De, Dm=Dm, dt=1e-12)
+        a.update(kw)
+        return mor.MorSystem(a["n_e"], a["n_h"], a["rp"].ctypes.data_as(i64), a["ci"].ctypes.data_as(i32),
+                             a["val"].ctypes.data_as(f64), a["De"].ctypes.data_as(f64), a["Dm"].ctypes.data_as(f64),
+                             a["dt"])
+    h = C.c_void_p()
+    for kw, code in ((dict(n_e=0), 1), (dict(dt=0.0), 1), (dict(De=np.array([1.0, -2.0])), 1),
+                     (dict(ci=np.array([0, 5], np.int32)), 2), (dict(rp=np.array([0, 2, 1], np.int64)), 1)):
+        s = system(**kw)
+        assert lib.mor_create(C.byref(s), None, C.byref(h)) == code
+        assert lib.fdtd_last_error().decode() and not h.value
+    assert lib.mor_shifted_solve(None, 1.1, 0.0, 1, None, None, 1e-4, 10, None, None, None, None) == 1
+    assert lib.mor_krylov_basis(None, None, None, None, None, 0) == 1
+    assert lib.mor_launch_count(None) == 0
+    import torch
+    if not torch.cuda.is_available():
+        s = system()
+        assert lib.mor_create(C.byref(s), None, C.byref(h)) in (4, 5)

@@ -31,6 +31,29 @@ GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 TOL = {64: 1e-12, 32: 1e-4}
 TOL_MAX = {64: 1e-11, 32: 1e-3}
 
+GAMMA = 0.9999      # P:297, the enforcement's margin (prep.reduce.GAMMA)
+
+
+def edge_tolerance(prec, n_steps):
+    """Relative L2 bar of the refined-region subsets (interface rows; the reduced
+    state [e~; h~], one vector: with D-orthonormal bases |e~|^2 + |h~|^2 is twice
+    the block's discrete energy, and it swings between the two halves every
+    half period, so each half alone passes through zero).  DESIGN.md R15: the
+    modes the enforcement clips to sigma' = gamma 2/dt sit at
+    theta = pi - 2 sqrt(1 - gamma^2), where the leap-frog map is nearly
+    defective; state rounding noise u per step enters them amplified by
+    1 / sqrt(1 - gamma^2) = 70.7 and random-walks over the run, a floor of
+    1.5 u sqrt(n) / sqrt(1 - gamma^2) that no fp32 arithmetic choice changes
+    (measured on config 4: tensor-core, SIMT fp32 and fp64-accumulating
+    products, fp32 or fp32-pair K~' all give the same error, all of it in the
+    clipped modes; profiles/r02/c4_fp32_drift.txt).  fp64 keeps the north
+    star's 1e-12."""
+    if prec == 64:
+        return TOL[64]
+    u = 2.0 ** -24
+    return max(TOL[32], 1.5 * u * np.sqrt(n_steps) / np.sqrt(1.0 - GAMMA ** 2))
+
+
 CASES = [(2, 32, (0,)), (3, 64, (0,)), (3, 32, (0,)), (5, 32, (0,)), (4, 32, (0, 15))]
 
 
@@ -127,6 +150,7 @@ def golden_report(config, prec, members, golden_prec=None, **sim_kw):
             if same_model:
                 subsets["red_e"] = (ge, g["red_e"])
                 subsets["red_h"] = (gh, g["red_h"])
+                subsets["reduced"] = (np.concatenate([ge, gh]), np.concatenate([g["red_e"], g["red_h"]]))
             got[m]["sq"] += float(np.sum(ge ** 2) + np.sum(gh ** 2))
         for p in range(g["probes"].shape[1]):
             subsets[f"probe{p}"] = (probes[:, p, m], g["probes"][:, p])
@@ -149,8 +173,16 @@ def test_full_run_against_oracle_golden(config, prec, members):
     print(f"config {config} fp{prec} ({n_steps} steps, paths {paths}):",
           json.dumps({k: [float(f"{v[0]:.3e}"), float(f"{v[1]:.3e}")] for k, v in report.items()}))
     tol, tmax = TOL[prec], TOL_MAX[prec]
-    bad = {k: v for k, v in report.items() if v[0] > tol or v[1] > tmax}
-    assert not bad, (bad, paths)
+    edge = edge_tolerance(prec, n_steps)
+    bad = {}
+    for k, v in report.items():
+        name = k.split(".", 1)[1]
+        if name in ("red_e", "red_h"):
+            continue                      # reported; judged together as "reduced" (R15)
+        t = edge if name in ("interface", "reduced") else tol
+        if v[0] > t or v[1] > tmax * t / tol:
+            bad[k] = v
+    assert not bad, (bad, paths, edge)
 
 
 def test_config2_fp64_run_against_golden():
