@@ -205,6 +205,8 @@ int64_t fdtd_launch_count(const fdtd_t* h);
  *   8  leap-frog GEMV path for at least one large reduced block
  *  16  the 3-D tile stencil (W elements per thread, NS-plane TMA ring; with bit 2)
  *  32  tensor-core (tcgen05, 3xTF32) GEMM for y = S_E h~ of a batched leap-frog block
+ *  64  explicit rows of the next step evaluated inside the batched reduced GEMM (no pre-pass
+ *      launch in steady state; FDTD_NO_ROWFUSE=1 turns it off)
  * Environment overrides (testing): FDTD_PERSIST=0, FDTD_NO_TMA,
  * FDTD_FUSED=gemv|gemm, FDTD_KCHUNK=<planes>, FDTD_STENCIL_OLD=1 (the
  * reference TMA stencils instead of the tile stencil), FDTD_TILE=<W>,<NS>, FDTD_NO_TC=1

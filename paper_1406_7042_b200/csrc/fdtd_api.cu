@@ -256,6 +256,16 @@ struct Impl : public fdtd_t {
   // split step: the stencil items of the columns that hold
   // interface rows run first, the reduced update runs on a second stream
   // beside the rest of the stencil
+  // explicit rows fused into the reduced GEMM: the thread of
+  // reduced_gemm_kernel that finalises a y element evaluates that element's
+  // explicit row of the NEXT step, so the pre-pass launch disappears in steady
+  // state.  rows_ahead: the rows of the step about to run are already evaluated
+  // (false after create / set_state / fdtd_plane_device writes / a profiled step)
+  bool fuse_rows = false, rows_ahead = false;
+  T* g_alt = nullptr;                  // G of the other step parity (the reduced kernel reads one, writes the next)
+  int32_t* y_row_d = nullptr;          // [y_size / B] explicit row of each y element (-1: none)
+  int32_t* src_rows_d = nullptr;       // explicit rows without a y term
+  int n_src_rows = 0;
   bool split = false;
   int n_ifc = 0;                       // interface columns (first in colperm)
   int* colperm_d = nullptr;
@@ -289,7 +299,10 @@ struct Impl : public fdtd_t {
     T* f = F[(int)(host_step & 1)][which] + (int64_t)k * plane * B;
     const size_t w = (size_t)(nx + 1) * B * sizeof(T), pitch = (size_t)px * B * sizeof(T);
     if (dir == 0) CK(cudaMemcpy2DAsync(buf, w, f, pitch, w, (size_t)(ny + 1), cudaMemcpyDeviceToDevice, stream));
-    else CK(cudaMemcpy2DAsync(f, pitch, buf, w, w, (size_t)(ny + 1), cudaMemcpyDeviceToDevice, stream));
+    else {
+      CK(cudaMemcpy2DAsync(f, pitch, buf, w, w, (size_t)(ny + 1), cudaMemcpyDeviceToDevice, stream));
+      rows_ahead = false;
+    }
     return FDTD_OK;
   }
   int phase_times(double* ms, int n) override {
@@ -367,6 +380,10 @@ struct Impl : public fdtd_t {
   int setup_persist();
   int launch_persist(int64_t n, int64_t* count);
   int build_fused(const fdtd_probes* probes);
+  int prepass(int p, cudaStream_t st);
+  // G of the step of parity p: one buffer, or two with fused rows (the reduced
+  // kernel reads this step's while it writes the next step's)
+  T* g_of(int p) const { return (fuse_rows && p) ? g_alt : g_all; }
   int prologue(cudaStream_t st);
   int launch_step(int parity, cudaStream_t st, int64_t* count, bool profile = false);
   int step(int64_t n) override;
@@ -945,6 +962,22 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
         fdtd::RowPackR<T>* prd = dalloc<fdtd::RowPackR<T>>(nr);
         if (!rowpack_i || !prd || upload(rowpack_i, pi) || upload(prd, pr)) return FDTD_ECUDA;
         rowpack_r = prd;
+        // inverse map y element -> explicit row (one row per y element and member block)
+        bool inv_ok = (y_size % B) == 0;
+        std::vector<int32_t> yrow((size_t)std::max<int64_t>(y_size / B, 1), -1), srows;
+        for (int64_t r = 0; r < nr && inv_ok; ++r) {
+          if (yo[r] < 0) { srows.push_back((int32_t)r); continue; }
+          if (yo[r] % B != 0 || yo[r] / B >= (int64_t)yrow.size() || yrow[yo[r] / B] != -1) { inv_ok = false; break; }
+          yrow[yo[r] / B] = (int32_t)r;
+        }
+        if (inv_ok) {
+          y_row_d = dalloc<int32_t>(yrow.size());
+          src_rows_d = dalloc<int32_t>(std::max<size_t>(srows.size(), 1));
+          g_alt = dalloc<T>(std::max<int64_t>(y_size, 1));
+          if (!y_row_d || !src_rows_d || !g_alt || upload(y_row_d, yrow) || upload(src_rows_d, srows)) return FDTD_ECUDA;
+          CK(cudaMemsetAsync(g_alt, 0, sizeof(T) * std::max<int64_t>(y_size, 1), stream));
+          n_src_rows = (int)srows.size();
+        }
       }
     }
     for (int c = 0; c < 3; ++c) rows.row_of[c] = nullptr;
@@ -1194,8 +1227,13 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
   }
   bool any_tc = false;
   for (auto& D : blocks) any_tc |= D.tc;
+  // explicit rows fused into the reduced GEMM: 3-D tile path, every block in
+  // reduced_gemm_kernel, packed rows with an inverse y map
+  fuse_rows = dim == 3 && use_tile && !split && fused_gemm && !any_leap && any_fused && n_ctas > 0 && rowpack_i &&
+              y_row_d && g_alt && !getenv("FDTD_NO_ROWFUSE");
+  rows_ahead = false;
   path_bits = (persist ? 1 : 0) | (use_tma ? 2 : 0) | (fused_gemm ? 4 : 0) | (any_leap ? 8 : 0) | (use_tile ? 16 : 0) |
-              (any_tc ? 32 : 0);
+              (any_tc ? 32 : 0) | (fuse_rows ? 64 : 0);
   CK(cudaStreamSynchronize(stream));
   return FDTD_OK;
 }
@@ -1749,6 +1787,23 @@ int Impl<T>::prologue(cudaStream_t st) {
   return FDTD_OK;
 }
 
+// The explicit rows of the step of parity p (rows_prepass_*_kernel): E^{n+1} of
+// every interface / source row into the new parity, G published.
+template <typename T>
+int Impl<T>::prepass(int p, cudaStream_t st) {
+  fdtd::Fields<T> F0, F1;
+  for (int c = 0; c < 6; ++c) { F0.f[c] = F[p][c]; F1.f[c] = F[p ^ 1][c]; }
+  const int64_t nt = rows.n_rows * B;
+  if (rowpack_i)
+    fdtd::rows_prepass_packed_kernel<T><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(
+        rows.n_rows, rowpack_i, (const fdtd::RowPackR<T>*)rowpack_r, B, F0, F1, y_all, g_of(p), rows.wave,
+        rows.n_wave, rows.n_src, d_step + p, lossy ? 1 : 0);
+  else
+    fdtd::rows_prepass_kernel<T><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, B, F0, F1, y_all, d_step + p);
+  CK(cudaGetLastError());
+  return FDTD_OK;
+}
+
 template <typename T>
 int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   int64_t n = 0;
@@ -1771,16 +1826,11 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
     SB.col0 = n_ifc; SB.ncols = tsplit.ncols - n_ifc; SB.nitems = SB.ncols * nch;
   }
   const cudaStream_t rs = sp ? st2 : st;    // the reduced update's stream
-  if (dim == 3 && use_tile && rows.n_rows > 0) {
+  if (dim == 3 && use_tile && rows.n_rows > 0 && !(fuse_rows && rows_ahead)) {
     // explicit rows first: the tile stencil reads their E^{n+1} back from the new parity
-    const int64_t nt = rows.n_rows * B;
-    if (rowpack_i)
-      fdtd::rows_prepass_packed_kernel<T><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(
-          rows.n_rows, rowpack_i, (const fdtd::RowPackR<T>*)rowpack_r, B, F0, F1, y_all, rows.g_out, rows.wave,
-          rows.n_wave, rows.n_src, ds, lossy ? 1 : 0);
-    else
-      fdtd::rows_prepass_kernel<T><<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(rows, B, F0, F1, y_all, ds);
-    CK(cudaGetLastError());
+    // (with fused rows only when the previous step's reduced kernel has not done it)
+    int e = prepass(p, st);
+    if (e) return e;
     ++n;
   }
   if (dim == 3 && use_tile && sp) {
@@ -1906,7 +1956,15 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   P.e_in = eb[p]; P.e_out = eb[p ^ 1];
   P.h_in = hb[p]; P.h_out = hb[p ^ 1];
   P.y = y_all;
-  P.G = g_all;
+  P.G = g_of(p);
+  P.fuse_rows = fuse_rows ? 1 : 0;
+  if (fuse_rows) {
+    P.lossy_rows = lossy ? 1 : 0;
+    P.rp_i = rowpack_i; P.rp_r = rowpack_r; P.y_row = y_row_d; P.src_rows = src_rows_d; P.n_src_rows = n_src_rows;
+    P.Fn0 = F1; P.Fn1 = F0;
+    P.g_next = g_of(p ^ 1);
+    P.wave = rows.wave; P.n_wave = rows.n_wave; P.n_wsrc = rows.n_src;
+  }
   P.rows_per_cta = rows_per_cta;
   P.red_base[0] = eb[0];      // leap-frog blocks (fused blocks' probes are matrix rows)
   P.red_base[1] = hb[0];
@@ -1970,6 +2028,7 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   }
   mark(1, 1);
   CK(cudaGetLastError());
+  if (fuse_rows) rows_ahead = true;          // the reduced kernel evaluated the next step's rows
   if (profile) {
     CK(cudaEventSynchronize(ev[3]));
     for (int ph = 0; ph < NPHASE; ++ph) {
@@ -2031,6 +2090,13 @@ int Impl<T>::step(int64_t n) {
     while (done < chunk) {
       const int64_t left = chunk - done;
       if (!prof && graph_steps > 0 && (host_step & 1) == 0 && left >= graph_steps) {
+        if (fuse_rows && !rows_ahead) {
+          // the captured steps carry no pre-pass: evaluate the first step's rows here
+          int e = prepass((int)(host_step & 1), stream);
+          if (e) return e;
+          ++launches;
+          rows_ahead = true;
+        }
         if (!graph) {
           cudaStream_t cs;
           CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
@@ -2138,6 +2204,7 @@ int Impl<T>::get_state(int which, double* out, int64_t n) {
 template <typename T>
 int Impl<T>::set_state(int which, const double* in, int64_t n) {
   CK(cudaStreamSynchronize(stream));
+  rows_ahead = false;
   const int p = (int)(host_step & 1);
   if (which >= 0 && which <= 5) {
     if (n != S * B) return fail(FDTD_EINVAL, "set_state: n must be batch*S");

@@ -145,15 +145,15 @@ struct RowPackR {          // 32 (fp32) / 64 (fp64) bytes
   T a;                     // ca of the row's unknown (1 when lossless)
 };
 
+// One packed explicit row of member b: E^{n+1} from the old parity F0, the y
+// value yv (ignored without a y term) and the step's source sample; stored
+// into the new parity F1 and published to g_out.
 template <typename T>
-__global__ void __launch_bounds__(256)
-rows_prepass_packed_kernel(int64_t n_rows, const RowPackI* __restrict__ RI, const RowPackR<T>* __restrict__ RR,
-                           int B, Fields<T> F0, Fields<T> F1, const T* __restrict__ y, T* __restrict__ g_out,
-                           const T* __restrict__ wave, int64_t n_wave, int64_t n_src,
-                           const int64_t* __restrict__ d_step, int lossy) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_rows * B) return;
-  const int r = (int)(t / B), b = (int)(t % B);
+__device__ __forceinline__ void packed_row_eval(int r, int b, T yv, const RowPackI* __restrict__ RI,
+                                                const RowPackR<T>* __restrict__ RR, int B, const Fields<T>& F0,
+                                                const Fields<T>& F1, T* __restrict__ g_out,
+                                                const T* __restrict__ wave, int64_t n_wave, int64_t n_src,
+                                                int64_t step, int lossy) {
   const int4* pi = reinterpret_cast<const int4*>(RI + r);
   const int4 i0 = pi[0], i1 = pi[1], i2 = pi[2];
   const RowPackR<T> rr = RR[r];
@@ -167,8 +167,6 @@ rows_prepass_packed_kernel(int64_t n_rows, const RowPackI* __restrict__ RI, cons
   T h[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) h[k] = k < nt ? field((i2.x >> (8 * k)) & 0xff)[(int64_t)ho[k] * B + b] : (T)0;
-  const T yv = yo >= 0 ? y[yo + b] : (T)0;
-  const int64_t step = *d_step;
   const bool has_src = src >= 0 && step < n_wave;
   const T wv = has_src ? wave[(step * n_src + src) * B + b] : (T)0;
   T acc = 0;
@@ -181,6 +179,20 @@ rows_prepass_packed_kernel(int64_t n_rows, const RowPackI* __restrict__ RI, cons
   if (yo >= 0) g_out[yo + b] = e;
   T* o = ec == 0 ? F1.f[0] : ec == 1 ? F1.f[1] : F1.f[2];
   o[eo] = e;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+rows_prepass_packed_kernel(int64_t n_rows, const RowPackI* __restrict__ RI, const RowPackR<T>* __restrict__ RR,
+                           int B, Fields<T> F0, Fields<T> F1, const T* __restrict__ y, T* __restrict__ g_out,
+                           const T* __restrict__ wave, int64_t n_wave, int64_t n_src,
+                           const int64_t* __restrict__ d_step, int lossy) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_rows * B) return;
+  const int r = (int)(t / B), b = (int)(t % B);
+  const int yo = RI[r].y_off;
+  const T yv = yo >= 0 ? y[yo + b] : (T)0;
+  packed_row_eval<T>(r, b, yv, RI, RR, B, F0, F1, g_out, wave, n_wave, n_src, *d_step, lossy);
 }
 
 // ---------------------------------------------------------------------------
@@ -902,6 +914,20 @@ struct FusedParams {
   int nfb;
   int n_ctas, B, rows_per_cta;
   int tail_mode;                // 0: probes + step counter here; 1: divergence flag only (split step, §5.6)
+  // explicit rows of the NEXT step, evaluated by the thread that finalises their
+  // y (reduced_gemm_kernel): no pre-pass launch in steady state
+  int fuse_rows;                // 0: off
+  int lossy_rows;
+  const RowPackI* rp_i;
+  const void* rp_r;             // RowPackR<T>
+  const int32_t* y_row;         // [y elements / B] explicit row whose y term this is, -1: none
+  const int32_t* src_rows;      // explicit rows without a y term (sources off the interface)
+  int n_src_rows;
+  Fields<T> Fn0;                // next step's old parity (this step's output) ...
+  Fields<T> Fn1;                // ... and its new parity (this step's input buffers)
+  T* g_next;                    // next step's G (the other parity's buffer)
+  const T* wave;
+  int64_t n_wave, n_wsrc;
   const T* e_in; T* e_out;      // e~^{n+1} in, e~^{n+2} out
   const T* h_in; T* h_out;      // h~^{n+1/2} in, h~^{n+3/2} out
   T* y;
@@ -1230,8 +1256,19 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
       const T v = (T)vs;
       if (r >= FB.R || n >= N) continue;
       if (r < qh) P.h_out[FB.h_off + (int64_t)r * N + n] = v;
-      else if (r < qh + ni) P.y[FB.y_off + (int64_t)(r - qh) * N + n] = v;
-      else if (r < qh + ni + qe) P.e_out[FB.e_off + (int64_t)(r - qh - ni) * N + n] = v;
+      else if (r < qh + ni) {
+        const int64_t yi = FB.y_off + (int64_t)(r - qh) * N + n;
+        P.y[yi] = v;
+        if (P.fuse_rows) {
+          // this y element is final: its explicit row of the next step (the
+          // stencil of this step has finished, so H^{n+1} and E^{n+1} are final;
+          // the next step's new parity and G buffers are free)
+          const int er = P.y_row[yi / B];
+          if (er >= 0)
+            packed_row_eval<T>(er, (int)(yi % B), v, P.rp_i, reinterpret_cast<const RowPackR<T>*>(P.rp_r), B, P.Fn0,
+                               P.Fn1, P.g_next, P.wave, P.n_wave, P.n_wsrc, step + 1, P.lossy_rows);
+        }
+      } else if (r < qh + ni + qe) P.e_out[FB.e_off + (int64_t)(r - qh - ni) * N + n] = v;
       else {
         const int q = r - qh - ni - qe;
         const int p = FB.probe_id[q], in = FB.probe_inst[q];
@@ -1240,6 +1277,13 @@ reduced_gemm_kernel(const __grid_constant__ FusedParams<T> P) {
       }
       if (check && !finite_small((double)v)) bad = true;
     }
+  }
+  if (P.fuse_rows) {
+    // explicit rows without a y term (sources off the interface), spread over the grid
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)P.n_src_rows * P.B;
+         t += (int64_t)gridDim.x * blockDim.x)
+      packed_row_eval<T>(P.src_rows[t / P.B], (int)(t % P.B), (T)0, P.rp_i, reinterpret_cast<const RowPackR<T>*>(P.rp_r),
+                         P.B, P.Fn0, P.Fn1, P.g_next, P.wave, P.n_wave, P.n_wsrc, step + 1, P.lossy_rows);
   }
   // no CTA leaves (releasing its shared memory) before every rank has read it
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");

@@ -342,7 +342,8 @@ class Sim:
     def launch_count(self):
         return int(self.lib.fdtd_launch_count(self.h))
 
-    PATH_BITS = {1: "persistent2d", 2: "tma3d", 4: "fused_gemm", 8: "leapfrog", 16: "tile3d", 32: "tc_gemm"}
+    PATH_BITS = {1: "persistent2d", 2: "tma3d", 4: "fused_gemm", 8: "leapfrog", 16: "tile3d", 32: "tc_gemm",
+                 64: "fused_rows"}
 
     def path(self):
         """Kernel paths taken by step() (fdtd_path bit mask) as a list of names."""

@@ -510,3 +510,52 @@ def test_device_set_state_equals_host_set_state(case, prec, monkeypatch):
     a, b = run(True), run(False)
     for c in range(12):
         assert np.array_equal(a[c], b[c]), c
+
+
+@pytest.mark.parametrize("case,prec,graph", [("tiny5", 32, 0), ("tiny5", 32, 8), ("tiny5", 64, 8), ("tiny5", 64, 0)])
+def test_rows_fused_into_reduced_gemm_bitwise_equals_prepass(case, prec, graph, monkeypatch):
+    # the explicit rows of the next step evaluated by the reduced GEMM thread that
+    # finalises their y (no pre-pass launch in steady state)
+    # against the pre-pass launch every step: states, reduced states and probe
+    # series bit for bit -- eager and in CUDA graphs, across a set_state in the
+    # middle of the run (which invalidates the rows evaluated ahead), an odd number
+    # of steps (parity of the two G buffers) and a profiled step
+    from paper_1406_7042_b200.fdtd import Sim
+    from sampled_state import random_state
+    scn, prob = _prep(case, precision=prec)
+    prob = dict(prob, init={})
+    arrays, re_, rh_ = random_state(prob, seed=13)
+    arrays2, _, _ = random_state(prob, seed=14)
+    monkeypatch.setenv("FDTD_FUSED", "gemm")        # tiny5's few instances would take the GEMV kernel
+
+    def run(fused):
+        if fused:
+            monkeypatch.delenv("FDTD_NO_ROWFUSE", raising=False)
+        else:
+            monkeypatch.setenv("FDTD_NO_ROWFUSE", "1")
+        sim = Sim(prob, precision=prec, graph_steps=graph)
+        assert ("fused_rows" in sim.path()) == fused, sim.path()
+        for c in range(6):
+            sim.set_state(c, arrays[c])
+        sim.set_state(6, parity.gpu_reduced_order(re_, prob))
+        sim.set_state(7, parity.gpu_reduced_order(rh_, prob))
+        sim.step(19)
+        mid = [sim.get_state(c) for c in range(8)]
+        sim.set_state(3, arrays2[3])            # new Hx: the rows evaluated ahead are stale
+        sim.step(1)
+        sim.step(26)
+        sim.set_state(7, parity.gpu_reduced_order(0.5 * rh_, prob))
+        sim.step(17)
+        sim.sync()
+        out = [sim.get_state(c) for c in range(8)]
+        pr = sim.probe()
+        n = sim.launch_count()
+        sim.close()
+        return mid, out, pr, n
+
+    (ma, a, pa, na), (mb, b, pb, nb) = run(True), run(False)
+    assert na < nb
+    for c in range(8):
+        assert np.array_equal(ma[c], mb[c]), ("mid", c)
+        assert np.array_equal(a[c], b[c]), c
+    assert np.array_equal(pa, pb) and pa.shape[0] == 63
