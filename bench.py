@@ -513,6 +513,53 @@ def measure_rom(args, batch, steps=5, warmup=3, cpu=True, dmma_peak=None):
     return out
 
 
+def measure_mor(args, config=2):
+    """the Krylov basis of one refined region of ``config`` on
+    the device (mor_* calls, csrc/mor.cu: block Schur + batched CGS at the
+    paper's 1e-4, block Gram-Schmidt), timed through the public binding with
+    host buffers (uploads and the basis download included).  The host
+    preprocessing's time for the same basis is in profiles/r02/mor_bench.txt
+    (tools/mor_bench.py --host; too long for the default bench)."""
+    import torch
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
+    from mor_bench import region_system
+    from paper_1406_7042_b200 import mor as M
+    from synth import scenario
+    scn = scenario(config)
+    part, Bm, pts, q = region_system(scn)
+    Ne, Nh = part.Kff.shape
+    m = M.Mor(part.De_f, part.Dm_f, part.Kff, scn["dt"])
+    ts = []
+    for _ in range(3):
+        torch.cuda.synchronize(); w0 = time.perf_counter()
+        V1, V2, st = m.krylov_basis(Bm, np.arange(Ne), np.arange(Nh), q, pts, solve_tol=1e-4)
+        ts.append(time.perf_counter() - w0)
+    launches = m.launch_count() // 3
+    m.close()
+    t = min(ts[1:])
+    # algorithmic traffic of one CGS iteration and column (complex fp64 unless the point is real): two Schur
+    # applications (K^T: read x, write t; K: read t, x, write v) and the recursion's vector updates and dots
+    cplx = sum(1 for z in pts if complex(z).imag != 0)
+    el = 16.0 * cplx / len(pts) + 8.0 * (len(pts) - cplx) / len(pts)
+    # (CSR values and indices once per iteration of the whole block of columns)
+    per_it = el * (2 * (2 * Nh + 3 * Ne) + 17 * Ne)
+    csr = 2 * (2 * 12.0 * part.Kff.nnz + 8.0 * (Ne + Nh))
+    bytes_cgs = per_it * st["cgs_iterations"] + csr * st["cgs_iterations"] / Bm.shape[1]
+    hbm, hbm_kind = _peaks()
+    return {"value": t, "unit": "s per reduction (Krylov basis of the region, host buffers in / basis out)",
+            "higher_is_better": False, "dtype": "f64",
+            "config": {"workload": (f"config{config} region: K_ff {Ne} x {Nh} ({part.Kff.nnz} entries), {len(pts)} expansion "
+                                    f"points, block of {Bm.shape[1]}, q = {q}, CGS to 1e-4 (P:371)")},
+            "stats": st, "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": bytes_cgs / st["t_solve"] / 1e9 if st["t_solve"] > 0 else None,
+                         "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s",
+                         "frac": (bytes_cgs / st["t_solve"] / 1e9 / hbm) if st["t_solve"] > 0 else None,
+                         "traffic": None, "kernel": "batched CGS (spmm_kernel, cgs_v*, dot_partial_kernel)",
+                         "note": "13 kernels per CGS iteration of the column block, 4 iterations replayed as one "
+                                 f"CUDA graph; the solves' share of the reduction: {st['t_solve']:.2f} s of {t:.2f} s"},
+            "orth_err": [float(np.abs(V1.T @ V1 - np.eye(q)).max()), float(np.abs(V2.T @ V2 - np.eye(q)).max())]}
+
+
 def oracle_sample_worker(config, prec, seconds):
     """CPU-oracle timing of one workload in its own process (single-threaded
     SciPy), run beside the GPU measurements so the bench stays within minutes.
@@ -574,6 +621,10 @@ def bench_ours(args):
             per["rom2d_fp64_b9472"] = measure_rom(args, 9472, cpu=False, dmma_peak=pk)
         except Exception as ex:
             per["rom2d_fp64_b64"] = {"error": f"{type(ex).__name__}: {ex}"}
+        try:
+            per["mor_config2_region"] = measure_mor(args, 2)
+        except Exception as ex:
+            per["mor_config2_region"] = {"error": f"{type(ex).__name__}: {ex}"}
     if futs:
         for c, f in futs.items():
             try:

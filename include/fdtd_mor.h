@@ -64,8 +64,10 @@ typedef struct mor_system {
   double dt;               /* > 0                               */
 } mor_system;
 
-/* Validate, upload, build K^T on the device side's behalf.  stream: a
- * cudaStream_t (NULL = default stream). */
+/* Validate, upload, build K^T on the device side's behalf.  The handle works
+ * on an internal stream (the CGS iterations replay a captured CUDA graph) and
+ * every mor_* call returns synchronised; stream (a cudaStream_t, may be NULL)
+ * is only synchronised here. */
 int mor_create(const mor_system* sys, void* stream, mor_t** out);
 
 /* A(z) x = b for nrhs columns.  b_re / b_im / x_re / x_im are

@@ -13,7 +13,8 @@
 //   dot_partial_kernel   per-column inner products, fixed chunks, fixed-order
 //                        second stage inside the scalar kernels (deterministic)
 //   cgs_*                the batched CGS recursion: every column carries its own
-//                        rho / alpha / beta / residue and freezes when converged
+//                        rho / alpha / beta / residue and freezes when converged;
+//                        4 iterations (52 launches) replay as one captured graph
 //   gram_partial_kernel  G = V^H W of the block Gram-Schmidt (register tile of
 //                        KT basis vectors x MB block columns per thread, the
 //                        basis read once), gs_update_kernel W -= V G
@@ -239,6 +240,7 @@ struct CgsScal {
   T *rho, *rho_old, *alpha, *beta;
   double *nb, *res;
   int *active, *iters, *n_active;
+  int* it;          // the iteration about to run (device side, so that a captured graph replays)
 };
 
 template <class T>
@@ -252,7 +254,7 @@ __device__ __forceinline__ T sum_partials(const T* partial, int nch, int j) {
 template <class T>
 __global__ void cgs_init_kernel(CgsScal<T> S, const T* partial, int nch, int m) {
   int j = threadIdx.x;
-  if (j == 0) *S.n_active = 0;
+  if (j == 0) { *S.n_active = 0; *S.it = 1; }
   __syncthreads();
   if (j >= m) return;
   double nb = sqrt(creal(sum_partials(partial, nch, j)));
@@ -267,9 +269,14 @@ __global__ void cgs_init_kernel(CgsScal<T> S, const T* partial, int nch, int m) 
 
 // rho = <rt, r>, beta = rho / rho_old
 template <class T>
-__global__ void cgs_s1_kernel(CgsScal<T> S, const T* partial, int nch, int m, int it) {
+__global__ void cgs_s1_kernel(CgsScal<T> S, const T* partial, int nch, int m, int max_iter) {
   int j = threadIdx.x;
+  const int it = *S.it;
   if (j >= m || !S.active[j]) return;
+  if (it > max_iter) {                      // (a replayed graph past the cap: the column stays as it is)
+    S.active[j] = 0;
+    return;
+  }
   T rho = sum_partials(partial, nch, j);
   if (ciszero(rho) || !cfinite(rho)) {     // breakdown
     S.active[j] = 0;
@@ -282,8 +289,9 @@ __global__ void cgs_s1_kernel(CgsScal<T> S, const T* partial, int nch, int m, in
 
 // sigma = <rt, v>, alpha = rho / sigma
 template <class T>
-__global__ void cgs_s2_kernel(CgsScal<T> S, const T* partial, int nch, int m, int it) {
+__global__ void cgs_s2_kernel(CgsScal<T> S, const T* partial, int nch, int m) {
   int j = threadIdx.x;
+  const int it = *S.it;
   if (j >= m || !S.active[j]) return;
   T sigma = sum_partials(partial, nch, j);
   if (ciszero(sigma) || !cfinite(sigma)) {
@@ -297,9 +305,11 @@ __global__ void cgs_s2_kernel(CgsScal<T> S, const T* partial, int nch, int m, in
 
 // res = ||r|| / ||rhs||; converged columns freeze
 template <class T>
-__global__ void cgs_s3_kernel(CgsScal<T> S, const T* partial, int nch, int m, int it, double tol) {
+__global__ void cgs_s3_kernel(CgsScal<T> S, const T* partial, int nch, int m, double tol) {
   int j = threadIdx.x;
-  if (j == 0) *S.n_active = 0;
+  const int it = *S.it;
+  __syncthreads();
+  if (j == 0) { *S.n_active = 0; *S.it = it + 1; }
   __syncthreads();
   if (j >= m || !S.active[j]) return;
   double res = sqrt(creal(sum_partials(partial, nch, j))) / S.nb[j];
@@ -311,10 +321,10 @@ __global__ void cgs_s3_kernel(CgsScal<T> S, const T* partial, int nch, int m, in
 
 // u = r + beta q;  p = u + beta (q + beta p)
 template <class T>
-__global__ void cgs_v1_kernel(int64_t n, CgsScal<T> S, const T* r, const T* q, T* u, T* p, int64_t ld, int64_t ldx,
-                              int it) {
+__global__ void cgs_v1_kernel(int64_t n, CgsScal<T> S, const T* r, const T* q, T* u, T* p, int64_t ld, int64_t ldx) {
   int j = blockIdx.y;
   if (!S.active[j]) return;
+  const int it = *S.it;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int64_t o = (int64_t)j * ld + i;
@@ -582,8 +592,26 @@ struct Shifted {
   DevBuf<double> sc_d;
   DevBuf<int> sc_i;
   CgsScal<T> S;
+  // GIT iterations of the recursion captured once as a CUDA graph and replayed
+  // (the iteration number lives on the device); re-captured when the solution
+  // pointer, the block width or the stopping rule change
+  static constexpr int GIT = 4;
+  cudaGraphExec_t gexec = nullptr;
+  const T* g_x = nullptr;
+  int64_t g_ldx = 0;
+  int g_m = 0, g_max = 0;
+  double g_tol = 0;
+  int* h_active = nullptr;                 // pinned
   int64_t total_iters = 0, total_cols = 0;
   double worst_res = 0;
+
+  Shifted() = default;
+  Shifted(const Shifted&) = delete;
+  Shifted& operator=(const Shifted&) = delete;
+  ~Shifted() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (h_active) cudaFreeHost(h_active);
+  }
 
   int init(mor_t* h_, T z_, int mcap_) {
     h = h_; z = z_; mcap = mcap_;
@@ -602,10 +630,11 @@ struct Shifted {
     MCK(partial.alloc((size_t)mcap * nch));
     MCK(sc_T.alloc((size_t)4 * mcap));
     MCK(sc_d.alloc((size_t)2 * mcap));
-    MCK(sc_i.alloc((size_t)2 * mcap + 1));
+    MCK(sc_i.alloc((size_t)2 * mcap + 2));
+    MCK(cudaHostAlloc((void**)&h_active, sizeof(int), cudaHostAllocDefault));
     S.rho = sc_T.p; S.rho_old = sc_T.p + mcap; S.alpha = sc_T.p + 2 * mcap; S.beta = sc_T.p + 3 * mcap;
     S.nb = sc_d.p; S.res = sc_d.p + mcap;
-    S.active = sc_i.p; S.iters = sc_i.p + mcap; S.n_active = sc_i.p + 2 * mcap;
+    S.active = sc_i.p; S.iters = sc_i.p + mcap; S.n_active = sc_i.p + 2 * mcap; S.it = sc_i.p + 2 * mcap + 1;
     return FDTD_OK;
   }
 
@@ -652,22 +681,42 @@ struct Shifted {
       dot(r.p, ne, r.p, ne, m, false);
       cgs_init_kernel<T><<<1, 64, 0, h->st>>>(S, partial.p, nch, m);
       h->launches += 1;
-      int n_active = m;
-      for (int it = 1; it <= max_iter && n_active > 0; ++it) {
+      // one iteration of the recursion (13 launches)
+      auto iteration = [&]() {
         dot(rt.p, ne, r.p, ne, m, true);
-        cgs_s1_kernel<T><<<1, 64, 0, h->st>>>(S, partial.p, nch, m, it);
-        cgs_v1_kernel<T><<<grid1(ne, m), TPB, 0, h->st>>>(ne, S, r.p, q.p, u.p, p.p, ne, ldx, it);
+        cgs_s1_kernel<T><<<1, 64, 0, h->st>>>(S, partial.p, nch, m, max_iter);
+        cgs_v1_kernel<T><<<grid1(ne, m), TPB, 0, h->st>>>(ne, S, r.p, q.p, u.p, p.p, ne, ldx);
         schur_apply(p.p, ne, v.p, ne, m);
         dot(rt.p, ne, v.p, ne, m, true);
-        cgs_s2_kernel<T><<<1, 64, 0, h->st>>>(S, partial.p, nch, m, it);
+        cgs_s2_kernel<T><<<1, 64, 0, h->st>>>(S, partial.p, nch, m);
         cgs_v2_kernel<T><<<grid1(ne, m), TPB, 0, h->st>>>(ne, S, u.p, v.p, q.p, uh.p, ne, x, ldx);
         schur_apply(uh.p, ne, v.p, ne, m);         // w reuses v
         cgs_v3_kernel<T><<<grid1(ne, m), TPB, 0, h->st>>>(ne, S, v.p, r.p, ne);
         dot(r.p, ne, r.p, ne, m, true);
-        cgs_s3_kernel<T><<<1, 64, 0, h->st>>>(S, partial.p, nch, m, it, tol);
+        cgs_s3_kernel<T><<<1, 64, 0, h->st>>>(S, partial.p, nch, m, tol);
         h->launches += 6;
-        MCK(cudaMemcpyAsync(&n_active, S.n_active, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+      };
+      if (!gexec || g_x != x || g_ldx != ldx || g_m != m || g_max != max_iter || g_tol != tol) {
+        if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+        const int64_t l0 = h->launches;
+        cudaGraph_t gr = nullptr;
+        MCK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < GIT; ++i) iteration();
+        cudaError_t ce = cudaMemcpyAsync(h_active, S.n_active, sizeof(int), cudaMemcpyDeviceToHost, h->st);
+        cudaError_t ce2 = cudaStreamEndCapture(h->st, &gr);
+        h->launches = l0;                          // (capturing launches nothing)
+        MCK(ce);
+        MCK(ce2);
+        MCK(cudaGraphInstantiate(&gexec, gr, 0));
+        MCK(cudaGraphDestroy(gr));
+        g_x = x; g_ldx = ldx; g_m = m; g_max = max_iter; g_tol = tol;
+      }
+      int n_active = m;
+      for (int it = 0; it < max_iter && n_active > 0; it += GIT) {
+        MCK(cudaGraphLaunch(gexec, h->st));
+        h->launches += 13 * GIT;
         MCK(cudaStreamSynchronize(h->st));
+        n_active = *h_active;
       }
       std::vector<int> hi(m);
       std::vector<double> hr(m);
@@ -874,7 +923,13 @@ int mor_create(const mor_system* sys, void* stream, mor_t** out) {
   for (int64_t i = 0; i < ne; ++i) iDe[i] = 1.0 / sys->De[i];
   for (int64_t i = 0; i < nh; ++i) iDm[i] = 1.0 / sys->Dm[i];
   std::unique_ptr<mor_t, void (*)(mor_t*)> h(new mor_t, mor_destroy);
-  h->ne = ne; h->nh = nh; h->nnz = nnz; h->dt = sys->dt; h->st = (cudaStream_t)stream;
+  h->ne = ne; h->nh = nh; h->nnz = nnz; h->dt = sys->dt;
+  // an internal stream: the CGS iterations are captured into a CUDA graph, which
+  // the legacy default stream cannot do.  Every mor_* call takes host buffers
+  // and returns synchronised, so nothing is ordered against the caller's stream
+  // beyond a synchronise of it here.
+  if (stream) MCK(cudaStreamSynchronize((cudaStream_t)stream));
+  MCK(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
   auto up = [&](auto** dst, const auto* src, size_t n) -> cudaError_t {
     cudaError_t e = cudaMalloc((void**)dst, std::max<size_t>(n, 1) * sizeof(**dst));
     if (e != cudaSuccess) return e;
@@ -1007,6 +1062,7 @@ void mor_destroy(mor_t* h) {
   if (!h) return;
   cudaFree(h->rp); cudaFree(h->rpT); cudaFree(h->ci); cudaFree(h->ciT); cudaFree(h->val); cudaFree(h->valT);
   cudaFree(h->De); cudaFree(h->Dm); cudaFree(h->invDe); cudaFree(h->invDm);
+  if (h->st) cudaStreamDestroy(h->st);
   delete h;
 }
 

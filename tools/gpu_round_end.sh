@@ -9,7 +9,7 @@ python -c "import __graft_entry__ as g; g.build()" || exit 1
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
 ( time timeout 1800 python bench.py > $O/bench_default.json 2> $O/bench_default.err ) 2> $O/bench_time.txt
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
-for C in 4 5 2; do
+for C in 4 5; do
   CMD="python bench.py --config $C --steps 1 --warmup 3 --no-cpu --no-e2e --no-per-config"
   $CMD > $O/plain_c$C.json 2> $O/plain_c$C.err && \
   ncu --metrics gpu__time_duration.sum --clock-control none -s 1000 -c 600 --csv --log-file $O/launches_c$C.csv $CMD > $O/ncu_c$C.log 2>&1
