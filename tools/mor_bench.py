@@ -49,9 +49,29 @@ def main():
     ap.add_argument("--host", action="store_true")
     ap.add_argument("--tol", type=float, default=1e-4)
     ap.add_argument("--window", type=float, default=120e9)
+    ap.add_argument("--pipeline", action="store_true",
+                    help="the whole preprocessing of the configuration with the device reducer "
+                         "(prep.build_problem(reducer='gpu')), then a short stepped run of the result")
     a = ap.parse_args()
     cfg = int(a.config) if a.config.isdigit() else a.config
     scn = scenario(cfg)
+    if a.pipeline:
+        from paper_1406_7042_b200.fdtd import Sim
+        t0 = time.time()
+        prob, info = prep.build_problem(scn, cache=False, reducer="gpu", reducer_opts=dict(solve_tol=a.tol, window_bytes=a.window))
+        t_total = time.time() - t0
+        sim = Sim(prob)
+        for c, arr in (prob.get("init") or {}).items():
+            sim.set_state(int(c), arr)
+        sim.step(1000)
+        sim.sync()
+        pr = sim.probe()
+        sim.close()
+        print(json.dumps(dict(config=cfg, pipeline="gpu reducer", t_total_s=round(t_total, 1), t_assemble_s=round(info["t_assemble"], 1),
+                              blocks=[{k: (round(v, 3) if isinstance(v, float) else v) for k, v in b.items()} for b in info["blocks"]],
+                              mor_stats=info.get("mor_stats"), limit=2.0 / scn["dt"],
+                              probe_max_after_1000_steps=float(np.abs(pr).max()), finite=bool(np.all(np.isfinite(pr))))), flush=True)
+        return
     t0 = time.time()
     part, B, pts, q = region_system(scn)
     t_asm = time.time() - t0
