@@ -15,9 +15,9 @@
 //   cgs_*                the batched CGS recursion: every column carries its own
 //                        rho / alpha / beta / residue and freezes when converged;
 //                        4 iterations (52 launches) replay as one captured graph
-//   gram_partial_kernel  G = V^H W of the block Gram-Schmidt (register tile of
-//                        KT basis vectors x MB block columns per thread, the
-//                        basis read once), gs_update_kernel W -= V G
+//   gram_stream_kernel   G = V^H W of the block Gram-Schmidt (the block staged in
+//                        shared memory, every warp streams its basis vectors
+//                        through it: the basis read once), gs_update_kernel W -= V G
 //
 // The Arnoldi driver (host C++) mirrors the host preprocessing
 // (prep/reduce.py krylov_basis) step for step; only scalars (norms, residues,
@@ -227,11 +227,12 @@ __global__ void dot_partial_kernel(int64_t n, const T* a, int64_t lda, const T* 
 
 template <class T>
 __global__ void dot_finish_kernel(const T* partial, int nch, int m, T* out) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (j >= m) return;
-  T s = partial[(int64_t)j * nch];
-  for (int c = 1; c < nch; ++c) s = cadd(s, partial[(int64_t)j * nch + c]);
-  out[j] = s;
+  T s = cmake<T>(0, 0);
+  for (int c = lane; c < nch; c += 32) s = cadd(s, partial[(int64_t)j * nch + c]);
+  s = warp_sum(s);
+  if (lane == 0) out[j] = s;
 }
 
 // ------------------------------------------------------------------ batched CGS
@@ -372,55 +373,89 @@ __global__ void cgs_v3_kernel(int64_t n, CgsScal<T> S, const T* w, T* r, int64_t
 
 // ------------------------------------------------------------------ block Gram-Schmidt
 // partial[c][kk][mm] = sum over chunk c of conj(A[kk][i]) W[mm][i]
-template <class T, int KT, int MB>
-__global__ void __launch_bounds__(TPB) gram_partial_kernel(int64_t n, const T* __restrict__ A, int64_t lda, int k,
-                                                           const T* __restrict__ W, int64_t ldw, int m, T* partial,
-                                                           int nch) {
-  int c = blockIdx.x, k0 = blockIdx.y * KT, m0 = blockIdx.z * MB;
-  int64_t per = (n + nch - 1) / nch, lo = c * per, hi = min(n, lo + per);
-  T acc[KT][MB];
-#pragma unroll
-  for (int a = 0; a < KT; ++a)
-#pragma unroll
-    for (int b = 0; b < MB; ++b) acc[a][b] = cmake<T>(0, 0);
-  for (int64_t i = lo + threadIdx.x; i < hi; i += TPB) {
-    T av[KT], wv[MB];
-#pragma unroll
-    for (int a = 0; a < KT; ++a) av[a] = (k0 + a < k) ? cconj(A[(int64_t)(k0 + a) * lda + i]) : cmake<T>(0, 0);
-#pragma unroll
-    for (int b = 0; b < MB; ++b) wv[b] = (m0 + b < m) ? W[(int64_t)(m0 + b) * ldw + i] : cmake<T>(0, 0);
-#pragma unroll
-    for (int a = 0; a < KT; ++a)
-#pragma unroll
-      for (int b = 0; b < MB; ++b) cfma(acc[a][b], av[a], wv[b]);
-  }
-  __shared__ T sm[TPB / 32][KT * MB];
-  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int a = 0; a < KT; ++a)
-#pragma unroll
-    for (int b = 0; b < MB; ++b) {
-      T s = warp_sum(acc[a][b]);
-      if (lane == 0) sm[wid][a * MB + b] = s;
+// One CTA per chunk of rows and group of MB block columns.  The chunk is walked
+// in sub-chunks of GSUB rows: the W tile [MB][GSUB] is staged in shared memory
+// once, then every warp streams its basis vectors (kk = warp, warp + 8, ...)
+// through it -- GSUB / 32 independent coalesced loads per lane, MB accumulators,
+// one warp reduction per vector and sub-chunk -- so the basis is read exactly
+// once per Gram product and the block once.  The per-vector sums of a sub-chunk
+// are added to partial[] by the same lanes in sub-chunk order (deterministic).
+constexpr int GTPB = 384;          // threads of the Gram kernel (one CTA per SM: the W tile fills shared memory)
+constexpr int GROWS = 3072;        // rows of the W tile: MB x GROWS words = 192 KB
+template <class T, int MB, int KK>
+__global__ void __launch_bounds__(GTPB, 1) gram_stream_kernel(int64_t n, const T* __restrict__ A, int64_t lda, int k,
+                                                              const T* __restrict__ W, int64_t ldw, int m, T* partial,
+                                                              int nch) {
+  // KK basis vectors per warp pass share every shared-memory read of the W tile
+  // (one vector per pass was bound by shared-memory bandwidth, MB words of W
+  // per word of the basis: 2.2 TB/s), and the tile holds the CTA's whole chunk
+  // whenever it fits, so a vector is reduced across the warp once per chunk
+  extern __shared__ __align__(16) unsigned char gram_smem[];
+  T (*Ws)[GROWS] = reinterpret_cast<T (*)[GROWS]>(gram_smem);
+  const int c = blockIdx.x, m0 = blockIdx.y * MB;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t per = (n + nch - 1) / nch, lo = c * per, hi = min(n, lo + per);
+  bool first = true;
+  for (int64_t s0 = lo; s0 < hi || first; s0 += GROWS) {
+    const int rows = (int)max((int64_t)0, min((int64_t)GROWS, hi - s0));
+    const int rows32 = (rows + 31) & ~31;
+    __syncthreads();
+    for (int e = threadIdx.x; e < MB * rows32; e += GTPB) {
+      const int b = e / rows32, i = e % rows32;
+      Ws[b][i] = (m0 + b < m && i < rows) ? W[(int64_t)(m0 + b) * ldw + s0 + i] : cmake<T>(0, 0);
     }
-  __syncthreads();
-  if (threadIdx.x < KT * MB) {
-    int a = threadIdx.x / MB, b = threadIdx.x % MB;
-    if (k0 + a < k && m0 + b < m) {
-      T s = sm[0][threadIdx.x];
-      for (int w = 1; w < TPB / 32; ++w) s = cadd(s, sm[w][threadIdx.x]);
-      partial[((int64_t)c * k + k0 + a) * m + m0 + b] = s;
+    __syncthreads();
+    for (int kk = warp * KK; kk < k; kk += (GTPB / 32) * KK) {
+      const T* a[KK];
+#pragma unroll
+      for (int j = 0; j < KK; ++j) a[j] = A + (int64_t)min(kk + j, k - 1) * lda + s0;
+      T acc[KK][MB];
+#pragma unroll
+      for (int j = 0; j < KK; ++j)
+#pragma unroll
+        for (int b = 0; b < MB; ++b) acc[j][b] = cmake<T>(0, 0);
+#pragma unroll 4
+      for (int o = lane; o < rows32; o += 32) {
+        const bool in = o < rows;
+        T av[KK], wv[MB];
+#pragma unroll
+        for (int j = 0; j < KK; ++j) av[j] = in ? cconj(a[j][o]) : cmake<T>(0, 0);
+#pragma unroll
+        for (int b = 0; b < MB; ++b) wv[b] = Ws[b][o];
+#pragma unroll
+        for (int j = 0; j < KK; ++j)
+#pragma unroll
+          for (int b = 0; b < MB; ++b) cfma(acc[j][b], av[j], wv[b]);
+      }
+#pragma unroll
+      for (int j = 0; j < KK; ++j) {
+        T mine = cmake<T>(0, 0);
+#pragma unroll
+        for (int b = 0; b < MB; ++b) {
+          const T sum = warp_sum(acc[j][b]);
+          if (lane == b) mine = sum;
+        }
+        if (lane < MB && m0 + lane < m && kk + j < k) {
+          T* o = partial + ((int64_t)c * k + kk + j) * m + m0 + lane;
+          *o = first ? mine : cadd(*o, mine);
+        }
+      }
     }
+    first = false;
   }
 }
 
+// G[e] = sum over the chunks of partial[c][e]: one warp per element, lanes over
+// the chunks, a fixed shuffle tree (deterministic)
 template <class T>
 __global__ void gram_finish_kernel(const T* partial, int nch, int64_t km, T* G) {
-  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (e >= km) return;
-  T s = partial[e];
-  for (int c = 1; c < nch; ++c) s = cadd(s, partial[(int64_t)c * km + e]);
-  G[e] = s;
+  T s = cmake<T>(0, 0);
+  for (int c = lane; c < nch; c += 32) s = cadd(s, partial[(int64_t)c * km + e]);
+  s = warp_sum(s);
+  if (lane == 0) G[e] = s;
 }
 
 // W[mm][i] -= sum_kk A[kk][i] G[kk][mm]
@@ -484,8 +519,15 @@ double now_s() {
 }
 
 template <class T> struct GramTile;
-template <> struct GramTile<double> { static constexpr int KT = 4, MB = 8; };
-template <> struct GramTile<cd> { static constexpr int KT = 4, MB = 4; };
+template <> struct GramTile<double> { static constexpr int MB = 8, KK = 4; };     // W tile [MB][GROWS]: 192 KB either way
+template <> struct GramTile<cd> { static constexpr int MB = 4, KK = 4; };
+// chunks of the Gram product: ~3 CTAs per SM on long vectors (each CTA walks all the basis vectors of its rows)
+// (one CTA per SM; chunks of at most GROWS rows up to 8 waves of CTAs, longer chunks beyond)
+inline int gram_chunks(int64_t n) {
+  int64_t c = std::max<int64_t>(1, (n + GROWS - 1) / GROWS);
+  if (c > 148) c = (c + 147) / 148 * 148;            // whole waves of one CTA per SM
+  return (int)std::min<int64_t>(1184, c);
+}
 
 // Growing orthonormal set (mirror of prep/reduce.py _Basis): block classical
 // Gram-Schmidt twice against the set, then MGS (twice) inside the block with
@@ -501,7 +543,9 @@ struct DBasis {
 
   int init(mor_t* h_, int64_t n_, int cap_, int mmax_, double tol_) {
     h = h_; n = n_; cap = cap_; mmax = mmax_; tol = tol_; k = 0;
-    nch = chunks_for(n);
+    nch = gram_chunks(n);
+    MCK(cudaFuncSetAttribute(gram_stream_kernel<T, GramTile<T>::MB, GramTile<T>::KK>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(GramTile<T>::MB * GROWS * sizeof(T))));
     MCK(Vt.alloc((size_t)cap * n));
     MCK(W.alloc((size_t)mmax * n));
     MCK(G.alloc((size_t)cap * mmax));
@@ -513,10 +557,11 @@ struct DBasis {
   // W[0:m] -= A^T (conj(A) W) for the k_ rows starting at A
   int project(const T* A, int k_, T* Wp, int m) {
     using GT = GramTile<T>;
-    dim3 g1(nch, (k_ + GT::KT - 1) / GT::KT, (m + GT::MB - 1) / GT::MB);
-    gram_partial_kernel<T, GT::KT, GT::MB><<<g1, TPB, 0, h->st>>>(n, A, n, k_, Wp, n, m, partial.p, nch);
+    dim3 g1(nch, (m + GT::MB - 1) / GT::MB);
+    gram_stream_kernel<T, GT::MB, GT::KK><<<g1, GTPB, GT::MB * GROWS * sizeof(T), h->st>>>(n, A, n, k_, Wp, n, m,
+                                                                                          partial.p, nch);
     int64_t km = (int64_t)k_ * m;
-    gram_finish_kernel<T><<<(unsigned)((km + TPB - 1) / TPB), TPB, 0, h->st>>>(partial.p, nch, km, G.p);
+    gram_finish_kernel<T><<<(unsigned)((km * 32 + TPB - 1) / TPB), TPB, 0, h->st>>>(partial.p, nch, km, G.p);
     dim3 g2((unsigned)((n + TPB - 1) / TPB), (m + GT::MB - 1) / GT::MB);
     gs_update_kernel<T, GT::MB><<<g2, TPB, 0, h->st>>>(n, A, n, k_, G.p, m, Wp, n);
     h->launches += 3;
@@ -526,7 +571,7 @@ struct DBasis {
 
   int norms(const T* X, int64_t ldx, int m, std::vector<double>& out) {
     dot_partial_kernel<T><<<dim3(nch, m), TPB, 0, h->st>>>(n, X, ldx, X, ldx, partial.p, nch, nullptr);
-    dot_finish_kernel<T><<<(m + 63) / 64, 64, 0, h->st>>>(partial.p, nch, m, dots.p);
+    dot_finish_kernel<T><<<(m * 32 + 63) / 64, 64, 0, h->st>>>(partial.p, nch, m, dots.p);
     h->launches += 2;
     std::vector<T> tmp(m);
     MCK(cudaMemcpyAsync(tmp.data(), dots.p, m * sizeof(T), cudaMemcpyDeviceToHost, h->st));
