@@ -113,6 +113,13 @@ struct DevMem {
   void (*free_)(void*, void*) = nullptr;
   void* ctx = nullptr;
   std::vector<void*> owned;
+  // FDTD_GUARD=1 (debugging): every buffer sits between two 64 KB guard zones
+  // filled with 0xA5; check() (called by fdtd_sync) reports the first buffer whose
+  // guards a kernel has written -- out-of-bounds stores next to a buffer, which
+  // the serial step order can hide (a later kernel rewrites the victim)
+  static constexpr size_t GUARD = 64 * 1024;
+  bool guard = getenv("FDTD_GUARD") != nullptr;
+  std::vector<size_t> sizes;
   ~DevMem() {
     for (void* p : owned) {
       if (free_) free_(p, ctx);
@@ -121,11 +128,35 @@ struct DevMem {
   }
   void* get(size_t bytes) {
     if (bytes == 0) bytes = 16;
+    const size_t total = guard ? ((bytes + 255) / 256 * 256 + 2 * GUARD) : bytes;
     void* p = nullptr;
-    if (alloc) p = alloc(bytes, ctx);
-    else if (cudaMalloc(&p, bytes) != cudaSuccess) p = nullptr;
-    if (p) owned.push_back(p);
-    return p;
+    if (alloc) p = alloc(total, ctx);
+    else if (cudaMalloc(&p, total) != cudaSuccess) p = nullptr;
+    if (!p) return nullptr;
+    owned.push_back(p);
+    sizes.push_back(bytes);
+    if (!guard) return p;
+    cudaMemset(p, 0xA5, GUARD);
+    cudaMemset((char*)p + total - GUARD - ((bytes + 255) / 256 * 256 - bytes), 0xA5,
+               GUARD + ((bytes + 255) / 256 * 256 - bytes));
+    return (char*)p + GUARD;
+  }
+  // index of the first buffer with a damaged guard (-1: none); *where: byte offset relative to the buffer start
+  int check(long long* where) const {
+    if (!guard) return -1;
+    std::vector<unsigned char> h;
+    for (size_t b = 0; b < owned.size(); ++b) {
+      const size_t bytes = sizes[b], pad = (bytes + 255) / 256 * 256;
+      const size_t tail = GUARD + (pad - bytes);
+      h.resize(GUARD + tail);
+      cudaMemcpy(h.data(), owned[b], GUARD, cudaMemcpyDeviceToHost);
+      cudaMemcpy(h.data() + GUARD, (char*)owned[b] + GUARD + bytes, tail, cudaMemcpyDeviceToHost);
+      for (size_t i = 0; i < GUARD; ++i)
+        if (h[i] != 0xA5) { *where = (long long)i - (long long)GUARD; return (int)b; }
+      for (size_t i = 0; i < tail; ++i)
+        if (h[GUARD + i] != 0xA5) { *where = (long long)(bytes + i); return (int)b; }
+    }
+    return -1;
   }
 };
 
@@ -2146,6 +2177,13 @@ int Impl<T>::check_async() {
 template <typename T>
 int Impl<T>::sync() {
   CK(cudaStreamSynchronize(stream));
+  if (mem.guard) {
+    long long where = 0;
+    const int b = mem.check(&where);
+    if (b >= 0)
+      return fail(FDTD_ECUDA, "FDTD_GUARD: out-of-bounds write next to device buffer #%d (%zu bytes) at byte offset %lld",
+                  b, mem.sizes[b], where);
+  }
   return check_async();
 }
 

@@ -128,7 +128,7 @@ class Mor:
         st = np.zeros(len(STATS))
         _f._check(self.lib.mor_krylov_basis(self.h, C.byref(r), V1.ctypes.data_as(_f64p), V2.ctypes.data_as(_f64p),
                                             st.ctypes.data_as(_f64p), len(STATS)))
-        return V1.T.copy(), V2.T.copy(), dict(zip(STATS, st.tolist()))
+        return V1.T, V2.T, dict(zip(STATS, st.tolist()))          # (views: no 8 GB transposed copies at config 4's size)
 
     def launch_count(self):
         return int(self.lib.mor_launch_count(self.h))
