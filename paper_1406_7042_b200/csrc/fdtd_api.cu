@@ -119,6 +119,9 @@ struct DevMem {
   // the serial step order can hide (a later kernel rewrites the victim)
   static constexpr size_t GUARD = 64 * 1024;
   bool guard = getenv("FDTD_GUARD") != nullptr;
+  // the fill byte: FDTD_GUARD=1 -> 0xA5 (a tiny finite float); FDTD_GUARD=255 -> 0xFF (NaN in fp32 and fp64: an
+  // out-of-bounds READ that reaches the arithmetic then poisons the fields and trips the divergence check)
+  int pat = (getenv("FDTD_GUARD") && atoi(getenv("FDTD_GUARD")) > 1) ? (atoi(getenv("FDTD_GUARD")) & 0xff) : 0xA5;
   std::vector<size_t> sizes;
   ~DevMem() {
     for (void* p : owned) {
@@ -136,8 +139,8 @@ struct DevMem {
     owned.push_back(p);
     sizes.push_back(bytes);
     if (!guard) return p;
-    cudaMemset(p, 0xA5, GUARD);
-    cudaMemset((char*)p + total - GUARD - ((bytes + 255) / 256 * 256 - bytes), 0xA5,
+    cudaMemset(p, pat, GUARD);
+    cudaMemset((char*)p + total - GUARD - ((bytes + 255) / 256 * 256 - bytes), pat,
                GUARD + ((bytes + 255) / 256 * 256 - bytes));
     return (char*)p + GUARD;
   }
@@ -152,9 +155,9 @@ struct DevMem {
       cudaMemcpy(h.data(), owned[b], GUARD, cudaMemcpyDeviceToHost);
       cudaMemcpy(h.data() + GUARD, (char*)owned[b] + GUARD + bytes, tail, cudaMemcpyDeviceToHost);
       for (size_t i = 0; i < GUARD; ++i)
-        if (h[i] != 0xA5) { *where = (long long)i - (long long)GUARD; return (int)b; }
+        if (h[i] != (unsigned char)pat) { *where = (long long)i - (long long)GUARD; return (int)b; }
       for (size_t i = 0; i < tail; ++i)
-        if (h[GUARD + i] != 0xA5) { *where = (long long)(bytes + i); return (int)b; }
+        if (h[GUARD + i] != (unsigned char)pat) { *where = (long long)(bytes + i); return (int)b; }
     }
     return -1;
   }
