@@ -356,14 +356,14 @@ def measure(config, prec, steps, warmup, args, rank=0, world=1, local=0, headlin
                        "bound": "hbm", "avg_ms": grid_ms, "algorithmic_bytes_per_step": red_bytes,
                        "achieved_gbs": ach, "hbm_frac": ach / peak, "gflops": gf,
                        "roofline_gflops": roof, "frac": gf / roof,
-                       "note": "eager per-step launches with CUDA events (includes launch gaps)"}
+                       "note": "eager launches on a busy stream, CUDA events around each kernel group read back every 64 steps"}
         elif red_ms > 0:
             gf = red_flops / (red_ms * 1e-3) / 1e9
             reduced = {"kernel": "fused reduced update (reduced_fused_kernel / reduced_gemm_kernel)",
                        "bound": "latency (L2-resident M, one GEMM phase per step)", "avg_ms": red_ms,
                        "gflops": gf, "roofline_gflops": fp32_peak, "frac": gf / fp32_peak,
                        "algorithmic_gflop_per_step": red_flops / 1e9,
-                       "note": "eager per-step launch with CUDA events; SIMT fp32 FMA roofline"}
+                       "note": "eager launches on a busy stream, CUDA events read back every 64 steps; SIMT fp32 FMA roofline"}
     traffic = None
     tf = os.path.join(ROOT, "profiles", "stencil_traffic.json")
     if os.path.exists(tf):

@@ -215,7 +215,8 @@ int32_t fdtd_path(const fdtd_t* h);
 
 /* Per-phase tracing.  fdtd_profile(h, 1) resets the accumulators and makes the
  * following fdtd_step calls launch eagerly with CUDA events around each
- * kernel group (synchronising once per step); fdtd_profile(h, 0) returns to
+ * kernel group (read back every 64 steps, so the stream stays busy and the
+ * spans are kernel durations rather than launch latencies); fdtd_profile(h, 0) returns to
  * graph launches.  fdtd_phase_times writes the accumulated device time [ms] of
  * the phases {coarse stencil incl. explicit E rows, reduced chain incl.
  * probes, grid-path reduced kernels (large blocks only)} into ms[0..2] and,

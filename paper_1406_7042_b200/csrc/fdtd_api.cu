@@ -286,7 +286,11 @@ struct Impl : public fdtd_t {
   // per-phase tracing
   static constexpr int NPHASE = 3;       // stencil (+ explicit rows), reduced (+ probes), leapfrog GEMVs
   bool prof = false;
-  cudaEvent_t ev[2 * NPHASE] = {};
+  // event sets of up to NPOOL profiled steps are read back together, so the
+  // stream stays busy and the spans are kernel durations, not launch latencies
+  static constexpr int NPOOL = 64;
+  std::vector<cudaEvent_t> ev;         // [NPOOL][2 * NPHASE]
+  int prof_pending = 0;
   // split step: the stencil items of the columns that hold
   // interface rows run first, the reduced update runs on a second stream
   // beside the rest of the stencil
@@ -317,9 +321,27 @@ struct Impl : public fdtd_t {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
   }
+  int flush_profile() {
+    if (prof_pending == 0) return FDTD_OK;
+    CK(cudaEventSynchronize(ev[(size_t)(prof_pending - 1) * 2 * NPHASE + 3]));
+    for (int q = 0; q < prof_pending; ++q)
+      for (int ph = 0; ph < NPHASE; ++ph) {
+        if (ph == 2 && !any_leap) continue;
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev[(size_t)q * 2 * NPHASE + 2 * ph], ev[(size_t)q * 2 * NPHASE + 2 * ph + 1]));
+        phase_ms[ph] += ms;
+        phase_n[ph] += 1;
+      }
+    prof_pending = 0;
+    return FDTD_OK;
+  }
   int set_profile(int on) override {
-    if (on && !ev[0])
+    if (on && ev.empty()) {
+      ev.assign((size_t)NPOOL * 2 * NPHASE, nullptr);
       for (auto& e : ev) CK(cudaEventCreate(&e));
+    }
+    int e = flush_profile();
+    if (e) return e;
     prof = on != 0;
     for (int i = 0; i < NPHASE; ++i) { phase_ms[i] = 0; phase_n[i] = 0; }
     return FDTD_OK;
@@ -340,6 +362,8 @@ struct Impl : public fdtd_t {
     return FDTD_OK;
   }
   int phase_times(double* ms, int n) override {
+    int e = flush_profile();
+    if (e) return e;
     for (int i = 0; i < n && i < NPHASE; ++i) ms[i] = phase_n[i] ? phase_ms[i] : 0.0;
     for (int i = NPHASE; i < n; ++i) ms[i] = 0.0;
     if (n > NPHASE) ms[NPHASE] = (double)phase_n[0];
@@ -1842,7 +1866,9 @@ template <typename T>
 int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   int64_t n = 0;
   const int64_t* ds = d_step + p;          // this step's counter slot (the fused kernel writes the other)
-  auto mark = [&](int ph, int edge) { if (profile) cudaEventRecord(ev[2 * ph + edge], st); };
+  auto mark = [&](int ph, int edge) {
+    if (profile) cudaEventRecord(ev[(size_t)prof_pending * 2 * NPHASE + 2 * ph + edge], st);
+  };
   fdtd::Fields<T> F0, F1;
   for (int c = 0; c < 6; ++c) { F0.f[c] = F[p][c]; F1.f[c] = F[p ^ 1][c]; }
   // a1-a3 + a5: fused coarse stencil with the explicit rows evaluated in place
@@ -2063,15 +2089,9 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
   mark(1, 1);
   CK(cudaGetLastError());
   if (fuse_rows) rows_ahead = true;          // the reduced kernel evaluated the next step's rows
-  if (profile) {
-    CK(cudaEventSynchronize(ev[3]));
-    for (int ph = 0; ph < NPHASE; ++ph) {
-      if (ph == 2 && !any_leap) continue;
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, ev[2 * ph], ev[2 * ph + 1]));
-      phase_ms[ph] += ms;
-      phase_n[ph] += 1;
-    }
+  if (profile && ++prof_pending == NPOOL) {
+    int e = flush_profile();
+    if (e) return e;
   }
   *count += n;
   return FDTD_OK;
