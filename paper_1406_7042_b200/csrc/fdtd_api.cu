@@ -183,6 +183,9 @@ struct BlockDev {
   CUtensorMap se_map;                          // TMA map of SEp_d: [n_if][Kph] fp32, 32 x 128 boxes, 128-byte swizzle
   float* xs_d = nullptr;                       // h~ split for the tensor cores: [ceil(qh/32)][hi 512 | lo 512]
   int splits = 0;                              // > 0: tall-skinny fp32 GEMM kernels for the S_E products
+  bool wide = false;                           // S_E^T G on gemm_tn_f32_wide_kernel (N = 16)
+  int wide_ng = 2;                             // its member groups per column octet (2: 256 threads, measured 143 us on
+                                               // config 4; 4: 512 threads, 147 us; FDTD_WIDE_NG)
   int Kph = 0, Kpe = 0;                        // padded row pitches (multiples of 32 * VEC)
   // state offsets (elements) in the concatenated buffers
   int64_t e_off = 0, h_off = 0, y_off = 0;     // e/h buffers [q][N], y / G [n_if][N]
@@ -752,6 +755,17 @@ int Impl<T>::create(const fdtd_grid* g, const fdtd_materials* mat, const fdtd_in
         const int TC = 4 * 256 / (D.N / 4);
         const int ctile = (D.qh + TC - 1) / TC;
         D.splits = std::max(1, std::min(2 * 148 / ctile, D.n_if / 64));
+        // N = 16: the S_E^T G product on the 8 x 8 register-tile kernel, one CTA per SM
+        // (FDTD_NO_WIDE=1: the general 4 x 4 kernel)
+        if (D.N == 16 && D.qh % 2 == 0 && !getenv("FDTD_NO_WIDE")) {
+          D.wide = true;
+          D.splits = std::max(1, std::min(148 / ((D.qh + fdtd::WTC - 1) / fdtd::WTC), D.n_if / 64));
+          CK(cudaFuncSetAttribute(fdtd::gemm_tn_f32_wide_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  fdtd::gemm_tn_wide_smem()));
+          CK(cudaFuncSetAttribute(fdtd::gemm_tn_f32_wide_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  fdtd::gemm_tn_wide_smem()));
+          if (const char* e = getenv("FDTD_WIDE_NG")) D.wide_ng = atoi(e) == 2 ? 2 : 4;
+        }
         // the K~' products as split-K TN GEMMs on the stored transposes: 4 column
         // tiles x ks row splits fill the GPU (a 1024 x 1024 x 16 product is too
         // small for one CTA per row block)
@@ -1973,8 +1987,21 @@ int Impl<T>::launch_step(int p, cudaStream_t st, int64_t* count, bool profile) {
           // buffer, summed in a fixed order; y = S_E h~ (tensor cores or SIMT)
           n += launch_gemm_tn(D.qe, D.qh, D.Kph, D.N, D.ks, (const float*)D.Kp_d, (const float*)e,
                               D.part_d, rs);
-          n += launch_gemm_tn(D.n_if, D.qh, D.Kph, D.N, D.splits, (const float*)D.SEp_d,
-                              (const float*)(g_all + D.y_off), D.part_d + (size_t)D.ks * D.qh * D.N, rs);
+          if (D.wide) {
+            const dim3 gw((D.qh + fdtd::WTC - 1) / fdtd::WTC, D.splits);
+            if (D.wide_ng == 2)
+              fdtd::gemm_tn_f32_wide_kernel<2><<<gw, 256, fdtd::gemm_tn_wide_smem(), rs>>>(
+                  D.n_if, D.qh, D.Kph, (const float*)D.SEp_d, (const float*)(g_all + D.y_off),
+                  D.part_d + (size_t)D.ks * D.qh * D.N);
+            else
+              fdtd::gemm_tn_f32_wide_kernel<4><<<gw, 512, fdtd::gemm_tn_wide_smem(), rs>>>(
+                  D.n_if, D.qh, D.Kph, (const float*)D.SEp_d, (const float*)(g_all + D.y_off),
+                  D.part_d + (size_t)D.ks * D.qh * D.N);
+            ++n;
+          } else {
+            n += launch_gemm_tn(D.n_if, D.qh, D.Kph, D.N, D.splits, (const float*)D.SEp_d,
+                                (const float*)(g_all + D.y_off), D.part_d + (size_t)D.ks * D.qh * D.N, rs);
+          }
           fdtd::reduce_axpy_f32_kernel<<<(D.qh * D.N + 31) / 32, 256, 0, rs>>>(
               D.qh, D.N, D.ks + D.splits, D.part_d, nullptr, (const float*)D.gh_d, (float*)h,
               D.tc ? D.xs_d : nullptr);

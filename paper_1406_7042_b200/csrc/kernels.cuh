@@ -1672,6 +1672,113 @@ gemm_tn_f32_partial_kernel(int rows, int cols, int Kp, const float* __restrict__
   }
 }
 
+// gemm_tn partial for N = 16 members and long contractions (config 4's S_E^T G:
+// 65,024 rows): the same product as gemm_tn_f32_partial_kernel<4> with an
+// 8 column x 8 member register tile per thread.  The 4 x 4 tile of the general
+// kernel was bound by shared-memory traffic (ncu: fp64 pipe 38 % active, top
+// stalls short_scoreboard / mio_throttle: 4 shared loads per 16 DFMA plus the
+// fp32 -> fp64 conversion pass); here it is 8 loads per 64 DFMA.  One CTA per SM
+// covers up to 1,024 columns: chunks of WRC = 8 rows, cp.async 3-stage ring of
+// the fp32 chunk, converted once to fp64 in shared memory, fp64 accumulation of
+// the exact products (R14).  Thread (cq, nq): columns {256 j + 2 cq, 256 j + 2 cq
+// + 1 : j = 0..3} (so a warp's 16-byte loads are contiguous: no bank conflicts),
+// members nq * 8 .. nq * 8 + 7.
+constexpr int WRC = 8, WTC = 1024, WNS = 3;
+constexpr int gemm_tn_wide_smem() {
+  return WNS * WRC * WTC * 4 + WNS * WRC * 16 * 4 + WRC * WTC * 8 + WRC * 16 * 8;
+}
+// NG member groups per column octet: NG = 2 -> 8 members per thread, 256 threads; NG = 4 -> 4 members per
+// thread, 512 threads (twice the warps to hide the shared-memory and DFMA latencies)
+template <int NG>
+__global__ void __launch_bounds__(128 * NG, 1)
+gemm_tn_f32_wide_kernel(int rows, int cols, int Kp, const float* __restrict__ A, const float* __restrict__ G,
+                        double* __restrict__ part) {
+  constexpr int N = 16, NT = 128 * NG, MN = N / NG;      // threads, members per thread
+  extern __shared__ __align__(16) float smw[];
+  float* As = smw;                                   // [WNS][WRC][WTC]
+  float* Gs = As + WNS * WRC * WTC;                  // [WNS][WRC][N]
+  double* Ad = reinterpret_cast<double*>(Gs + WNS * WRC * N);   // [WRC][WTC]
+  double* Gd = Ad + WRC * WTC;                       // [WRC][N]
+  const int tid = threadIdx.x;
+  const int nq = tid % NG, cq = tid / NG;
+  const int c0 = blockIdx.x * WTC;
+  const int r_begin = (int)((int64_t)rows * blockIdx.y / gridDim.y);
+  const int r_end = (int)((int64_t)rows * (blockIdx.y + 1) / gridDim.y);
+  const int nch = (r_end - r_begin + WRC - 1) / WRC;
+  auto issue = [&](int ch) {
+    if (ch < nch) {
+      const int r0 = r_begin + ch * WRC;
+      float* da = As + (size_t)(ch % WNS) * WRC * WTC;
+      float* dg = Gs + (size_t)(ch % WNS) * WRC * N;
+      for (int q = tid; q < WRC * (WTC / 4); q += NT) {
+        const int rr = q / (WTC / 4), c4 = (q % (WTC / 4)) * 4;
+        const int r = r0 + rr;
+        const bool ok = r < r_end && c0 + c4 < Kp;
+        cp_async16(da + rr * WTC + c4, A + (int64_t)(ok ? r : r_begin) * Kp + (ok ? c0 + c4 : 0), ok);
+      }
+      if (tid < WRC * (N / 4)) {
+        const int rr = tid / (N / 4), n4 = (tid % (N / 4)) * 4;
+        const int r = r0 + rr;
+        const bool ok = r < r_end;
+        cp_async16(dg + rr * N + n4, G + (int64_t)(ok ? r : r_begin) * N + n4, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  issue(1);
+  double acc[8][MN];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = 0; c < MN; ++c) acc[i][c] = 0.0;
+  for (int ch = 0; ch < nch; ++ch) {
+    issue(ch + 2);
+    cp_async_wait<2>();
+    __syncthreads();
+    {
+      const float2* a2 = reinterpret_cast<const float2*>(As + (size_t)(ch % WNS) * WRC * WTC);
+      double2* d2 = reinterpret_cast<double2*>(Ad);
+      for (int q = tid; q < WRC * WTC / 2; q += NT) {
+        const float2 v = a2[q];
+        d2[q] = make_double2((double)v.x, (double)v.y);
+      }
+      const float* gg = Gs + (size_t)(ch % WNS) * WRC * N;
+      if (tid < WRC * N) Gd[tid] = (double)gg[tid];
+    }
+    __syncthreads();
+    const double* a = Ad + cq * 2;
+    const double* gq = Gd + nq * MN;
+#pragma unroll 2
+    for (int rr = 0; rr < WRC; ++rr) {
+      double av[8], gv[MN];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double2 t = *reinterpret_cast<const double2*>(a + rr * WTC + j * 256);
+        av[2 * j] = t.x; av[2 * j + 1] = t.y;
+      }
+#pragma unroll
+      for (int j = 0; j < MN / 2; ++j) {
+        const double2 t = *reinterpret_cast<const double2*>(gq + rr * N + 2 * j);
+        gv[2 * j] = t.x; gv[2 * j + 1] = t.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int c = 0; c < MN; ++c) acc[i][c] = fma(av[i], gv[c], acc[i][c]);
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = c0 + (i >> 1) * 256 + cq * 2 + (i & 1);
+    if (c >= cols) continue;
+    double2* o = reinterpret_cast<double2*>(part + ((int64_t)blockIdx.y * cols + c) * N + nq * MN);
+#pragma unroll
+    for (int j = 0; j < MN / 2; ++j) o[j] = make_double2(acc[i][2 * j], acc[i][2 * j + 1]);
+  }
+}
+
 // h[c][n] += g[c] (T[c][n] + sum_s part[s][c][n])   (splits in order; T optional)
 // xs (optional, N = 16): the new h~ split for the tensor-core GEMM of
 // tc_gemm.cuh -- per 32-row chunk of h~, [hi | lo] tiles of [16 n][32 k] in
